@@ -1,0 +1,181 @@
+/*
+ * sorsvd_b200.h — C ABI of the B200-native SOR-SVD hot path.
+ *
+ * This is the drop-in boundary for the reference's header-only C++ API
+ * (/root/reference/proj/include/sorsvd). Plain pointers and sizes only; no
+ * torch or C++ types cross it. Matrices are row-major, element (i,j) at
+ * p[i*ld + j], exactly the reference Matrix layout (matrix.hpp:61).
+ *
+ * Error convention: every entry point returns a sorsvd_status. The codes
+ * mirror the reference exception taxonomy (errors.hpp:9-26):
+ *   SORSVD_ERR_SHAPE     <-> sorsvd::shape_error      (errors.hpp:9)
+ *   SORSVD_ERR_PARAMETER <-> sorsvd::parameter_error  (errors.hpp:14)
+ *   SORSVD_ERR_NUMERICAL <-> sorsvd::numerical_error  (errors.hpp:24)
+ * plus device-side failures. sorsvd_last_error() returns the message of the
+ * last failure on a context (the reference's exception what()).
+ *
+ * Threading: a context is bound to one device and is not thread-safe; use one
+ * per host thread (the reference functions are pure and re-entrant,
+ * the context only owns streams, workspaces and graphs).
+ */
+#ifndef SORSVD_B200_H
+#define SORSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sorsvd_status {
+    SORSVD_OK = 0,
+    SORSVD_ERR_SHAPE = 1,
+    SORSVD_ERR_PARAMETER = 2,
+    SORSVD_ERR_NUMERICAL = 3,
+    SORSVD_ERR_CUDA = 4,
+    SORSVD_ERR_NCCL = 5,
+    SORSVD_ERR_OOM = 6,
+    SORSVD_ERR_UNSUPPORTED = 7,
+    SORSVD_ERR_INTERNAL = 8
+} sorsvd_status;
+
+typedef enum sorsvd_dtype { SORSVD_F64 = 0, SORSVD_F32 = 1 } sorsvd_dtype;
+
+/* SketchMethod (sketch.hpp:13) */
+typedef enum sorsvd_method { SORSVD_SOR = 0, SORSVD_SOR_POWER = 1, SORSVD_RSVD = 2, SORSVD_TSR = 3 } sorsvd_method;
+
+/* FlopVariant (sketch.hpp:176) */
+typedef enum sorsvd_flop_variant {
+    SORSVD_FLOPS_SOR_3PASS = 0,
+    SORSVD_FLOPS_SOR_2PASS = 1,
+    SORSVD_FLOPS_SOR_POWER_2Q3 = 2,
+    SORSVD_FLOPS_SOR_POWER_2Q2 = 3
+} sorsvd_flop_variant;
+
+/* desc.flags */
+#define SORSVD_FLAG_OMEGA_GIVEN 0x1u  /* use the caller's Omega instead of gaussian_matrix(n,ell,seed) */
+#define SORSVD_FLAG_NO_GRAPH 0x2u     /* issue kernels directly (no CUDA-graph replay) */
+#define SORSVD_FLAG_STAGE_TIMES 0x4u  /* per-stage CUDA-event times in stats (implies NO_GRAPH) */
+#define SORSVD_FLAG_BASIC 0x8u        /* sor_svd semantics: require q == 0 (sketch.hpp:116-119) */
+
+typedef struct sorsvd_ctx sorsvd_ctx;
+
+/* Problem descriptor: SketchConfig (sketch.hpp:29-34) + the matrix shape. */
+typedef struct sorsvd_desc {
+    int64_t m;        /* rows of A held by this rank (all rows when world == 1) */
+    int64_t n;        /* columns of A */
+    int64_t lda;      /* leading dimension of A (>= n) */
+    int32_t k;        /* target rank */
+    int32_t ell;      /* sketch size, k <= ell < min(m_global, n) */
+    int32_t q;        /* power iterations */
+    int32_t single_pass; /* SketchConfig::single_pass (not supported yet -> SORSVD_ERR_UNSUPPORTED) */
+    uint64_t seed;    /* Omega = gaussian_matrix(n, ell, seed) unless OMEGA_GIVEN */
+    int32_t dtype;    /* sorsvd_dtype of A (SORSVD_F64 only in this build) */
+    uint32_t flags;
+    int64_t m_global; /* total rows over all ranks (0 -> m) */
+} sorsvd_desc;
+
+typedef struct sorsvd_stats {
+    double ms_total;     /* device time of the call (CUDA events) */
+    double ms_h2d;       /* host->device copies (host-buffer entry points) */
+    double ms_d2h;       /* device->host copies */
+    double ms_passes;    /* STAGE_TIMES only: the 2q+2 sketch passes */
+    double ms_qr;        /* STAGE_TIMES only: TSQR of T1 and T2 */
+    double ms_project;   /* STAGE_TIMES only: M = Q1^T A Q2 */
+    double ms_svd;       /* STAGE_TIMES only: Jacobi SVD of M */
+    double ms_basis;     /* STAGE_TIMES only: U = Q1 Ut, V = Q2 Vt */
+    double flops_passes; /* 2*m*n*ell*passes (BASELINE metric numerator) */
+    double bytes_passes; /* m*n*sizeof(A)*passes */
+    int32_t passes;      /* LowRankApprox::passes (sketch.hpp:104) */
+    int32_t method;      /* sorsvd_method */
+    int32_t launches;    /* kernel launches issued for the call */
+    int32_t jacobi_sweeps;
+} sorsvd_stats;
+
+/* ---- context -------------------------------------------------------------- */
+int sorsvd_ctx_create(int device, sorsvd_ctx** out);
+/* Multi-GPU: one context per rank (one process per GPU). unique_id is the
+ * 128-byte NCCL id produced by sorsvd_nccl_unique_id on rank 0 and broadcast
+ * by the caller (e.g. torch.distributed). */
+int sorsvd_nccl_unique_id(void* out128);
+int sorsvd_ctx_create_dist(int device, int rank, int world, const void* unique_id128, sorsvd_ctx** out);
+void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
+const char* sorsvd_last_error(const sorsvd_ctx* ctx);
+/* Bind the context to a caller stream (cudaStream_t, may be 0 for the
+ * context's own stream). */
+int sorsvd_set_stream(sorsvd_ctx* ctx, void* stream);
+int sorsvd_ctx_rank(const sorsvd_ctx* ctx, int* rank, int* world);
+
+/* ---- sor_svd_power (sketch.hpp:87) / sor_svd (sketch.hpp:116) ---------------
+ * Host buffers: A (m x lda), omega (n x ell, or NULL -> drawn from seed),
+ * outputs U (m x k), sigma (k), V (n x k). Includes H2D/D2H. */
+int sorsvd_sor_svd_power(sorsvd_ctx* ctx, const sorsvd_desc* desc, const void* A, const double* omega,
+                         double* U, double* sigma, double* V, sorsvd_stats* stats);
+/* Device buffers (already resident in HBM on the context's device). When
+ * omega is NULL the host draws gaussian_matrix(n, ell, seed) and uploads it. */
+int sorsvd_sor_svd_power_device(sorsvd_ctx* ctx, const sorsvd_desc* desc, const void* dA,
+                                const double* dOmega, double* dU, double* dSigma, double* dV,
+                                sorsvd_stats* stats);
+
+/* ---- RPCA by inexact ALM --------------- */
+typedef struct sorsvd_rpca_desc {
+    int64_t m, n, ldd;
+    double lambda;        /* <= 0 -> 1/sqrt(max(m,n)) */
+    double mu0;           /* <= 0 -> 1.25/sigma_1(D) estimated on the device */
+    double mu_bar_factor; /* mu_bar = mu_bar_factor * mu0 (default 1e7) */
+    double rho;           /* 1.6 */
+    double tol;           /* 1e-7 */
+    int32_t max_iter;
+    int32_t ell;          /* sketch size = truncation rank */
+    int32_t q;
+    int32_t dtype;
+    uint64_t seed;        /* iteration it uses seed + it */
+    uint32_t flags;
+    int32_t pad_;
+} sorsvd_rpca_desc;
+
+typedef struct sorsvd_rpca_result {
+    int32_t iterations;
+    int32_t rank_l;      /* count of shrunk sigma > 1e-8 * max */
+    int32_t converged;
+    int32_t launches;
+    int64_t nnz_s;
+    double rel_error;    /* ||D-L-S||_F / ||D||_F */
+    double mu0;
+    double ms_total;
+    double ms_h2d;
+    double ms_d2h;
+} sorsvd_rpca_result;
+
+/* Host buffers D (m x ldd) -> L, S (m x n, dense row-major). */
+int sorsvd_rpca_alm(sorsvd_ctx* ctx, const sorsvd_rpca_desc* desc, const double* D, double* L, double* S,
+                    sorsvd_rpca_result* res);
+/* Device buffers. L may be NULL (factors only). */
+int sorsvd_rpca_alm_device(sorsvd_ctx* ctx, const sorsvd_rpca_desc* desc, const double* dD, double* dL,
+                           double* dS, sorsvd_rpca_result* res);
+
+/* ---- stage-level entry points (kernel unit tests) ------------------------- */
+/* thin_qr (dense.hpp:114): dT (m x ldt) -> dQ (m x ldq), dR (k x ldr); device. */
+int sorsvd_thin_qr_device(sorsvd_ctx* ctx, int64_t m, int32_t k, const double* dT, int64_t ldt, double* dQ,
+                          int64_t ldq, double* dR, int64_t ldr);
+/* full_svd of a square k x k (dense.hpp:65): device buffers, row-major. */
+int sorsvd_small_svd_device(sorsvd_ctx* ctx, int32_t k, const double* dM, int64_t ldm, double* dU,
+                            int64_t ldu, double* dS, double* dV, int64_t ldv, int32_t* sweeps);
+/* matmul (dense.hpp:20) restricted to the skinny shapes of the path:
+ * C = op(A) * B, op(A) = A (ta=0, A is M x K) or A^T (ta=1, A is K x M). */
+int sorsvd_matmul_device(sorsvd_ctx* ctx, int32_t ta, int64_t M, int64_t K, int32_t N, const double* dA,
+                         int64_t lda, const double* dB, int64_t ldb, double* dC, int64_t ldc);
+
+/* ---- host helpers mirroring random.hpp / sketch.hpp ----------------------- */
+uint64_t sorsvd_sub_seed(uint64_t seed, uint64_t stream);                    /* random.hpp:24 */
+int sorsvd_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out, int nthreads); /* random.hpp:60 */
+long long sorsvd_flop_estimate(long long m, long long n, long long ell, long long k, long long q,
+                               int variant);                                  /* sketch.hpp:178 */
+int sorsvd_validate_sketch(int64_t m, int64_t n, int32_t k, int32_t ell, int32_t q); /* sketch.hpp:62 */
+const char* sorsvd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SORSVD_B200_H */

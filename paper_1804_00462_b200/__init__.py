@@ -1,0 +1,411 @@
+"""B200-native SOR-SVD (arXiv 1804.00462) and ALM-RPCA — Python host API.
+
+Mirrors the reference C++ API (/root/reference/proj/include/sorsvd):
+
+    sor_svd_power(a, k, cfg)  -> LowRankApprox      sketch.hpp:87
+    sor_svd(a, k, cfg)        -> LowRankApprox      sketch.hpp:116
+    SketchConfig / LowRankApprox / SketchMethod      sketch.hpp:13-48
+    flop_estimate / FlopVariant                      sketch.hpp:176-196
+    gaussian_matrix / sub_seed                       random.hpp:24,60
+    thin_qr / full_svd / matmul (device, skinny)     dense.hpp:114,65,20
+    rpca_alm / RpcaConfig / RpcaResult
+    ShapeError / ParameterError / NumericalError     errors.hpp:9-26
+
+Every call goes through the C ABI of the sm_100a library
+(include/sorsvd_b200.h, paper_1804_00462_b200/_lib/libsorsvd_b200.so). Host
+(numpy) inputs use the host-buffer entry points (H2D/D2H inside); CUDA torch
+tensors use the device entry points on torch's current stream. There is no
+CPU fallback: without the library or a GPU every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _capi as C
+
+__all__ = [
+    "SketchMethod", "SketchConfig", "LowRankApprox", "FlopVariant", "RpcaConfig", "RpcaResult", "Context",
+    "ShapeError", "ParameterError", "NumericalError", "CudaError", "NcclError", "UnsupportedError",
+    "sor_svd_power", "sor_svd", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
+    "flop_estimate", "validate_sketch", "thin_qr", "full_svd", "matmul", "default_context", "version",
+]
+
+
+# ----------------------------------------------------------------- errors --
+class ShapeError(ValueError):
+    """sorsvd::shape_error (errors.hpp:9)"""
+
+
+class ParameterError(ValueError):
+    """sorsvd::parameter_error (errors.hpp:14)"""
+
+
+class NumericalError(RuntimeError):
+    """sorsvd::numerical_error (errors.hpp:24)"""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class NcclError(RuntimeError):
+    pass
+
+
+class UnsupportedError(NotImplementedError):
+    pass
+
+
+_ERRORS = {C.ERR_SHAPE: ShapeError, C.ERR_PARAMETER: ParameterError, C.ERR_NUMERICAL: NumericalError,
+           C.ERR_CUDA: CudaError, C.ERR_NCCL: NcclError, C.ERR_OOM: MemoryError,
+           C.ERR_UNSUPPORTED: UnsupportedError, C.ERR_INTERNAL: RuntimeError}
+
+
+def _check(rc: int, ctx=None):
+    if rc != C.OK:
+        msg = C.lib().sorsvd_last_error(ctx).decode(errors="replace")
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+# ------------------------------------------------------------------ types --
+class SketchMethod(enum.IntEnum):
+    """sketch.hpp:13"""
+    sor = 0
+    sor_power = 1
+    rsvd = 2
+    tsr = 3
+
+
+class FlopVariant(enum.IntEnum):
+    """sketch.hpp:176"""
+    sor_3pass = 0
+    sor_2pass = 1
+    sor_power_2q3 = 2
+    sor_power_2q2 = 3
+
+
+@dataclass
+class SketchConfig:
+    """sketch.hpp:29-34"""
+    ell: int = 0
+    q: int = 0
+    seed: int = 0
+    single_pass: bool = False
+
+
+@dataclass
+class LowRankApprox:
+    """sketch.hpp:39-48 (u: m x k, sigma: k, v: n x k)."""
+    u: object
+    sigma: object
+    v: object
+    method: SketchMethod
+    passes: int
+    ell: int
+    q: int
+    seed: int
+    stats: dict = field(default_factory=dict)
+
+
+@dataclass
+class RpcaConfig:
+    """SPEC.md:356-360 (ledger: SURVEY.md Appendix B). lam/mu0 <= 0 select
+    the defaults 1/sqrt(max(m,n)) and 1.25/sigma_1(X)."""
+    lam: float = 0.0
+    mu0: float = 0.0
+    mu_bar_factor: float = 1e7
+    rho: float = 1.6
+    tol: float = 1e-7
+    max_iter: int = 500
+    ell: int = 10
+    q: int = 1
+    seed: int = 0
+
+
+@dataclass
+class RpcaResult:
+    """SPEC.md:361-365"""
+    l: object
+    s: object
+    iterations: int
+    rel_error: float
+    rank_l: int
+    nnz_s: int
+    converged: bool
+    mu0: float = 0.0
+    stats: dict = field(default_factory=dict)
+
+
+# ---------------------------------------------------------------- context --
+class Context:
+    """Owns a device context (streams, workspaces, cached CUDA graphs).
+
+    Multi-GPU: Context(device, rank=r, world=w, nccl_id=bytes) with the id from
+    Context.nccl_unique_id() on rank 0, broadcast by the caller."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+        h = ctypes.c_void_p()
+        if world > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ParameterError("parameter: world > 1 needs the 128-byte NCCL unique id")
+            buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            _check(C.lib().sorsvd_ctx_create_dist(device, rank, world, ctypes.cast(buf, ctypes.c_void_p),
+                                                   ctypes.byref(h)))
+        else:
+            _check(C.lib().sorsvd_ctx_create(device, ctypes.byref(h)))
+        self._h = h
+        self.device = device
+        self.rank = rank
+        self.world = world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(C.lib().sorsvd_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+        return buf.raw
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, stream_ptr: int):
+        _check(C.lib().sorsvd_set_stream(self._h, ctypes.c_void_p(stream_ptr)), self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            C.lib().sorsvd_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+def version() -> str:
+    return C.lib().sorsvd_version().decode()
+
+
+# ---------------------------------------------------------- host helpers --
+def sub_seed(seed: int, stream: int) -> int:
+    """random.hpp:24"""
+    return int(C.lib().sorsvd_sub_seed(seed & (2**64 - 1), stream & (2**64 - 1)))
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int, nthreads: int = 0) -> np.ndarray:
+    """random.hpp:60 — bit-identical to the reference draw (host, threaded)."""
+    if rows < 1 or cols < 1:
+        raise ShapeError("shape: matrix dimensions must be positive")
+    out = np.empty((rows, cols), dtype=np.float64)
+    _check(C.lib().sorsvd_gaussian_matrix(rows, cols, seed & (2**64 - 1), out.ctypes.data_as(C.c_dp), nthreads))
+    return out
+
+
+def flop_estimate(m: int, n: int, ell: int, k: int, q: int, variant: FlopVariant) -> int:
+    """sketch.hpp:178"""
+    v = C.lib().sorsvd_flop_estimate(m, n, ell, k, q, int(variant))
+    if v < 0:
+        raise ParameterError("parameter: flop_estimate requires positive dimensions and q >= 0")
+    return int(v)
+
+
+def validate_sketch(m: int, n: int, k: int, ell: int, q: int) -> None:
+    """sketch.hpp:62-69"""
+    _check(C.lib().sorsvd_validate_sketch(m, n, k, ell, q))
+
+
+# ------------------------------------------------------------- internals --
+def _is_torch_cuda(x) -> bool:
+    try:
+        import torch
+    except ImportError:
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _torch_stream(ctx: Context, dev_tensor):
+    import torch
+    ctx.set_stream(torch.cuda.current_stream(dev_tensor.device).cuda_stream)
+
+
+def _desc(m, n, lda, k, cfg: SketchConfig, flags: int, m_global: int = 0) -> C.SorsvdDesc:
+    return C.SorsvdDesc(m, n, lda, k, cfg.ell, cfg.q, int(cfg.single_pass), cfg.seed & (2**64 - 1), C.F64,
+                        flags, m_global)
+
+
+# -------------------------------------------------------------- hot path --
+def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Context] = None,
+                  stage_times: bool = False, use_graph: bool = True, m_global: int = 0,
+                  _basic: bool = False) -> LowRankApprox:
+    """Subspace-orbit randomized SVD with q power iterations (sketch.hpp:87).
+
+    a: numpy float64 (m, n) on the host, or a CUDA float64 torch tensor.
+    omega: optional (n, ell) test matrix; default gaussian_matrix(n, ell, seed)
+    exactly as the reference draws it (sketch.hpp:90)."""
+    flags = 0
+    if omega is not None:
+        flags |= C.FLAG_OMEGA_GIVEN
+    if stage_times:
+        flags |= C.FLAG_STAGE_TIMES
+    if not use_graph:
+        flags |= C.FLAG_NO_GRAPH
+    if _basic:
+        flags |= C.FLAG_BASIC
+    st = C.SorsvdStats()
+    if _is_torch_cuda(a):
+        import torch
+        if a.dtype != torch.float64 or a.dim() != 2 or a.stride(1) != 1:
+            raise ShapeError("shape: device input must be a row-major float64 matrix")
+        ctx = ctx or default_context(a.device.index or 0)
+        _torch_stream(ctx, a)
+        m, n = a.shape
+        lda = a.stride(0)
+        d = _desc(m, n, lda, k, cfg, flags, m_global)
+        u = torch.empty((m, k), dtype=torch.float64, device=a.device)
+        s = torch.empty((k,), dtype=torch.float64, device=a.device)
+        v = torch.empty((n, k), dtype=torch.float64, device=a.device)
+        om_ptr = None
+        if omega is not None:
+            om = torch.as_tensor(omega, dtype=torch.float64, device=a.device).contiguous()
+            om_ptr = om.data_ptr()
+        _check(C.lib().sorsvd_sor_svd_power_device(ctx.handle, ctypes.byref(d), a.data_ptr(), om_ptr,
+                                                   u.data_ptr(), s.data_ptr(), v.data_ptr(), ctypes.byref(st)),
+               ctx.handle)
+    else:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.ndim != 2:
+            raise ShapeError("shape: input must be a matrix")
+        ctx = ctx or default_context(0)
+        m, n = a.shape
+        d = _desc(m, n, n, k, cfg, flags, m_global)
+        if k < 1:
+            validate_sketch(m_global or m, n, k, cfg.ell, cfg.q)
+        u = np.empty((m, k))
+        s = np.empty((k,))
+        v = np.empty((n, k))
+        om_p = None
+        if omega is not None:
+            om = np.ascontiguousarray(omega, dtype=np.float64)
+            if om.shape != (n, cfg.ell):
+                raise ShapeError("shape: omega must be n x ell")
+            om_p = om.ctypes.data_as(C.c_dp)
+        _check(C.lib().sorsvd_sor_svd_power(ctx.handle, ctypes.byref(d), a.ctypes.data_as(ctypes.c_void_p), om_p,
+                                            u.ctypes.data_as(C.c_dp), s.ctypes.data_as(C.c_dp),
+                                            v.ctypes.data_as(C.c_dp), ctypes.byref(st)), ctx.handle)
+    method = SketchMethod.sor if cfg.q == 0 else SketchMethod.sor_power
+    return LowRankApprox(u, s, v, method, st.passes, cfg.ell, cfg.q, cfg.seed, st.as_dict())
+
+
+def sor_svd(a, k: int, cfg: SketchConfig, **kw) -> LowRankApprox:
+    """Basic form; requires cfg.q == 0 (sketch.hpp:116-119)."""
+    if cfg.q != 0:
+        raise ParameterError("parameter: sor_svd requires q == 0; use sor_svd_power")
+    return sor_svd_power(a, k, cfg, _basic=True, **kw)
+
+
+# ----------------------------------------------------- stage entry points --
+def thin_qr(t, ctx: Optional[Context] = None):
+    """dense.hpp:114 on a CUDA float64 tensor (tall-skinny, k <= 256): (q, r)."""
+    import torch
+    if not _is_torch_cuda(t) or t.dtype != torch.float64:
+        raise ShapeError("shape: thin_qr expects a CUDA float64 tensor")
+    ctx = ctx or default_context(t.device.index or 0)
+    _torch_stream(ctx, t)
+    t = t.contiguous()
+    m, k = t.shape
+    q = torch.empty((m, k), dtype=torch.float64, device=t.device)
+    r = torch.empty((k, k), dtype=torch.float64, device=t.device)
+    _check(C.lib().sorsvd_thin_qr_device(ctx.handle, m, k, t.data_ptr(), k, q.data_ptr(), k, r.data_ptr(), k),
+           ctx.handle)
+    return q, r
+
+
+def full_svd(mat, ctx: Optional[Context] = None):
+    """dense.hpp:65 for a small square CUDA float64 matrix: (u, sigma, v, sweeps)."""
+    import torch
+    if not _is_torch_cuda(mat) or mat.dtype != torch.float64 or mat.shape[0] != mat.shape[1]:
+        raise ShapeError("shape: full_svd expects a square CUDA float64 tensor")
+    ctx = ctx or default_context(mat.device.index or 0)
+    _torch_stream(ctx, mat)
+    mat = mat.contiguous()
+    k = mat.shape[0]
+    u = torch.empty((k, k), dtype=torch.float64, device=mat.device)
+    v = torch.empty((k, k), dtype=torch.float64, device=mat.device)
+    s = torch.empty((k,), dtype=torch.float64, device=mat.device)
+    sw = C.c_i32()
+    _check(C.lib().sorsvd_small_svd_device(ctx.handle, k, mat.data_ptr(), k, u.data_ptr(), k, s.data_ptr(),
+                                           v.data_ptr(), k, ctypes.byref(sw)), ctx.handle)
+    return u, s, v, sw.value
+
+
+def matmul(a, b, transpose_a: bool = False, ctx: Optional[Context] = None):
+    """dense.hpp:20 restricted to skinny products: op(a) @ b with b narrow."""
+    import torch
+    if not (_is_torch_cuda(a) and _is_torch_cuda(b)):
+        raise ShapeError("shape: matmul expects CUDA float64 tensors")
+    ctx = ctx or default_context(a.device.index or 0)
+    _torch_stream(ctx, a)
+    a = a.contiguous()
+    b = b.contiguous()
+    M, K = (a.shape[1], a.shape[0]) if transpose_a else a.shape
+    if b.shape[0] != K:
+        raise ShapeError(f"shape: matmul inner dimensions {K} and {b.shape[0]} differ")
+    N = b.shape[1]
+    c = torch.empty((M, N), dtype=torch.float64, device=a.device)
+    _check(C.lib().sorsvd_matmul_device(ctx.handle, int(transpose_a), M, K, N, a.data_ptr(), a.shape[1],
+                                        b.data_ptr(), N, c.data_ptr(), N), ctx.handle)
+    return c
+
+
+# ------------------------------------------------------------------- RPCA --
+def rpca_default_config(m: int, n: int, ell: int = 10, q: int = 1, seed: int = 0) -> RpcaConfig:
+    """SPEC.md:395-403 (mu0 left to the device estimate; ell given by the caller)."""
+    return RpcaConfig(lam=1.0 / math.sqrt(max(m, n)), mu0=0.0, mu_bar_factor=1e7, rho=1.6, tol=1e-7,
+                      max_iter=500, ell=ell, q=q, seed=seed)
+
+
+def rpca_alm(x, cfg: RpcaConfig, ctx: Optional[Context] = None, want_l: bool = True) -> RpcaResult:
+    """Inexact ALM RPCA with SOR-SVD per iteration."""
+    res = C.RpcaRes()
+    if _is_torch_cuda(x):
+        import torch
+        ctx = ctx or default_context(x.device.index or 0)
+        _torch_stream(ctx, x)
+        m, n = x.shape
+        d = C.RpcaDesc(m, n, x.stride(0), cfg.lam, cfg.mu0, cfg.mu_bar_factor, cfg.rho, cfg.tol, cfg.max_iter,
+                       cfg.ell, cfg.q, C.F64, cfg.seed & (2**64 - 1), 0, 0)
+        s = torch.empty((m, n), dtype=torch.float64, device=x.device)
+        l = torch.empty((m, n), dtype=torch.float64, device=x.device) if want_l else None
+        _check(C.lib().sorsvd_rpca_alm_device(ctx.handle, ctypes.byref(d), x.data_ptr(),
+                                              l.data_ptr() if l is not None else None, s.data_ptr(),
+                                              ctypes.byref(res)), ctx.handle)
+    else:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        ctx = ctx or default_context(0)
+        m, n = x.shape
+        d = C.RpcaDesc(m, n, n, cfg.lam, cfg.mu0, cfg.mu_bar_factor, cfg.rho, cfg.tol, cfg.max_iter, cfg.ell,
+                       cfg.q, C.F64, cfg.seed & (2**64 - 1), 0, 0)
+        s = np.empty((m, n))
+        l = np.empty((m, n)) if want_l else None
+        _check(C.lib().sorsvd_rpca_alm(ctx.handle, ctypes.byref(d), x.ctypes.data_as(C.c_dp),
+                                       l.ctypes.data_as(C.c_dp) if l is not None else None,
+                                       s.ctypes.data_as(C.c_dp), ctypes.byref(res)), ctx.handle)
+    stats = {f: getattr(res, f) for f, _ in res._fields_}
+    return RpcaResult(l, s, res.iterations, res.rel_error, res.rank_l, res.nnz_s, bool(res.converged), res.mu0,
+                      stats)

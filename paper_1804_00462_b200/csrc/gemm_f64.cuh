@@ -1,0 +1,208 @@
+// K1/K2/K4/K6: FP64 skinny-GEMM engine on the sm_100a DMMA pipe.
+//
+// Every product on the SOR-SVD path (sketch.hpp:95,96,100-102,105,107 ->
+// cblas_dgemm, dense.hpp:30) has one huge dimension (m or n of A), one huge
+// reduction or output dimension, and one narrow dimension (k <= 256). This
+// kernel computes
+//     C[M x N] = alpha * op(A)[M x K] * B[K x N]
+// with op(A) = A (A row-major M x K, "NN": T1 = A*Omega, Y = A*Q2, U = Q1*Ut)
+//   or op(A) = A^T (A stored K x M row-major, "TN": T2 = A^T*T1, M = Q1^T*Y),
+// B row-major with its columns zero-padded to a multiple of 8 (N chunks of
+// up to 128 columns per CTA, grid.y), and split-K over grid.z with
+// deterministic partial buffers reduced by reduce_splits_kernel.
+//
+// Tiles: 8 warps along M, each owning an (8*FM) x (8*FN) accumulator block of
+// m8n8k4 DMMA fragments (FP64 tensor core, 37 TFLOP/s measured on B200);
+// A and B tiles are staged through a 4-stage cp.async (LDGSTS) ring in shared
+// memory with +4-double row padding so every fragment read is bank-conflict
+// free. A is streamed exactly once per pass (the dominant HBM traffic).
+#pragma once
+#include "common.cuh"
+
+namespace sorsvd_dev {
+
+struct GemmArgs {
+    const double* A;
+    int64_t lda;
+    const double* B;
+    int64_t ldb;
+    int64_t b_seg_stride;  // segmented GEMM: B for segment s is B + s*b_seg_stride
+    double* C;
+    int64_t ldc;
+    int64_t c_split_stride;  // split z writes C + z*c_split_stride
+    int64_t M;
+    int64_t K;
+    int64_t k_chunk;        // K range per split (multiple of BK)
+    const int* tile_row0;   // optional explicit M-tile table (segmented GEMM)
+    const int* tile_rows;
+    const int* tile_seg;
+    double alpha;
+};
+
+constexpr int kGemmThreads = 256;
+constexpr int kGemmBK = 16;
+constexpr int kGemmStages = 4;
+
+template <int FM, int FN, bool TA>
+struct GemmShape {
+    static constexpr int BM = 8 * 8 * FM;
+    static constexpr int BN = 8 * FN;
+    static constexpr int BK = kGemmBK;
+    static constexpr int LDA_S = TA ? (BM + 4) : (BK + 4);  // padded smem strides (== 4 mod 8)
+    static constexpr int LDB_S = BN + 4;
+    static constexpr int A_STAGE = TA ? BK * LDA_S : BM * LDA_S;
+    static constexpr int B_STAGE = BK * LDB_S;
+    static constexpr int STAGE = A_STAGE + B_STAGE;
+    static constexpr size_t SMEM = (size_t)kGemmStages * STAGE * sizeof(double);
+};
+
+template <int FM, int FN, bool TA, bool V16>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
+    using S = GemmShape<FM, FN, TA>;
+    extern __shared__ __align__(128) double smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+
+    int64_t row0, rows;
+    int seg = 0;
+    if (p.tile_row0) {
+        row0 = p.tile_row0[blockIdx.x];
+        rows = p.tile_rows[blockIdx.x];
+        seg = p.tile_seg[blockIdx.x];
+    } else {
+        row0 = (int64_t)blockIdx.x * S::BM;
+        rows = p.M - row0 < S::BM ? p.M - row0 : S::BM;
+    }
+    const int ncol0 = blockIdx.y * S::BN;
+    const double* __restrict__ Bp = p.B + seg * p.b_seg_stride + ncol0;
+    const double* __restrict__ Ap = p.A;
+    const int64_t kBegin = (int64_t)blockIdx.z * p.k_chunk;
+    int64_t kEnd = kBegin + p.k_chunk;
+    if (kEnd > p.K) kEnd = p.K;
+    const int KT = kEnd > kBegin ? (int)((kEnd - kBegin + S::BK - 1) / S::BK) : 0;
+
+    auto load_stage = [&](int slot, int kt) {
+        double* As = smem + slot * S::STAGE;
+        double* Bs = As + S::A_STAGE;
+        const int64_t k0 = kBegin + (int64_t)kt * S::BK;
+        if (!TA) {
+            if (V16) {
+                for (int id = tid; id < S::BM * (S::BK / 2); id += kGemmThreads) {
+                    const int r = id / (S::BK / 2), c = id % (S::BK / 2);
+                    const int64_t kk = k0 + 2 * c;
+                    int bytes = 0;
+                    const double* src = Ap;
+                    if (r < rows && kk < kEnd) {
+                        const int64_t rem = (kEnd - kk) * 8;
+                        bytes = rem >= 16 ? 16 : (int)rem;
+                        src = Ap + (row0 + r) * p.lda + kk;
+                    }
+                    cp_async16(As + r * S::LDA_S + 2 * c, src, bytes);
+                }
+            } else {
+                for (int id = tid; id < S::BM * S::BK; id += kGemmThreads) {
+                    const int r = id / S::BK, c = id % S::BK;
+                    const int64_t kk = k0 + c;
+                    const bool ok = r < rows && kk < kEnd;
+                    cp_async8(As + r * S::LDA_S + c, ok ? Ap + (row0 + r) * p.lda + kk : Ap, ok ? 8 : 0);
+                }
+            }
+        } else {
+            if (V16) {
+                for (int id = tid; id < S::BK * (S::BM / 2); id += kGemmThreads) {
+                    const int kr = id / (S::BM / 2), c = id % (S::BM / 2);
+                    const int64_t kk = k0 + kr;
+                    int bytes = 0;
+                    const double* src = Ap;
+                    if (kk < kEnd && 2 * c < rows) {
+                        const int64_t rem = (rows - 2 * c) * 8;
+                        bytes = rem >= 16 ? 16 : (int)rem;
+                        src = Ap + kk * p.lda + row0 + 2 * c;
+                    }
+                    cp_async16(As + kr * S::LDA_S + 2 * c, src, bytes);
+                }
+            } else {
+                for (int id = tid; id < S::BK * S::BM; id += kGemmThreads) {
+                    const int kr = id / S::BM, c = id % S::BM;
+                    const int64_t kk = k0 + kr;
+                    const bool ok = kk < kEnd && c < rows;
+                    cp_async8(As + kr * S::LDA_S + c, ok ? Ap + kk * p.lda + row0 + c : Ap, ok ? 8 : 0);
+                }
+            }
+        }
+        for (int id = tid; id < S::BK * (S::BN / 2); id += kGemmThreads) {
+            const int kr = id / (S::BN / 2), c = id % (S::BN / 2);
+            const int64_t kk = k0 + kr;
+            const bool ok = kk < kEnd;
+            cp_async16(Bs + kr * S::LDB_S + 2 * c, ok ? Bp + kk * p.ldb + 2 * c : Bp, ok ? 16 : 0);
+        }
+    };
+
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < kGemmStages - 1; ++s) {
+        if (s < KT) load_stage(s, s);
+        cp_async_commit();
+    }
+    const int wrow = warp * 8 * FM;
+    for (int kt = 0; kt < KT; ++kt) {
+        cp_async_wait<kGemmStages - 2>();
+        __syncthreads();
+        {
+            const int nk = kt + kGemmStages - 1;
+            if (nk < KT) load_stage(nk % kGemmStages, nk);
+            cp_async_commit();
+        }
+        const double* As = smem + (kt % kGemmStages) * S::STAGE;
+        const double* Bs = As + S::A_STAGE;
+#pragma unroll
+        for (int ks = 0; ks < S::BK / 4; ++ks) {
+            double a[FM], b[FN];
+#pragma unroll
+            for (int fm = 0; fm < FM; ++fm)
+                a[fm] = TA ? As[(ks * 4 + t4) * S::LDA_S + wrow + fm * 8 + g]
+                           : As[(wrow + fm * 8 + g) * S::LDA_S + ks * 4 + t4];
+#pragma unroll
+            for (int fn = 0; fn < FN; ++fn) b[fn] = Bs[(ks * 4 + t4) * S::LDB_S + fn * 8 + g];
+#pragma unroll
+            for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+                for (int fn = 0; fn < FN; ++fn) dmma884(acc[fm][fn][0], acc[fm][fn][1], a[fm], b[fn]);
+        }
+    }
+    cp_async_wait<0>();
+
+    double* Cp = p.C + (int64_t)blockIdx.z * p.c_split_stride + ncol0;
+#pragma unroll
+    for (int fm = 0; fm < FM; ++fm) {
+        const int r = wrow + fm * 8 + g;
+        if (r < rows) {
+            double* crow = Cp + (row0 + r) * p.ldc + 2 * t4;
+#pragma unroll
+            for (int fn = 0; fn < FN; ++fn)
+                *reinterpret_cast<double2*>(crow + fn * 8) =
+                    make_double2(p.alpha * acc[fm][fn][0], p.alpha * acc[fm][fn][1]);
+        }
+    }
+}
+
+// out[i] = sum_{s<S} ws[s*stride + i], fixed summation order (deterministic).
+__global__ void reduce_splits_kernel(const double* __restrict__ ws, int64_t count2, int S, int64_t stride,
+                                     double* __restrict__ out) {
+    const int64_t n2 = count2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+        double2 acc = reinterpret_cast<const double2*>(ws)[i];
+        for (int s = 1; s < S; ++s) {
+            const double2 v = reinterpret_cast<const double2*>(ws + s * stride)[i];
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+        reinterpret_cast<double2*>(out)[i] = acc;
+    }
+}
+
+}  // namespace sorsvd_dev

@@ -1,0 +1,171 @@
+// K7/K8: fused inexact-ALM RPCA update.
+//
+// One sweep over the m x n data per ALM iteration. For every entry the
+// low-rank value l_ij = sum_r U_ir * S_{1/mu}(z_r) * V_jr is produced on the
+// FP64 tensor core (DMMA m8n8k4 fragments of the rank-ell outer product, the
+// factors read straight from L2) and consumed in registers, so L is never
+// materialised:
+//     s'  = S_{lambda/mu}(d - l + y/mu)
+//     y'  = y + mu (d - l - s')
+//     w'  = d - s' + y'/mu'   (next iteration's SOR-SVD input)
+//     res += (d - l - s')^2   (stopping test)
+// Traffic: read D, Y; write S, Y, W (40 B/entry). The residual is reduced
+// deterministically (per-block partials, fixed-order final sum).
+#pragma once
+#include "common.cuh"
+
+namespace sorsvd_dev {
+
+constexpr int kRpcaThreads = 256;  // 8 warps -> 64 x 64 tile (warps 4 x 2, 16 x 32 each)
+
+struct RpcaArgs {
+    const double* D;
+    int64_t ldd;
+    double* S;       // m x ldx
+    double* Y;
+    double* W;       // next SOR-SVD input (may be null in the final L pass)
+    double* L;       // final pass only: dense L output (ldl)
+    int64_t ldx;
+    int64_t ldl;
+    const double* U; // m x ldu (left factors from SOR-SVD)
+    int64_t ldu;
+    const double* V; // n x ldv
+    int64_t ldv;
+    const double* sig;  // ell singular values (unshrunk)
+    int64_t m, n;
+    int k;
+    double mu, mu_next, eps;  // eps = lambda / mu
+    double* partial;          // per-block residual^2 partials
+    int mode;                 // 0 = ALM update, 1 = write L only
+};
+
+__global__ void __launch_bounds__(kRpcaThreads) rpca_update_kernel(RpcaArgs a) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+    const int64_t i0 = (int64_t)blockIdx.y * 64 + (warp >> 1) * 16;
+    const int64_t j0 = (int64_t)blockIdx.x * 64 + (warp & 1) * 32;
+    const double inv = 1.0 / a.mu;
+    double acc[2][4][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int kk0 = 0; kk0 < a.k; kk0 += 4) {
+        const int kk = kk0 + t4;
+        const double z = kk < a.k ? fmax(a.sig[kk] - inv, 0.0) : 0.0;
+        double af[2], bf[4];
+#pragma unroll
+        for (int fm = 0; fm < 2; ++fm) {
+            const int64_t i = i0 + fm * 8 + g;
+            af[fm] = (kk < a.k && i < a.m) ? a.U[i * a.ldu + kk] * z : 0.0;
+        }
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) {
+            const int64_t j = j0 + fn * 8 + g;
+            bf[fn] = (kk < a.k && j < a.n) ? a.V[j * a.ldv + kk] : 0.0;
+        }
+#pragma unroll
+        for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+            for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
+    }
+    double res = 0.0;
+#pragma unroll
+    for (int fm = 0; fm < 2; ++fm) {
+        const int64_t i = i0 + fm * 8 + g;
+        if (i >= a.m) continue;
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t j = j0 + fn * 8 + 2 * t4 + h;
+                if (j >= a.n) continue;
+                const double l = acc[fm][fn][h];
+                if (a.mode == 1) {
+                    a.L[i * a.ldl + j] = l;
+                    continue;
+                }
+                const double d = a.D[i * a.ldd + j];
+                const double y = a.Y[i * a.ldx + j];
+                const double t = d - l + y / a.mu;
+                const double sh = fabs(t) - a.eps;
+                const double s = sh > 0.0 ? (t > 0.0 ? sh : -sh) : 0.0;
+                const double r = d - l - s;
+                const double yn = y + a.mu * r;
+                a.S[i * a.ldx + j] = s;
+                a.Y[i * a.ldx + j] = yn;
+                if (a.W) a.W[i * a.ldx + j] = d - s + yn / a.mu_next;
+                res = fma(r, r, res);
+            }
+        }
+    }
+    if (a.mode == 1) return;
+    __shared__ double red[kRpcaThreads / 32];
+    res = warp_sum(res);
+    if (lane == 0) red[warp] = res;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kRpcaThreads / 32; ++w) t += red[w];
+        a.partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// Deterministic single-block reduction of partials: out[0] = sum, (sqrt into out[1]).
+__global__ void sum_partials_kernel(const double* __restrict__ p, int64_t n, double* out) {
+    __shared__ double red[32];
+    double t = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) t += p[i];
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        out[0] = s;
+        out[1] = sqrt(s);
+    }
+}
+
+// Per-block partial sums of squares of a row-major m x n matrix (||D||_F).
+__global__ void sumsq_partials_kernel(const double* __restrict__ x, int64_t m, int64_t n, int64_t ld,
+                                      double* partial) {
+    double t = 0.0;
+    const int64_t total = m * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        const double v = x[i * ld + j];
+        t = fma(v, v, t);
+    }
+    __shared__ double red[32];
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        partial[blockIdx.x] = s;
+    }
+}
+
+// Per-block nonzero counts (||S||_0).
+__global__ void nnz_partials_kernel(const double* __restrict__ x, int64_t m, int64_t n, int64_t ld,
+                                    unsigned long long* partial) {
+    unsigned long long c = 0;
+    const int64_t total = m * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        c += x[i * ld + j] != 0.0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    __shared__ unsigned long long red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        partial[blockIdx.x] = s;
+    }
+}
+
+}  // namespace sorsvd_dev

@@ -1,0 +1,1380 @@
+// Host runtime + C ABI for the B200 SOR-SVD hot path (include/sorsvd_b200.h).
+//
+// The context owns one CUDA stream (plus a side stream for the concurrent
+// TSQRs), grow-only device workspaces, per-shape TSQR plans and a cache of
+// captured CUDA graphs, so a repeated sor_svd_power call (benchmarks, every
+// RPCA iteration) is a single cudaGraphLaunch. With world > 1 (one process
+// per GPU) A is row-sharded; the Aᵀ·T1 partials and the projected core are
+// summed with NCCL all-reduce and the TSQR R factors cross GPUs as an
+// all-gather of k x k blocks. An in-process "emulated"
+// mode runs G row shards on one GPU with the same schedule, replacing NCCL by
+// on-device sums, for tests on a single B200.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/sorsvd_b200.h"
+#include "common.cuh"
+#include "gemm_f64.cuh"
+#include "host_api.hpp"
+#include "jacobi_f64.cuh"
+#include "rpca_f64.cuh"
+#include "tsqr_f64.cuh"
+
+using namespace sorsvd_dev;
+
+namespace {
+
+struct Error {
+    int status;
+    std::string msg;
+};
+
+thread_local std::string g_global_err;
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            throw Error{e_ == cudaErrorMemoryAllocation ? SORSVD_ERR_OOM : SORSVD_ERR_CUDA,        \
+                        std::string("cuda: ") + cudaGetErrorString(e_) + " at " #call};           \
+    } while (0)
+
+
+// NCCL is resolved lazily with dlopen so the library never pins an NCCL
+// version into a process: inside torch the already-loaded libnccl.so.2 is
+// reused (RTLD_NOLOAD first); elsewhere the system one is opened on first
+// multi-GPU use. nccl.h is used for types only.
+struct NcclApi {
+    bool tried = false;
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.tried) {
+        api.tried = true;
+        api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!api.h) api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!api.h) api.h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (api.h) {
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
+            api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
+            api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+        }
+    }
+    if (!api.h || !api.AllReduce || !api.CommInitRank)
+        throw Error{SORSVD_ERR_NCCL, "nccl: libnccl.so.2 not loadable"};
+    return api;
+}
+
+#define NCK(call)                                                                                  \
+    do {                                                                                           \
+        ncclResult_t r_ = (call);                                                                  \
+        if (r_ != ncclSuccess)                                                                     \
+            throw Error{SORSVD_ERR_NCCL, std::string("nccl: ") + nccl().GetErrorString(r_) + " at " #call}; \
+    } while (0)
+
+inline int pad8(int k) { return (k + 7) & ~7; }
+inline int npad(int ell) { return ell <= 128 ? pad8(ell) : ((ell + 127) / 128) * 128; }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct QrPlan {
+    int64_t rows = 0;
+    int k = 0, Np = 0;
+    bool smem = true;
+    int P = 1;
+    std::vector<int64_t> row0;
+    std::vector<int> rcnt;
+    std::vector<int> nodes;  // nodes[0] = P leaves, ..., nodes[L] = 1
+    int max_leaf_rows = 0;
+    // device tables
+    int64_t* d_row0 = nullptr;
+    int* d_rows = nullptr;
+    // segmented GEMM tile tables: [0] leaves, [l] level l (l >= 1)
+    std::vector<int*> t_row0, t_rows, t_seg;
+    std::vector<int> t_count;
+    // buffers
+    std::vector<double*> R;      // per level: nodes[l] * k * k
+    std::vector<double*> QN;     // per level l >= 1: nodes[l] * 2k * Np
+    std::vector<double*> C;      // per level l in [0, L-1): children C's of level l+1 nodes
+    double* scratch = nullptr;   // global fallback
+    std::vector<void*> owned;
+};
+
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+};
+
+}  // namespace
+
+struct sorsvd_ctx {
+    int device = 0;
+    int rank = 0, world = 1;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr, stream = nullptr, side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_a = nullptr, ev_b = nullptr;
+    cudaEvent_t ev_st[8] = {};
+    cudaEvent_t ev_h[4] = {};
+    std::string err;
+    std::map<std::string, Buf> bufs;
+    std::map<std::string, std::unique_ptr<QrPlan>> plans;
+    std::map<std::string, GraphEntry> graphs;
+    ncclComm_t comm = nullptr;
+    int launches = 0;
+    bool capturing = false;
+    std::vector<double> host_omega;
+};
+
+namespace {
+
+void invalidate_graphs(sorsvd_ctx* c) {
+    for (auto& kv : c->graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    c->graphs.clear();
+}
+
+double* dbuf(sorsvd_ctx* c, const std::string& name, size_t count, bool zero = false) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(double);
+    Buf& b = c->bufs[name];
+    if (b.bytes < bytes) {
+        if (c->capturing) throw Error{SORSVD_ERR_INTERNAL, "workspace growth during graph capture: " + name};
+        invalidate_graphs(c);
+        if (b.p) CK(cudaFree(b.p));
+        b.p = nullptr;
+        CK(cudaMalloc(&b.p, bytes));
+        b.bytes = bytes;
+        CK(cudaMemset(b.p, 0, bytes));
+    } else if (zero) {
+        CK(cudaMemsetAsync(b.p, 0, bytes, c->stream));
+    }
+    return static_cast<double*>(b.p);
+}
+
+void check_launch(sorsvd_ctx* c) {
+    CK(cudaGetLastError());
+    c->launches++;
+}
+
+// ---------------------------------------------------------------- GEMM ----
+struct GemmCall {
+    bool ta = false;
+    const double* A = nullptr;
+    int64_t lda = 0;
+    int64_t M = 0, K = 0;
+    const double* B = nullptr;
+    int64_t ldb = 0;
+    int N = 0;  // padded column count (multiple of 8, or of 128 when > 128)
+    double* C = nullptr;
+    int64_t ldc = 0;
+    double alpha = 1.0;
+    // segmented
+    const int* tile_row0 = nullptr;
+    const int* tile_rows = nullptr;
+    const int* tile_seg = nullptr;
+    int ntiles = 0;
+    int64_t b_seg_stride = 0;
+    int force_splits = 0;
+    const char* ws_name = "gemm_ws";
+};
+
+template <int FM, int FN, bool TA, bool V16>
+void launch_gemm_t(const GemmArgs& a, dim3 grid, cudaStream_t s) {
+    using S = GemmShape<FM, FN, TA>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(gemm_f64_kernel<FM, FN, TA, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)S::SMEM));
+        attr_set = true;
+    }
+    gemm_f64_kernel<FM, FN, TA, V16><<<grid, kGemmThreads, S::SMEM, s>>>(a);
+}
+
+template <int FN>
+void dispatch_fn(bool ta, bool v16, const GemmArgs& a, dim3 grid, cudaStream_t s) {
+    constexpr int FM = FN <= 4 ? 4 : 2;
+    if (ta) {
+        if (v16) launch_gemm_t<FM, FN, true, true>(a, grid, s);
+        else launch_gemm_t<FM, FN, true, false>(a, grid, s);
+    } else {
+        if (v16) launch_gemm_t<FM, FN, false, true>(a, grid, s);
+        else launch_gemm_t<FM, FN, false, false>(a, grid, s);
+    }
+}
+
+int gemm_bm_for(int N) {
+    const int FN = N <= 128 ? N / 8 : 16;
+    return 64 * (FN <= 4 ? 4 : 2);
+}
+
+void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
+    if (g.N <= 0 || g.N % 8 != 0 || (g.N > 128 && g.N % 128 != 0))
+        throw Error{SORSVD_ERR_INTERNAL, "gemm: bad padded N"};
+    const int FN = g.N <= 128 ? g.N / 8 : 16;
+    const int gy = g.N <= 128 ? 1 : g.N / 128;
+    const int BM = gemm_bm_for(g.N);
+    const int64_t gx = g.tile_row0 ? g.ntiles : cdiv(g.M, BM);
+    if (gx == 0) return;
+    int S = 1;
+    if (g.force_splits > 0) {
+        S = g.force_splits;
+    } else if (!g.tile_row0) {
+        const int64_t base = gx * gy;
+        const int64_t maxS = std::max<int64_t>(1, std::min<int64_t>(512, g.K / 128));
+        double best = 1e300;
+        for (int64_t cand = 1; cand <= maxS; ++cand) {
+            const double waves = (double)cdiv(base * cand, c->num_sms);
+            const double cost = waves * ((double)g.K / cand + 96.0) + (cand > 1 ? 0.02 * cand * g.M * g.N / (double)c->num_sms : 0.0);
+            if (cost < best * 0.999) {
+                best = cost;
+                S = (int)cand;
+            }
+        }
+    }
+    GemmArgs a{};
+    a.A = g.A;
+    a.lda = g.lda;
+    a.B = g.B;
+    a.ldb = g.ldb;
+    a.b_seg_stride = g.b_seg_stride;
+    a.M = g.M;
+    a.K = g.K;
+    a.alpha = g.alpha;
+    a.tile_row0 = g.tile_row0;
+    a.tile_rows = g.tile_rows;
+    a.tile_seg = g.tile_seg;
+    const int64_t kchunk = cdiv(cdiv(g.K, S), kGemmBK) * kGemmBK;
+    a.k_chunk = std::max<int64_t>(kchunk, kGemmBK);
+    double* ws = nullptr;
+    if (S > 1) {
+        ws = dbuf(c, g.ws_name, (size_t)S * g.M * g.ldc);
+        a.C = ws;
+        a.ldc = g.ldc;
+        a.c_split_stride = g.M * g.ldc;
+    } else {
+        a.C = g.C;
+        a.ldc = g.ldc;
+        a.c_split_stride = 0;
+    }
+    const bool aligned = ((uintptr_t)g.A % 16) == 0 && (g.lda % 2) == 0;
+    const bool v16 = aligned;
+    dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)S);
+    switch (FN) {
+#define FN_CASE(n) \
+    case n: dispatch_fn<n>(g.ta, v16, a, grid, s); break;
+        FN_CASE(1) FN_CASE(2) FN_CASE(3) FN_CASE(4) FN_CASE(5) FN_CASE(6) FN_CASE(7) FN_CASE(8)
+        FN_CASE(9) FN_CASE(10) FN_CASE(11) FN_CASE(12) FN_CASE(13) FN_CASE(14) FN_CASE(15) FN_CASE(16)
+#undef FN_CASE
+        default: throw Error{SORSVD_ERR_INTERNAL, "gemm: FN"};
+    }
+    check_launch(c);
+    if (S > 1) {
+        if (g.ldc % 2) throw Error{SORSVD_ERR_INTERNAL, "gemm: odd ldc with splits"};
+        const int64_t count2 = g.M * g.ldc / 2;
+        const int blocks = (int)std::min<int64_t>(cdiv(count2, 256), (int64_t)c->num_sms * 8);
+        reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, g.M * g.ldc, g.C);
+        check_launch(c);
+    }
+}
+
+// ---------------------------------------------------------------- TSQR ----
+constexpr int kQrSmemMaxK = 112;
+
+size_t qr_leaf_smem(int k, int rows, bool smem) {
+    const size_t head = 2 * (size_t)((k + 1) & ~1);
+    return (head + (smem ? (size_t)(rows | 1) * k : 0)) * sizeof(double);
+}
+size_t qr_node_smem(int k, bool smem) {
+    const size_t head = 2 * (size_t)((k + 1) & ~1);
+    return (head + (smem ? (size_t)(2 * k + 1) * k : 0)) * sizeof(double);
+}
+
+void build_seg_tiles(const std::vector<int64_t>& seg_row0, const std::vector<int>& seg_rows, int BM,
+                     std::vector<int>& r0, std::vector<int>& rc, std::vector<int>& sg) {
+    for (size_t s = 0; s < seg_row0.size(); ++s)
+        for (int off = 0; off < seg_rows[s]; off += BM) {
+            r0.push_back((int)(seg_row0[s] + off));
+            rc.push_back(std::min(BM, seg_rows[s] - off));
+            sg.push_back((int)s);
+        }
+}
+
+template <typename T>
+T* upload(QrPlan* p, const std::vector<T>& v) {
+    T* d = nullptr;
+    CK(cudaMalloc(&d, std::max<size_t>(v.size(), 1) * sizeof(T)));
+    if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    p->owned.push_back(d);
+    return d;
+}
+
+double* dalloc(QrPlan* p, size_t count) {
+    double* d = nullptr;
+    CK(cudaMalloc(&d, std::max<size_t>(count, 1) * sizeof(double)));
+    CK(cudaMemset(d, 0, std::max<size_t>(count, 1) * sizeof(double)));
+    p->owned.push_back(d);
+    return d;
+}
+
+// Build (or fetch) the TSQR plan for `rows` x k. leaves_given > 0 builds a
+// plan whose level-0 "leaves" are external k x k R blocks (the cross-GPU tree).
+QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const char* tag) {
+    const std::string key = std::string(tag) + ":" + std::to_string(rows) + "x" + std::to_string(k) + "g" + std::to_string(leaves_given);
+    auto it = c->plans.find(key);
+    if (it != c->plans.end()) return it->second.get();
+    if (c->capturing) throw Error{SORSVD_ERR_INTERNAL, "qr plan creation during capture"};
+    invalidate_graphs(c);
+    auto p = std::make_unique<QrPlan>();
+    p->rows = rows;
+    p->k = k;
+    p->Np = npad(k);
+    p->smem = k <= kQrSmemMaxK;
+    if (leaves_given > 0) {
+        p->P = leaves_given;
+    } else {
+        int64_t bmax;
+        if (p->smem) {
+            const int64_t budget = kQrSmemBudget / 8 - 2 * ((k + 1) & ~1);
+            bmax = std::min<int64_t>(budget / k - 1, 4096);
+        } else {
+            bmax = std::max<int64_t>(2 * k, 512);
+        }
+        p->P = (int)std::max<int64_t>(1, cdiv(rows, bmax));
+        const int64_t base = rows / p->P, extra = rows % p->P;
+        int64_t r = 0;
+        for (int i = 0; i < p->P; ++i) {
+            const int cnt = (int)(base + (i < extra ? 1 : 0));
+            p->row0.push_back(r);
+            p->rcnt.push_back(cnt);
+            p->max_leaf_rows = std::max(p->max_leaf_rows, cnt);
+            r += cnt;
+        }
+        if (p->P > 1 && base < k) throw Error{SORSVD_ERR_INTERNAL, "tsqr: leaf shorter than k"};
+        p->d_row0 = upload(p.get(), p->row0);
+        p->d_rows = upload(p.get(), p->rcnt);
+    }
+    p->nodes.push_back(p->P);
+    while (p->nodes.back() > 1) p->nodes.push_back((p->nodes.back() + 1) / 2);
+    const int L = (int)p->nodes.size() - 1;
+    const int Np = p->Np;
+    const int BM = gemm_bm_for(Np);
+    p->t_row0.assign(L + 1, nullptr);
+    p->t_rows.assign(L + 1, nullptr);
+    p->t_seg.assign(L + 1, nullptr);
+    p->t_count.assign(L + 1, 0);
+    p->R.assign(L + 1, nullptr);
+    p->QN.assign(L + 1, nullptr);
+    p->C.assign(L + 1, nullptr);
+    for (int l = 0; l <= L; ++l) p->R[l] = dalloc(p.get(), (size_t)p->nodes[l] * k * k);
+    for (int l = 1; l <= L; ++l) p->QN[l] = dalloc(p.get(), (size_t)p->nodes[l] * 2 * k * Np);
+    for (int l = 0; l < L; ++l) p->C[l] = dalloc(p.get(), (size_t)p->nodes[l + 1] * 2 * k * Np);
+    // leaf product tiles
+    if (leaves_given == 0 && L >= 1) {
+        std::vector<int> r0, rc, sg;
+        build_seg_tiles(p->row0, p->rcnt, BM, r0, rc, sg);
+        p->t_row0[0] = upload(p.get(), r0);
+        p->t_rows[0] = upload(p.get(), rc);
+        p->t_seg[0] = upload(p.get(), sg);
+        p->t_count[0] = (int)r0.size();
+    }
+    // node product tiles for levels 1..L-1 (level L's product is the identity)
+    for (int l = 1; l < L; ++l) {
+        std::vector<int64_t> sr0;
+        std::vector<int> src;
+        for (int i = 0; i < p->nodes[l]; ++i) {
+            sr0.push_back((int64_t)i * 2 * k);
+            src.push_back(2 * k);
+        }
+        std::vector<int> r0, rc, sg;
+        build_seg_tiles(sr0, src, BM, r0, rc, sg);
+        p->t_row0[l] = upload(p.get(), r0);
+        p->t_rows[l] = upload(p.get(), rc);
+        p->t_seg[l] = upload(p.get(), sg);
+        p->t_count[l] = (int)r0.size();
+    }
+    if (!p->smem) {
+        size_t sc = (size_t)(rows + p->P) * k;
+        size_t nodes_total = 0;
+        for (int l = 1; l <= L; ++l) nodes_total += p->nodes[l];
+        sc = std::max(sc, nodes_total * ((size_t)(2 * k + 1) * k + 1));
+        p->scratch = dalloc(p.get(), sc);
+    }
+    QrPlan* raw = p.get();
+    c->plans[key] = std::move(p);
+    return raw;
+}
+
+void set_smem_attr(const void* fn, size_t bytes) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+// Factor: leaves (from T) + tree levels. apply_root_sign: the plan's root is
+// the global root (diag(R) >= 0). Leaf explicit Qs are written in place in T
+// (or straight into Q when the leaf is the root).
+void qr_factor(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int64_t ldq, bool root_sign,
+               cudaStream_t s, const double* Rleaves = nullptr) {
+    const int k = p->k;
+    const int L = (int)p->nodes.size() - 1;
+    if (!Rleaves) {
+        LeafArgs la{};
+        la.T = T;
+        la.ldt = ldt;
+        const bool direct = (L == 0 && root_sign);
+        la.Qout = direct ? Q : T;
+        la.ldq = direct ? ldq : ldt;
+        la.row0 = p->d_row0;
+        la.rows = p->d_rows;
+        la.k = k;
+        la.R = p->R[0];
+        la.ldr = k;
+        la.scratch = p->scratch;
+        la.is_root = (L == 0 && root_sign) ? 1 : 0;
+        const size_t sm = qr_leaf_smem(k, p->max_leaf_rows, p->smem);
+        if (p->smem) {
+            set_smem_attr((const void*)tsqr_leaf_kernel<true>, sm);
+            tsqr_leaf_kernel<true><<<p->P, kQrThreads, sm, s>>>(la);
+        } else {
+            set_smem_attr((const void*)tsqr_leaf_kernel<false>, sm);
+            tsqr_leaf_kernel<false><<<p->P, kQrThreads, sm, s>>>(la);
+        }
+        check_launch(c);
+    }
+    for (int l = 1; l <= L; ++l) {
+        NodeArgs na{};
+        na.Rin = (l == 1 && Rleaves) ? Rleaves : p->R[l - 1];
+        na.nin = p->nodes[l - 1];
+        na.Rout = p->R[l];
+        na.Qnode = p->QN[l];
+        na.ldq = p->Np;
+        na.k = k;
+        na.ldr = k;
+        na.scratch = p->scratch;
+        na.is_root = (l == L && root_sign) ? 1 : 0;
+        const size_t sm = qr_node_smem(k, p->smem);
+        if (p->smem) {
+            set_smem_attr((const void*)tsqr_node_kernel<true>, sm);
+            tsqr_node_kernel<true><<<p->nodes[l], kQrThreads, sm, s>>>(na);
+        } else {
+            set_smem_attr((const void*)tsqr_node_kernel<false>, sm);
+            tsqr_node_kernel<false><<<p->nodes[l], kQrThreads, sm, s>>>(na);
+        }
+        check_launch(c);
+    }
+}
+
+// Top-down: push C factors down the tree, finish with Q = Q_leaf * C_leaf.
+// Cin (k x Np, optional) multiplies the plan's root from the right (the
+// cross-GPU path factor); without it the root Q already carries the signs.
+// Returns the level-0 C array (one k x Np block per leaf) when leaf_out is
+// null (used by the cross-GPU tree to hand each rank its factor).
+void qr_formq(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int64_t ldq, const double* Cin,
+              cudaStream_t s, bool leaves_are_blocks = false) {
+    const int k = p->k, Np = p->Np;
+    const int L = (int)p->nodes.size() - 1;
+    if (L == 0) {
+        if (Cin) {  // local root is a single leaf: Q = Qleaf * Cin
+            GemmCall g;
+            g.A = T;
+            g.lda = ldt;
+            g.M = p->rows;
+            g.K = k;
+            g.B = Cin;
+            g.ldb = Np;
+            g.N = Np;
+            g.C = Q;
+            g.ldc = ldq;
+            g.force_splits = 1;
+            run_gemm(c, g, s);
+        }
+        return;
+    }
+    // level L-1 children factors: root Q (2k x Np), optionally times Cin
+    const double* Ccur;
+    if (Cin) {
+        GemmCall g;
+        g.A = p->QN[L];
+        g.lda = Np;
+        g.M = 2 * k;
+        g.K = k;
+        g.B = Cin;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = p->C[L - 1];
+        g.ldc = Np;
+        g.force_splits = 1;
+        run_gemm(c, g, s);
+        Ccur = p->C[L - 1];
+    } else {
+        Ccur = p->QN[L];
+    }
+    for (int l = L - 1; l >= 1; --l) {
+        GemmCall g;
+        g.A = p->QN[l];
+        g.lda = Np;
+        g.M = (int64_t)p->nodes[l] * 2 * k;
+        g.K = k;
+        g.B = Ccur;
+        g.ldb = Np;
+        g.b_seg_stride = (int64_t)k * Np;
+        g.N = Np;
+        g.C = p->C[l - 1];
+        g.ldc = Np;
+        g.tile_row0 = p->t_row0[l];
+        g.tile_rows = p->t_rows[l];
+        g.tile_seg = p->t_seg[l];
+        g.ntiles = p->t_count[l];
+        g.force_splits = 1;
+        run_gemm(c, g, s);
+        Ccur = p->C[l - 1];
+    }
+    if (leaves_are_blocks) {
+        // caller reads the per-leaf factors from p->C[0] (or QN[L] when L == 1 and no Cin)
+        return;
+    }
+    GemmCall g;
+    g.A = T;
+    g.lda = ldt;
+    g.M = p->rows;
+    g.K = k;
+    g.B = Ccur;
+    g.ldb = Np;
+    g.b_seg_stride = (int64_t)k * Np;
+    g.N = Np;
+    g.C = Q;
+    g.ldc = ldq;
+    g.tile_row0 = p->t_row0[0];
+    g.tile_rows = p->t_rows[0];
+    g.tile_seg = p->t_seg[0];
+    g.ntiles = p->t_count[0];
+    g.force_splits = 1;
+    run_gemm(c, g, s);
+}
+
+const double* qr_leaf_factors(QrPlan* p, bool had_cin) {
+    const int L = (int)p->nodes.size() - 1;
+    if (L == 1 && !had_cin) return p->QN[1];
+    return p->C[0];
+}
+
+// ---------------------------------------------------------------- Jacobi --
+void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int ldu, double* S, double* V, int ldv,
+                int* sweeps, cudaStream_t s) {
+    JacobiArgs a{};
+    a.M = M;
+    a.ldm = ldm;
+    a.k = k;
+    a.U = U;
+    a.ldu = ldu;
+    a.S = S;
+    a.V = V;
+    a.ldv = ldv;
+    a.max_sweeps = 60;
+    a.sweeps_out = sweeps;
+    const int ld = k | 1;
+    const bool smem = k <= kQrSmemMaxK;
+    const size_t tail = (size_t)k * sizeof(double) + 2 * (size_t)k * sizeof(int) + 64;
+    if (smem) {
+        const size_t sm = 2 * (size_t)ld * k * sizeof(double) + tail;
+        if (k <= 32) {
+            set_smem_attr((const void*)jacobi_svd_kernel<4, true>, sm);
+            jacobi_svd_kernel<4, true><<<1, kJacobiThreads, sm, s>>>(a);
+        } else {
+            set_smem_attr((const void*)jacobi_svd_kernel<8, true>, sm);
+            jacobi_svd_kernel<8, true><<<1, kJacobiThreads, sm, s>>>(a);
+        }
+    } else {
+        a.scratch = dbuf(c, "jacobi_scratch", 2 * (size_t)ld * k);
+        const size_t sm = tail;
+        set_smem_attr((const void*)jacobi_svd_kernel<16, false>, sm);
+        jacobi_svd_kernel<16, false><<<1, kJacobiThreads, sm, s>>>(a);
+    }
+    check_launch(c);
+}
+
+// ------------------------------------------------------------- pipeline ----
+struct SorBuffers {
+    double *T1, *T2, *Q1, *Q2, *Y, *Mk, *Uk, *Vk, *Sk, *Uo, *Vo;
+    int* sweeps;
+};
+
+struct SorProblem {
+    const double* A;
+    int64_t m, n, lda;
+    int k, ell, q;
+    int Np;
+    int64_t m_global;
+};
+
+SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan** p2, QrPlan** pg) {
+    SorBuffers b{};
+    const int Np = P.Np;
+    b.T1 = dbuf(c, "T1", (size_t)P.m * Np);
+    b.T2 = dbuf(c, "T2", (size_t)P.n * Np);
+    b.Q1 = dbuf(c, "Q1", (size_t)P.m * Np);
+    b.Q2 = dbuf(c, "Q2", (size_t)P.n * Np);
+    b.Y = dbuf(c, "Y", (size_t)P.m * Np);
+    b.Mk = dbuf(c, "Mk", (size_t)Np * Np);
+    b.Uk = dbuf(c, "Uk", (size_t)Np * Np);
+    b.Vk = dbuf(c, "Vk", (size_t)Np * Np);
+    b.Sk = dbuf(c, "Sk", (size_t)Np);
+    b.Uo = dbuf(c, "Uo", (size_t)P.m * Np);
+    b.Vo = dbuf(c, "Vo", (size_t)P.n * Np);
+    b.sweeps = reinterpret_cast<int*>(dbuf(c, "sweeps", 1));
+    *p1 = get_qr_plan(c, P.m, P.ell, 0, "T1");
+    *p2 = get_qr_plan(c, P.n, P.ell, 0, "T2");
+    *pg = c->world > 1 ? get_qr_plan(c, (int64_t)c->world * P.ell, P.ell, c->world, "G") : nullptr;
+    if (c->world > 1) {
+        dbuf(c, "Rg", (size_t)c->world * P.ell * P.ell);
+        dbuf(c, "CinLocal", (size_t)P.ell * Np);
+    }
+    return b;
+}
+
+void allreduce_sum(sorsvd_ctx* c, double* buf, size_t count, cudaStream_t s) {
+    if (c->world <= 1) return;
+    NCK(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, s));
+}
+
+void record_stage(sorsvd_ctx* c, bool timing, int idx) {
+    if (timing) CK(cudaEventRecord(c->ev_st[idx], c->stream));
+}
+
+// Enqueue one sor_svd_power on c->stream (T2 must already hold Omega, padded).
+void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, QrPlan* pg,
+                 bool timing) {
+    cudaStream_t s = c->stream;
+    const int Np = P.Np, ell = P.ell;
+    record_stage(c, timing, 0);
+    for (int i = 0; i <= P.q; ++i) {
+        GemmCall g1;  // T1 = A * T2     (sketch.hpp:95)
+        g1.A = P.A;
+        g1.lda = P.lda;
+        g1.M = P.m;
+        g1.K = P.n;
+        g1.B = b.T2;
+        g1.ldb = Np;
+        g1.N = Np;
+        g1.C = b.T1;
+        g1.ldc = Np;
+        run_gemm(c, g1, s);
+        GemmCall g2;  // T2 = A^T * T1   (sketch.hpp:96)
+        g2.ta = true;
+        g2.A = P.A;
+        g2.lda = P.lda;
+        g2.M = P.n;
+        g2.K = P.m;
+        g2.B = b.T1;
+        g2.ldb = Np;
+        g2.N = Np;
+        g2.C = b.T2;
+        g2.ldc = Np;
+        run_gemm(c, g2, s);
+        allreduce_sum(c, b.T2, (size_t)P.n * Np, s);
+    }
+    record_stage(c, timing, 1);
+    // Q1 = thin_qr(T1).q, Q2 = thin_qr(T2).q concurrently (sketch.hpp:98-99)
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    if (c->world > 1) {
+        qr_factor(c, p1, b.T1, Np, b.Q1, Np, false, s);
+        const int L1 = (int)p1->nodes.size() - 1;
+        double* Rg = dbuf(c, "Rg", (size_t)c->world * ell * ell);
+        NCK(nccl().AllGather(p1->R[L1], Rg, (size_t)ell * ell, ncclDouble, c->comm, s));
+        qr_factor(c, pg, nullptr, 0, nullptr, 0, true, s, Rg);
+        qr_formq(c, pg, nullptr, 0, nullptr, 0, nullptr, s, true);
+        const double* Cg = qr_leaf_factors(pg, false) + (size_t)c->rank * ell * Np;
+        qr_formq(c, p1, b.T1, Np, b.Q1, Np, Cg, s);
+    } else {
+        qr_factor(c, p1, b.T1, Np, b.Q1, Np, true, s);
+        qr_formq(c, p1, b.T1, Np, b.Q1, Np, nullptr, s);
+    }
+    qr_factor(c, p2, b.T2, Np, b.Q2, Np, true, c->side);
+    qr_formq(c, p2, b.T2, Np, b.Q2, Np, nullptr, c->side);
+    CK(cudaEventRecord(c->ev_join, c->side));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    record_stage(c, timing, 2);
+    // M = Q1^T (A Q2)   (sketch.hpp:100-102)
+    {
+        GemmCall g;
+        g.A = P.A;
+        g.lda = P.lda;
+        g.M = P.m;
+        g.K = P.n;
+        g.B = b.Q2;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = b.Y;
+        g.ldc = Np;
+        run_gemm(c, g, s);
+        GemmCall h;
+        h.ta = true;
+        h.A = b.Q1;
+        h.lda = Np;
+        h.M = ell;
+        h.K = P.m;
+        h.B = b.Y;
+        h.ldb = Np;
+        h.N = Np;
+        h.C = b.Mk;
+        h.ldc = Np;
+        run_gemm(c, h, s);
+        allreduce_sum(c, b.Mk, (size_t)ell * Np, s);
+    }
+    record_stage(c, timing, 3);
+    // truncated_svd(M, k)   (sketch.hpp:103)
+    run_jacobi(c, ell, b.Mk, Np, b.Uk, Np, b.Sk, b.Vk, Np, b.sweeps, s);
+    record_stage(c, timing, 4);
+    // U = Q1 Ut_k, V = Q2 Vt_k   (sketch.hpp:105,107)
+    {
+        GemmCall g;
+        g.A = b.Q1;
+        g.lda = Np;
+        g.M = P.m;
+        g.K = ell;
+        g.B = b.Uk;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = b.Uo;
+        g.ldc = Np;
+        run_gemm(c, g, s);
+        GemmCall h;
+        h.A = b.Q2;
+        h.lda = Np;
+        h.M = P.n;
+        h.K = ell;
+        h.B = b.Vk;
+        h.ldb = Np;
+        h.N = Np;
+        h.C = b.Vo;
+        h.ldc = Np;
+        run_gemm(c, h, s);
+    }
+    record_stage(c, timing, 5);
+}
+
+std::string sor_key(const SorProblem& P, const void* dOmega, const void* dU, const void* dS, const void* dV) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "sor:%p:%lld:%lld:%lld:%d:%d:%d:%p:%p:%p:%p", (const void*)P.A, (long long)P.m,
+             (long long)P.n, (long long)P.lda, P.k, P.ell, P.q, dOmega, dU, dS, dV);
+    return buf;
+}
+
+void validate(const sorsvd_desc* d) {
+    if (!d) throw Error{SORSVD_ERR_PARAMETER, "parameter: null descriptor"};
+    const int64_t mg = d->m_global > 0 ? d->m_global : d->m;
+    if (d->m < 1 || d->n < 1) throw Error{SORSVD_ERR_SHAPE, "shape: matrix dimensions must be positive"};
+    if (d->lda < d->n) throw Error{SORSVD_ERR_SHAPE, "shape: lda < n"};
+    if (const char* e = sorsvd_host::validate_sketch(mg, d->n, d->k, d->ell, d->q))
+        throw Error{SORSVD_ERR_PARAMETER, e};
+    if ((d->flags & SORSVD_FLAG_BASIC) && d->q != 0)
+        throw Error{SORSVD_ERR_PARAMETER, "parameter: sor_svd requires q == 0; use sor_svd_power"};
+    if (d->single_pass) throw Error{SORSVD_ERR_UNSUPPORTED, "single_pass (m_approx) is not implemented in this build"};
+    if (d->dtype != SORSVD_F64) throw Error{SORSVD_ERR_UNSUPPORTED, "only SORSVD_F64 is implemented in this build"};
+    if (d->ell > 256) throw Error{SORSVD_ERR_UNSUPPORTED, "ell > 256 not supported in FP64"};
+}
+
+// Core device-side call. dOmega: n x ell dense (or null: drawn on the host).
+void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const double* dA, const double* dOmega, double* dU,
+                double* dS, double* dV, sorsvd_stats* st) {
+    validate(d);
+    SorProblem P{};
+    P.A = dA;
+    P.m = d->m;
+    P.n = d->n;
+    P.lda = d->lda;
+    P.k = d->k;
+    P.ell = d->ell;
+    P.q = d->q;
+    P.Np = npad(d->ell);
+    P.m_global = d->m_global > 0 ? d->m_global : d->m;
+    QrPlan *p1, *p2, *pg;
+    SorBuffers b = prepare_sor(c, P, &p1, &p2, &pg);
+    const double* om = dOmega;
+    if (!om || !(d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+        c->host_omega.resize((size_t)P.n * P.ell);
+        sorsvd_host::gaussian_fill(c->host_omega.data(), (uint64_t)P.n * P.ell, d->seed, 0);
+        double* dom = dbuf(c, "omega_up", (size_t)P.n * P.ell);
+        CK(cudaMemcpyAsync(dom, c->host_omega.data(), (size_t)P.n * P.ell * 8, cudaMemcpyHostToDevice, c->stream));
+        om = dom;
+    }
+    const bool timing = (d->flags & SORSVD_FLAG_STAGE_TIMES) != 0;
+    const bool use_graph = !timing && !(d->flags & SORSVD_FLAG_NO_GRAPH) && !getenv("SORSVD_NO_GRAPH");
+    CK(cudaEventRecord(c->ev_a, c->stream));
+    const int launches0 = c->launches;
+    int launches = 0;
+    auto enqueue_all = [&]() {
+        // T2 <- Omega (padded)
+        CK(cudaMemsetAsync(b.T2, 0, (size_t)P.n * P.Np * 8, c->stream));
+        CK(cudaMemcpy2DAsync(b.T2, (size_t)P.Np * 8, om, (size_t)P.ell * 8, (size_t)P.ell * 8, (size_t)P.n,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        enqueue_sor(c, P, b, p1, p2, pg, timing);
+        CK(cudaMemcpy2DAsync(dU, (size_t)P.k * 8, b.Uo, (size_t)P.Np * 8, (size_t)P.k * 8, (size_t)P.m,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpy2DAsync(dV, (size_t)P.k * 8, b.Vo, (size_t)P.Np * 8, (size_t)P.k * 8, (size_t)P.n,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(dS, b.Sk, (size_t)P.k * 8, cudaMemcpyDeviceToDevice, c->stream));
+    };
+    if (use_graph) {
+        const std::string key = sor_key(P, om, dU, dS, dV);
+        auto it = c->graphs.find(key);
+        if (it == c->graphs.end()) {
+            // warm-up run outside capture sets kernel attributes
+            enqueue_all();
+            CK(cudaStreamSynchronize(c->stream));
+            const int l0 = c->launches;
+            cudaGraph_t graph;
+            c->capturing = true;
+            CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue_all();
+            } catch (...) {
+                cudaStreamEndCapture(c->stream, &graph);
+                c->capturing = false;
+                throw;
+            }
+            CK(cudaStreamEndCapture(c->stream, &graph));
+            c->capturing = false;
+            GraphEntry ge;
+            CK(cudaGraphInstantiate(&ge.exec, graph, 0));
+            CK(cudaGraphDestroy(graph));
+            ge.launches = c->launches - l0;
+            c->graphs[key] = ge;
+            it = c->graphs.find(key);
+            CK(cudaEventRecord(c->ev_a, c->stream));
+        }
+        CK(cudaGraphLaunch(it->second.exec, c->stream));
+        launches = it->second.launches;
+    } else {
+        enqueue_all();
+        launches = c->launches - launches0;
+    }
+    CK(cudaEventRecord(c->ev_b, c->stream));
+    if (st) {
+        CK(cudaEventSynchronize(c->ev_b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+        st->ms_total = ms;
+        const int passes = 2 * d->q + 3;
+        st->passes = passes;
+        st->method = d->q == 0 ? SORSVD_SOR : SORSVD_SOR_POWER;
+        st->flops_passes = 2.0 * (double)d->m * d->n * d->ell * passes;
+        st->bytes_passes = (double)d->m * d->n * 8.0 * passes;
+        st->launches = launches;
+        int sw = 0;
+        CK(cudaMemcpy(&sw, b.sweeps, sizeof(int), cudaMemcpyDeviceToHost));
+        st->jacobi_sweeps = sw;
+        if (timing) {
+            float t[5];
+            for (int i = 0; i < 5; ++i) CK(cudaEventElapsedTime(&t[i], c->ev_st[i], c->ev_st[i + 1]));
+            st->ms_passes = t[0];
+            st->ms_qr = t[1];
+            st->ms_project = t[2];
+            st->ms_svd = t[3];
+            st->ms_basis = t[4];
+        }
+    }
+}
+
+// ----------------------------------------------------------------- RPCA ----
+double device_sumsq(sorsvd_ctx* c, const double* x, int64_t m, int64_t n, int64_t ld) {
+    const int blocks = c->num_sms * 4;
+    double* part = dbuf(c, "rp_part2", (size_t)blocks);
+    double* tot = dbuf(c, "rp_tot2", 2);
+    sumsq_partials_kernel<<<blocks, 256, 0, c->stream>>>(x, m, n, ld, part);
+    check_launch(c);
+    sum_partials_kernel<<<1, 1024, 0, c->stream>>>(part, blocks, tot);
+    check_launch(c);
+    double h[2];
+    CK(cudaMemcpyAsync(h, tot, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return h[0];
+}
+
+void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, double* dL, double* dSout,
+                 sorsvd_rpca_result* res) {
+    if (!d) throw Error{SORSVD_ERR_PARAMETER, "parameter: null descriptor"};
+    const int64_t m = d->m, n = d->n, ldd = d->ldd;
+    if (m < 2 || n < 2 || ldd < n) throw Error{SORSVD_ERR_SHAPE, "shape: bad RPCA matrix shape"};
+    if (d->rho <= 1.0 || d->tol <= 0.0 || d->ell < 1 || d->max_iter < 1)
+        throw Error{SORSVD_ERR_PARAMETER, "parameter: rpca config invalid (rho > 1, tol > 0, ell >= 1)"};
+    if (const char* e = sorsvd_host::validate_sketch(m, n, d->ell, d->ell, d->q)) throw Error{SORSVD_ERR_PARAMETER, e};
+    if (d->dtype != SORSVD_F64) throw Error{SORSVD_ERR_UNSUPPORTED, "only SORSVD_F64 is implemented"};
+    const int ell = d->ell;
+    const double lambda = d->lambda > 0 ? d->lambda : 1.0 / std::sqrt((double)std::max(m, n));
+    CK(cudaEventRecord(c->ev_h[2], c->stream));
+    const int launches0 = c->launches;
+    double* S = dSout ? dSout : dbuf(c, "rp_S", (size_t)m * n);
+    double* Y = dbuf(c, "rp_Y", (size_t)m * n);
+    double* W = dbuf(c, "rp_W", (size_t)m * n);
+    double* U = dbuf(c, "rp_U", (size_t)m * ell);
+    double* V = dbuf(c, "rp_V", (size_t)n * ell);
+    double* sig = dbuf(c, "rp_sig", (size_t)ell);
+    const double dnorm = std::sqrt(device_sumsq(c, dD, m, n, ldd));
+    sorsvd_rpca_result r{};
+    if (dnorm == 0.0) {  // X = 0 -> L = S = 0 in one iteration
+        CK(cudaMemsetAsync(S, 0, (size_t)m * n * 8, c->stream));
+        if (dL) CK(cudaMemsetAsync(dL, 0, (size_t)m * n * 8, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        r.iterations = 1;
+        r.converged = 1;
+        if (res) *res = r;
+        return;
+    }
+    double mu = d->mu0;
+    if (!(mu > 0.0)) {  // 1.25 / sigma_1(D): randomized estimate with power iterations
+        sorsvd_desc e{};
+        e.m = m;
+        e.n = n;
+        e.lda = ldd;
+        e.ell = (int)std::min<int64_t>(8, std::min(m, n) - 1);
+        e.k = 1;
+        e.q = 6;
+        e.seed = d->seed ^ 0x5bd1e995ULL;
+        e.dtype = SORSVD_F64;
+        double* u1 = dbuf(c, "rp_est_u", (size_t)m);
+        double* v1 = dbuf(c, "rp_est_v", (size_t)n);
+        double* s1 = dbuf(c, "rp_est_s", 1);
+        sor_device(c, &e, dD, nullptr, u1, s1, v1, nullptr);
+        double h = 0.0;
+        CK(cudaMemcpyAsync(&h, s1, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        mu = 1.25 / h;
+    }
+    r.mu0 = mu;
+    const double mu_bar = (d->mu_bar_factor > 0 ? d->mu_bar_factor : 1e7) * mu;
+    CK(cudaMemsetAsync(S, 0, (size_t)m * n * 8, c->stream));
+    CK(cudaMemsetAsync(Y, 0, (size_t)m * n * 8, c->stream));
+    const dim3 grid((unsigned)cdiv(n, 64), (unsigned)cdiv(m, 64));
+    const int64_t nblk = (int64_t)grid.x * grid.y;
+    double* part = dbuf(c, "rp_part", (size_t)nblk);
+    double* tot = dbuf(c, "rp_tot", 2);
+    std::vector<double> hsig(ell);
+    double mu_last = mu;
+    int it = 0;
+    double rel = 0.0;
+    int rank = 0;
+    bool conv = false;
+    while (it < d->max_iter) {
+        sorsvd_desc sd{};
+        sd.m = m;
+        sd.n = n;
+        sd.lda = it == 0 ? ldd : n;
+        sd.k = ell;
+        sd.ell = ell;
+        sd.q = d->q;
+        sd.seed = d->seed + (uint64_t)it;
+        sd.dtype = SORSVD_F64;
+        sd.flags = d->flags & SORSVD_FLAG_NO_GRAPH;
+        sor_device(c, &sd, it == 0 ? dD : W, nullptr, U, sig, V, nullptr);
+        const double mu_next = std::min(d->rho * mu, mu_bar);
+        RpcaArgs a{};
+        a.D = dD;
+        a.ldd = ldd;
+        a.S = S;
+        a.Y = Y;
+        a.W = W;
+        a.ldx = n;
+        a.U = U;
+        a.ldu = ell;
+        a.V = V;
+        a.ldv = ell;
+        a.sig = sig;
+        a.m = m;
+        a.n = n;
+        a.k = ell;
+        a.mu = mu;
+        a.mu_next = mu_next;
+        a.eps = lambda / mu;
+        a.partial = part;
+        a.mode = 0;
+        rpca_update_kernel<<<grid, kRpcaThreads, 0, c->stream>>>(a);
+        check_launch(c);
+        sum_partials_kernel<<<1, 1024, 0, c->stream>>>(part, nblk, tot);
+        check_launch(c);
+        double h[2];
+        CK(cudaMemcpyAsync(h, tot, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hsig.data(), sig, ell * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        mu_last = mu;
+        rank = 0;
+        const double z0 = std::max(hsig[0] - 1.0 / mu, 0.0);
+        for (int j = 0; j < ell; ++j)
+            if (std::max(hsig[j] - 1.0 / mu, 0.0) > 1e-8 * z0) ++rank;
+        mu = mu_next;
+        ++it;
+        rel = std::sqrt(h[0]) / dnorm;
+        if (!std::isfinite(rel)) throw Error{SORSVD_ERR_NUMERICAL, "numerical: rpca produced a non-finite iterate"};
+        if (rel < d->tol) {
+            conv = true;
+            break;
+        }
+    }
+    if (dL) {
+        RpcaArgs a{};
+        a.L = dL;
+        a.ldl = n;
+        a.U = U;
+        a.ldu = ell;
+        a.V = V;
+        a.ldv = ell;
+        a.sig = sig;
+        a.m = m;
+        a.n = n;
+        a.k = ell;
+        a.mu = mu_last;
+        a.mode = 1;
+        rpca_update_kernel<<<grid, kRpcaThreads, 0, c->stream>>>(a);
+        check_launch(c);
+    }
+    const int blocks = c->num_sms * 4;
+    unsigned long long* np = reinterpret_cast<unsigned long long*>(dbuf(c, "rp_nnz", (size_t)blocks));
+    nnz_partials_kernel<<<blocks, 256, 0, c->stream>>>(S, m, n, n, np);
+    check_launch(c);
+    std::vector<unsigned long long> hn(blocks);
+    CK(cudaMemcpyAsync(hn.data(), np, blocks * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaEventRecord(c->ev_h[3], c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    long long nnz = 0;
+    for (auto v : hn) nnz += (long long)v;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev_h[2], c->ev_h[3]));
+    r.iterations = it;
+    r.rank_l = rank;
+    r.converged = conv ? 1 : 0;
+    r.nnz_s = nnz;
+    r.rel_error = rel;
+    r.ms_total = ms;
+    r.launches = c->launches - launches0;
+    if (res) *res = r;
+}
+
+int fail(sorsvd_ctx* c, const Error& e) {
+    if (c) c->err = e.msg;
+    g_global_err = e.msg;
+    if (c && c->capturing) c->capturing = false;
+    return e.status;
+}
+
+template <typename F>
+int guarded(sorsvd_ctx* c, F&& f) {
+    try {
+        if (c) CK(cudaSetDevice(c->device));
+        f();
+        return SORSVD_OK;
+    } catch (const Error& e) {
+        return fail(c, e);
+    } catch (const std::bad_alloc&) {
+        return fail(c, Error{SORSVD_ERR_OOM, "host allocation failed"});
+    } catch (const std::exception& e) {
+        return fail(c, Error{SORSVD_ERR_INTERNAL, e.what()});
+    }
+}
+
+void ctx_init(sorsvd_ctx* c, int device) {
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    CK(cudaEventCreate(&c->ev_a));
+    CK(cudaEventCreate(&c->ev_b));
+    for (auto& e : c->ev_st) CK(cudaEventCreate(&e));
+    for (auto& e : c->ev_h) CK(cudaEventCreate(&e));
+}
+
+}  // namespace
+
+// ================================================================ C ABI ====
+extern "C" {
+
+const char* sorsvd_version(void) { return "sorsvd-b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+int sorsvd_ctx_create(int device, sorsvd_ctx** out) {
+    if (!out) return SORSVD_ERR_PARAMETER;
+    auto* c = new sorsvd_ctx();
+    int rc = guarded(nullptr, [&] { ctx_init(c, device); });
+    if (rc != SORSVD_OK) {
+        delete c;
+        *out = nullptr;
+        return rc;
+    }
+    *out = c;
+    return SORSVD_OK;
+}
+
+int sorsvd_nccl_unique_id(void* out128) {
+    return guarded(nullptr, [&] {
+        ncclUniqueId id;
+        NCK(nccl().GetUniqueId(&id));
+        static_assert(sizeof(id) == 128, "nccl id size");
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+int sorsvd_ctx_create_dist(int device, int rank, int world, const void* unique_id128, sorsvd_ctx** out) {
+    if (!out || world < 1 || rank < 0 || rank >= world) return SORSVD_ERR_PARAMETER;
+    auto* c = new sorsvd_ctx();
+    int rc = guarded(nullptr, [&] {
+        ctx_init(c, device);
+        c->rank = rank;
+        c->world = world;
+        if (world > 1) {
+            ncclUniqueId id;
+            std::memcpy(&id, unique_id128, sizeof(id));
+            NCK(nccl().CommInitRank(&c->comm, world, id, rank));
+        }
+    });
+    if (rc != SORSVD_OK) {
+        delete c;
+        *out = nullptr;
+        return rc;
+    }
+    *out = c;
+    return SORSVD_OK;
+}
+
+void sorsvd_ctx_destroy(sorsvd_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    invalidate_graphs(c);
+    for (auto& kv : c->plans)
+        for (void* p : kv.second->owned) cudaFree(p);
+    for (auto& kv : c->bufs)
+        if (kv.second.p) cudaFree(kv.second.p);
+    if (c->comm) nccl().CommDestroy(c->comm);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_join);
+    cudaEventDestroy(c->ev_a);
+    cudaEventDestroy(c->ev_b);
+    for (auto& e : c->ev_st) cudaEventDestroy(e);
+    for (auto& e : c->ev_h) cudaEventDestroy(e);
+    cudaStreamDestroy(c->side);
+    cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+const char* sorsvd_last_error(const sorsvd_ctx* c) { return c ? c->err.c_str() : g_global_err.c_str(); }
+
+int sorsvd_set_stream(sorsvd_ctx* c, void* stream) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
+        if (s != c->stream) invalidate_graphs(c);
+        c->stream = s;
+    });
+}
+
+int sorsvd_ctx_rank(const sorsvd_ctx* c, int* rank, int* world) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    if (rank) *rank = c->rank;
+    if (world) *world = c->world;
+    return SORSVD_OK;
+}
+
+int sorsvd_sor_svd_power_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const double* dOmega,
+                                double* dU, double* dSigma, double* dV, sorsvd_stats* st) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (!dA || !dU || !dSigma || !dV) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        sor_device(c, d, static_cast<const double*>(dA), dOmega, dU, dSigma, dV, st);
+    });
+}
+
+int sorsvd_sor_svd_power(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const double* omega, double* U,
+                         double* sigma, double* V, sorsvd_stats* st) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        validate(d);
+        if (!A || !U || !sigma || !V) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        const size_t abytes = (size_t)d->m * d->lda * 8;
+        cudaEvent_t e0 = c->ev_h[0], e1 = c->ev_h[1], e2 = c->ev_h[2], e3 = c->ev_h[3];
+        CK(cudaEventRecord(e0, c->stream));
+        double* dA = dbuf(c, "hostA", (size_t)d->m * d->lda);
+        CK(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, c->stream));
+        const double* dOm = nullptr;
+        if (omega && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+            double* p = dbuf(c, "hostOm", (size_t)d->n * d->ell);
+            CK(cudaMemcpyAsync(p, omega, (size_t)d->n * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
+            dOm = p;
+        }
+        CK(cudaEventRecord(e1, c->stream));
+        double* dU = dbuf(c, "hostU", (size_t)d->m * d->k);
+        double* dS = dbuf(c, "hostS", (size_t)d->k);
+        double* dV = dbuf(c, "hostV", (size_t)d->n * d->k);
+        sorsvd_stats local{};
+        sor_device(c, d, dA, dOm, dU, dS, dV, &local);
+        CK(cudaEventRecord(e2, c->stream));
+        CK(cudaMemcpyAsync(U, dU, (size_t)d->m * d->k * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(V, dV, (size_t)d->n * d->k * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(sigma, dS, (size_t)d->k * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaEventRecord(e3, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        float h2d = 0.f, d2h = 0.f;
+        CK(cudaEventElapsedTime(&h2d, e0, e1));
+        CK(cudaEventElapsedTime(&d2h, e2, e3));
+        local.ms_h2d = h2d;
+        local.ms_d2h = d2h;
+        if (st) *st = local;
+    });
+}
+
+int sorsvd_thin_qr_device(sorsvd_ctx* c, int64_t m, int32_t k, const double* dT, int64_t ldt, double* dQ,
+                          int64_t ldq, double* dR, int64_t ldr) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (m < k || k < 1) throw Error{SORSVD_ERR_SHAPE, "shape: thin_qr requires rows >= cols"};
+        if (k > 256) throw Error{SORSVD_ERR_UNSUPPORTED, "thin_qr: k > 256"};
+        const int Np = npad(k);
+        QrPlan* p = get_qr_plan(c, m, k, 0, "api");
+        double* T = dbuf(c, "qrT", (size_t)m * Np, true);
+        double* Q = dbuf(c, "qrQ", (size_t)m * Np, true);
+        CK(cudaMemcpy2DAsync(T, (size_t)Np * 8, dT, (size_t)ldt * 8, (size_t)k * 8, (size_t)m,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        qr_factor(c, p, T, Np, Q, Np, true, c->stream);
+        qr_formq(c, p, T, Np, Q, Np, nullptr, c->stream);
+        CK(cudaMemcpy2DAsync(dQ, (size_t)ldq * 8, Q, (size_t)Np * 8, (size_t)k * 8, (size_t)m,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        const int L = (int)p->nodes.size() - 1;
+        if (dR)
+            CK(cudaMemcpy2DAsync(dR, (size_t)ldr * 8, p->R[L], (size_t)k * 8, (size_t)k * 8, (size_t)k,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sorsvd_small_svd_device(sorsvd_ctx* c, int32_t k, const double* dM, int64_t ldm, double* dU, int64_t ldu,
+                            double* dS, double* dV, int64_t ldv, int32_t* sweeps) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (k < 1 || k > 512) throw Error{SORSVD_ERR_PARAMETER, "parameter: k out of range"};
+        int* dsw = reinterpret_cast<int*>(dbuf(c, "sweeps_svd", 1));
+        run_jacobi(c, k, dM, (int)ldm, dU, (int)ldu, dS, dV, (int)ldv, dsw, c->stream);
+        int sw = 0;
+        CK(cudaMemcpyAsync(&sw, dsw, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (sweeps) *sweeps = sw;
+    });
+}
+
+int sorsvd_matmul_device(sorsvd_ctx* c, int32_t ta, int64_t M, int64_t K, int32_t N, const double* dA,
+                         int64_t lda, const double* dB, int64_t ldb, double* dC, int64_t ldc) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (M < 1 || K < 1 || N < 1) throw Error{SORSVD_ERR_SHAPE, "shape: matmul dims must be positive"};
+        const int Np = npad(N);
+        double* Bp = dbuf(c, "mmB", (size_t)K * Np, true);
+        double* Cp = dbuf(c, "mmC", (size_t)M * Np);
+        CK(cudaMemcpy2DAsync(Bp, (size_t)Np * 8, dB, (size_t)ldb * 8, (size_t)N * 8, (size_t)K,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        GemmCall g;
+        g.ta = ta != 0;
+        g.A = dA;
+        g.lda = lda;
+        g.M = M;
+        g.K = K;
+        g.B = Bp;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = Cp;
+        g.ldc = Np;
+        run_gemm(c, g, c->stream);
+        CK(cudaMemcpy2DAsync(dC, (size_t)ldc * 8, Cp, (size_t)Np * 8, (size_t)N * 8, (size_t)M,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sorsvd_rpca_alm_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, double* dL, double* dS,
+                           sorsvd_rpca_result* res) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (!dD || !dS) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        rpca_device(c, d, dD, dL, dS, res);
+    });
+}
+
+int sorsvd_rpca_alm(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* D, double* L, double* S,
+                    sorsvd_rpca_result* res) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (!d) throw Error{SORSVD_ERR_PARAMETER, "parameter: null descriptor"};
+        if (!D || !S) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        const size_t cells = (size_t)d->m * d->n;
+        CK(cudaEventRecord(c->ev_h[0], c->stream));
+        double* dD = dbuf(c, "rp_hostD", (size_t)d->m * d->ldd);
+        CK(cudaMemcpyAsync(dD, D, (size_t)d->m * d->ldd * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaEventRecord(c->ev_h[1], c->stream));
+        double* dS = dbuf(c, "rp_hostS", cells);
+        double* dL = L ? dbuf(c, "rp_hostL", cells) : nullptr;
+        sorsvd_rpca_result r{};
+        rpca_device(c, d, dD, dL, dS, &r);
+        float h2d = 0.f;
+        CK(cudaEventElapsedTime(&h2d, c->ev_h[0], c->ev_h[1]));
+        CK(cudaEventRecord(c->ev_h[0], c->stream));
+        CK(cudaMemcpyAsync(S, dS, cells * 8, cudaMemcpyDeviceToHost, c->stream));
+        if (L) CK(cudaMemcpyAsync(L, dL, cells * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaEventRecord(c->ev_h[1], c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        float d2h = 0.f;
+        CK(cudaEventElapsedTime(&d2h, c->ev_h[0], c->ev_h[1]));
+        r.ms_h2d = h2d;
+        r.ms_d2h = d2h;
+        if (res) *res = r;
+    });
+}
+
+uint64_t sorsvd_sub_seed(uint64_t seed, uint64_t stream) { return sorsvd_host::sub_seed(seed, stream); }
+
+int sorsvd_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out, int nthreads) {
+    if (rows < 1 || cols < 1 || !out) {
+        g_global_err = "shape: matrix dimensions must be positive";
+        return SORSVD_ERR_SHAPE;
+    }
+    sorsvd_host::gaussian_fill(out, (uint64_t)rows * cols, seed, nthreads);
+    return SORSVD_OK;
+}
+
+long long sorsvd_flop_estimate(long long m, long long n, long long ell, long long k, long long q, int variant) {
+    const long long v = sorsvd_host::flop_estimate(m, n, ell, k, q, variant);
+    if (v < 0) g_global_err = "parameter: flop_estimate requires positive dimensions and q >= 0";
+    return v;
+}
+
+int sorsvd_validate_sketch(int64_t m, int64_t n, int32_t k, int32_t ell, int32_t q) {
+    if (const char* e = sorsvd_host::validate_sketch(m, n, k, ell, q)) {
+        g_global_err = e;
+        return SORSVD_ERR_PARAMETER;
+    }
+    return SORSVD_OK;
+}
+
+}  // extern "C"

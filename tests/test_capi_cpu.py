@@ -1,0 +1,90 @@
+"""CPU: the C-ABI library loads, exports every symbol include/*.h declares,
+and its host-side helpers (random.hpp / sketch.hpp mirrors) agree with the
+oracle. No device compute here."""
+import ctypes
+import glob
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import sorsvd_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for mt in re.finditer(r"^\s*[A-Za-z_][\w\s\*]*?\b(sorsvd_\w+)\s*\(", src, flags=re.M):
+            names.add(mt.group(1))
+    return names
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1804_00462_b200 import _capi
+    if not os.path.exists(_capi.LIB_PATH):
+        from paper_1804_00462_b200 import build as B
+        B.build()
+    return _capi.lib()
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _declared_functions()
+    assert len(names) >= 19, names
+    for n in names:
+        assert hasattr(lib, n), n
+    from paper_1804_00462_b200 import _capi
+    assert names == {s[0] for s in _capi.SIGNATURES}
+
+
+def test_library_is_sm100a():
+    from paper_1804_00462_b200 import _capi
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _capi.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_gaussian_matrix_matches_reference_stream(lib):
+    import paper_1804_00462_b200 as P
+    for (r, c, s) in [(7, 5, 123), (3, 3, 0), (1, 9, 2**64 - 1), (301, 77, 42)]:
+        for nt in (1, 3, 8):
+            assert np.array_equal(P.gaussian_matrix(r, c, s, nthreads=nt), O.gaussian_matrix(r, c, s))
+    big = P.gaussian_matrix(1000, 333, 5)  # multi-threaded path, odd split points
+    assert np.array_equal(big, O.gaussian_matrix(1000, 333, 5))
+
+
+def test_sub_seed_and_flops(lib):
+    import paper_1804_00462_b200 as P
+    for s in (0, 1, 42, 2**63):
+        for t in range(4):
+            assert P.sub_seed(s, t) == O.sub_seed(s, t)
+    assert P.flop_estimate(1000, 1000, 38, 20, 0, P.FlopVariant.sor_3pass) == 239813744
+    for v in range(4):
+        assert P.flop_estimate(4000, 4000, 100, 100, 1, v) == O.flop_estimate(4000, 4000, 100, 100, 1, v)
+    with pytest.raises(P.ParameterError):
+        P.flop_estimate(-1, 4, 2, 1, 0, 0)
+
+
+def test_validate_sketch_codes(lib):
+    import paper_1804_00462_b200 as P
+    for args in [(1, 5, 1, 1, 0), (5, 5, 0, 1, 0), (5, 5, 3, 2, 0), (5, 5, 2, 5, 0), (5, 5, 1, 2, -1)]:
+        with pytest.raises(P.ParameterError):
+            P.validate_sketch(*args)
+    P.validate_sketch(5, 5, 2, 4, 0)
+
+
+def test_context_without_gpu_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_1804_00462_b200 as P
+    with pytest.raises(P.CudaError):
+        P.Context(0)
+    with pytest.raises(P.CudaError):
+        P.sor_svd_power(np.ones((10, 8)), 2, P.SketchConfig(3, 0, 1))

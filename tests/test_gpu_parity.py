@@ -1,0 +1,276 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on
+the same inputs and the same host-drawn Omega. Tolerances follow the north
+star (FP64: sigma rel <= 1e-10, low-rank rel Frobenius <= 1e-9), raised to
+10x the reference's own perturbation floor where the reference itself is
+rounding-chaotic."""
+import numpy as np
+import pytest
+
+from oracle import sorsvd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_00462_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    import torch
+    return torch
+
+
+def _check_parity(got, ref_sigma, ref_u, ref_v, ds=None, dl=0.0, tol_s=1e-10, tol_lr=1e-9):
+    s = np.asarray(got.sigma)
+    es = O.sigma_rel_err(s, ref_sigma)
+    lim = np.maximum(tol_s, 10 * ds) if ds is not None else tol_s
+    assert np.all(es <= lim), (es.max(), es)
+    lr = O.lowrank_rel_diff(np.asarray(got.u), s, np.asarray(got.v), ref_u, ref_sigma, ref_v)
+    assert lr <= max(tol_lr, 10 * dl), lr
+    return es.max(), lr
+
+
+# ------------------------------------------------------------ kernel units --
+@pytest.mark.parametrize("M,K,N,ta", [(1000, 700, 20, False), (1000, 700, 20, True), (4001, 999, 100, False),
+                                      (3999, 1001, 100, True), (257, 129, 8, False), (513, 2049, 256, True),
+                                      (20000, 300, 10, False), (300, 20000, 10, True), (33, 17, 3, False)])
+def test_matmul_skinny(P, torch_mod, M, K, N, ta):
+    rng = np.random.default_rng(M + K + N)
+    a = rng.standard_normal((K, M) if ta else (M, K))
+    b = rng.standard_normal((K, N))
+    ref = (a.T if ta else a) @ b
+    got = P.matmul(torch_mod.from_numpy(a).cuda(), torch_mod.from_numpy(b).cuda(), transpose_a=ta).cpu().numpy()
+    scale = np.abs(a).max() * np.abs(b).max() * K
+    assert np.abs(got - ref).max() <= 1e-14 * scale
+
+
+@pytest.mark.parametrize("m,k", [(50, 10), (2, 1), (1000, 20), (4000, 100), (300, 112), (25344, 10), (9000, 37),
+                                 (1500, 128), (2000, 256)])
+def test_thin_qr_vs_oracle(P, torch_mod, m, k):
+    t = O.gaussian_matrix(m, k, m * 7 + k)
+    q_ref, r_ref = O.thin_qr(t)
+    q, r = P.thin_qr(torch_mod.from_numpy(t).cuda())
+    q = q.cpu().numpy()
+    r = r.cpu().numpy()
+    assert np.abs(q.T @ q - np.eye(k)).max() < 1e-13
+    assert np.abs(q @ r - t).max() < 1e-13 * np.abs(t).max() * np.sqrt(m)
+    assert np.all(np.diag(r) >= 0)
+    assert np.allclose(np.tril(r, -1), 0)
+    np.testing.assert_allclose(q, q_ref, atol=1e-11)
+    np.testing.assert_allclose(r, r_ref, atol=1e-11 * np.abs(r_ref).max())
+
+
+def test_thin_qr_rank_deficient(P, torch_mod):
+    t = O.gaussian_matrix(500, 8, 3)
+    t[:, 5] = 0.0
+    t[:, 6] = t[:, 1]
+    q, r = P.thin_qr(torch_mod.from_numpy(t).cuda())
+    q = q.cpu().numpy()
+    assert np.abs(q.T @ q - np.eye(8)).max() < 1e-13
+    assert np.abs(q @ r.cpu().numpy() - t).max() < 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 20, 33, 100, 112, 128, 256])
+def test_small_svd_vs_oracle(P, torch_mod, k):
+    mm = O.gaussian_matrix(k, k, 1000 + k)
+    u_ref, s_ref, v_ref = O.full_svd(mm)
+    u, s, v, sweeps = P.full_svd(torch_mod.from_numpy(mm).cuda())
+    u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+    assert np.all(np.diff(s) <= 0)
+    np.testing.assert_allclose(s, s_ref, rtol=1e-12, atol=1e-14 * s_ref[0])
+    assert np.abs(u.T @ u - np.eye(k)).max() < 1e-13
+    assert np.abs(v.T @ v - np.eye(k)).max() < 1e-13
+    assert np.abs((u * s) @ v.T - mm).max() < 1e-13 * s_ref[0] * k
+    # sign canonicalisation (dense.hpp:80-95) makes the factors comparable directly
+    gap = np.min(np.abs(np.diff(s_ref))) if k > 1 else 1.0
+    if gap > 1e-6 * s_ref[0]:
+        np.testing.assert_allclose(u, u_ref, atol=1e-10)
+        np.testing.assert_allclose(v, v_ref, atol=1e-10)
+
+
+def test_small_svd_graded(P, torch_mod):
+    # strongly graded spectrum: one-sided Jacobi keeps relative accuracy
+    k = 60
+    u0, _ = np.linalg.qr(O.gaussian_matrix(k, k, 1))
+    v0, _ = np.linalg.qr(O.gaussian_matrix(k, k, 2))
+    sig = 10.0 ** (-np.arange(k) / 6.0)
+    mm = (u0 * sig) @ v0.T
+    _, s, _, _ = P.full_svd(torch_mod.from_numpy(mm).cuda())
+    s_ref = np.linalg.svd(mm, compute_uv=False)
+    np.testing.assert_allclose(s.cpu().numpy()[:40], s_ref[:40], rtol=1e-9)
+
+
+# ----------------------------------------------------- sor_svd_power parity --
+def test_golden_cases_host_api(P, golden):
+    g, meta = golden
+    for name in meta["cases"]:
+        md = meta["meta"][name]
+        A = g[name + "_A"]
+        cfg = P.SketchConfig(md["ell"], md["q"], md["seed"])
+        f = P.sor_svd_power(A, md["k"], cfg)
+        assert f.passes == md["passes"] and int(f.method) == md["method"]
+        _, ds, dl = O.perturbation_floor(A, md["k"], O.SketchConfig(md["ell"], md["q"], md["seed"]))
+        _check_parity(f, g[name + "_s"], g[name + "_u"], g[name + "_v"], ds, dl)
+
+
+def test_rank1_spec_example(P, golden):
+    g, _ = golden
+    A = g["rank1_A"]
+    f = P.sor_svd(A, 1, P.SketchConfig(4, 0, 93))
+    err = np.linalg.norm(A - (f.u * f.sigma) @ f.v.T) / np.linalg.norm(A)
+    assert err < 1e-10
+    _check_parity(f, g["rank1_s"], g["rank1_u"], g["rank1_v"])
+
+
+def test_config1_full(P, golden):
+    g, _ = golden
+    A = O.gen_c1(1)
+    f = P.sor_svd_power(A, 20, P.SketchConfig(20, 0, 7))
+    es, lr = _check_parity(f, g["c1_s"], g["c1_u"], g["c1_v"])
+    # raw factors match too (same sign conventions as the reference)
+    np.testing.assert_allclose(f.u, g["c1_u"], atol=1e-9)
+    np.testing.assert_allclose(f.v, g["c1_v"], atol=1e-9)
+
+
+def test_config1_device_api_and_determinism(P, torch_mod, golden):
+    g, _ = golden
+    A = torch_mod.from_numpy(O.gen_c1(1)).cuda()
+    f1 = P.sor_svd_power(A, 20, P.SketchConfig(20, 0, 7))
+    f2 = P.sor_svd_power(A, 20, P.SketchConfig(20, 0, 7))
+    f3 = P.sor_svd_power(A, 20, P.SketchConfig(20, 0, 7), use_graph=False)
+    for f in (f2, f3):
+        assert torch_mod.equal(f1.sigma, f.sigma) and torch_mod.equal(f1.u, f.u) and torch_mod.equal(f1.v, f.v)
+    _check_parity(type(f1)(f1.u.cpu().numpy(), f1.sigma.cpu().numpy(), f1.v.cpu().numpy(), f1.method, f1.passes,
+                           20, 0, 7), g["c1_s"], g["c1_u"], g["c1_v"])
+
+
+def test_explicit_omega_equals_seeded(P):
+    A = O.gaussian_matrix(120, 90, 4)
+    om = O.gaussian_matrix(90, 10, 55)
+    f1 = P.sor_svd_power(A, 6, P.SketchConfig(10, 1, 55))
+    f2 = P.sor_svd_power(A, 6, P.SketchConfig(10, 1, 999), omega=om)
+    np.testing.assert_array_equal(f1.sigma, f2.sigma)
+
+
+@pytest.mark.parametrize("m,n,k,ell,q", [(400, 300, 10, 10, 0), (300, 400, 10, 14, 2), (1000, 64, 8, 8, 1),
+                                         (64, 1000, 8, 8, 1), (2001, 1500, 50, 60, 1), (3, 3, 1, 2, 0)])
+def test_shapes_vs_oracle(P, m, n, k, ell, q):
+    A = O.gen_lowrank_decay(m, n, min(m, n) - 1 if min(m, n) < 40 else 40, lambda j: 2.0 ** (-j / 4), 1e-8, m + n)
+    cfg = O.SketchConfig(ell, q, 17)
+    base, ds, dl = O.perturbation_floor(A, k, cfg)
+    f = P.sor_svd_power(A, k, P.SketchConfig(ell, q, 17))
+    _check_parity(f, base.sigma, base.u, base.v, ds, dl)
+
+
+def test_config2_full(P):
+    A = O.gen_c2(2)
+    cfg = O.SketchConfig(100, 1, 21)
+    base, ds, dl = O.perturbation_floor(A, 100, cfg, trials=2)
+    f = P.sor_svd_power(A, 100, P.SketchConfig(100, 1, 21))
+    _check_parity(f, base.sigma, base.u, base.v, ds, dl)
+    # Frobenius approximation error within 1% of the oracle's, interlacing
+    import torch
+    At = torch.from_numpy(A).cuda()
+    def fro(u, s, v):
+        return float(torch.linalg.norm(At - (torch.from_numpy(u).cuda() * torch.from_numpy(s).cuda()) @ torch.from_numpy(v).cuda().T))
+    e_gpu, e_ref = fro(f.u, f.sigma, f.v), fro(base.u, base.sigma, base.v)
+    assert abs(e_gpu - e_ref) <= 0.01 * e_ref
+    sig_true = 1.0 / np.arange(1, 101) ** 2
+    assert np.all(f.sigma <= sig_true + 1e-9)
+
+
+def test_config3_scaled_k256(P):
+    # C3 distributions at 1/10 x 1/10 scale with the full k = 256 (global-memory TSQR/Jacobi paths)
+    A = O.gen_lowrank_decay(20000, 2000, 256, lambda j: 10.0 ** (-j / 64.0), 1e-3, 3)
+    cfg = O.SketchConfig(256, 1, 31)
+    base, ds, dl = O.perturbation_floor(A, 256, cfg, trials=1)
+    f = P.sor_svd_power(A, 256, P.SketchConfig(256, 1, 31))
+    _check_parity(f, base.sigma, base.u, base.v, ds, dl)
+
+
+def test_ell_greater_than_k(P):
+    A = O.gen_lowrank_decay(500, 400, 30, lambda j: 1.0 / j, 1e-6, 8)
+    cfg = O.SketchConfig(24, 1, 3)
+    base, ds, dl = O.perturbation_floor(A, 12, cfg)
+    f = P.sor_svd_power(A, 12, P.SketchConfig(24, 1, 3))
+    assert f.u.shape == (500, 12) and f.v.shape == (400, 12)
+    _check_parity(f, base.sigma, base.u, base.v, ds, dl)
+
+
+def test_errors(P):
+    A = np.ones((10, 8))
+    with pytest.raises(P.ParameterError):
+        P.sor_svd_power(A, 2, P.SketchConfig(8, 0, 1))   # ell >= min(m,n)
+    with pytest.raises(P.ParameterError):
+        P.sor_svd_power(A, 3, P.SketchConfig(2, 0, 1))   # ell < k
+    with pytest.raises(P.ParameterError):
+        P.sor_svd_power(A, 0, P.SketchConfig(2, 0, 1))   # k < 1
+    with pytest.raises(P.ParameterError):
+        P.sor_svd_power(A, 1, P.SketchConfig(2, -1, 1))  # q < 0
+    with pytest.raises(P.ParameterError):
+        P.sor_svd(A, 1, P.SketchConfig(2, 1, 1))         # sor_svd requires q == 0
+    with pytest.raises(P.ParameterError):
+        P.sor_svd_power(np.ones((1, 8)), 1, P.SketchConfig(1, 0, 1))
+    with pytest.raises(P.UnsupportedError):
+        P.sor_svd_power(A, 2, P.SketchConfig(3, 0, 1, single_pass=True))
+    # the context survives errors
+    f = P.sor_svd_power(O.gaussian_matrix(10, 8, 1), 2, P.SketchConfig(3, 0, 1))
+    assert np.all(np.isfinite(f.sigma))
+
+
+def test_zero_matrix(P):
+    f = P.sor_svd_power(np.zeros((50, 40)), 3, P.SketchConfig(5, 1, 2))
+    assert np.all(f.sigma == 0.0)
+    assert np.all(np.isfinite(f.u)) and np.all(np.isfinite(f.v))
+
+
+def test_stage_times(P):
+    A = O.gaussian_matrix(2000, 1500, 3)
+    f = P.sor_svd_power(A, 50, P.SketchConfig(50, 1, 3), stage_times=True)
+    st = f.stats
+    assert st["ms_passes"] > 0 and st["ms_qr"] > 0 and st["ms_svd"] > 0
+    assert st["passes"] == 5 and st["launches"] > 5
+
+
+# -------------------------------------------------------------------- RPCA --
+def test_rpca_golden(P, golden):
+    g, meta = golden
+    md = meta["meta"]["rpca100"]
+    cfg = P.RpcaConfig(lam=md["lam"], mu0=md["mu0"], ell=md["ell"], q=md["q"], seed=md["seed"], max_iter=100)
+    r = P.rpca_alm(g["rpca100_X"], cfg)
+    assert r.converged and r.iterations == md["iterations"]
+    assert r.rank_l == md["rank"] and r.nnz_s == md["nnz"]
+    assert abs(r.rel_error - md["rel"]) <= 1e-3 * md["rel"] + 1e-12
+    np.testing.assert_allclose(r.l, g["rpca100_L"], atol=1e-8 * np.abs(g["rpca100_L"]).max())
+    np.testing.assert_allclose(r.s, g["rpca100_S"], atol=1e-8 * 50)
+
+
+def test_rpca_c4_scaled_vs_oracle(P):
+    D, L0, S0 = O.gen_c4(4, m=2534, n=300)
+    mu0 = 1.25 / O.norm_spectral(D)
+    ocfg = O.RpcaConfig(lam=1 / np.sqrt(2534), mu0=mu0, ell=10, q=1, seed=9, max_iter=100)
+    ro = O.rpca_alm(D, ocfg)
+    r = P.rpca_alm(D, P.RpcaConfig(lam=ocfg.lam, mu0=mu0, ell=10, q=1, seed=9, max_iter=100))
+    assert r.iterations == ro.iterations and r.converged == ro.converged
+    assert r.rank_l == ro.rank_l and r.nnz_s == ro.nnz_s
+    assert np.linalg.norm(r.l - ro.l) <= 1e-9 * np.linalg.norm(ro.l)
+    assert np.linalg.norm(r.s - ro.s) <= 1e-9 * np.linalg.norm(ro.s)
+
+
+def test_rpca_zero_input(P):
+    r = P.rpca_alm(np.zeros((30, 20)), P.RpcaConfig(ell=3, q=1, seed=1))
+    assert r.iterations == 1 and r.converged and np.all(r.l == 0) and np.all(r.s == 0)
+
+
+def test_rpca_mu0_estimate(P):
+    D, _, _ = O.gen_c4(4, m=1000, n=120)
+    r = P.rpca_alm(D, P.RpcaConfig(lam=1 / np.sqrt(1000), mu0=0.0, ell=10, q=1, seed=2, max_iter=100))
+    exact = 1.25 / O.norm_spectral(D)
+    assert abs(r.mu0 - exact) <= 1e-6 * exact
+    assert r.converged
