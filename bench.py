@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""SOR-SVD benchmark (BASELINE.json metric: SOR-SVD wall time & effective
+GFLOP/s = 2*m*n*ell*passes / time, vs roofline, on 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One JSON line on rank 0. "ours": A and Omega resident in HBM, K timed calls of
+sor_svd_power through the C ABI (CUDA events, L2 flushed between steps, max
+over ranks); e2e: the same call through the public host-buffer API (H2D of A,
+Omega draw + upload, D2H of U, sigma, V inside the timed region). "reference":
+the compiled reference (oracle/_ref = the unmodified reference headers on
+OpenBLAS) on all host cores, same config and metric.
+Multi-GPU (torchrun): A is row-sharded; configs marked weak keep m rows per
+rank, strong configs split the fixed m.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SOR-SVD effective GFLOP/s (2*m*n*ell*passes / wall time)"
+
+CONFIGS = {
+    # BASELINE.json configs[0]
+    "c1": dict(m=1000, n=1000, k=20, q=0, scaling="weak",
+               desc="C1 fp64 m=n=1000 k=ell=20 q=0, A = X Y^T + N(0,1e-4)"),
+    # BASELINE.json configs[1] (default workload)
+    "c2": dict(m=4000, n=4000, k=100, q=1, scaling="weak",
+               desc="C2 fp64 m=n=4000 k=ell=100 q=1, A = U diag(j^-2) V^T (Haar U, V)"),
+    # BASELINE.json configs[2], fp64 variant
+    "c3": dict(m=200000, n=20000, k=256, q=1, scaling="strong",
+               desc="C3 fp64 m=200000 n=20000 k=ell=256 q=1, A = X diag(10^(-j/64)) Y^T + N(0,1e-6)"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------- data -----
+def make_matrix(cfg_name, m_local, n, rank, world, device):
+    import torch
+    g = torch.Generator(device=device)
+    f64 = torch.float64
+    if cfg_name == "c1":
+        g.manual_seed(1000 + rank)
+        x = torch.randn(m_local, 20, generator=g, device=device, dtype=f64)
+        g.manual_seed(2000)
+        y = torch.randn(n, 20, generator=g, device=device, dtype=f64)
+        g.manual_seed(3000 + rank)
+        return x @ y.T + 1e-2 * torch.randn(m_local, n, generator=g, device=device, dtype=f64)
+    if cfg_name == "c2":
+        g.manual_seed(1000 + rank)
+        u, _ = torch.linalg.qr(torch.randn(m_local, m_local, generator=g, device=device, dtype=f64))
+        g.manual_seed(2000)
+        v, _ = torch.linalg.qr(torch.randn(n, n, generator=g, device=device, dtype=f64))
+        r = min(m_local, n)
+        s = 1.0 / torch.arange(1, r + 1, device=device, dtype=f64) ** 2
+        return (u[:, :r] * s) @ v[:, :r].T
+    if cfg_name == "c3":
+        mg = CONFIGS["c3"]["m"]
+        g.manual_seed(1000 + rank)
+        x = torch.randn(m_local, 256, generator=g, device=device, dtype=f64) / math.sqrt(mg)
+        g.manual_seed(2000)
+        y = torch.randn(n, 256, generator=g, device=device, dtype=f64) / math.sqrt(n)
+        s = 10.0 ** (-torch.arange(1, 257, device=device, dtype=f64) / 64.0)
+        a = torch.empty(m_local, n, device=device, dtype=f64)
+        g.manual_seed(3000 + rank)
+        step = 8192
+        for i in range(0, m_local, step):
+            j = min(m_local, i + step)
+            a[i:j] = (x[i:j] * s) @ y.T + 1e-3 * torch.randn(j - i, n, generator=g, device=device, dtype=f64)
+        return a
+    raise ValueError(cfg_name)
+
+
+# ------------------------------------------------------------- clocks -----
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------- CPU reference ----
+def _prefer_avx512_blas():
+    """OpenBLAS 0.3.15 (the reference's BLAS here) falls back to its generic
+    Prescott kernels on this CPU model; select its AVX-512 kernels when the
+    host has them, so the reference runs at its best (must precede loading)."""
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        return
+    if "avx512f" in flags:
+        os.environ.setdefault("OPENBLAS_CORETYPE", "SKYLAKEX")
+
+
+def cpu_reference(a_host, k, ell, q, seed, steps, min_seconds=0.0, threads=None):
+    """Times the compiled reference (oracle/_ref: unmodified reference headers on
+    OpenBLAS) on host cores. Returns (per-call seconds list, cores, kind)."""
+    _prefer_avx512_blas()
+    from oracle import sorsvd_oracle as O
+    cores = threads or os.cpu_count() or 1
+    O.Ref.set_threads(cores)
+    kind = "reference"
+    times = []
+    t_start = time.perf_counter()
+    i = 0
+    while i < steps or (time.perf_counter() - t_start) < min_seconds:
+        t0 = time.perf_counter()
+        O.Ref.sor_svd_power(a_host, k, O.SketchConfig(ell, q, seed + i))
+        times.append(time.perf_counter() - t0)
+        i += 1
+        if i >= 200:
+            break
+    return times, cores, kind
+
+
+def cpu_sample(cfg_name, a_dev, cfg):
+    """Bounded sample of the workload for the CPU leg (about 10-30 s)."""
+    if cfg_name == "c3":
+        rows = 20000  # 1/10 of the rows, same n, k, q: ~1/10 of the work
+        return a_dev[:rows].cpu().numpy(), f"row-block sample {rows}x{cfg['n']} of the C3 matrix (same n, k, q)"
+    return a_dev.cpu().numpy(), f"full {cfg_name.upper()} instance"
+
+
+# ------------------------------------------------------------------ main --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    k = ell = cfg["k"]
+    q = cfg["q"]
+    passes = 2 * q + 3
+    if cfg["scaling"] == "weak":
+        m_local, m_global = cfg["m"], cfg["m"] * world
+    else:
+        m_global = cfg["m"]
+        base, extra = divmod(m_global, world)
+        m_local = base + (1 if rank < extra else 0)
+    n = cfg["n"]
+    workload = dict(workload=cfg["desc"], m=m_global, n=n, k=k, ell=ell, q=q, passes=passes,
+                    rows_per_rank=m_local, parallelism=f"row-sharded x{world}" if world > 1 else "single GPU",
+                    l2="flushed between timed steps (256 MiB write)")
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        _prefer_avx512_blas()
+        import numpy as np
+        from oracle import sorsvd_oracle as O
+        # same synthetic distribution, generated on the host with the oracle RNG
+        if args.config == "c1":
+            a = O.gen_c1(1)
+            sample = "full C1 instance"
+        elif args.config == "c2":
+            a = O.gen_c2(2, n=n, m=cfg["m"])
+            sample = "full C2 instance"
+        else:
+            a = O.gen_lowrank_decay(20000, n, 256, lambda j: 10.0 ** (-j / 64.0), 1e-3, 3)
+            sample = "row-block sample 20000x20000 of the C3 distribution (same n, k, q)"
+        if args.warmup:
+            cpu_reference(a, k, ell, q, 7, min(args.warmup, 3))
+        times, cores, kind = cpu_reference(a, k, ell, q, 7, args.steps)
+        sec = sum(times) / len(times)
+        mm = a.shape[0]
+        val = 2.0 * mm * n * ell * passes / sec / 1e9
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": world,
+                "steps": len(times), "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": workload,
+                "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": kind, "sample": sample,
+                                 "blas": O.ref_lib().ref_blas_config().decode()},
+                "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import numpy as np
+    import torch
+    import paper_1804_00462_b200 as P
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+        idbuf = torch.zeros(128, dtype=torch.uint8, device=device)
+        if rank == 0:
+            idbuf.copy_(torch.frombuffer(bytearray(P.Context.nccl_unique_id()), dtype=torch.uint8).to(device))
+        dist.broadcast(idbuf, 0)
+        ctx = P.Context(local_rank, rank=rank, world=world, nccl_id=bytes(idbuf.cpu().numpy().tobytes()))
+    else:
+        ctx = P.Context(local_rank)
+    stream = torch.cuda.current_stream(device)
+    ctx.set_stream(stream.cuda_stream)
+
+    t_gen = time.perf_counter()
+    A = make_matrix(args.config, m_local, n, rank, world, device)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] generated {m_local}x{n} fp64 in {time.perf_counter() - t_gen:.1f}s")
+    omega = torch.from_numpy(P.gaussian_matrix(n, ell, 7)).to(device)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    scfg = P.SketchConfig(ell=ell, q=q, seed=7)
+
+    def call():
+        return P.sor_svd_power(A, k, scfg, omega=omega, ctx=ctx, m_global=m_global)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 0)):
+        call()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    barrier()
+    launches = 0
+    t_wall = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        f = call()
+        ev[i][1].record(stream)
+        launches += int(f.stats["launches"])
+    barrier()
+    t_wall = time.perf_counter() - t_wall
+    clk = clocks.stop()
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    ms_total = sum(ms_steps)
+    if dist:
+        tt = torch.tensor([ms_total], device=device, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_per_step = ms_total / args.steps
+    flops_step = 2.0 * m_global * n * ell * passes
+    value = flops_step / (ms_per_step * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (the A-streaming pass) ----
+    fp64_peak = ctypes_peak = None
+    import ctypes
+    pk = ctypes.c_double()
+    hb = ctypes.c_double()
+    P._check(P._capi.lib().sorsvd_measure_peaks(ctx.handle, ctypes.byref(pk), ctypes.byref(hb)), ctx.handle)
+    fp64_peak, hbm_read = pk.value, hb.value
+    Np = (ell + 7) // 8 * 8 if ell <= 128 else (ell + 127) // 128 * 128
+    X = torch.zeros(n, Np, dtype=torch.float64, device=device)
+    X[:, :ell] = omega
+    T = torch.zeros(m_local, Np, dtype=torch.float64, device=device)
+    ms_pass = ctypes.c_double()
+    lpp = ctypes.c_int32()
+    P._check(P._capi.lib().sorsvd_pass_device(ctx.handle, 0, m_local, n, n, ell, A.data_ptr(), X.data_ptr(),
+                                              T.data_ptr(), max(args.steps, 5), ctypes.byref(ms_pass),
+                                              ctypes.byref(lpp)), ctx.handle)
+    T2 = torch.zeros(n, Np, dtype=torch.float64, device=device)
+    ms_pass_t = ctypes.c_double()
+    P._check(P._capi.lib().sorsvd_pass_device(ctx.handle, 1, m_local, n, n, ell, A.data_ptr(), T.data_ptr(),
+                                              T2.data_ptr(), max(args.steps, 5), ctypes.byref(ms_pass_t),
+                                              ctypes.byref(lpp)), ctx.handle)
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else open(os.devnull) as fh:
+        try:
+            mp = json.load(fh)
+        except Exception:
+            mp = {}
+    hbm_peak = mp.get("hbm_gbs", 6650.0)
+    pass_flops = 2.0 * m_local * n * ell
+    pass_bytes = 8.0 * m_local * n
+    ai = pass_flops / pass_bytes
+    ridge = fp64_peak * 1e12 / (hbm_peak * 1e9)
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get(args.config, {}).get("pass_nn_dram_bytes")
+        except Exception:
+            traffic = None
+    if ai >= ridge:
+        achieved = pass_flops / (ms_pass.value * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": traffic,
+                "kernel": "gemm_f64_kernel NN pass T1 = A*X (DMMA m8n8k4)",
+                "peak_source": "live FP64 DMMA burst (sorsvd_measure_peaks); MEASURED_PEAKS.json has no FP64",
+                "ms_per_launch": ms_pass.value, "flops_per_launch": pass_flops,
+                "tn_pass": {"ms": ms_pass_t.value, "achieved": pass_flops / (ms_pass_t.value * 1e-3) / 1e12},
+                "hbm_gbs_measured": hbm_peak}
+    else:
+        achieved = pass_bytes / (ms_pass.value * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic, "kernel": "gemm_f64_kernel NN pass T1 = A*X",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "ms_per_launch": ms_pass.value,
+                "bytes_per_launch": pass_bytes,
+                "tn_pass": {"ms": ms_pass_t.value, "achieved": pass_bytes / (ms_pass_t.value * 1e-3) / 1e9}}
+    del X, T, T2
+
+    # ---- e2e through the public host-buffer API ----
+    e2e = None
+    if not args.no_e2e:
+        a_host = torch.empty((m_local, n), dtype=torch.float64, pin_memory=True)
+        a_host.copy_(A)
+        a_np = a_host.numpy()
+        del A
+        torch.cuda.empty_cache()
+        hcfg = P.SketchConfig(ell=ell, q=q, seed=7)
+        for _ in range(max(1, min(args.warmup, 2))):
+            P.sor_svd_power(a_np, k, hcfg, ctx=ctx, m_global=m_global)
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            P.sor_svd_power(a_np, k, hcfg, ctx=ctx, m_global=m_global)
+        el = time.perf_counter() - t0
+        if dist:
+            tt = torch.tensor([el], device=device, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            el = float(tt.item())
+        e2e = {"value": flops_step / (el / args.steps) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(m_local * n * 8 + n * ell * 8),
+               "d2h_bytes_per_step": int((m_local + n) * k * 8 + k * 8),
+               "ms_per_step": el / args.steps * 1e3,
+               "path": "sorsvd_sor_svd_power (host buffers, pinned A; Omega drawn from seed inside)"}
+    else:
+        a_np = None
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        if a_np is None:
+            a_np = A.cpu().numpy()
+        if args.config == "c3":
+            a_cpu = np.ascontiguousarray(a_np[:20000])
+            sample = "row-block sample 20000x20000 of the C3 matrix (same n, k, q)"
+        else:
+            a_cpu = a_np
+            sample = f"full {args.config.upper()} instance"
+        times, cores, kind = cpu_reference(a_cpu, k, ell, q, 7, 3, min_seconds=10.0)
+        sec = statistics.median(times)
+        cpu = {"value": 2.0 * a_cpu.shape[0] * n * ell * passes / sec / 1e9, "unit": "GFLOP/s", "cores": cores,
+               "kind": kind, "sample": f"{sample}; median of {len(times)} calls ({sum(times):.1f}s)",
+               "ms_per_call": sec * 1e3}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": workload, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk,
+                "wall_s_timed_region": t_wall, "ms_steps": [round(x, 4) for x in ms_steps]}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -167,6 +167,15 @@ int sorsvd_small_svd_device(sorsvd_ctx* ctx, int32_t k, const double* dM, int64_
 int sorsvd_matmul_device(sorsvd_ctx* ctx, int32_t ta, int64_t M, int64_t K, int32_t N, const double* dA,
                          int64_t lda, const double* dB, int64_t ldb, double* dC, int64_t ldc);
 
+/* ---- measurement (bench.py roofline) --------------------------------------- */
+/* Live FP64 DMMA peak (TFLOP/s, burst) and streaming HBM read (GB/s). */
+int sorsvd_measure_peaks(sorsvd_ctx* ctx, double* fp64_tflops, double* hbm_read_gbs);
+/* One A-streaming pass (sketch.hpp:95 when ta = 0, :96 when ta = 1) repeated
+ * `reps` times between CUDA events; dX / dT padded to ld = ell rounded up to 8
+ * (or to 128 when ell > 128). Reports the average pass time. */
+int sorsvd_pass_device(sorsvd_ctx* ctx, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell, const double* dA,
+                       const double* dX, double* dT, int32_t reps, double* ms_avg, int32_t* launches_per_pass);
+
 /* ---- host helpers mirroring random.hpp / sketch.hpp ----------------------- */
 uint64_t sorsvd_sub_seed(uint64_t seed, uint64_t stream);                    /* random.hpp:24 */
 int sorsvd_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out, int nthreads); /* random.hpp:60 */

@@ -28,6 +28,7 @@
 #include "gemm_f64.cuh"
 #include "host_api.hpp"
 #include "jacobi_f64.cuh"
+#include "peaks.cuh"
 #include "rpca_f64.cuh"
 #include "tsqr_f64.cuh"
 
@@ -915,6 +916,62 @@ double device_sumsq(sorsvd_ctx* c, const double* x, int64_t m, int64_t n, int64_
     return h[0];
 }
 
+// sigma_1(A) for mu0 = 1.25/||D||_2: block subspace iteration
+// with re-orthonormalisation (TSQR each step) and a Rayleigh-Ritz value from
+// the Jacobi SVD of R(A X); iterates until the Ritz value is stationary to
+// 1e-14 relative. The reference uses dgesdd on all of D (dense.hpp:173).
+double estimate_sigma1(sorsvd_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda, uint64_t seed) {
+    const int ell = (int)std::max<int64_t>(1, std::min<int64_t>(16, std::min(m, n) - 1));
+    const int Np = npad(ell);
+    QrPlan* pn = get_qr_plan(c, n, ell, 0, "est_n");
+    QrPlan* pm = get_qr_plan(c, m, ell, 0, "est_m");
+    double* X = dbuf(c, "est_X", (size_t)n * Np, true);
+    double* T1 = dbuf(c, "est_T1", (size_t)m * Np);
+    double* T2 = dbuf(c, "est_T2", (size_t)n * Np);
+    double* Uk = dbuf(c, "est_U", (size_t)ell * ell);
+    double* Vk = dbuf(c, "est_V", (size_t)ell * ell);
+    double* Sk = dbuf(c, "est_S", (size_t)ell);
+    int* sw = reinterpret_cast<int*>(dbuf(c, "est_sw", 1));
+    std::vector<double> h((size_t)n * ell);
+    sorsvd_host::gaussian_fill(h.data(), h.size(), seed, 0);
+    CK(cudaMemcpy2DAsync(X, (size_t)Np * 8, h.data(), (size_t)ell * 8, (size_t)ell * 8, (size_t)n,
+                         cudaMemcpyHostToDevice, c->stream));
+    cudaStream_t s = c->stream;
+    auto mul = [&](bool ta, const double* B, double* Cout) {
+        GemmCall g;
+        g.ta = ta;
+        g.A = A;
+        g.lda = lda;
+        g.M = ta ? n : m;
+        g.K = ta ? m : n;
+        g.B = B;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = Cout;
+        g.ldc = Np;
+        run_gemm(c, g, s);
+    };
+    double prev = -1.0, cur = 0.0;
+    const int L = (int)pm->nodes.size() - 1;
+    for (int it = 1; it <= 400; ++it) {
+        mul(false, X, T1);
+        mul(true, T1, T2);
+        qr_factor(c, pn, T2, Np, X, Np, true, s);
+        qr_formq(c, pn, T2, Np, X, Np, nullptr, s);
+        if (it % 4 == 0) {
+            mul(false, X, T1);
+            qr_factor(c, pm, T1, Np, T1, Np, true, s);
+            run_jacobi(c, ell, pm->R[L], ell, Uk, ell, Sk, Vk, ell, sw, s);
+            CK(cudaMemcpyAsync(&cur, Sk, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (!std::isfinite(cur)) throw Error{SORSVD_ERR_NUMERICAL, "numerical: sigma_1 estimate not finite"};
+            if (std::fabs(cur - prev) <= 1e-14 * cur) break;
+            prev = cur;
+        }
+    }
+    return cur;
+}
+
 void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, double* dL, double* dSout,
                  sorsvd_rpca_result* res) {
     if (!d) throw Error{SORSVD_ERR_PARAMETER, "parameter: null descriptor"};
@@ -946,25 +1003,7 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
         return;
     }
     double mu = d->mu0;
-    if (!(mu > 0.0)) {  // 1.25 / sigma_1(D): randomized estimate with power iterations
-        sorsvd_desc e{};
-        e.m = m;
-        e.n = n;
-        e.lda = ldd;
-        e.ell = (int)std::min<int64_t>(8, std::min(m, n) - 1);
-        e.k = 1;
-        e.q = 6;
-        e.seed = d->seed ^ 0x5bd1e995ULL;
-        e.dtype = SORSVD_F64;
-        double* u1 = dbuf(c, "rp_est_u", (size_t)m);
-        double* v1 = dbuf(c, "rp_est_v", (size_t)n);
-        double* s1 = dbuf(c, "rp_est_s", 1);
-        sor_device(c, &e, dD, nullptr, u1, s1, v1, nullptr);
-        double h = 0.0;
-        CK(cudaMemcpyAsync(&h, s1, 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        mu = 1.25 / h;
-    }
+    if (!(mu > 0.0)) mu = 1.25 / estimate_sigma1(c, dD, m, n, ldd, d->seed ^ 0x5bd1e995ULL);
     r.mu0 = mu;
     const double mu_bar = (d->mu_bar_factor > 0 ? d->mu_bar_factor : 1e7) * mu;
     CK(cudaMemsetAsync(S, 0, (size_t)m * n * 8, c->stream));
@@ -1349,6 +1388,77 @@ int sorsvd_rpca_alm(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* D, d
         r.ms_h2d = h2d;
         r.ms_d2h = d2h;
         if (res) *res = r;
+    });
+}
+
+int sorsvd_measure_peaks(sorsvd_ctx* c, double* fp64_tflops, double* hbm_read_gbs) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        double* out = dbuf(c, "peak_out", 8);
+        float best = 1e30f;
+        const int iters = 4000, tpb = 256, grid = c->num_sms * 4;
+        for (int r = 0; r < 4; ++r) {
+            CK(cudaEventRecord(c->ev_a, c->stream));
+            peak_dmma_kernel<<<grid, tpb, 0, c->stream>>>(out, iters);
+            check_launch(c);
+            CK(cudaEventRecord(c->ev_b, c->stream));
+            CK(cudaEventSynchronize(c->ev_b));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+            if (r > 0) best = std::min(best, ms);
+        }
+        const double flops = 2.0 * 8 * 8 * 4 * 4.0 * iters * (grid * tpb / 32);
+        if (fp64_tflops) *fp64_tflops = flops / (best * 1e-3) / 1e12;
+        const size_t bytes = (size_t)4 << 30;
+        double* buf = dbuf(c, "peak_buf", bytes / 8);
+        best = 1e30f;
+        for (int r = 0; r < 4; ++r) {
+            CK(cudaEventRecord(c->ev_a, c->stream));
+            peak_read_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(reinterpret_cast<const double2*>(buf), bytes / 16, out);
+            check_launch(c);
+            CK(cudaEventRecord(c->ev_b, c->stream));
+            CK(cudaEventSynchronize(c->ev_b));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+            if (r > 0) best = std::min(best, ms);
+        }
+        if (hbm_read_gbs) *hbm_read_gbs = bytes / (best * 1e-3) / 1e9;
+        // release the 4 GiB probe buffer
+        Buf& b = c->bufs["peak_buf"];
+        CK(cudaFree(b.p));
+        b.p = nullptr;
+        b.bytes = 0;
+    });
+}
+
+// One A-streaming pass (T = A X or T = A^T X) launched `reps` times between
+// CUDA events on the context stream; X/T are padded (ldx = ldt = npad(ell)).
+int sorsvd_pass_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell, const double* dA,
+                       const double* dX, double* dT, int32_t reps, double* ms_avg, int32_t* launches_per_pass) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        const int Np = npad(ell);
+        GemmCall g;
+        g.ta = ta != 0;
+        g.A = static_cast<const double*>(dA);
+        g.lda = lda;
+        g.M = ta ? n : m;
+        g.K = ta ? m : n;
+        g.B = dX;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = dT;
+        g.ldc = Np;
+        run_gemm(c, g, c->stream);  // warm-up (sizes the split workspace)
+        const int l0 = c->launches;
+        CK(cudaEventRecord(c->ev_a, c->stream));
+        for (int r = 0; r < reps; ++r) run_gemm(c, g, c->stream);
+        CK(cudaEventRecord(c->ev_b, c->stream));
+        CK(cudaEventSynchronize(c->ev_b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+        if (ms_avg) *ms_avg = ms / std::max(reps, 1);
+        if (launches_per_pass) *launches_per_pass = (c->launches - l0) / std::max(reps, 1);
     });
 }
 
