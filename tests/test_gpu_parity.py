@@ -174,8 +174,8 @@ def test_config2_full(P):
     with q = 1 and no re-orthonormalisation the trailing sketch directions sit
     at sigma^4 ~ 1e-16 and the reference's own trailing sigmas move by up to
     ~1e-1 under 1e-16 input noise. Parity is therefore asserted (a) per sigma
-    on the determined part of the spectrum (floor envelope <= 1e-8) at
-    max(1e-10, 10 x floor), (b) on the low-rank approximation truncated to
+    on the determined part of the spectrum (floor envelope <= 1e-10) at
+    max(1e-10, 10 x floor), within 100 x floor on the transition band (floor <= 1e-6), (b) on the low-rank approximation truncated to
     that part, and (c) on the whole result through the Frobenius
     approximation error (within 1% of the oracle's) and interlacing."""
     A = O.gen_c2(2)
@@ -183,10 +183,12 @@ def test_config2_full(P):
     base, ds, dl = O.perturbation_floor(A, 100, cfg, trials=3)
     f = P.sor_svd_power(A, 100, P.SketchConfig(100, 1, 21))
     env = np.maximum.accumulate(ds)
-    jd = int(np.searchsorted(env, 1e-8))  # determined part: env[:jd] <= 1e-8
-    assert jd >= 30, jd
-    es = O.sigma_rel_err(f.sigma[:jd], base.sigma[:jd])
-    assert np.all(es <= np.maximum(1e-10, 10 * env[:jd])), es
+    jd = int(np.searchsorted(env, 1e-10))  # determined part: the oracle reproduces to <= 1e-10
+    jt = int(np.searchsorted(env, 1e-6))   # transition band
+    assert jd >= 25, jd
+    es = O.sigma_rel_err(f.sigma, base.sigma)
+    assert np.all(es[:jd] <= np.maximum(1e-10, 10 * env[:jd])), es[:jd]
+    assert np.all(es[jd:jt] <= 100 * env[jd:jt]), es[jd:jt]
     lr = O.lowrank_rel_diff(f.u[:, :jd], f.sigma[:jd], f.v[:, :jd], base.u[:, :jd], base.sigma[:jd], base.v[:, :jd])
     assert lr <= max(1e-9, 10 * dl), lr
     import torch
