@@ -1,0 +1,377 @@
+// K3 (v2): cluster-distributed Householder QR of one tall block per cluster.
+//
+// Replaces the LAPACK pair behind thin_qr (dense.hpp:114-134: dgeqrf + dorgqr
+// + diag(R) >= 0 at :127-132) for the sketches T1 (m x k) and T2 (n x k)
+// (sketch.hpp:98-99), and serves as the leaf / node kernel of the TSQR tree
+// when a sketch is larger than one cluster can hold.
+//
+// A block of `rows` x k is spread by rows over the C CTAs of a thread-block
+// cluster (C <= 16, non-portable size), each CTA keeping its rows
+// column-major in shared memory (<= ~210 KB). Reflector j needs, over all
+// rows, ||x_{j+1:}||^2, alpha = x_j, the row-j entries and the dots
+// s_c = sum_{i>j} x_i A(i,c); with v = [1; x/(alpha-beta)] every
+// d_c = A(j,c) + s_c/(alpha-beta), so ONE cluster reduction per reflector
+// (partials in shared memory, double-buffered, summed in fixed CTA order over
+// DSMEM -> identical on every CTA, deterministic) gives beta, tau and all
+// d_c. The explicit Q is then formed in place (dorg2r order, one reduction
+// per reflector), the root applies the reference sign convention, and the
+// rows go back to global memory. No tree at all when the whole sketch fits in
+// one cluster (C1, C2, C4: up to 16 x 210 KB).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace sorsvd_dev {
+
+namespace cg = cooperative_groups;
+
+constexpr int kCqrThreads = 512;
+constexpr int kCqrSmemBudget = 212 * 1024;
+
+struct CqrArgs {
+    const double* in;     // row-major input, block b starts at in + row0[b]*ldi
+    int64_t ldi;
+    double* qout;         // explicit Q rows (row-major), same row indexing; may alias in
+    int64_t ldq;
+    const int64_t* row0;  // per block
+    const int* rows;      // per block
+    int k;
+    double* R;            // per block k x ldr (row-major), zeros below the diagonal
+    int ldr;
+    int root_sign;        // apply diag(R) >= 0 (dense.hpp:127-132)
+};
+
+// shared-memory layout (doubles): A[ld*k] | red[2*RW] | S[RW] | tau[k] | sgn[k]
+__host__ __device__ inline int cqr_rw(int k) { return 2 * k + 4; }
+__host__ __device__ inline size_t cqr_smem_bytes(int Rb, int k) {
+    const int ld = Rb | 1;
+    return ((size_t)ld * k + 3 * (size_t)cqr_rw(k) + 2 * (size_t)k + 8) * sizeof(double);
+}
+
+// Process up to 4 owned columns c0, c0+cs, ... of a warp together: the
+// per-column shuffle reductions overlap and x / v are read once per row.
+template <int NC>
+struct ColGroup {
+    double* y[NC];
+    bool on[NC];
+    __device__ ColGroup(double* A, int ld, int c0, int cs, int cend) {
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            const int c = c0 + q * cs;
+            on[q] = c < cend;
+            y[q] = A + (size_t)(on[q] ? c : c0) * ld;
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks();
+    const int r = (int)cl.block_rank();
+    const int b = blockIdx.x / C;
+    const int rows = a.rows[b];
+    const int64_t row0 = a.row0[b];
+    const int k = a.k;
+    const int Rb = (rows + C - 1) / C;
+    const int lr0 = r * Rb;
+    const int nr = max(0, min(Rb, rows - lr0));
+    const int ld = Rb | 1;
+    const int RW = cqr_rw(k);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+
+    extern __shared__ __align__(16) double sm[];
+    double* A = sm;
+    double* red = A + (size_t)ld * k;
+    double* S = red + 2 * RW;
+    double* tau = S + RW;
+    double* sgn = tau + k;
+    __shared__ double sclA[512];   // 1/(alpha-beta) per reflector (deferred column scaling)
+    __shared__ double betaA[512];  // R(j,j) per reflector
+    __shared__ double* peers[16];
+
+    for (int e = tid; e < nr * k; e += blockDim.x) {
+        const int i = e / k, c = e - i * k;
+        A[(size_t)c * ld + i] = a.in[(row0 + lr0 + i) * a.ldi + c];
+    }
+    if (tid < C) peers[tid] = cl.map_shared_rank(red, tid);
+    __syncthreads();
+
+    // fixed-order cluster sum of red[off + idx] over the C CTAs (loads issued back to back)
+    auto csum = [&](int off, int idx) {
+        double v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = q < C ? peers[q][off + idx] : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) s += v[q];
+        return s;
+    };
+    auto first_owned = [&](int lo) { return lo + ((warp - lo) % nw + nw) % nw; };
+
+    // ------------------------------------------------------------ factor --
+    // Partial payload for reflector j (nt = k-j-1 trailing columns):
+    //   P[0] = sum_{i>j} x_i^2, P[1] = A(j,j), P[2+t] = sum_{i>j} x_i A(i,j+1+t),
+    //   P[2+nt+t] = A(j, j+1+t)   (row j entries come from its owner CTA, 0 elsewhere)
+    // Step j's fused pass updates the trailing columns with H_j and at the same
+    // time accumulates step j+1's payload against the (already updated) column j+1.
+    {
+        double* P = red;  // prologue: payload of reflector 0
+        const int nt = k - 1;
+        const int i0 = max(0, 1 - lr0);
+        const int jo = -lr0;
+        const bool owner = jo >= 0 && jo < nr;
+        const double* x = A;
+        for (int vc = warp; vc <= nt; vc += nw) {
+            const double* y = A + (size_t)vc * ld;
+            double s = 0.0;
+            for (int i = i0 + lane; i < nr; i += 32) s = fma(x[i], y[i], s);
+            s = warp_sum(s);
+            if (lane == 0) P[vc == 0 ? 0 : 1 + vc] = s;
+        }
+        for (int c = tid; c <= nt; c += blockDim.x) {
+            const double v = owner ? A[(size_t)c * ld + jo] : 0.0;
+            if (c == 0) P[1] = v;
+            else P[1 + nt + c] = v;
+        }
+    }
+    for (int j = 0; j < k; ++j) {
+        double* P = red + (j & 1) * RW;
+        double* Pn = red + ((j + 1) & 1) * RW;
+        const int nt = k - j - 1;
+        const int i0 = max(0, j + 1 - lr0);  // local rows with global index > j
+        const int jo = j - lr0;
+        const bool owner = jo >= 0 && jo < nr;
+        cl.sync();
+        for (int idx = tid; idx < 2 + 2 * nt; idx += blockDim.x) S[idx] = csum((int)(P - red), idx);
+        __syncthreads();
+        const double ss = S[0], alpha = S[1];
+        double t = 0.0, beta = alpha, scal = 0.0;
+        if (ss != 0.0) {
+            beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+            t = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        if (tid == 0) {
+            tau[j] = t;
+            sgn[j] = (a.root_sign && beta < 0.0) ? -1.0 : 1.0;
+            sclA[j] = scal;
+            betaA[j] = beta;
+        }
+        const double* x = A + (size_t)j * ld;  // reflector j, still unscaled (v_i = scal * x_i)
+        // deferred: finish column j-1 (scale into v, diagonal <- beta); nobody reads it this step
+        if (j >= 1 && warp == (j - 1) % nw) {
+            double* xm = A + (size_t)(j - 1) * ld;
+            const double sm1 = sclA[j - 1];
+            for (int i = max(0, j - lr0) + lane; i < nr; i += 32) xm[i] *= sm1;
+            const int jm = j - 1 - lr0;
+            if (lane == 0 && jm >= 0 && jm < nr) xm[jm] = betaA[j - 1];
+        }
+        // column j+1 first (its owner): apply H_j, then the next reflector's norm and alpha
+        const int i0n = max(0, j + 2 - lr0);
+        const int jon = j + 1 - lr0;
+        const bool ownern = jon >= 0 && jon < nr;
+        if (nt > 0 && warp == (j + 1) % nw) {
+            double* y = A + (size_t)(j + 1) * ld;
+            const double d = (S[2 + nt] + scal * S[2]) * t;
+            if (t != 0.0) {
+                for (int i = i0 + lane; i < nr; i += 32) y[i] = fma(-d * scal, x[i], y[i]);
+                if (owner && lane == 0) y[jo] -= d;
+            }
+            __syncwarp();
+            double s = 0.0;
+            for (int i = i0n + lane; i < nr; i += 32) s = fma(y[i], y[i], s);
+            s = warp_sum(s);
+            if (lane == 0) {
+                Pn[0] = s;
+                Pn[1] = ownern ? y[jon] : 0.0;
+            }
+        }
+        __syncthreads();
+        // fused pass over the remaining trailing columns c > j+1
+        if (nt > 1) {
+            const double* xn = A + (size_t)(j + 1) * ld;  // next reflector (updated, unscaled)
+            const int ntn = nt - 1;
+            for (int c0 = first_owned(j + 2); c0 < k; c0 += 4 * nw) {
+                ColGroup<4> g(A, ld, c0, nw, k);
+                double dd[4], sn[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int c = c0 + q * nw;
+                    dd[q] = g.on[q] ? (S[2 + nt + (c - j - 1)] + scal * S[2 + (c - j - 1)]) * t : 0.0;
+                    sn[q] = 0.0;
+                }
+                if (owner && lane == 0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (g.on[q]) g.y[q][jo] -= dd[q];
+                }
+                for (int i = i0 + lane; i < nr; i += 32) {
+                    const double vi = scal * x[i];
+                    const double xi = (i >= i0n) ? xn[i] : 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (g.on[q]) {
+                            const double yv = fma(-dd[q], vi, g.y[q][i]);
+                            g.y[q][i] = yv;
+                            sn[q] = fma(xi, yv, sn[q]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) sn[q] = warp_sum(sn[q]);
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (g.on[q]) {
+                            const int c = c0 + q * nw;
+                            Pn[2 + (c - j - 2)] = sn[q];
+                            Pn[2 + ntn + (c - j - 2)] = ownern ? g.y[q][jon] : 0.0;
+                        }
+                    }
+                }
+            }
+        }
+        // (no barrier here: the next step starts with cl.sync)
+    }
+    __syncthreads();
+    if (warp == (k - 1) % nw) {  // deferred finish of the last reflector column
+        double* xm = A + (size_t)(k - 1) * ld;
+        const double sm1 = sclA[k - 1];
+        for (int i = max(0, k - lr0) + lane; i < nr; i += 32) xm[i] *= sm1;
+        const int jm = k - 1 - lr0;
+        if (lane == 0 && jm >= 0 && jm < nr) xm[jm] = betaA[k - 1];
+    }
+    __syncthreads();
+
+    // R (owners of rows < k), sign-fixed at the root
+    double* Rb_out = a.R + (int64_t)b * k * a.ldr;
+    for (int e = tid; e < nr * k; e += blockDim.x) {
+        const int i = e / k, c = e - i * k;
+        const int gi = lr0 + i;
+        if (gi < k) Rb_out[(int64_t)gi * a.ldr + c] = c >= gi ? sgn[gi] * A[(size_t)c * ld + i] : 0.0;
+    }
+    __syncthreads();  // R is read from A before form-Q overwrites it
+
+    // ------------------------------------------------------------ form Q --
+    // Q = H_0 ... H_{k-1} [I; 0] in place (dorg2r order). Step j applies H_j to
+    // the columns c > j, and in the same pass accumulates step j-1's dots
+    // v_{j-1}^T Q(:, c >= j). Column j keeps its reflector v_j during step j
+    // (everyone reads it); its owner finishes it at the start of step j-1,
+    // and its step-(j-1) dot uses the closed form of the finished column:
+    // Q(:,j) = [0; 1 - t_j; -t_j v_j(j+1:)].
+    cl.sync();  // peers are done with the factor's reduction buffers
+    int par = 0;
+    auto finish_col = [&](int c) {
+        double* x = A + (size_t)c * ld;
+        const double tc = tau[c];
+        for (int i = lane; i < nr; i += 32) {
+            const int gi = lr0 + i;
+            x[i] = gi > c ? -tc * x[i] : (gi == c ? 1.0 - tc : 0.0);
+        }
+        __syncwarp();
+    };
+    for (int j = k - 1; j >= 0; --j) {
+        const int nt = k - j - 1;
+        const int jo = j - lr0;
+        const bool owner = jo >= 0 && jo < nr;
+        const double tj = tau[j];
+        const double* v = A + (size_t)j * ld;
+        const bool reduce = nt > 0 && tj != 0.0;  // identical on every CTA
+        if (reduce) {
+            double* P = red + (par & 1) * RW;
+            cl.sync();
+            for (int idx = tid; idx < nt; idx += blockDim.x) S[idx] = csum((int)(P - red), idx);
+            ++par;
+        }
+        __syncthreads();
+        double* Pn = red + (par & 1) * RW;  // payload of step j-1
+        const bool next = j >= 1 && tau[j - 1] != 0.0;
+        const double* vn = A + (size_t)(j >= 1 ? j - 1 : 0) * ld;
+        const int jon = j - 1 - lr0;
+        const bool ownern = jon >= 0 && jon < nr;
+        const int i0n = max(0, j - lr0);      // rows > j-1
+        const int i0 = max(0, j + 1 - lr0);   // rows > j
+        // column j (still v_j): its step-(j-1) dot in closed form
+        if (next && warp == j % nw) {
+            double s = 0.0;
+            for (int i = i0 + lane; i < nr; i += 32) s = fma(vn[i], -tj * v[i], s);
+            s = warp_sum(s);
+            if (lane == 0) Pn[0] = s + (owner ? vn[jo] * (1.0 - tj) : 0.0);
+        }
+        // columns c > j: finish column j+1 (first use as a Q column), apply H_j, dots with v_{j-1}
+        for (int c0 = first_owned(j + 1); c0 < k; c0 += 4 * nw) {
+            if (c0 == j + 1) finish_col(j + 1);
+            ColGroup<4> g(A, ld, c0, nw, k);
+            double dd[4], sn[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                dd[q] = (reduce && g.on[q]) ? S[c0 + q * nw - j - 1] * tj : 0.0;
+                sn[q] = 0.0;
+            }
+            if (owner && lane == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (g.on[q]) g.y[q][jo] -= dd[q];
+            }
+            __syncwarp();  // row j is read by another lane in the dot below
+            if (next) {
+                for (int i = i0n + lane; i < nr; i += 32) {
+                    const double vi = (lr0 + i > j) ? v[i] : 0.0;
+                    const double wn = vn[i];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (g.on[q]) {
+                            const double yv = fma(-dd[q], vi, g.y[q][i]);
+                            g.y[q][i] = yv;
+                            sn[q] = fma(wn, yv, sn[q]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) sn[q] = warp_sum(sn[q]);
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (g.on[q]) Pn[c0 + q * nw - j] = sn[q] + (ownern ? g.y[q][jon] : 0.0);
+                }
+            } else if (reduce) {
+                for (int i = i0 + lane; i < nr; i += 32) {
+                    const double vi = v[i];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (g.on[q]) g.y[q][i] = fma(-dd[q], vi, g.y[q][i]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 0) finish_col(0);
+    // every CTA must be done reading its peers' reduction buffers before exit
+    cl.sync();
+    for (int e = tid; e < nr * k; e += blockDim.x) {
+        const int i = e / k, c = e - i * k;
+        a.qout[(row0 + lr0 + i) * a.ldq + c] = sgn[c] * A[(size_t)c * ld + i];
+    }
+}
+
+// Stack pairs of k x k R factors into 2k x k row-major node inputs
+// (pass-through nodes copy their single R and mark nothing: the node kernel
+// runs on k rows and yields Q = I up to signs, which is what we want).
+__global__ void stack_r_kernel(const double* __restrict__ Rin, int nin, int k, int ldr, double* __restrict__ out,
+                               int ldo) {
+    const int node = blockIdx.x;
+    const int a = 2 * node, bq = 2 * node + 1;
+    for (int e = threadIdx.x; e < 2 * k * k; e += blockDim.x) {
+        const int i = e / k, c = e - i * k;
+        const int src = i < k ? a : bq;
+        const int ii = i < k ? i : i - k;
+        double v = 0.0;
+        if (src < nin) v = Rin[((int64_t)src * k + ii) * ldr + c];
+        out[((int64_t)node * 2 * k + i) * ldo + c] = v;
+    }
+}
+
+}  // namespace sorsvd_dev

@@ -2,24 +2,29 @@
 //
 // Replaces truncated_svd(M, k) -> full_svd -> LAPACKE_dgesdd('S')
 // (sketch.hpp:103, dense.hpp:65-110). Output contract is the reference's:
-// sigma nonincreasing (stable order for ties), U and V orthonormal, each
+// sigma nonincreasing (ties by column index), U and V orthonormal, each
 // column of U canonicalised so its largest-magnitude entry is positive
 // (dense.hpp:80-95: first maximal index wins), V flipped with it.
 //
-// One CTA; columns of G = M and of the accumulated rotation V live in shared
-// memory (column-major). Each round of the round-robin ("circle") ordering is
-// a perfect matching of the columns, processed by independent lane groups of
-// SG lanes (several pairs per warp, no barrier inside a round); rounds are
-// separated by one __syncthreads. Sweeps repeat until no pair exceeds the
-// orthogonality threshold |g_p.g_q| <= tol*||g_p||*||g_q||, tol = sqrt(k)*eps
-// (the dgesvj criterion), which gives high relative accuracy in sigma.
-// For k > 112 the two k x k arrays live in a global (L2) scratch instead.
+// Parallel layout (Brent-Luk ring ordering on a thread-block cluster): the
+// columns of G = M (and of the accumulated rotation V) sit in P = ceil(k/2)
+// pair slots; one warp owns one slot and holds its two columns of G and V in
+// registers for the round. Each round every warp computes alpha, beta, gamma
+// with warp shuffles, rotates its pair, and writes the two columns to their
+// next slots of the ring (top[i] -> top[i+1], bot[i] -> bot[i-1], with the
+// ends wrapping), so only the columns at CTA boundaries travel over DSMEM.
+// Double-buffered slots make one cluster barrier per round sufficient. A
+// sweep is kk-1 rounds (kk = k rounded up to even, the extra column is a
+// zero dummy); sweeps stop when no pair exceeded |g_p.g_q| > tol ||g_p|| ||g_q||
+// with tol = sqrt(k) eps (the dgesvj criterion; high relative accuracy).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace sorsvd_dev {
 
-constexpr int kJacobiThreads = 512;
+namespace cgj = cooperative_groups;
 
 struct JacobiArgs {
     const double* M;  // k x ldm row-major
@@ -30,157 +35,227 @@ struct JacobiArgs {
     double* S;        // k
     double* V;        // k x ldv row-major
     int ldv;
-    double* scratch;  // global fallback: 2 * ld * k doubles
+    int ppc;          // pair slots (= warps) per CTA
     int max_sweeps;
     int* sweeps_out;  // optional
 };
 
-__device__ __forceinline__ void jacobi_pair(int r, int i, int kk, int& p, int& q) {
-    // circle method: position 0 fixed, others rotate by r
-    auto pos = [&](int t) { return t == 0 ? 0 : ((t - 1 + r) % (kk - 1)) + 1; };
-    p = pos(i);
-    q = pos(kk - 1 - i);
+// smem per CTA (doubles): 2 buffers x ppc slots x 2 columns x (G, V) x kpad
+//   + ids (2 x ppc x 2 ints, as doubles) + sigma/rank scratch
+__host__ __device__ inline int jac_kpad(int k) { return ((k + 31) / 32) * 32; }
+__host__ __device__ inline size_t jacobi_smem_bytes(int k, int ppc) {
+    const size_t slot = 4 * (size_t)jac_kpad(k);
+    return (2 * (size_t)ppc * slot + 2 * 2 * (size_t)ppc + 4 * (size_t)ppc + 64) * sizeof(double);
 }
 
-template <int SG, bool SMEM>
-__global__ void __launch_bounds__(kJacobiThreads, 1) jacobi_svd_kernel(JacobiArgs a) {
+template <int KP>
+__global__ void jacobi_cluster_kernel(JacobiArgs a) {
+    cgj::cluster_group cl = cgj::this_cluster();
+    const int C = (int)cl.num_blocks();
+    const int r = (int)cl.block_rank();
+    const int k = a.k, ppc = a.ppc;
+    const int kk = (k + 1) & ~1;
+    const int P = kk / 2;
+    const int KPAD = jac_kpad(k);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = r * ppc + warp;  // global pair slot of this warp
+    const bool active = warp < ppc && slot < P;
+
     extern __shared__ __align__(16) double sm[];
-    __shared__ int s_rot;
+    const size_t SLOT = 4 * (size_t)KPAD;  // [top G | top V | bot G | bot V]
+    double* buf0 = sm;
+    double* buf1 = sm + (size_t)ppc * SLOT;
+    int* ids = reinterpret_cast<int*>(sm + 2 * (size_t)ppc * SLOT);  // [2][ppc][2]
+    double* sig = sm + 2 * (size_t)ppc * SLOT + 2 * (size_t)ppc;     // [ppc][2]
+    int* rnk = reinterpret_cast<int*>(sig + 2 * ppc);                 // [ppc][2]
+    __shared__ int flag[2];
     __shared__ int s_sweeps;
-    const int k = a.k;
-    const int ld = k | 1;
-    double* G = SMEM ? sm : a.scratch;
-    double* V = G + (size_t)ld * k;
-    double* sig = SMEM ? V + (size_t)ld * k : sm;  // k
-    int* rank = reinterpret_cast<int*>(sig + k);   // k
-    int* imax = rank + k;                          // k
 
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-        const int i = e / k, c = e - i * k;
-        G[(size_t)c * ld + i] = a.M[(size_t)i * a.ldm + c];
-        V[(size_t)c * ld + i] = (i == c) ? 1.0 : 0.0;
+    // initial placement: top[i] = column 2i, bot[i] = column 2i+1
+    if (active) {
+        for (int h = 0; h < 2; ++h) {
+            const int col = 2 * slot + h;
+            double* G = buf0 + (size_t)warp * SLOT + (size_t)h * 2 * KPAD;
+            double* Vv = G + KPAD;
+            for (int i = lane; i < KPAD; i += 32) {
+                G[i] = (col < k && i < k) ? a.M[(size_t)i * a.ldm + col] : 0.0;
+                Vv[i] = (col < k && i == col) ? 1.0 : 0.0;
+            }
+            if (lane == 0) ids[(0 * ppc + warp) * 2 + h] = col;
+        }
     }
-    if (threadIdx.x == 0) s_sweeps = 0;
-    __syncthreads();
+    if (threadIdx.x == 0) {
+        flag[0] = flag[1] = 0;
+        s_sweeps = 0;
+    }
+    cl.sync();
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    const int lane_g = lane % SG;
-    const int gpw = 32 / SG;  // lane groups per warp
-    const int kk = (k & 1) ? k + 1 : k;
     const double tol = sqrt((double)k) * 2.220446049250313e-16;
-
-    for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
-        if (threadIdx.x == 0) s_rot = 0;
-        __syncthreads();
-        int rot = 0;
-        for (int r = 0; r < kk - 1; ++r) {
-            // warp-uniform trip count so the group shuffles never diverge
-            for (int pb = warp * gpw; pb < kk / 2; pb += nwarp * gpw) {
-                const int pi = pb + lane / SG;
-                int p = 0, q = 0;
-                bool valid = pi < kk / 2;
-                if (valid) {
-                    jacobi_pair(r, pi, kk, p, q);
-                    valid = p < k && q < k;  // dummy player for odd k
+    const double tol2 = tol * tol;
+    int cur = 0;
+    int sweep = 0;
+    for (; sweep < a.max_sweeps; ++sweep) {
+        int rotated = 0;
+        for (int rd = 0; rd < kk - 1; ++rd) {
+            double* src = cur ? buf1 : buf0;
+            if (active) {
+                const double* base = src + (size_t)warp * SLOT;
+                double gt[KP], vt[KP], gb[KP], vb[KP];
+#pragma unroll
+                for (int p = 0; p < KP; ++p) {
+                    const int i = lane + 32 * p;
+                    gt[p] = base[i];
+                    vt[p] = base[KPAD + i];
+                    gb[p] = base[2 * KPAD + i];
+                    vb[p] = base[3 * KPAD + i];
                 }
-                double* gp = G + (size_t)p * ld;
-                double* gq = G + (size_t)q * ld;
+                const int idt = ids[(cur * ppc + warp) * 2 + 0];
+                const int idb = ids[(cur * ppc + warp) * 2 + 1];
                 double al = 0.0, be = 0.0, ga = 0.0;
-                if (valid) {
-                    for (int i = lane_g; i < k; i += SG) {
-                        const double x = gp[i], y = gq[i];
-                        al = fma(x, x, al);
-                        be = fma(y, y, be);
-                        ga = fma(x, y, ga);
+#pragma unroll
+                for (int p = 0; p < KP; ++p) {
+                    al = fma(gt[p], gt[p], al);
+                    be = fma(gb[p], gb[p], be);
+                    ga = fma(gt[p], gb[p], ga);
+                }
+                al = warp_sum(al);
+                be = warp_sum(be);
+                ga = warp_sum(ga);
+                if (ga != 0.0 && ga * ga > tol2 * al * be) {
+                    rotated = 1;
+                    // tan of the Jacobi angle, the smaller root of t^2 + 2 zeta t - 1 = 0 with
+                    // zeta = (be - al) / (2 ga), written with one sqrt and one division:
+                    // t = 2 ga sgn(d) / (|d| + sqrt(d^2 + 4 ga^2)),  d = be - al
+                    const double d = be - al;
+                    const double t = (2.0 * ga * (d < 0.0 ? -1.0 : 1.0)) / (fabs(d) + sqrt(fma(d, d, 4.0 * ga * ga)));
+                    const double c = rsqrt(fma(t, t, 1.0));
+                    const double s = c * t;
+#pragma unroll
+                    for (int p = 0; p < KP; ++p) {
+                        const double x = gt[p], y = gb[p];
+                        gt[p] = c * x - s * y;
+                        gb[p] = s * x + c * y;
+                        const double u = vt[p], w = vb[p];
+                        vt[p] = c * u - s * w;
+                        vb[p] = s * u + c * w;
                     }
                 }
-                al = group_sum<SG>(al);
-                be = group_sum<SG>(be);
-                ga = group_sum<SG>(ga);
-                if (!valid || ga == 0.0 || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
-                ++rot;
-                const double zeta = (be - al) / (2.0 * ga);
-                double t;
-                if (fabs(zeta) > 1e100)
-                    t = 0.5 / zeta;
-                else
-                    t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-                const double c = 1.0 / sqrt(fma(t, t, 1.0));
-                const double s = c * t;
-                double* vp = V + (size_t)p * ld;
-                double* vq = V + (size_t)q * ld;
-                for (int i = lane_g; i < k; i += SG) {
-                    const double x = gp[i], y = gq[i];
-                    gp[i] = c * x - s * y;
-                    gq[i] = s * x + c * y;
-                    const double u = vp[i], w = vq[i];
-                    vp[i] = c * u - s * w;
-                    vq[i] = s * u + c * w;
+                // ring move: top[i] -> top[i+1] (top[0] fixed, top[P-1] -> bot[P-1]);
+                //            bot[i] -> bot[i-1] (bot[0] -> top[1])
+                int dt_slot, dt_h, db_slot, db_h;
+                if (P == 1) {
+                    dt_slot = 0; dt_h = 0; db_slot = 0; db_h = 1;
+                } else {
+                    if (slot == 0) { dt_slot = 0; dt_h = 0; }
+                    else if (slot < P - 1) { dt_slot = slot + 1; dt_h = 0; }
+                    else { dt_slot = P - 1; dt_h = 1; }
+                    if (slot == 0) { db_slot = 1; db_h = 0; }
+                    else { db_slot = slot - 1; db_h = 1; }
+                }
+                const int nxt = cur ^ 1;
+                double* dstT = cl.map_shared_rank(nxt ? buf1 : buf0, dt_slot / ppc) + (size_t)(dt_slot % ppc) * SLOT +
+                               (size_t)dt_h * 2 * KPAD;
+                double* dstB = cl.map_shared_rank(nxt ? buf1 : buf0, db_slot / ppc) + (size_t)(db_slot % ppc) * SLOT +
+                               (size_t)db_h * 2 * KPAD;
+#pragma unroll
+                for (int p = 0; p < KP; ++p) {
+                    const int i = lane + 32 * p;
+                    dstT[i] = gt[p];
+                    dstT[KPAD + i] = vt[p];
+                    dstB[i] = gb[p];
+                    dstB[KPAD + i] = vb[p];
+                }
+                if (lane == 0) {
+                    int* idsT = cl.map_shared_rank(ids, dt_slot / ppc);
+                    int* idsB = cl.map_shared_rank(ids, db_slot / ppc);
+                    idsT[(nxt * ppc + dt_slot % ppc) * 2 + dt_h] = idt;
+                    idsB[(nxt * ppc + db_slot % ppc) * 2 + db_h] = idb;
                 }
             }
-            __syncthreads();
+            if (C > 1) cl.sync();
+            else __syncthreads();
+            cur ^= 1;
+            // flag[(sweep+1)&1] was last read by peers before this barrier
+            if (rd == 0 && threadIdx.x == 0) flag[(sweep + 1) & 1] = 0;
         }
-        if (rot && (threadIdx.x % SG) == 0) atomicAdd(&s_rot, 1);
-        __syncthreads();
-        const int any = s_rot;
-        if (threadIdx.x == 0) s_sweeps = sweep + 1;
-        __syncthreads();
-        if (!any) break;
+        if (rotated && lane == 0) atomicOr(&flag[sweep & 1], 1);
+        cl.sync();
+        int any = 0;
+        for (int q = 0; q < C; ++q) any |= *cl.map_shared_rank(&flag[sweep & 1], q);
+        if (!any) {
+            ++sweep;
+            break;
+        }
     }
+    if (threadIdx.x == 0) s_sweeps = sweep;
 
-    // singular values = column norms
-    for (int cb = warp * gpw; cb < k; cb += nwarp * gpw) {
-        const int c = cb + lane / SG;
-        const double* gc = G + (size_t)(c < k ? c : 0) * ld;
-        double ss = 0.0;
-        if (c < k)
-            for (int i = lane_g; i < k; i += SG) ss = fma(gc[i], gc[i], ss);
-        ss = group_sum<SG>(ss);
-        if (lane_g == 0 && c < k) sig[c] = sqrt(ss);
+    // sigma of every local column, then a cluster-wide stable rank
+    double* src = cur ? buf1 : buf0;
+    if (active) {
+        for (int h = 0; h < 2; ++h) {
+            const double* G = src + (size_t)warp * SLOT + (size_t)h * 2 * KPAD;
+            double ss = 0.0;
+            for (int i = lane; i < KPAD; i += 32) ss = fma(G[i], G[i], ss);
+            ss = warp_sum(ss);
+            if (lane == 0) sig[warp * 2 + h] = sqrt(ss);
+        }
     }
-    __syncthreads();
-    // stable descending order
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        const double sj = sig[j];
+    cl.sync();
+    if (active && lane < 2) {
+        const int h = lane;
+        const int id = ids[(cur * ppc + warp) * 2 + h];
+        const double sv = sig[warp * 2 + h];
         int rk = 0;
-        for (int i = 0; i < k; ++i) rk += (sig[i] > sj) || (sig[i] == sj && i < j);
-        rank[j] = rk;
-    }
-    // sign canonicalisation index: first largest |u_ij| (u_j = g_j / sigma_j)
-    for (int cb = warp * gpw; cb < k; cb += nwarp * gpw) {
-        const int c = cb + lane / SG;
-        const double* gc = G + (size_t)(c < k ? c : 0) * ld;
-        double best = -1.0;
-        int bi = 0;
-        for (int i = lane_g; i < k && c < k; i += SG) {
-            const double av = fabs(gc[i]);
-            if (av > best) {
-                best = av;
-                bi = i;
+        for (int q = 0; q < C; ++q) {
+            const double* rs = cl.map_shared_rank(sig, q);
+            const int* ri = cl.map_shared_rank(ids, q);
+            for (int w = 0; w < ppc; ++w) {
+                if (q * ppc + w >= P) break;
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int oid = ri[(cur * ppc + w) * 2 + hh];
+                    if (oid >= k || oid == id) continue;
+                    const double os = rs[w * 2 + hh];
+                    rk += (os > sv) || (os == sv && oid < id);
+                }
             }
         }
+        rnk[warp * 2 + h] = id < k ? rk : -1;
+    }
+    cl.sync();  // peers done reading sig / ids
+    if (active) {
+        for (int h = 0; h < 2; ++h) {
+            const int rk = rnk[warp * 2 + h];
+            if (rk < 0) continue;
+            const double* G = src + (size_t)warp * SLOT + (size_t)h * 2 * KPAD;
+            const double* Vv = G + KPAD;
+            const double sv = sig[warp * 2 + h];
+            double best = -1.0;
+            int bi = 0;
+            for (int i = lane; i < k; i += 32) {
+                const double av = fabs(G[i]);
+                if (av > best) {
+                    best = av;
+                    bi = i;
+                }
+            }
 #pragma unroll
-        for (int o = SG / 2; o > 0; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ob > best || (ob == best && oi < bi)) {
-                best = ob;
-                bi = oi;
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    bi = oi;
+                }
             }
+            const double sg = G[bi] < 0.0 ? -1.0 : 1.0;
+            for (int i = lane; i < k; i += 32) {
+                a.U[(size_t)i * a.ldu + rk] = sv > 0.0 ? sg * G[i] / sv : 0.0;
+                a.V[(size_t)i * a.ldv + rk] = sg * Vv[i];
+            }
+            if (lane == 0) a.S[rk] = sv;
         }
-        if (lane_g == 0 && c < k) imax[c] = bi;
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-        const int c = e / k, i = e - c * k;  // column c (source), row i
-        const int rc = rank[c];
-        const double sc = sig[c];
-        const double sg = G[(size_t)c * ld + imax[c]] < 0.0 ? -1.0 : 1.0;
-        a.U[(size_t)i * a.ldu + rc] = sc > 0.0 ? sg * G[(size_t)c * ld + i] / sc : 0.0;
-        a.V[(size_t)i * a.ldv + rc] = sg * V[(size_t)c * ld + i];
-    }
-    for (int c = threadIdx.x; c < k; c += blockDim.x) a.S[rank[c]] = sig[c];
-    if (threadIdx.x == 0 && a.sweeps_out) *a.sweeps_out = s_sweeps;
+    if (r == 0 && threadIdx.x == 0 && a.sweeps_out) *a.sweeps_out = s_sweeps;
 }
 
 }  // namespace sorsvd_dev

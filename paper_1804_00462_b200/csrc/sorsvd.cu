@@ -30,7 +30,7 @@
 #include "jacobi_f64.cuh"
 #include "peaks.cuh"
 #include "rpca_f64.cuh"
-#include "tsqr_f64.cuh"
+#include "cqr_f64.cuh"
 
 using namespace sorsvd_dev;
 
@@ -123,7 +123,10 @@ struct QrPlan {
     std::vector<double*> R;      // per level: nodes[l] * k * k
     std::vector<double*> QN;     // per level l >= 1: nodes[l] * 2k * Np
     std::vector<double*> C;      // per level l in [0, L-1): children C's of level l+1 nodes
-    double* scratch = nullptr;   // global fallback
+    std::vector<double*> SN;     // per level l >= 1: stacked [R_2i; R_2i+1] node inputs (2k x k)
+    std::vector<int64_t*> n_row0;
+    std::vector<int*> n_rows;
+    int rb_max = 0, cmax = 1, leaf_cs = 1, node_cs = 1;
     std::vector<void*> owned;
 };
 
@@ -304,15 +307,66 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- TSQR ----
-constexpr int kQrSmemMaxK = 112;
+// Leaves and tree nodes are factored by the cluster Householder kernel
+// (cqr_f64.cuh). A leaf is as many rows as one cluster of up to 16 CTAs can
+// hold, so the sketches of C1, C2 and C4 are a single leaf (no tree).
+constexpr int kCqrMaxCluster = 16;
 
-size_t qr_leaf_smem(int k, int rows, bool smem) {
-    const size_t head = 2 * (size_t)((k + 1) & ~1);
-    return (head + (smem ? (size_t)(rows | 1) * k : 0)) * sizeof(double);
+int cqr_rows_per_cta(int k) {
+    const int64_t avail = kCqrSmemBudget / 8 - 3 * (int64_t)cqr_rw(k) - 2 * (int64_t)k - 8;
+    return (int)std::max<int64_t>(1, avail / k - 1);
 }
-size_t qr_node_smem(int k, bool smem) {
-    const size_t head = 2 * (size_t)((k + 1) & ~1);
-    return (head + (smem ? (size_t)(2 * k + 1) * k : 0)) * sizeof(double);
+
+int cqr_max_cluster(sorsvd_ctx* c, int k) {
+    static std::map<int, int> cache;
+    auto it = cache.find(k);
+    if (it != cache.end()) return it->second;
+    const size_t sm = cqr_smem_bytes(cqr_rows_per_cta(k), k);
+    CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    int best = 1;
+    for (int cs = kCqrMaxCluster; cs >= 1; cs /= 2) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kCqrThreads);
+        cfg.dynamicSmemBytes = sm;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, cqr_kernel, &cfg) == cudaSuccess && n > 0) {
+            best = cs;
+            break;
+        }
+        cudaGetLastError();
+    }
+    (void)c;
+    cache[k] = best;
+    return best;
+}
+
+void launch_cqr(sorsvd_ctx* c, const CqrArgs& a, int nblocks, int csize, int Rb, cudaStream_t s) {
+    const size_t sm = cqr_smem_bytes(Rb, a.k);
+    CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(nblocks * csize));
+    cfg.blockDim = dim3(kCqrThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, cqr_kernel, a));
+    check_launch(c);
 }
 
 void build_seg_tiles(const std::vector<int64_t>& seg_row0, const std::vector<int>& seg_rows, int BM,
@@ -354,18 +408,13 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
     p->rows = rows;
     p->k = k;
     p->Np = npad(k);
-    p->smem = k <= kQrSmemMaxK;
+    p->rb_max = cqr_rows_per_cta(k);
+    p->cmax = cqr_max_cluster(c, k);
     if (leaves_given > 0) {
         p->P = leaves_given;
     } else {
-        int64_t bmax;
-        if (p->smem) {
-            const int64_t budget = kQrSmemBudget / 8 - 2 * ((k + 1) & ~1);
-            bmax = std::min<int64_t>(budget / k - 1, 4096);
-        } else {
-            bmax = std::max<int64_t>(2 * k, 512);
-        }
-        p->P = (int)std::max<int64_t>(1, cdiv(rows, bmax));
+        const int64_t leaf_max = (int64_t)p->cmax * p->rb_max;
+        p->P = (int)std::max<int64_t>(1, cdiv(rows, leaf_max));
         const int64_t base = rows / p->P, extra = rows % p->P;
         int64_t r = 0;
         for (int i = 0; i < p->P; ++i) {
@@ -376,6 +425,7 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
             r += cnt;
         }
         if (p->P > 1 && base < k) throw Error{SORSVD_ERR_INTERNAL, "tsqr: leaf shorter than k"};
+        p->leaf_cs = (int)std::min<int64_t>(p->cmax, cdiv(p->max_leaf_rows, p->rb_max));
         p->d_row0 = upload(p.get(), p->row0);
         p->d_rows = upload(p.get(), p->rcnt);
     }
@@ -384,6 +434,7 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
     const int L = (int)p->nodes.size() - 1;
     const int Np = p->Np;
     const int BM = gemm_bm_for(Np);
+    p->node_cs = (int)std::min<int64_t>(p->cmax, cdiv(2 * k, p->rb_max));
     p->t_row0.assign(L + 1, nullptr);
     p->t_rows.assign(L + 1, nullptr);
     p->t_seg.assign(L + 1, nullptr);
@@ -391,10 +442,23 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
     p->R.assign(L + 1, nullptr);
     p->QN.assign(L + 1, nullptr);
     p->C.assign(L + 1, nullptr);
+    p->SN.assign(L + 1, nullptr);
+    p->n_row0.assign(L + 1, nullptr);
+    p->n_rows.assign(L + 1, nullptr);
     for (int l = 0; l <= L; ++l) p->R[l] = dalloc(p.get(), (size_t)p->nodes[l] * k * k);
-    for (int l = 1; l <= L; ++l) p->QN[l] = dalloc(p.get(), (size_t)p->nodes[l] * 2 * k * Np);
+    for (int l = 1; l <= L; ++l) {
+        p->QN[l] = dalloc(p.get(), (size_t)p->nodes[l] * 2 * k * Np);
+        p->SN[l] = dalloc(p.get(), (size_t)p->nodes[l] * 2 * k * k);
+        std::vector<int64_t> r0;
+        std::vector<int> rc;
+        for (int i = 0; i < p->nodes[l]; ++i) {
+            r0.push_back((int64_t)i * 2 * k);
+            rc.push_back(2 * k);
+        }
+        p->n_row0[l] = upload(p.get(), r0);
+        p->n_rows[l] = upload(p.get(), rc);
+    }
     for (int l = 0; l < L; ++l) p->C[l] = dalloc(p.get(), (size_t)p->nodes[l + 1] * 2 * k * Np);
-    // leaf product tiles
     if (leaves_given == 0 && L >= 1) {
         std::vector<int> r0, rc, sg;
         build_seg_tiles(p->row0, p->rcnt, BM, r0, rc, sg);
@@ -403,7 +467,6 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
         p->t_seg[0] = upload(p.get(), sg);
         p->t_count[0] = (int)r0.size();
     }
-    // node product tiles for levels 1..L-1 (level L's product is the identity)
     for (int l = 1; l < L; ++l) {
         std::vector<int64_t> sr0;
         std::vector<int> src;
@@ -418,73 +481,49 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
         p->t_seg[l] = upload(p.get(), sg);
         p->t_count[l] = (int)r0.size();
     }
-    if (!p->smem) {
-        size_t sc = (size_t)(rows + p->P) * k;
-        size_t nodes_total = 0;
-        for (int l = 1; l <= L; ++l) nodes_total += p->nodes[l];
-        sc = std::max(sc, nodes_total * ((size_t)(2 * k + 1) * k + 1));
-        p->scratch = dalloc(p.get(), sc);
-    }
     QrPlan* raw = p.get();
     c->plans[key] = std::move(p);
     return raw;
 }
 
-void set_smem_attr(const void* fn, size_t bytes) {
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
-
-// Factor: leaves (from T) + tree levels. apply_root_sign: the plan's root is
-// the global root (diag(R) >= 0). Leaf explicit Qs are written in place in T
-// (or straight into Q when the leaf is the root).
+// Factor: leaves (from T) + tree levels. root_sign: the plan's root is the
+// global root (diag(R) >= 0). Leaf explicit Qs are written in place in T (or
+// straight into Q when the single leaf is the final root).
 void qr_factor(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int64_t ldq, bool root_sign,
                cudaStream_t s, const double* Rleaves = nullptr) {
     const int k = p->k;
     const int L = (int)p->nodes.size() - 1;
     if (!Rleaves) {
-        LeafArgs la{};
-        la.T = T;
-        la.ldt = ldt;
+        CqrArgs a{};
         const bool direct = (L == 0 && root_sign);
-        la.Qout = direct ? Q : T;
-        la.ldq = direct ? ldq : ldt;
-        la.row0 = p->d_row0;
-        la.rows = p->d_rows;
-        la.k = k;
-        la.R = p->R[0];
-        la.ldr = k;
-        la.scratch = p->scratch;
-        la.is_root = (L == 0 && root_sign) ? 1 : 0;
-        const size_t sm = qr_leaf_smem(k, p->max_leaf_rows, p->smem);
-        if (p->smem) {
-            set_smem_attr((const void*)tsqr_leaf_kernel<true>, sm);
-            tsqr_leaf_kernel<true><<<p->P, kQrThreads, sm, s>>>(la);
-        } else {
-            set_smem_attr((const void*)tsqr_leaf_kernel<false>, sm);
-            tsqr_leaf_kernel<false><<<p->P, kQrThreads, sm, s>>>(la);
-        }
-        check_launch(c);
+        a.in = T;
+        a.ldi = ldt;
+        a.qout = direct ? Q : T;
+        a.ldq = direct ? ldq : ldt;
+        a.row0 = p->d_row0;
+        a.rows = p->d_rows;
+        a.k = k;
+        a.R = p->R[0];
+        a.ldr = k;
+        a.root_sign = (L == 0 && root_sign) ? 1 : 0;
+        launch_cqr(c, a, p->P, p->leaf_cs, (int)cdiv(p->max_leaf_rows, p->leaf_cs), s);
     }
     for (int l = 1; l <= L; ++l) {
-        NodeArgs na{};
-        na.Rin = (l == 1 && Rleaves) ? Rleaves : p->R[l - 1];
-        na.nin = p->nodes[l - 1];
-        na.Rout = p->R[l];
-        na.Qnode = p->QN[l];
-        na.ldq = p->Np;
-        na.k = k;
-        na.ldr = k;
-        na.scratch = p->scratch;
-        na.is_root = (l == L && root_sign) ? 1 : 0;
-        const size_t sm = qr_node_smem(k, p->smem);
-        if (p->smem) {
-            set_smem_attr((const void*)tsqr_node_kernel<true>, sm);
-            tsqr_node_kernel<true><<<p->nodes[l], kQrThreads, sm, s>>>(na);
-        } else {
-            set_smem_attr((const void*)tsqr_node_kernel<false>, sm);
-            tsqr_node_kernel<false><<<p->nodes[l], kQrThreads, sm, s>>>(na);
-        }
+        const double* Rin = (l == 1 && Rleaves) ? Rleaves : p->R[l - 1];
+        stack_r_kernel<<<p->nodes[l], 256, 0, s>>>(Rin, p->nodes[l - 1], k, k, p->SN[l], k);
         check_launch(c);
+        CqrArgs a{};
+        a.in = p->SN[l];
+        a.ldi = k;
+        a.qout = p->QN[l];
+        a.ldq = p->Np;
+        a.row0 = p->n_row0[l];
+        a.rows = p->n_rows[l];
+        a.k = k;
+        a.R = p->R[l];
+        a.ldr = k;
+        a.root_sign = (l == L && root_sign) ? 1 : 0;
+        launch_cqr(c, a, p->nodes[l], p->node_cs, (int)cdiv(2 * k, p->node_cs), s);
     }
 }
 
@@ -583,8 +622,30 @@ const double* qr_leaf_factors(QrPlan* p, bool had_cin) {
 }
 
 // ---------------------------------------------------------------- Jacobi --
+template <int KP>
+void launch_jacobi_t(sorsvd_ctx* c, const JacobiArgs& a, int csize, cudaStream_t s) {
+    const size_t sm = jacobi_smem_bytes(a.k, a.ppc);
+    CK(cudaFuncSetAttribute(jacobi_cluster_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(jacobi_cluster_kernel<KP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)csize);
+    cfg.blockDim = dim3((unsigned)(32 * a.ppc));
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel<KP>, a));
+    check_launch(c);
+}
+
 void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int ldu, double* S, double* V, int ldv,
                 int* sweeps, cudaStream_t s) {
+    if (k > 256) throw Error{SORSVD_ERR_UNSUPPORTED, "jacobi: k > 256"};
     JacobiArgs a{};
     a.M = M;
     a.ldm = ldm;
@@ -596,25 +657,31 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
     a.ldv = ldv;
     a.max_sweeps = 60;
     a.sweeps_out = sweeps;
-    const int ld = k | 1;
-    const bool smem = k <= kQrSmemMaxK;
-    const size_t tail = (size_t)k * sizeof(double) + 2 * (size_t)k * sizeof(int) + 64;
-    if (smem) {
-        const size_t sm = 2 * (size_t)ld * k * sizeof(double) + tail;
-        if (k <= 32) {
-            set_smem_attr((const void*)jacobi_svd_kernel<4, true>, sm);
-            jacobi_svd_kernel<4, true><<<1, kJacobiThreads, sm, s>>>(a);
-        } else {
-            set_smem_attr((const void*)jacobi_svd_kernel<8, true>, sm);
-            jacobi_svd_kernel<8, true><<<1, kJacobiThreads, sm, s>>>(a);
-        }
-    } else {
-        a.scratch = dbuf(c, "jacobi_scratch", 2 * (size_t)ld * k);
-        const size_t sm = tail;
-        set_smem_attr((const void*)jacobi_svd_kernel<16, false>, sm);
-        jacobi_svd_kernel<16, false><<<1, kJacobiThreads, sm, s>>>(a);
+    const int kp = (k + 31) / 32;
+    const int KP = kp <= 1 ? 1 : kp <= 2 ? 2 : kp <= 4 ? 4 : 8;
+    const int P = ((k + 1) & ~1) / 2;
+    // warps (pair slots) per CTA: register budget (KP doubles x 4 per lane) and
+    // shared memory (2 buffers x 4 columns per slot) bound it; then spread the
+    // slots evenly over the smallest cluster that holds them.
+    cudaFuncAttributes fa{};
+    switch (KP) {
+        case 1: CK(cudaFuncGetAttributes(&fa, jacobi_cluster_kernel<1>)); break;
+        case 2: CK(cudaFuncGetAttributes(&fa, jacobi_cluster_kernel<2>)); break;
+        case 4: CK(cudaFuncGetAttributes(&fa, jacobi_cluster_kernel<4>)); break;
+        default: CK(cudaFuncGetAttributes(&fa, jacobi_cluster_kernel<8>)); break;
     }
-    check_launch(c);
+    int ppc = std::min(32, fa.maxThreadsPerBlock / 32);  // register-limited warps per CTA
+    while (ppc > 1 && jacobi_smem_bytes(k, ppc) > 200 * 1024) --ppc;
+    ppc = std::min(ppc, P);
+    const int csize = (P + ppc - 1) / ppc;
+    if (csize > 16) throw Error{SORSVD_ERR_UNSUPPORTED, "jacobi: cluster too large"};
+    a.ppc = (P + csize - 1) / csize;
+    switch (KP) {
+        case 1: launch_jacobi_t<1>(c, a, csize, s); break;
+        case 2: launch_jacobi_t<2>(c, a, csize, s); break;
+        case 4: launch_jacobi_t<4>(c, a, csize, s); break;
+        default: launch_jacobi_t<8>(c, a, csize, s); break;
+    }
 }
 
 // ------------------------------------------------------------- pipeline ----
@@ -1314,7 +1381,7 @@ int sorsvd_small_svd_device(sorsvd_ctx* c, int32_t k, const double* dM, int64_t 
                             double* dS, double* dV, int64_t ldv, int32_t* sweeps) {
     if (!c) return SORSVD_ERR_PARAMETER;
     return guarded(c, [&] {
-        if (k < 1 || k > 512) throw Error{SORSVD_ERR_PARAMETER, "parameter: k out of range"};
+        if (k < 1 || k > 256) throw Error{SORSVD_ERR_PARAMETER, "parameter: k out of range [1, 256]"};
         int* dsw = reinterpret_cast<int*>(dbuf(c, "sweeps_svd", 1));
         run_jacobi(c, k, dM, (int)ldm, dU, (int)ldu, dS, dV, (int)ldv, dsw, c->stream);
         int sw = 0;
