@@ -1,0 +1,67 @@
+// TEST: the drop-in C++ front end (include/sorsvd_b200.hpp) used exactly as a
+// reference caller would, on the reference's own types, next to the
+// reference's CPU sor_svd_power. Built by tests/cpp/Makefile against the
+// unmodified reference headers (needs /root/reference at build time only).
+#include <sorsvd/matrixgen.hpp>
+#include <sorsvd/sketch.hpp>
+
+#include "sorsvd_b200.hpp"
+
+#include <cmath>
+#include <cstdio>
+
+using namespace sorsvd;
+
+static double max_rel(const std::vector<double>& a, const std::vector<double>& b) {
+    double m = 0;
+    for (size_t i = 0; i < a.size(); ++i) m = std::max(m, std::fabs(a[i] - b[i]) / std::fabs(b[i]));
+    return m;
+}
+
+int main() {
+    int fails = 0;
+    // Config 1 shape (BASELINE.json configs[0]): A = X Y^T + 1e-2 E
+    Matrix x = gaussian_matrix(1000, 20, sub_seed(1, 1));
+    Matrix y = gaussian_matrix(1000, 20, sub_seed(1, 2));
+    Matrix a = matmul(x, y, Trans::none, Trans::transpose) + 1e-2 * gaussian_matrix(1000, 1000, sub_seed(1, 3));
+    SketchConfig cfg;
+    cfg.ell = 20;
+    cfg.q = 0;
+    cfg.seed = 7;
+    LowRankApprox ref = sor_svd_power(a, 20, cfg);
+    LowRankApprox gpu = cuda::sor_svd_power(a, 20, cfg);
+    const double es = max_rel(gpu.sigma, ref.sigma);
+    const double ea = std::sqrt(std::pow(norm(a - reconstruct(gpu), NormKind::frobenius), 2)) /
+                      norm(a, NormKind::frobenius);
+    const double er = norm(a - reconstruct(ref), NormKind::frobenius) / norm(a, NormKind::frobenius);
+    std::printf("C1 sigma max rel err %.3e, approx err gpu %.6e ref %.6e, passes %d/%d, method %s/%s\n", es, ea, er,
+                gpu.passes, ref.passes, to_string(gpu.method), to_string(ref.method));
+    fails += !(es <= 1e-10) + (gpu.passes != ref.passes) + (gpu.method != ref.method) +
+             !(std::fabs(ea - er) <= 1e-9 * er + 1e-12);
+    // power form on a polynomial-decay matrix (matrixgen.hpp:80)
+    Matrix p = gen_polydecay(300, 5);
+    cfg.ell = 12;
+    cfg.q = 2;
+    cfg.seed = 3;
+    LowRankApprox r2 = sor_svd_power(p, 10, cfg), g2 = cuda::sor_svd_power(p, 10, cfg);
+    std::printf("polydecay sigma max rel err %.3e\n", max_rel(g2.sigma, r2.sigma));
+    fails += !(max_rel(g2.sigma, r2.sigma) <= 1e-8);
+    // error behaviour mirrors the reference exceptions
+    try {
+        cfg.ell = 400;
+        cuda::sor_svd_power(p, 10, cfg);
+        ++fails;
+    } catch (const parameter_error& e) {
+        std::printf("parameter_error: %s\n", e.what());
+    }
+    try {
+        cfg.ell = 12;
+        cfg.q = 1;
+        cuda::sor_svd(p, 10, cfg);
+        ++fails;
+    } catch (const parameter_error& e) {
+        std::printf("parameter_error: %s\n", e.what());
+    }
+    std::printf(fails ? "FAIL (%d)\n" : "OK\n", fails);
+    return fails ? 1 : 0;
+}
