@@ -40,6 +40,8 @@ struct CqrArgs {
     double* R;            // per block k x ldr (row-major), zeros below the diagonal
     int ldr;
     int root_sign;        // apply diag(R) >= 0 (dense.hpp:127-132)
+    const int* pred;      // optional: no-op when *pred == pred_skip (CholeskyQR2 accepted)
+    int pred_skip;
 };
 
 // shared-memory layout (doubles): A[ld*k] | red[2*RW] | S[RW] | tau[k] | sgn[k]
@@ -66,6 +68,7 @@ struct ColGroup {
 };
 
 __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
+    if (a.pred && *a.pred == a.pred_skip) return;  // uniform over the cluster
     cg::cluster_group cl = cg::this_cluster();
     const int C = (int)cl.num_blocks();
     const int r = (int)cl.block_rank();
@@ -361,7 +364,8 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
 // (pass-through nodes copy their single R and mark nothing: the node kernel
 // runs on k rows and yields Q = I up to signs, which is what we want).
 __global__ void stack_r_kernel(const double* __restrict__ Rin, int nin, int k, int ldr, double* __restrict__ out,
-                               int ldo) {
+                               int ldo, const int* pred, int pred_skip) {
+    if (pred && *pred == pred_skip) return;
     const int node = blockIdx.x;
     const int a = 2 * node, bq = 2 * node + 1;
     for (int e = threadIdx.x; e < 2 * k * k; e += blockDim.x) {

@@ -37,6 +37,8 @@ struct GemmArgs {
     const int* tile_rows;
     const int* tile_seg;
     double alpha;
+    const int* pred;  // optional device flag: the launch is a no-op when *pred == pred_skip
+    int pred_skip;
 };
 
 constexpr int kGemmThreads = 256;
@@ -59,6 +61,7 @@ struct GemmShape {
 template <int FM, int FN, bool TA, bool V16>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
     using S = GemmShape<FM, FN, TA>;
+    if (p.pred && *p.pred == p.pred_skip) return;
     extern __shared__ __align__(128) double smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
 
@@ -192,7 +195,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
 
 // out[i] = sum_{s<S} ws[s*stride + i], fixed summation order (deterministic).
 __global__ void reduce_splits_kernel(const double* __restrict__ ws, int64_t count2, int S, int64_t stride,
-                                     double* __restrict__ out) {
+                                     double* __restrict__ out, const int* pred, int pred_skip) {
+    if (pred && *pred == pred_skip) return;
     const int64_t n2 = count2;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
         double2 acc = reinterpret_cast<const double2*>(ws)[i];

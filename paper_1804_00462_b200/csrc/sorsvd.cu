@@ -30,6 +30,7 @@
 #include "jacobi_f64.cuh"
 #include "peaks.cuh"
 #include "rpca_f64.cuh"
+#include "cholqr_f64.cuh"
 #include "cqr_f64.cuh"
 
 using namespace sorsvd_dev;
@@ -127,6 +128,11 @@ struct QrPlan {
     std::vector<int64_t*> n_row0;
     std::vector<int*> n_rows;
     int rb_max = 0, cmax = 1, leaf_cs = 1, node_cs = 1;
+    // CholeskyQR2 fast path
+    double *G1 = nullptr, *G2 = nullptr, *Ri1 = nullptr, *Ri2 = nullptr, *R1 = nullptr, *Qtmp = nullptr,
+           *cwork = nullptr;
+    int* flag = nullptr;
+    std::string ws_name;  // per-plan split-K workspace (the two sketches' QRs run concurrently)
     std::vector<void*> owned;
 };
 
@@ -153,6 +159,8 @@ struct sorsvd_ctx {
     int launches = 0;
     bool capturing = false;
     std::vector<double> host_omega;
+    const int* pred = nullptr;  // predication of every launch (CholeskyQR2 vs Householder)
+    int pred_skip = 0;
 };
 
 namespace {
@@ -272,6 +280,8 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
     a.tile_row0 = g.tile_row0;
     a.tile_rows = g.tile_rows;
     a.tile_seg = g.tile_seg;
+    a.pred = c->pred;
+    a.pred_skip = c->pred_skip;
     const int64_t kchunk = cdiv(cdiv(g.K, S), kGemmBK) * kGemmBK;
     a.k_chunk = std::max<int64_t>(kchunk, kGemmBK);
     double* ws = nullptr;
@@ -301,7 +311,7 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         if (g.ldc % 2) throw Error{SORSVD_ERR_INTERNAL, "gemm: odd ldc with splits"};
         const int64_t count2 = g.M * g.ldc / 2;
         const int blocks = (int)std::min<int64_t>(cdiv(count2, 256), (int64_t)c->num_sms * 8);
-        reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, g.M * g.ldc, g.C);
+        reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, g.M * g.ldc, g.C, c->pred, c->pred_skip);
         check_launch(c);
     }
 }
@@ -349,7 +359,10 @@ int cqr_max_cluster(sorsvd_ctx* c, int k) {
     return best;
 }
 
-void launch_cqr(sorsvd_ctx* c, const CqrArgs& a, int nblocks, int csize, int Rb, cudaStream_t s) {
+void launch_cqr(sorsvd_ctx* c, const CqrArgs& a0, int nblocks, int csize, int Rb, cudaStream_t s) {
+    CqrArgs a = a0;
+    a.pred = c->pred;
+    a.pred_skip = c->pred_skip;
     const size_t sm = cqr_smem_bytes(Rb, a.k);
     CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -405,6 +418,7 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
     if (c->capturing) throw Error{SORSVD_ERR_INTERNAL, "qr plan creation during capture"};
     invalidate_graphs(c);
     auto p = std::make_unique<QrPlan>();
+    p->ws_name = "ws_" + key;
     p->rows = rows;
     p->k = k;
     p->Np = npad(k);
@@ -481,6 +495,16 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
         p->t_seg[l] = upload(p.get(), sg);
         p->t_count[l] = (int)r0.size();
     }
+    if (leaves_given == 0) {
+        p->G1 = dalloc(p.get(), (size_t)Np * Np);
+        p->G2 = dalloc(p.get(), (size_t)Np * Np);
+        p->Ri1 = dalloc(p.get(), (size_t)Np * Np);
+        p->Ri2 = dalloc(p.get(), (size_t)Np * Np);
+        p->R1 = dalloc(p.get(), (size_t)k * k);
+        p->cwork = dalloc(p.get(), (size_t)k * k);
+        p->Qtmp = dalloc(p.get(), (size_t)rows * Np);
+        p->flag = reinterpret_cast<int*>(dalloc(p.get(), 1));
+    }
     QrPlan* raw = p.get();
     c->plans[key] = std::move(p);
     return raw;
@@ -510,7 +534,7 @@ void qr_factor(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int6
     }
     for (int l = 1; l <= L; ++l) {
         const double* Rin = (l == 1 && Rleaves) ? Rleaves : p->R[l - 1];
-        stack_r_kernel<<<p->nodes[l], 256, 0, s>>>(Rin, p->nodes[l - 1], k, k, p->SN[l], k);
+        stack_r_kernel<<<p->nodes[l], 256, 0, s>>>(Rin, p->nodes[l - 1], k, k, p->SN[l], k, c->pred, c->pred_skip);
         check_launch(c);
         CqrArgs a{};
         a.in = p->SN[l];
@@ -613,6 +637,103 @@ void qr_formq(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int64
     g.ntiles = p->t_count[0];
     g.force_splits = 1;
     run_gemm(c, g, s);
+}
+
+struct PredScope {
+    sorsvd_ctx* c;
+    const int* saved;
+    int saved_skip;
+    PredScope(sorsvd_ctx* c_, const int* flag, int skip) : c(c_), saved(c_->pred), saved_skip(c_->pred_skip) {
+        c->pred = flag;
+        c->pred_skip = skip;
+    }
+    ~PredScope() {
+        c->pred = saved;
+        c->pred_skip = saved_skip;
+    }
+};
+
+void launch_chol(sorsvd_ctx* c, const CholArgs& a, cudaStream_t s) {
+    const size_t sm = (size_t)a.k * a.k * sizeof(double) <= 200 * 1024 ? (size_t)a.k * a.k * sizeof(double) : 0;
+    CK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(sm, 1)));
+    chol_inv_kernel<<<1, kCholThreads, sm, s>>>(a);
+    check_launch(c);
+}
+
+// Full single-GPU thin QR of T (rows x k): CholeskyQR2 when the sketch is well
+// conditioned, the cluster Householder TSQR otherwise (device-side choice,
+// cholqr_f64.cuh). T is left intact by the CholeskyQR2 path; the Householder
+// path may overwrite it. Final R (diag >= 0) lands in p->R[L].
+void qr_run(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int64_t ldq, cudaStream_t s) {
+    const int k = p->k, Np = p->Np;
+    const int L = (int)p->nodes.size() - 1;
+    auto gram = [&](const double* X, int64_t ldx, double* G) {
+        GemmCall g;
+        g.ta = true;
+        g.A = X;
+        g.lda = ldx;
+        g.M = k;
+        g.K = p->rows;
+        g.B = X;
+        g.ldb = ldx;
+        g.N = Np;
+        g.C = G;
+        g.ldc = Np;
+        g.ws_name = p->ws_name.c_str();
+        run_gemm(c, g, s);
+    };
+    auto rmul = [&](const double* X, int64_t ldx, const double* Ri, double* Out, int64_t ldo) {
+        GemmCall g;
+        g.A = X;
+        g.lda = ldx;
+        g.M = p->rows;
+        g.K = k;
+        g.B = Ri;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = Out;
+        g.ldc = ldo;
+        g.ws_name = p->ws_name.c_str();
+        run_gemm(c, g, s);
+    };
+    if (ldt != Np) throw Error{SORSVD_ERR_INTERNAL, "qr_run: T must be padded to Np"};
+    gram(T, ldt, p->G1);
+    CholArgs a1{};
+    a1.G = p->G1;
+    a1.ldg = Np;
+    a1.k = k;
+    a1.Rinv = p->Ri1;
+    a1.ldr = Np;
+    a1.work = p->cwork;
+    a1.flag = p->flag;
+    a1.pass = 1;
+    a1.Rf = p->R1;
+    a1.ldf = k;
+    launch_chol(c, a1, s);
+    {
+        PredScope ps(c, p->flag, 1);  // skipped when pass 1 rejected
+        rmul(T, ldt, p->Ri1, p->Qtmp, Np);
+        gram(p->Qtmp, Np, p->G2);
+    }
+    CholArgs a2 = a1;
+    a2.G = p->G2;
+    a2.Rinv = p->Ri2;
+    a2.pass = 2;
+    a2.Rf = nullptr;
+    a2.R1 = p->R1;
+    a2.ldr1 = k;
+    a2.Rout = p->R[L];
+    a2.ldo = k;
+    launch_chol(c, a2, s);
+    {
+        PredScope ps(c, p->flag, 1);
+        rmul(p->Qtmp, Np, p->Ri2, Q, ldq);
+    }
+    {
+        PredScope ps(c, p->flag, 0);  // Householder only when CholeskyQR2 was rejected
+        qr_factor(c, p, T, ldt, Q, ldq, true, s);
+        qr_formq(c, p, T, ldt, Q, ldq, nullptr, s);
+    }
 }
 
 const double* qr_leaf_factors(QrPlan* p, bool had_cin) {
@@ -778,11 +899,9 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         const double* Cg = qr_leaf_factors(pg, false) + (size_t)c->rank * ell * Np;
         qr_formq(c, p1, b.T1, Np, b.Q1, Np, Cg, s);
     } else {
-        qr_factor(c, p1, b.T1, Np, b.Q1, Np, true, s);
-        qr_formq(c, p1, b.T1, Np, b.Q1, Np, nullptr, s);
+        qr_run(c, p1, b.T1, Np, b.Q1, Np, s);
     }
-    qr_factor(c, p2, b.T2, Np, b.Q2, Np, true, c->side);
-    qr_formq(c, p2, b.T2, Np, b.Q2, Np, nullptr, c->side);
+    qr_run(c, p2, b.T2, Np, b.Q2, Np, c->side);
     CK(cudaEventRecord(c->ev_join, c->side));
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     record_stage(c, timing, 2);
@@ -1365,8 +1484,7 @@ int sorsvd_thin_qr_device(sorsvd_ctx* c, int64_t m, int32_t k, const double* dT,
         double* Q = dbuf(c, "qrQ", (size_t)m * Np, true);
         CK(cudaMemcpy2DAsync(T, (size_t)Np * 8, dT, (size_t)ldt * 8, (size_t)k * 8, (size_t)m,
                              cudaMemcpyDeviceToDevice, c->stream));
-        qr_factor(c, p, T, Np, Q, Np, true, c->stream);
-        qr_formq(c, p, T, Np, Q, Np, nullptr, c->stream);
+        qr_run(c, p, T, Np, Q, Np, c->stream);
         CK(cudaMemcpy2DAsync(dQ, (size_t)ldq * 8, Q, (size_t)Np * 8, (size_t)k * 8, (size_t)m,
                              cudaMemcpyDeviceToDevice, c->stream));
         const int L = (int)p->nodes.size() - 1;
