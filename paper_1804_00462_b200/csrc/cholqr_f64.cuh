@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_inv_kernel(CholArgs a) {
             pmin = fmin(pmin, d);
         }
         __syncthreads();
+        if (s_bad) break;  // not positive definite: reject early (uniform: shared flag)
         const double r = s_piv[0];
         for (int i = j + 1 + tid; i < k; i += blockDim.x) L[(size_t)i * k + j] /= r;
         __syncthreads();

@@ -92,12 +92,32 @@ __global__ void jacobi_cluster_kernel(JacobiArgs a) {
 
     const double tol = sqrt((double)k) * 2.220446049250313e-16;
     const double tol2 = tol * tol;
+    // ring destinations of this slot's two columns (fixed for the whole run):
+    // top[i] -> top[i+1] (top[0] fixed, top[P-1] -> bot[P-1]); bot[i] -> bot[i-1] (bot[0] -> top[1])
+    int dts = 0, dth = 0, dbs = 0, dbh = 1;
+    if (P > 1) {
+        if (slot == 0) { dts = 0; dth = 0; }
+        else if (slot < P - 1) { dts = slot + 1; dth = 0; }
+        else { dts = P - 1; dth = 1; }
+        if (slot == 0) { dbs = 1; dbh = 0; }
+        else { dbs = slot - 1; dbh = 1; }
+    }
+    double* dstT[2];
+    double* dstB[2];
+    {
+        const size_t offT = (size_t)(dts % ppc) * SLOT + (size_t)dth * 2 * KPAD;
+        const size_t offB = (size_t)(dbs % ppc) * SLOT + (size_t)dbh * 2 * KPAD;
+        dstT[0] = cl.map_shared_rank(buf0, dts / ppc) + offT;
+        dstT[1] = cl.map_shared_rank(buf1, dts / ppc) + offT;
+        dstB[0] = cl.map_shared_rank(buf0, dbs / ppc) + offB;
+        dstB[1] = cl.map_shared_rank(buf1, dbs / ppc) + offB;
+    }
     int cur = 0;
-    int sweep = 0;
+    int sweep = 0, rounds = 0;
     for (; sweep < a.max_sweeps; ++sweep) {
         int rotated = 0;
-        for (int rd = 0; rd < kk - 1; ++rd) {
-            double* src = cur ? buf1 : buf0;
+        for (int rd = 0; rd < kk - 1; ++rd, ++rounds) {
+            const double* src = cur ? buf1 : buf0;
             if (active) {
                 const double* base = src + (size_t)warp * SLOT;
                 double gt[KP], vt[KP], gb[KP], vb[KP];
@@ -109,8 +129,6 @@ __global__ void jacobi_cluster_kernel(JacobiArgs a) {
                     gb[p] = base[2 * KPAD + i];
                     vb[p] = base[3 * KPAD + i];
                 }
-                const int idt = ids[(cur * ppc + warp) * 2 + 0];
-                const int idb = ids[(cur * ppc + warp) * 2 + 1];
                 double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
                 for (int p = 0; p < KP; ++p) {
@@ -118,58 +136,39 @@ __global__ void jacobi_cluster_kernel(JacobiArgs a) {
                     be = fma(gb[p], gb[p], be);
                     ga = fma(gt[p], gb[p], ga);
                 }
-                al = warp_sum(al);
-                be = warp_sum(be);
-                ga = warp_sum(ga);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                }
                 if (ga != 0.0 && ga * ga > tol2 * al * be) {
                     rotated = 1;
-                    // tan of the Jacobi angle, the smaller root of t^2 + 2 zeta t - 1 = 0 with
-                    // zeta = (be - al) / (2 ga), written with one sqrt and one division:
-                    // t = 2 ga sgn(d) / (|d| + sqrt(d^2 + 4 ga^2)),  d = be - al
+                    // tan of the Jacobi angle (smaller root of t^2 + 2 zeta t - 1 = 0)
                     const double d = be - al;
                     const double t = (2.0 * ga * (d < 0.0 ? -1.0 : 1.0)) / (fabs(d) + sqrt(fma(d, d, 4.0 * ga * ga)));
                     const double c = rsqrt(fma(t, t, 1.0));
-                    const double s = c * t;
+                    const double sn = c * t;
 #pragma unroll
                     for (int p = 0; p < KP; ++p) {
                         const double x = gt[p], y = gb[p];
-                        gt[p] = c * x - s * y;
-                        gb[p] = s * x + c * y;
+                        gt[p] = c * x - sn * y;
+                        gb[p] = sn * x + c * y;
                         const double u = vt[p], w = vb[p];
-                        vt[p] = c * u - s * w;
-                        vb[p] = s * u + c * w;
+                        vt[p] = c * u - sn * w;
+                        vb[p] = sn * u + c * w;
                     }
                 }
-                // ring move: top[i] -> top[i+1] (top[0] fixed, top[P-1] -> bot[P-1]);
-                //            bot[i] -> bot[i-1] (bot[0] -> top[1])
-                int dt_slot, dt_h, db_slot, db_h;
-                if (P == 1) {
-                    dt_slot = 0; dt_h = 0; db_slot = 0; db_h = 1;
-                } else {
-                    if (slot == 0) { dt_slot = 0; dt_h = 0; }
-                    else if (slot < P - 1) { dt_slot = slot + 1; dt_h = 0; }
-                    else { dt_slot = P - 1; dt_h = 1; }
-                    if (slot == 0) { db_slot = 1; db_h = 0; }
-                    else { db_slot = slot - 1; db_h = 1; }
-                }
                 const int nxt = cur ^ 1;
-                double* dstT = cl.map_shared_rank(nxt ? buf1 : buf0, dt_slot / ppc) + (size_t)(dt_slot % ppc) * SLOT +
-                               (size_t)dt_h * 2 * KPAD;
-                double* dstB = cl.map_shared_rank(nxt ? buf1 : buf0, db_slot / ppc) + (size_t)(db_slot % ppc) * SLOT +
-                               (size_t)db_h * 2 * KPAD;
+                double* dT = dstT[nxt];
+                double* dB = dstB[nxt];
 #pragma unroll
                 for (int p = 0; p < KP; ++p) {
                     const int i = lane + 32 * p;
-                    dstT[i] = gt[p];
-                    dstT[KPAD + i] = vt[p];
-                    dstB[i] = gb[p];
-                    dstB[KPAD + i] = vb[p];
-                }
-                if (lane == 0) {
-                    int* idsT = cl.map_shared_rank(ids, dt_slot / ppc);
-                    int* idsB = cl.map_shared_rank(ids, db_slot / ppc);
-                    idsT[(nxt * ppc + dt_slot % ppc) * 2 + dt_h] = idt;
-                    idsB[(nxt * ppc + db_slot % ppc) * 2 + db_h] = idb;
+                    dT[i] = gt[p];
+                    dT[KPAD + i] = vt[p];
+                    dB[i] = gb[p];
+                    dB[KPAD + i] = vb[p];
                 }
             }
             if (C > 1) cl.sync();
@@ -188,6 +187,20 @@ __global__ void jacobi_cluster_kernel(JacobiArgs a) {
         }
     }
     if (threadIdx.x == 0) s_sweeps = sweep;
+    // column origins after `rounds` ring shifts of the 2P-1 non-fixed positions
+    if (active && lane < 2) {
+        const int h = lane;
+        const int Lc = 2 * P - 1;
+        const int x = (h == 0) ? (slot == 0 ? -1 : slot - 1) : (2 * P - 2 - slot);
+        int os = 0, oh = 0;
+        if (x >= 0) {
+            const int y = ((x - rounds % Lc) % Lc + Lc) % Lc;
+            if (y < P - 1) { os = y + 1; oh = 0; }
+            else { os = 2 * P - 2 - y; oh = 1; }
+        }
+        ids[(cur * ppc + warp) * 2 + h] = 2 * os + oh;
+    }
+    __syncthreads();
 
     // sigma of every local column, then a cluster-wide stable rank
     double* src = cur ? buf1 : buf0;
@@ -256,6 +269,173 @@ __global__ void jacobi_cluster_kernel(JacobiArgs a) {
         }
     }
     if (r == 0 && threadIdx.x == 0 && a.sweeps_out) *a.sweeps_out = s_sweeps;
+}
+
+// Single-CTA variant (2 k^2 doubles fit in shared memory, k <= ~116): G and V
+// columns stay at fixed places (column-major by column id); round r pairs the
+// columns of the circle ordering directly (no data movement), one warp per
+// pair holds the pair's two G columns in registers, the V columns are
+// rotated in place (each column belongs to one pair per round), and rounds
+// are separated by one __syncthreads. PPW pairs per warp are interleaved so
+// their shuffle chains and square roots overlap.
+__device__ __forceinline__ void jac_round_pair(int r, int i, int kk, int& p, int& q) {
+    auto pos = [&](int t) { return t == 0 ? 0 : ((t - 1 + r) % (kk - 1)) + 1; };
+    p = pos(i);
+    q = pos(kk - 1 - i);
+}
+
+template <int KP, int PPW>
+__global__ void __launch_bounds__(PPW == 1 ? 1024 : 512, 1) jacobi_cta_kernel(JacobiArgs a) {
+    const int k = a.k;
+    const int kk = (k + 1) & ~1;
+    const int P = kk / 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    extern __shared__ __align__(16) double sm[];
+    double* G = sm;                         // column c at G + c*k
+    double* V = sm + (size_t)k * k;
+    double* sig = V + (size_t)k * k;        // [k]
+    int* rnk = reinterpret_cast<int*>(sig + k);
+    __shared__ int flag;
+    __shared__ int s_sweeps;
+
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        const int i = e / k, c = e - i * k;
+        G[(size_t)c * k + i] = a.M[(size_t)i * a.ldm + c];
+        V[(size_t)c * k + i] = (i == c) ? 1.0 : 0.0;
+    }
+    if (threadIdx.x == 0) s_sweeps = 0;
+    __syncthreads();
+
+    const double tol = sqrt((double)k) * 2.220446049250313e-16;
+    const double tol2 = tol * tol;
+    int sweep = 0;
+    for (; sweep < a.max_sweeps; ++sweep) {
+        if (threadIdx.x == 0) flag = 0;
+        int rotated = 0;
+        for (int rd = 0; rd < kk - 1; ++rd) {
+            for (int pb = warp * PPW; pb < P; pb += nwarp * PPW) {
+                int cp[PPW], cq[PPW];
+                bool act[PPW];
+                double gp[PPW][KP], gq[PPW][KP];
+                double al[PPW], be[PPW], ga[PPW];
+#pragma unroll
+                for (int t = 0; t < PPW; ++t) {
+                    int pp = 0, qq = 0;
+                    act[t] = pb + t < P;
+                    if (act[t]) jac_round_pair(rd, pb + t, kk, pp, qq);
+                    act[t] = act[t] && pp < k && qq < k;  // dummy column for odd k
+                    cp[t] = act[t] ? pp : 0;
+                    cq[t] = act[t] ? qq : 0;
+                    al[t] = be[t] = ga[t] = 0.0;
+#pragma unroll
+                    for (int p = 0; p < KP; ++p) {
+                        const int i = lane + 32 * p;
+                        const bool in = act[t] && i < k;
+                        gp[t][p] = in ? G[(size_t)cp[t] * k + i] : 0.0;
+                        gq[t][p] = in ? G[(size_t)cq[t] * k + i] : 0.0;
+                        al[t] = fma(gp[t][p], gp[t][p], al[t]);
+                        be[t] = fma(gq[t][p], gq[t][p], be[t]);
+                        ga[t] = fma(gp[t][p], gq[t][p], ga[t]);
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                    for (int t = 0; t < PPW; ++t) {
+                        al[t] += __shfl_xor_sync(0xffffffffu, al[t], o);
+                        be[t] += __shfl_xor_sync(0xffffffffu, be[t], o);
+                        ga[t] += __shfl_xor_sync(0xffffffffu, ga[t], o);
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < PPW; ++t) {
+                    if (!(act[t] && ga[t] != 0.0 && ga[t] * ga[t] > tol2 * al[t] * be[t])) continue;
+                    rotated = 1;
+                    // tan of the Jacobi angle (smaller root of t^2 + 2 zeta t - 1 = 0)
+                    const double d = be[t] - al[t];
+                    const double tt =
+                        (2.0 * ga[t] * (d < 0.0 ? -1.0 : 1.0)) / (fabs(d) + sqrt(fma(d, d, 4.0 * ga[t] * ga[t])));
+                    const double c = rsqrt(fma(tt, tt, 1.0));
+                    const double sn = c * tt;
+                    double* Gp = G + (size_t)cp[t] * k;
+                    double* Gq = G + (size_t)cq[t] * k;
+                    double* Vp = V + (size_t)cp[t] * k;
+                    double* Vq = V + (size_t)cq[t] * k;
+#pragma unroll
+                    for (int p = 0; p < KP; ++p) {
+                        const int i = lane + 32 * p;
+                        if (i < k) {
+                            const double x = gp[t][p], y = gq[t][p];
+                            Gp[i] = c * x - sn * y;
+                            Gq[i] = sn * x + c * y;
+                            const double u = Vp[i], w = Vq[i];
+                            Vp[i] = c * u - sn * w;
+                            Vq[i] = sn * u + c * w;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (rotated && lane == 0) atomicOr(&flag, 1);
+        __syncthreads();
+        const int any = flag;
+        __syncthreads();
+        if (!any) {
+            ++sweep;
+            break;
+        }
+    }
+    if (threadIdx.x == 0) s_sweeps = sweep;
+    for (int c = warp; c < k; c += nwarp) {
+        double ss = 0.0;
+        for (int i = lane; i < k; i += 32) ss = fma(G[(size_t)c * k + i], G[(size_t)c * k + i], ss);
+        ss = warp_sum(ss);
+        if (lane == 0) sig[c] = sqrt(ss);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        const double sv = sig[c];
+        int rk = 0;
+        for (int f = 0; f < k; ++f) rk += (sig[f] > sv) || (sig[f] == sv && f < c);
+        rnk[c] = rk;
+    }
+    __syncthreads();
+    for (int c = warp; c < k; c += nwarp) {
+        const int rk = rnk[c];
+        const double* Gc = G + (size_t)c * k;
+        const double* Vc = V + (size_t)c * k;
+        const double sv = sig[c];
+        double best = -1.0;
+        int bi = 0;
+        for (int i = lane; i < k; i += 32) {
+            const double av = fabs(Gc[i]);
+            if (av > best) {
+                best = av;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        const double sg = Gc[bi] < 0.0 ? -1.0 : 1.0;
+        for (int i = lane; i < k; i += 32) {
+            a.U[(size_t)i * a.ldu + rk] = sv > 0.0 ? sg * Gc[i] / sv : 0.0;
+            a.V[(size_t)i * a.ldv + rk] = sg * Vc[i];
+        }
+        if (lane == 0) a.S[rk] = sv;
+    }
+    if (threadIdx.x == 0 && a.sweeps_out) *a.sweeps_out = s_sweeps;
+}
+
+__host__ __device__ inline size_t jacobi_cta_smem_bytes(int k) {
+    return (2 * (size_t)k * k + 2 * (size_t)k) * sizeof(double);
 }
 
 }  // namespace sorsvd_dev

@@ -781,9 +781,15 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
     const int kp = (k + 31) / 32;
     const int KP = kp <= 1 ? 1 : kp <= 2 ? 2 : kp <= 4 ? 4 : 8;
     const int P = ((k + 1) & ~1) / 2;
-    // warps (pair slots) per CTA: register budget (KP doubles x 4 per lane) and
-    // shared memory (2 buffers x 4 columns per slot) bound it; then spread the
-    // slots evenly over the smallest cluster that holds them.
+    if (k <= 32 && jacobi_cta_smem_bytes(k) <= 212 * 1024) {
+        // small k: one CTA, G and V in shared memory (no cluster barrier needed)
+        const int warps = std::min(P, 32);
+        const size_t sm = jacobi_cta_smem_bytes(k);
+        CK(cudaFuncSetAttribute(jacobi_cta_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        jacobi_cta_kernel<1, 1><<<1, 32 * warps, sm, s>>>(a);
+        check_launch(c);
+        return;
+    }
     cudaFuncAttributes fa{};
     switch (KP) {
         case 1: CK(cudaFuncGetAttributes(&fa, jacobi_cluster_kernel<1>)); break;
@@ -791,9 +797,11 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
         case 4: CK(cudaFuncGetAttributes(&fa, jacobi_cluster_kernel<4>)); break;
         default: CK(cudaFuncGetAttributes(&fa, jacobi_cluster_kernel<8>)); break;
     }
+    // spread the pair slots over up to 16 CTAs (per-round work is issue bound,
+    // so more SMs per round win over the cost of the cluster barrier)
     int ppc = std::min(32, fa.maxThreadsPerBlock / 32);  // register-limited warps per CTA
     while (ppc > 1 && jacobi_smem_bytes(k, ppc) > 200 * 1024) --ppc;
-    ppc = std::min(ppc, P);
+    ppc = std::min(ppc, std::max(1, (P + 15) / 16));
     const int csize = (P + ppc - 1) / ppc;
     if (csize > 16) throw Error{SORSVD_ERR_UNSUPPORTED, "jacobi: cluster too large"};
     a.ppc = (P + csize - 1) / csize;
