@@ -360,6 +360,226 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
     }
 }
 
+// Register-resident variant: thread t owns column c = t % k over a chunk of
+// CH consecutive local rows (chunk = t / k), so the block's rows live in
+// registers and every per-reflector sweep is a register FMA stream with the
+// current reflector column broadcast from shared memory (all lanes of a warp
+// read the same x_i). Per reflector: owners publish x / row j -> barrier ->
+// per-(column, chunk) dots -> barrier -> per-column chunk sums (fixed order)
+// into the cluster payload -> cluster reduction -> register update. Same
+// math and payload as cqr_kernel; used when k * ceil(rows_per_cta / CH)
+// threads fit one CTA.
+// max threads per CTA for a CH-double register stream (64K registers / (2 CH + ~30))
+__host__ __device__ constexpr int cqr_reg_maxt(int CH) {
+    return CH <= 32 ? 512 : 256;
+}
+
+template <int CH>
+__global__ void __launch_bounds__(cqr_reg_maxt(CH), 1) cqr_reg_kernel(CqrArgs a) {
+    if (a.pred && *a.pred == a.pred_skip) return;
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks();
+    const int r = (int)cl.block_rank();
+    const int b = blockIdx.x / C;
+    const int rows = a.rows[b];
+    const int64_t row0 = a.row0[b];
+    const int k = a.k;
+    const int Rb = (rows + C - 1) / C;
+    const int lr0 = r * Rb;
+    const int nr = max(0, min(Rb, rows - lr0));
+    const int nch = (Rb + CH - 1) / CH;
+    const int RW = cqr_rw(k);
+    const int tid = threadIdx.x;
+    const int col = tid % k, chunk = tid / k;
+    const bool own = chunk < nch;
+    const int i0 = chunk * CH;  // first local row of this thread's chunk
+
+    extern __shared__ __align__(16) double sm[];
+    double* xb = sm;                          // [nch*CH] current reflector column (rows > j), 0 elsewhere
+    double* rowj = xb + (size_t)nch * CH;     // [k]  row j of the block
+    double* part = rowj + k;                  // [nch][k] per-chunk partial dots
+    double* red = part + (size_t)nch * k;     // [2][RW] cluster payload
+    double* S = red + 2 * RW;                 // [RW]
+    double* tau = S + RW;                     // [k]
+    double* sgn = tau + k;                    // [k]
+    __shared__ double* peers[16];
+
+    double v[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+        const int li = i0 + q;
+        v[q] = (own && li < nr) ? a.in[(row0 + lr0 + li) * a.ldi + col] : 0.0;
+    }
+    if (tid < C) peers[tid] = cl.map_shared_rank(red, tid);
+    __syncthreads();
+    auto csum = [&](int off, int idx) {  // fixed-order sum, 8 remote loads in flight at a time
+        double s = 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double t[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) t[q] = 8 * h + q < C ? peers[8 * h + q][off + idx] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s += t[q];
+        }
+        return s;
+    };
+
+    // ------------------------------------------------------------ factor --
+    int par = 0;
+    for (int j = 0; j < k; ++j) {
+        const int nt = k - j - 1;
+        const int jl = j - lr0;  // local index of global row j (owner iff 0 <= jl < nr)
+        double* P = red + (par & 1) * RW;
+        ++par;
+        // publish x_j (rows > j) and row j
+        if (own && col == j) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int li = i0 + q;
+                xb[li] = (li < nr && lr0 + li > j) ? v[q] : 0.0;
+            }
+        }
+        if (own && jl >= i0 && jl < i0 + CH && jl < nr && col >= j) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q)
+                if (i0 + q == jl) rowj[col] = v[q];
+        }
+        __syncthreads();
+        if (own && col >= j) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < CH; q += 2) {
+                s0 = fma(xb[i0 + q], v[q], s0);
+                s1 = fma(xb[i0 + q + 1], v[q + 1], s1);
+            }
+            part[chunk * k + col] = s0 + s1;
+        }
+        __syncthreads();
+        const bool ownerj = jl >= 0 && jl < nr;
+        for (int vc = tid; vc <= nt; vc += blockDim.x) {
+            const int c = j + vc;
+            double s = 0.0;
+            for (int h = 0; h < nch; ++h) s += part[h * k + c];
+            const double rv = ownerj ? rowj[c] : 0.0;
+            if (vc == 0) {
+                P[0] = s;
+                P[1] = rv;
+            } else {
+                P[1 + vc] = s;
+                P[1 + nt + vc] = rv;
+            }
+        }
+        cl.sync();
+        for (int idx = tid; idx < 2 + 2 * nt; idx += blockDim.x) S[idx] = csum((int)(P - red), idx);
+        __syncthreads();
+        const double ss = S[0], alpha = S[1];
+        double t = 0.0, beta = alpha, scal = 0.0;
+        if (ss != 0.0) {
+            beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+            t = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        if (tid == 0) {
+            tau[j] = t;
+            sgn[j] = (a.root_sign && beta < 0.0) ? -1.0 : 1.0;
+        }
+        if (own && col > j && t != 0.0) {
+            const double d = (S[2 + nt + (col - j - 1)] + scal * S[2 + (col - j - 1)]) * t;
+            const double ds = d * scal;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int li = i0 + q;
+                v[q] = fma(-ds, xb[li], v[q]);  // xb is 0 for rows <= j and padding rows
+                if (li == jl && li < nr) v[q] -= d;  // v_j = 1 at row j
+            }
+        } else if (own && col == j) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int li = i0 + q;
+                if (li < nr && lr0 + li > j) v[q] *= scal;
+                if (li == jl) v[q] = beta;
+            }
+        }
+        __syncthreads();
+    }
+    // R rows (< k) from their owners, sign-fixed at the root
+    double* Ro = a.R + (int64_t)b * k * a.ldr;
+    if (own) {
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            const int li = i0 + q, gi = lr0 + li;
+            if (li < nr && gi < k) Ro[(int64_t)gi * a.ldr + col] = col >= gi ? sgn[gi] * v[q] : 0.0;
+        }
+    }
+
+    // ------------------------------------------------------------ form Q --
+    cl.sync();  // peers are done with the factor's payload buffers
+    for (int j = k - 1; j >= 0; --j) {
+        const int nt = k - j - 1;
+        const int jl = j - lr0;
+        const double tj = tau[j];
+        // publish v_j (1 at row j, reflector below, 0 above)
+        if (own && col == j) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int li = i0 + q;
+                const int gi = lr0 + li;
+                xb[li] = (li < nr && gi > j) ? v[q] : (li == jl && li < nr ? 1.0 : 0.0);
+            }
+        }
+        __syncthreads();
+        if (nt > 0 && tj != 0.0) {
+            double* P = red + (par & 1) * RW;
+            ++par;
+            if (own && col > j) {
+                double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                for (int q = 0; q < CH; q += 2) {
+                    s0 = fma(xb[i0 + q], v[q], s0);
+                    s1 = fma(xb[i0 + q + 1], v[q + 1], s1);
+                }
+                part[chunk * k + col] = s0 + s1;
+            }
+            __syncthreads();
+            for (int vc = tid; vc < nt; vc += blockDim.x) {
+                double s = 0.0;
+                for (int h = 0; h < nch; ++h) s += part[h * k + j + 1 + vc];
+                P[vc] = s;
+            }
+            cl.sync();
+            for (int idx = tid; idx < nt; idx += blockDim.x) S[idx] = csum((int)(P - red), idx);
+            __syncthreads();
+            if (own && col > j) {
+                const double d = S[col - j - 1] * tj;
+#pragma unroll
+                for (int q = 0; q < CH; ++q) v[q] = fma(-d, xb[i0 + q], v[q]);
+            }
+        }
+        if (own && col == j) {  // finish column j (dorg2r)
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int gi = lr0 + i0 + q;
+                v[q] = gi > j ? -tj * v[q] : (gi == j ? 1.0 - tj : 0.0);
+            }
+        }
+        __syncthreads();
+    }
+    cl.sync();  // every CTA done reading its peers' payload buffers
+    if (own) {
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            const int li = i0 + q;
+            if (li < nr) a.qout[(row0 + lr0 + li) * a.ldq + col] = sgn[col] * v[q];
+        }
+    }
+}
+
+__host__ __device__ inline size_t cqr_reg_smem_bytes(int Rb, int k, int CH) {
+    const int nch = (Rb + CH - 1) / CH;
+    return ((size_t)nch * CH + k + (size_t)nch * k + 3 * (size_t)cqr_rw(k) + 2 * (size_t)k + 8) * sizeof(double);
+}
+
 // Stack pairs of k x k R factors into 2k x k row-major node inputs
 // (pass-through nodes copy their single R and mark nothing: the node kernel
 // runs on k rows and yields Q = I up to signs, which is what we want).

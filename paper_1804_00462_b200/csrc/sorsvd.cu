@@ -359,10 +359,106 @@ int cqr_max_cluster(sorsvd_ctx* c, int k) {
     return best;
 }
 
-void launch_cqr(sorsvd_ctx* c, const CqrArgs& a0, int nblocks, int csize, int Rb, cudaStream_t s) {
+struct RegCfg {
+    int ch = 0, threads = 0, csize = 0;
+};
+
+template <int CH>
+int cqr_reg_max_threads() {
+    static int t = -1;
+    if (t < 0) {
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, cqr_reg_kernel<CH>));
+        t = std::min(1024, fa.maxThreadsPerBlock) / 32 * 32;
+    }
+    return t;
+}
+
+int cqr_reg_threads_for(int ch) {
+    switch (ch) {
+        case 16: return cqr_reg_max_threads<16>();
+        case 24: return cqr_reg_max_threads<24>();
+        case 32: return cqr_reg_max_threads<32>();
+        case 48: return cqr_reg_max_threads<48>();
+        default: return cqr_reg_max_threads<64>();
+    }
+}
+
+// Register-resident configuration for a block of `rows` x k over at most
+// `cmax` CTAs: smallest chunk (shortest per-thread stream) that fits.
+RegCfg cqr_reg_choose(int k, int64_t rows, int cmax) {
+    RegCfg best;
+    for (int ch : {16, 24, 32, 48, 64}) {
+        const int tmax = cqr_reg_threads_for(ch);
+        const int nch_max = tmax / k;
+        if (nch_max < 1) continue;
+        const int64_t rows_cta = (int64_t)nch_max * ch;
+        const int64_t C = cdiv(rows, rows_cta);
+        if (C > cmax) continue;
+        const int Rb = (int)cdiv(rows, C);
+        const int nch = (Rb + ch - 1) / ch;
+        const int threads = (k * nch + 31) / 32 * 32;
+        if (cqr_reg_smem_bytes(Rb, k, ch) > 200 * 1024 || threads > tmax) continue;
+        best.ch = ch;
+        best.threads = threads;
+        best.csize = (int)C;
+        return best;
+    }
+    return best;
+}
+
+int64_t cqr_reg_capacity(int k, int cmax) {
+    int64_t cap = 0;
+    for (int ch : {16, 24, 32, 48, 64}) {
+        const int nch_max = cqr_reg_threads_for(ch) / k;
+        cap = std::max<int64_t>(cap, (int64_t)cmax * nch_max * ch);
+    }
+    return cap;
+}
+
+template <int CH>
+void launch_cqr_reg_t(sorsvd_ctx* c, const CqrArgs& a, int nblocks, const RegCfg& rc, int Rb, cudaStream_t s) {
+    const size_t sm = cqr_reg_smem_bytes(Rb, a.k, CH);
+    CK(cudaFuncSetAttribute(cqr_reg_kernel<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(cqr_reg_kernel<CH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(nblocks * rc.csize));
+    cfg.blockDim = dim3((unsigned)rc.threads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = rc.csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, cqr_reg_kernel<CH>, a));
+    check_launch(c);
+}
+
+// Factor + explicit Q of `nblocks` blocks of at most `rows_max` rows each:
+// register-resident kernel when a configuration fits, shared-memory kernel
+// otherwise.
+void launch_cqr(sorsvd_ctx* c, const CqrArgs& a0, int nblocks, int rows_max, int cmax_smem, int rb_smem,
+                cudaStream_t s) {
     CqrArgs a = a0;
     a.pred = c->pred;
     a.pred_skip = c->pred_skip;
+    const RegCfg rc = getenv("SORSVD_CQR_SMEM") ? RegCfg{} : cqr_reg_choose(a.k, rows_max, kCqrMaxCluster);
+    if (rc.ch) {
+        const int Rb = (int)cdiv(rows_max, rc.csize);
+        switch (rc.ch) {
+            case 16: launch_cqr_reg_t<16>(c, a, nblocks, rc, Rb, s); break;
+            case 24: launch_cqr_reg_t<24>(c, a, nblocks, rc, Rb, s); break;
+            case 32: launch_cqr_reg_t<32>(c, a, nblocks, rc, Rb, s); break;
+            case 48: launch_cqr_reg_t<48>(c, a, nblocks, rc, Rb, s); break;
+            default: launch_cqr_reg_t<64>(c, a, nblocks, rc, Rb, s); break;
+        }
+        return;
+    }
+    const int csize = (int)std::min<int64_t>(cmax_smem, cdiv(rows_max, rb_smem));
+    const int Rb = (int)cdiv(rows_max, csize);
     const size_t sm = cqr_smem_bytes(Rb, a.k);
     CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -427,7 +523,10 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
     if (leaves_given > 0) {
         p->P = leaves_given;
     } else {
-        const int64_t leaf_max = (int64_t)p->cmax * p->rb_max;
+        // the per-reflector latency (cluster reduction) dominates, so the
+        // fewest tree levels win: leaves as large as either kernel can hold
+        const int64_t reg_cap = getenv("SORSVD_CQR_SMEM") ? 0 : cqr_reg_capacity(k, kCqrMaxCluster);
+        const int64_t leaf_max = std::max<int64_t>(reg_cap, (int64_t)p->cmax * p->rb_max);
         p->P = (int)std::max<int64_t>(1, cdiv(rows, leaf_max));
         const int64_t base = rows / p->P, extra = rows % p->P;
         int64_t r = 0;
@@ -530,7 +629,7 @@ void qr_factor(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int6
         a.R = p->R[0];
         a.ldr = k;
         a.root_sign = (L == 0 && root_sign) ? 1 : 0;
-        launch_cqr(c, a, p->P, p->leaf_cs, (int)cdiv(p->max_leaf_rows, p->leaf_cs), s);
+        launch_cqr(c, a, p->P, p->max_leaf_rows, p->cmax, p->rb_max, s);
     }
     for (int l = 1; l <= L; ++l) {
         const double* Rin = (l == 1 && Rleaves) ? Rleaves : p->R[l - 1];
@@ -547,7 +646,7 @@ void qr_factor(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int6
         a.R = p->R[l];
         a.ldr = k;
         a.root_sign = (l == L && root_sign) ? 1 : 0;
-        launch_cqr(c, a, p->nodes[l], p->node_cs, (int)cdiv(2 * k, p->node_cs), s);
+        launch_cqr(c, a, p->nodes[l], 2 * k, p->cmax, p->rb_max, s);
     }
 }
 
