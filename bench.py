@@ -40,6 +40,9 @@ CONFIGS = {
     # BASELINE.json configs[2], fp64 variant
     "c3": dict(m=200000, n=20000, k=256, q=1, scaling="strong",
                desc="C3 fp64 m=200000 n=20000 k=ell=256 q=1, A = X diag(10^(-j/64)) Y^T + N(0,1e-6)"),
+    # BASELINE.json configs[2], fp32 variant (TF32 tensor-core passes, FP64 QR/SVD)
+    "c3f32": dict(m=200000, n=20000, k=256, q=1, scaling="strong", dtype="f32",
+                  desc="C3 fp32 m=200000 n=20000 k=ell=256 q=1 (TF32 tcgen05 passes), same A rounded to fp32"),
 }
 
 
@@ -67,19 +70,19 @@ def make_matrix(cfg_name, m_local, n, rank, world, device):
         r = min(m_local, n)
         s = 1.0 / torch.arange(1, r + 1, device=device, dtype=f64) ** 2
         return (u[:, :r] * s) @ v[:, :r].T
-    if cfg_name == "c3":
+    if cfg_name in ("c3", "c3f32"):
         mg = CONFIGS["c3"]["m"]
         g.manual_seed(1000 + rank)
         x = torch.randn(m_local, 256, generator=g, device=device, dtype=f64) / math.sqrt(mg)
         g.manual_seed(2000)
         y = torch.randn(n, 256, generator=g, device=device, dtype=f64) / math.sqrt(n)
         s = 10.0 ** (-torch.arange(1, 257, device=device, dtype=f64) / 64.0)
-        a = torch.empty(m_local, n, device=device, dtype=f64)
+        a = torch.empty(m_local, n, device=device, dtype=torch.float32 if cfg_name == "c3f32" else f64)
         g.manual_seed(3000 + rank)
         step = 8192
         for i in range(0, m_local, step):
             j = min(m_local, i + step)
-            a[i:j] = (x[i:j] * s) @ y.T + 1e-3 * torch.randn(j - i, n, generator=g, device=device, dtype=f64)
+            a[i:j] = ((x[i:j] * s) @ y.T + 1e-3 * torch.randn(j - i, n, generator=g, device=device, dtype=f64)).to(a.dtype)
         return a
     raise ValueError(cfg_name)
 
@@ -305,36 +308,65 @@ def main():
     value = flops_step / (ms_per_step * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel (the A-streaming pass) ----
-    fp64_peak = ctypes_peak = None
     import ctypes
+    f32 = cfg.get("dtype") == "f32"
+    esz = 4 if f32 else 8
     pk = ctypes.c_double()
     hb = ctypes.c_double()
     P._check(P._capi.lib().sorsvd_measure_peaks(ctx.handle, ctypes.byref(pk), ctypes.byref(hb)), ctx.handle)
-    fp64_peak, hbm_read = pk.value, hb.value
-    Np = (ell + 7) // 8 * 8 if ell <= 128 else (ell + 127) // 128 * 128
-    X = torch.zeros(n, Np, dtype=torch.float64, device=device)
-    X[:, :ell] = omega
-    T = torch.zeros(m_local, Np, dtype=torch.float64, device=device)
-    ms_pass = ctypes.c_double()
-    lpp = ctypes.c_int32()
-    P._check(P._capi.lib().sorsvd_pass_device(ctx.handle, 0, m_local, n, n, ell, A.data_ptr(), X.data_ptr(),
-                                              T.data_ptr(), max(args.steps, 5), ctypes.byref(ms_pass),
-                                              ctypes.byref(lpp)), ctx.handle)
-    T2 = torch.zeros(n, Np, dtype=torch.float64, device=device)
-    ms_pass_t = ctypes.c_double()
-    P._check(P._capi.lib().sorsvd_pass_device(ctx.handle, 1, m_local, n, n, ell, A.data_ptr(), T.data_ptr(),
-                                              T2.data_ptr(), max(args.steps, 5), ctypes.byref(ms_pass_t),
-                                              ctypes.byref(lpp)), ctx.handle)
-    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else open(os.devnull) as fh:
+    fp64_peak = pk.value
+    mp = {}
+    mp_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp_path):
         try:
-            mp = json.load(fh)
+            mp = json.load(open(mp_path))
         except Exception:
             mp = {}
     hbm_peak = mp.get("hbm_gbs", 6650.0)
+    if f32:
+        # TF32 peak: a plain library GEMM (cuBLAS TF32, 8192^3) measured live, like the bf16 entry
+        torch.backends.cuda.matmul.allow_tf32 = True
+        xa = torch.randn(8192, 8192, device=device, dtype=torch.float32)
+        xb = torch.randn(8192, 8192, device=device, dtype=torch.float32)
+        for _ in range(3):
+            xa @ xb
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e30
+        for _ in range(5):
+            e0.record(stream)
+            xa @ xb
+            e1.record(stream)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        tensor_peak = 2.0 * 8192 ** 3 / (best * 1e-3) / 1e12
+        peak_src = "live cuBLAS TF32 8192^3 GEMM (burst); MEASURED_PEAKS.json has no TF32 entry"
+        del xa, xb
+        Np = ((ell + 31) // 32) * 32 if ell <= 256 else ((ell + 255) // 256) * 256
+        tdt = torch.float32
+        pass_fn = P._capi.lib().sorsvd_pass_f32_device
+        kname = "tc_gemm_tf32_kernel (tcgen05.mma kind::tf32, TMA, TMEM)"
+    else:
+        tensor_peak = fp64_peak
+        peak_src = "live FP64 DMMA burst (sorsvd_measure_peaks); MEASURED_PEAKS.json has no FP64 entry"
+        Np = (ell + 7) // 8 * 8 if ell <= 128 else (ell + 127) // 128 * 128
+        tdt = torch.float64
+        pass_fn = P._capi.lib().sorsvd_pass_device
+        kname = "gemm_f64_kernel (DMMA m8n8k4, cp.async ring)"
+    X = torch.zeros(n, Np, dtype=tdt, device=device)
+    X[:, :ell] = omega.to(tdt)
+    T = torch.zeros(m_local, Np, dtype=tdt, device=device)
+    ms_pass = ctypes.c_double()
+    lpp = ctypes.c_int32()
+    P._check(pass_fn(ctx.handle, 0, m_local, n, n, ell, A.data_ptr(), X.data_ptr(), T.data_ptr(), max(args.steps, 5),
+                     ctypes.byref(ms_pass), ctypes.byref(lpp)), ctx.handle)
+    T2 = torch.zeros(n, Np, dtype=tdt, device=device)
+    ms_pass_t = ctypes.c_double()
+    P._check(pass_fn(ctx.handle, 1, m_local, n, n, ell, A.data_ptr(), T.data_ptr(), T2.data_ptr(), max(args.steps, 5),
+                     ctypes.byref(ms_pass_t), ctypes.byref(lpp)), ctx.handle)
     pass_flops = 2.0 * m_local * n * ell
-    pass_bytes = 8.0 * m_local * n
+    pass_bytes = float(esz) * m_local * n
     ai = pass_flops / pass_bytes
-    ridge = fp64_peak * 1e12 / (hbm_peak * 1e9)
+    ridge = tensor_peak * 1e12 / (hbm_peak * 1e9)
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
@@ -344,17 +376,15 @@ def main():
             traffic = None
     if ai >= ridge:
         achieved = pass_flops / (ms_pass.value * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": traffic,
-                "kernel": "gemm_f64_kernel NN pass T1 = A*X (DMMA m8n8k4)",
-                "peak_source": "live FP64 DMMA burst (sorsvd_measure_peaks); MEASURED_PEAKS.json has no FP64",
-                "ms_per_launch": ms_pass.value, "flops_per_launch": pass_flops,
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TFLOP/s",
+                "frac": achieved / tensor_peak, "traffic": traffic, "kernel": kname + ", NN pass T1 = A*X",
+                "peak_source": peak_src, "ms_per_launch": ms_pass.value, "flops_per_launch": pass_flops,
                 "tn_pass": {"ms": ms_pass_t.value, "achieved": pass_flops / (ms_pass_t.value * 1e-3) / 1e12},
-                "hbm_gbs_measured": hbm_peak}
+                "hbm_gbs_measured": hbm_peak, "hbm_frac": pass_bytes / (ms_pass.value * 1e-3) / 1e9 / hbm_peak}
     else:
         achieved = pass_bytes / (ms_pass.value * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": traffic, "kernel": "gemm_f64_kernel NN pass T1 = A*X",
+                "traffic": traffic, "kernel": kname + ", NN pass T1 = A*X",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "ms_per_launch": ms_pass.value,
                 "bytes_per_launch": pass_bytes,
                 "tn_pass": {"ms": ms_pass_t.value, "achieved": pass_bytes / (ms_pass_t.value * 1e-3) / 1e9}}
@@ -363,7 +393,7 @@ def main():
     # ---- e2e through the public host-buffer API ----
     e2e = None
     if not args.no_e2e:
-        a_host = torch.empty((m_local, n), dtype=torch.float64, pin_memory=True)
+        a_host = torch.empty((m_local, n), dtype=A.dtype, pin_memory=True)
         a_host.copy_(A)
         a_np = a_host.numpy()
         del A
@@ -381,7 +411,7 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             el = float(tt.item())
         e2e = {"value": flops_step / (el / args.steps) / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(m_local * n * 8 + n * ell * 8),
+               "h2d_bytes_per_step": int(m_local * n * esz + n * ell * 8),
                "d2h_bytes_per_step": int((m_local + n) * k * 8 + k * 8),
                "ms_per_step": el / args.steps * 1e3,
                "path": "sorsvd_sor_svd_power (host buffers, pinned A; Omega drawn from seed inside)"}
@@ -393,8 +423,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         if a_np is None:
             a_np = A.cpu().numpy()
-        if args.config == "c3":
-            a_cpu = np.ascontiguousarray(a_np[:20000])
+        if args.config in ("c3", "c3f32"):
+            a_cpu = np.ascontiguousarray(a_np[:20000], dtype=np.float64)
             sample = "row-block sample 20000x20000 of the C3 matrix (same n, k, q)"
         else:
             a_cpu = a_np
@@ -408,8 +438,8 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": workload, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32/tf32" if f32 else "f64",
+                "data": "synthetic", "config": workload, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk,
                 "wall_s_timed_region": t_wall, "ms_steps": [round(x, 4) for x in ms_steps]}
         print(json.dumps(line), flush=True)

@@ -167,6 +167,11 @@ int sorsvd_small_svd_device(sorsvd_ctx* ctx, int32_t k, const double* dM, int64_
 int sorsvd_matmul_device(sorsvd_ctx* ctx, int32_t ta, int64_t M, int64_t K, int32_t N, const double* dA,
                          int64_t lda, const double* dB, int64_t ldb, double* dC, int64_t ldc);
 
+/* FP32 operands on the tensor cores (tcgen05 kind::tf32, FP32 accumulation);
+ * A must be 16-byte aligned with lda % 4 == 0. */
+int sorsvd_matmul_f32_device(sorsvd_ctx* ctx, int32_t ta, int64_t M, int64_t K, int32_t N, const float* dA,
+                             int64_t lda, const float* dB, int64_t ldb, float* dC, int64_t ldc);
+
 /* ---- measurement (bench.py roofline) --------------------------------------- */
 /* Live FP64 DMMA peak (TFLOP/s, burst) and streaming HBM read (GB/s). */
 int sorsvd_measure_peaks(sorsvd_ctx* ctx, double* fp64_tflops, double* hbm_read_gbs);
@@ -175,6 +180,12 @@ int sorsvd_measure_peaks(sorsvd_ctx* ctx, double* fp64_tflops, double* hbm_read_
  * (or to 128 when ell > 128). Reports the average pass time. */
 int sorsvd_pass_device(sorsvd_ctx* ctx, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell, const double* dA,
                        const double* dX, double* dT, int32_t reps, double* ms_avg, int32_t* launches_per_pass);
+
+/* The same for an fp32 A on the TF32 tensor cores (dX / dT padded to ell
+ * rounded up to 32, or to 256 when ell > 256). */
+int sorsvd_pass_f32_device(sorsvd_ctx* ctx, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell,
+                           const float* dA, const float* dX, float* dT, int32_t reps, double* ms_avg,
+                           int32_t* launches_per_pass);
 
 /* ---- host helpers mirroring random.hpp / sketch.hpp ----------------------- */
 uint64_t sorsvd_sub_seed(uint64_t seed, uint64_t stream);                    /* random.hpp:24 */

@@ -244,8 +244,8 @@ def _torch_stream(ctx: Context, dev_tensor):
     ctx.set_stream(torch.cuda.current_stream(dev_tensor.device).cuda_stream)
 
 
-def _desc(m, n, lda, k, cfg: SketchConfig, flags: int, m_global: int = 0) -> C.SorsvdDesc:
-    return C.SorsvdDesc(m, n, lda, k, cfg.ell, cfg.q, int(cfg.single_pass), cfg.seed & (2**64 - 1), C.F64,
+def _desc(m, n, lda, k, cfg: SketchConfig, flags: int, m_global: int = 0, dtype: int = C.F64) -> C.SorsvdDesc:
+    return C.SorsvdDesc(m, n, lda, k, cfg.ell, cfg.q, int(cfg.single_pass), cfg.seed & (2**64 - 1), dtype,
                         flags, m_global)
 
 
@@ -255,7 +255,9 @@ def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Contex
                   _basic: bool = False) -> LowRankApprox:
     """Subspace-orbit randomized SVD with q power iterations (sketch.hpp:87).
 
-    a: numpy float64 (m, n) on the host, or a CUDA float64 torch tensor.
+    a: numpy (m, n) on the host or a CUDA torch tensor; float64 runs the FP64
+    path, float32 runs the passes on the TF32 tensor cores (QR and the core
+    SVD stay FP64; results are FP64).
     omega: optional (n, ell) test matrix; default gaussian_matrix(n, ell, seed)
     exactly as the reference draws it (sketch.hpp:90)."""
     flags = 0
@@ -270,13 +272,13 @@ def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Contex
     st = C.SorsvdStats()
     if _is_torch_cuda(a):
         import torch
-        if a.dtype != torch.float64 or a.dim() != 2 or a.stride(1) != 1:
-            raise ShapeError("shape: device input must be a row-major float64 matrix")
+        if a.dtype not in (torch.float64, torch.float32) or a.dim() != 2 or a.stride(1) != 1:
+            raise ShapeError("shape: device input must be a row-major float64 or float32 matrix")
         ctx = ctx or default_context(a.device.index or 0)
         _torch_stream(ctx, a)
         m, n = a.shape
         lda = a.stride(0)
-        d = _desc(m, n, lda, k, cfg, flags, m_global)
+        d = _desc(m, n, lda, k, cfg, flags, m_global, C.F32 if a.dtype == torch.float32 else C.F64)
         u = torch.empty((m, k), dtype=torch.float64, device=a.device)
         s = torch.empty((k,), dtype=torch.float64, device=a.device)
         v = torch.empty((n, k), dtype=torch.float64, device=a.device)
@@ -288,14 +290,13 @@ def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Contex
                                                    u.data_ptr(), s.data_ptr(), v.data_ptr(), ctypes.byref(st)),
                ctx.handle)
     else:
-        a = np.ascontiguousarray(a, dtype=np.float64)
+        a = np.asarray(a)
+        a = np.ascontiguousarray(a, dtype=np.float32 if a.dtype == np.float32 else np.float64)
         if a.ndim != 2:
             raise ShapeError("shape: input must be a matrix")
         ctx = ctx or default_context(0)
         m, n = a.shape
-        d = _desc(m, n, n, k, cfg, flags, m_global)
-        if k < 1:
-            validate_sketch(m_global or m, n, k, cfg.ell, cfg.q)
+        d = _desc(m, n, n, k, cfg, flags, m_global, C.F32 if a.dtype == np.float32 else C.F64)
         u = np.empty((m, k))
         s = np.empty((k,))
         v = np.empty((n, k))
@@ -355,7 +356,8 @@ def full_svd(mat, ctx: Optional[Context] = None):
 
 
 def matmul(a, b, transpose_a: bool = False, ctx: Optional[Context] = None):
-    """dense.hpp:20 restricted to skinny products: op(a) @ b with b narrow."""
+    """dense.hpp:20 restricted to skinny products: op(a) @ b with b narrow.
+    float64 -> FP64 DMMA kernel; float32 -> tcgen05 TF32 kernel (FP32 accumulate)."""
     import torch
     if not (_is_torch_cuda(a) and _is_torch_cuda(b)):
         raise ShapeError("shape: matmul expects CUDA float64 tensors")
@@ -367,6 +369,13 @@ def matmul(a, b, transpose_a: bool = False, ctx: Optional[Context] = None):
     if b.shape[0] != K:
         raise ShapeError(f"shape: matmul inner dimensions {K} and {b.shape[0]} differ")
     N = b.shape[1]
+    if a.dtype == torch.float32:
+        # FP32 operands go to the tcgen05 TF32 tensor-core kernel (FP32 accumulation)
+        b = b.to(torch.float32)
+        c = torch.empty((M, N), dtype=torch.float32, device=a.device)
+        _check(C.lib().sorsvd_matmul_f32_device(ctx.handle, int(transpose_a), M, K, N, a.data_ptr(), a.shape[1],
+                                                b.data_ptr(), N, c.data_ptr(), N), ctx.handle)
+        return c
     c = torch.empty((M, N), dtype=torch.float64, device=a.device)
     _check(C.lib().sorsvd_matmul_device(ctx.handle, int(transpose_a), M, K, N, a.data_ptr(), a.shape[1],
                                         b.data_ptr(), N, c.data_ptr(), N), ctx.handle)

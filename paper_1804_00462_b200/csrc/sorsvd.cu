@@ -30,6 +30,7 @@
 #include "jacobi_f64.cuh"
 #include "peaks.cuh"
 #include "rpca_f64.cuh"
+#include "tc_gemm_f32.cuh"
 #include "cholqr_f64.cuh"
 #include "cqr_f64.cuh"
 
@@ -314,6 +315,134 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, g.M * g.ldc, g.C, c->pred, c->pred_skip);
         check_launch(c);
     }
+}
+
+// ------------------------------------------------------ TF32 tcgen05 GEMM ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+        if (!ptr || q != cudaDriverEntryPointSuccess)
+            throw Error{SORSVD_ERR_CUDA, "cuda: cuTensorMapEncodeTiled unavailable"};
+        fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+// 2-D fp32 tensor map over a row-major (rows x cols, ld) matrix, box {bx (inner), by}, 128B swizzle.
+CUtensorMap make_map_f32(const float* base, int64_t rows, int64_t cols, int64_t ld, int bx, int by, bool mn_major) {
+    if (((uintptr_t)base % 16) || ((ld * 4) % 16)) throw Error{SORSVD_ERR_SHAPE, "shape: fp32 operand must be 16B aligned (ld % 4 == 0)"};
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error{SORSVD_ERR_CUDA, "cuda: cuTensorMapEncodeTiled failed " + std::to_string((int)r)};
+    return m;
+}
+
+inline int npad32(int ell) { return ell <= 256 ? ((ell + 31) / 32) * 32 : ((ell + 255) / 256) * 256; }
+
+template <int BN, bool TA>
+void launch_tc_t(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, dim3 grid, cudaStream_t s) {
+    using S = TcShape<BN>;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(tc_gemm_tf32_kernel<BN, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+        attr = true;
+    }
+    tc_gemm_tf32_kernel<BN, TA><<<grid, kTcThreads, S::SMEM, s>>>(ma, mb, a);
+}
+
+template <bool TA>
+void dispatch_tc(int BN, const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, dim3 grid, cudaStream_t s) {
+    switch (BN) {
+        case 32: launch_tc_t<32, TA>(ma, mb, a, grid, s); break;
+        case 64: launch_tc_t<64, TA>(ma, mb, a, grid, s); break;
+        case 96: launch_tc_t<96, TA>(ma, mb, a, grid, s); break;
+        case 128: launch_tc_t<128, TA>(ma, mb, a, grid, s); break;
+        case 160: launch_tc_t<160, TA>(ma, mb, a, grid, s); break;
+        case 192: launch_tc_t<192, TA>(ma, mb, a, grid, s); break;
+        case 224: launch_tc_t<224, TA>(ma, mb, a, grid, s); break;
+        case 256: launch_tc_t<256, TA>(ma, mb, a, grid, s); break;
+        default: throw Error{SORSVD_ERR_INTERNAL, "tc gemm: BN"};
+    }
+}
+
+// C (M x N fp32, ldc) = op(A) * B on the tensor cores (TF32 in, FP32 accumulate).
+// op(A) = A (A: M x K row-major) or A^T (A: K x M row-major); B: K x N row-major,
+// N a multiple of 32 (<= 256) or of 256.
+void run_tc_gemm(sorsvd_ctx* c, bool ta, const float* A, int64_t lda, int64_t M, int64_t K, const float* B,
+                 int64_t ldb, int N, float* C, int64_t ldc, cudaStream_t s, const char* ws_name = "tc_ws") {
+    if (N % 32 || (N > 256 && N % 256)) throw Error{SORSVD_ERR_INTERNAL, "tc gemm: bad N"};
+    const int BN = N <= 256 ? N : 256;
+    const int gy = N / BN;
+    const int64_t gx = cdiv(M, kTcBM);
+    int S = 1;
+    {
+        const int64_t base = gx * gy;
+        const int64_t maxS = std::max<int64_t>(1, std::min<int64_t>(64, K / 512));
+        double best = 1e300;
+        for (int64_t cand = 1; cand <= maxS; ++cand) {
+            const double waves = (double)cdiv(base * cand, c->num_sms);
+            const double cost = waves * ((double)K / cand + 256.0) + (cand > 1 ? 0.02 * cand * M * N / (double)c->num_sms : 0.0);
+            if (cost < best * 0.999) {
+                best = cost;
+                S = (int)cand;
+            }
+        }
+    }
+    const CUtensorMap ma = ta ? make_map_f32(A, K, M, lda, 32, kTcBK, true) : make_map_f32(A, M, K, lda, kTcBK, kTcBM, false);
+    const CUtensorMap mb = make_map_f32(B, K, N, ldb, 32, kTcBK, true);
+    TcArgs a{};
+    a.M = M;
+    a.K = K;
+    a.k_chunk = std::max<int64_t>(kTcBK, cdiv(cdiv(K, S), kTcBK) * kTcBK);
+    a.pred = c->pred;
+    a.pred_skip = c->pred_skip;
+    float* ws = nullptr;
+    if (S > 1) {
+        ws = reinterpret_cast<float*>(dbuf(c, ws_name, (size_t)S * M * ldc / 2 + 1));
+        a.C = ws;
+        a.ldc = ldc;
+        a.c_split_stride = M * ldc;
+    } else {
+        a.C = C;
+        a.ldc = ldc;
+    }
+    dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)S);
+    if (ta) dispatch_tc<true>(BN, ma, mb, a, grid, s);
+    else dispatch_tc<false>(BN, ma, mb, a, grid, s);
+    check_launch(c);
+    if (S > 1) {
+        const int64_t count4 = M * ldc / 4;
+        const int blocks = (int)std::min<int64_t>(cdiv(count4, 256), (int64_t)c->num_sms * 8);
+        reduce_splits_f32_kernel<<<blocks, 256, 0, s>>>(ws, count4, S, M * ldc, C, c->pred, c->pred_skip);
+        check_launch(c);
+    }
+}
+
+void cast_to_f64(sorsvd_ctx* c, const float* in, int64_t ldi, double* out, int64_t ldo, int64_t rows, int cols,
+                 cudaStream_t s) {
+    const int blocks = (int)std::min<int64_t>(cdiv(rows * cols, 256), (int64_t)c->num_sms * 8);
+    cast_f32_to_f64_kernel<<<blocks, 256, 0, s>>>(in, ldi, out, ldo, rows, cols);
+    check_launch(c);
+}
+void cast_to_f32(sorsvd_ctx* c, const double* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int cols,
+                 cudaStream_t s) {
+    const int blocks = (int)std::min<int64_t>(cdiv(rows * cols, 256), (int64_t)c->num_sms * 8);
+    cast_f64_to_f32_kernel<<<blocks, 256, 0, s>>>(in, ldi, out, ldo, rows, cols);
+    check_launch(c);
 }
 
 // ---------------------------------------------------------------- TSQR ----
@@ -915,14 +1044,18 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
 // ------------------------------------------------------------- pipeline ----
 struct SorBuffers {
     double *T1, *T2, *Q1, *Q2, *Y, *Mk, *Uk, *Vk, *Sk, *Uo, *Vo;
+    float *T1f = nullptr, *T2f = nullptr, *Q2f = nullptr, *Yf = nullptr;  // FP32 path
     int* sweeps;
 };
 
 struct SorProblem {
-    const double* A;
+    const double* A;   // FP64 A (dtype F64)
+    const float* Af;   // FP32 A (dtype F32): passes on the TF32 tensor cores
+    int dtype;
     int64_t m, n, lda;
     int k, ell, q;
-    int Np;
+    int Np;            // FP64 padded width (npad)
+    int Np32;          // FP32 padded width for the tcgen05 passes (npad32)
     int64_t m_global;
 };
 
@@ -941,6 +1074,13 @@ SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan**
     b.Uo = dbuf(c, "Uo", (size_t)P.m * Np);
     b.Vo = dbuf(c, "Vo", (size_t)P.n * Np);
     b.sweeps = reinterpret_cast<int*>(dbuf(c, "sweeps", 1));
+    if (P.dtype == SORSVD_F32) {
+        auto fbuf = [&](const char* nm, size_t count) { return reinterpret_cast<float*>(dbuf(c, nm, count / 2 + 2, true)); };
+        b.T1f = fbuf("T1f", (size_t)P.m * P.Np32);
+        b.T2f = fbuf("T2f", (size_t)P.n * P.Np32);
+        b.Q2f = fbuf("Q2f", (size_t)P.n * P.Np32);
+        b.Yf = fbuf("Yf", (size_t)P.m * P.Np32);
+    }
     *p1 = get_qr_plan(c, P.m, P.ell, 0, "T1");
     *p2 = get_qr_plan(c, P.n, P.ell, 0, "T2");
     *pg = c->world > 1 ? get_qr_plan(c, (int64_t)c->world * P.ell, P.ell, c->world, "G") : nullptr;
@@ -967,6 +1107,12 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     const int Np = P.Np, ell = P.ell;
     record_stage(c, timing, 0);
     for (int i = 0; i <= P.q; ++i) {
+        if (P.dtype == SORSVD_F32) {  // TF32 tensor-core passes (tc_gemm_f32.cuh)
+            run_tc_gemm(c, false, P.Af, P.lda, P.m, P.n, b.T2f, P.Np32, P.Np32, b.T1f, P.Np32, s);
+            run_tc_gemm(c, true, P.Af, P.lda, P.n, P.m, b.T1f, P.Np32, P.Np32, b.T2f, P.Np32, s);
+            if (c->world > 1) NCK(nccl().AllReduce(b.T2f, b.T2f, (size_t)P.n * P.Np32, ncclFloat, ncclSum, c->comm, s));
+            continue;
+        }
         GemmCall g1;  // T1 = A * T2     (sketch.hpp:95)
         g1.A = P.A;
         g1.lda = P.lda;
@@ -992,6 +1138,10 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         run_gemm(c, g2, s);
         allreduce_sum(c, b.T2, (size_t)P.n * Np, s);
     }
+    if (P.dtype == SORSVD_F32) {  // the QR / SVD stages run in FP64
+        cast_to_f64(c, b.T1f, P.Np32, b.T1, Np, P.m, ell, s);
+        cast_to_f64(c, b.T2f, P.Np32, b.T2, Np, P.n, ell, s);
+    }
     record_stage(c, timing, 1);
     // Q1 = thin_qr(T1).q, Q2 = thin_qr(T2).q concurrently (sketch.hpp:98-99)
     CK(cudaEventRecord(c->ev_fork, s));
@@ -1013,6 +1163,11 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     record_stage(c, timing, 2);
     // M = Q1^T (A Q2)   (sketch.hpp:100-102)
+    if (P.dtype == SORSVD_F32) {
+        cast_to_f32(c, b.Q2, Np, b.Q2f, P.Np32, P.n, ell, s);
+        run_tc_gemm(c, false, P.Af, P.lda, P.m, P.n, b.Q2f, P.Np32, P.Np32, b.Yf, P.Np32, s);
+        cast_to_f64(c, b.Yf, P.Np32, b.Y, Np, P.m, ell, s);
+    }
     {
         GemmCall g;
         g.A = P.A;
@@ -1024,7 +1179,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g.N = Np;
         g.C = b.Y;
         g.ldc = Np;
-        run_gemm(c, g, s);
+        if (P.dtype == SORSVD_F64) run_gemm(c, g, s);
         GemmCall h;
         h.ta = true;
         h.A = b.Q1;
@@ -1073,7 +1228,8 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
 
 std::string sor_key(const SorProblem& P, const void* dOmega, const void* dU, const void* dS, const void* dV) {
     char buf[512];
-    snprintf(buf, sizeof buf, "sor:%p:%lld:%lld:%lld:%d:%d:%d:%p:%p:%p:%p", (const void*)P.A, (long long)P.m,
+    snprintf(buf, sizeof buf, "sor:%p:%lld:%lld:%lld:%d:%d:%d:%p:%p:%p:%p",
+             P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m,
              (long long)P.n, (long long)P.lda, P.k, P.ell, P.q, dOmega, dU, dS, dV);
     return buf;
 }
@@ -1088,16 +1244,21 @@ void validate(const sorsvd_desc* d) {
     if ((d->flags & SORSVD_FLAG_BASIC) && d->q != 0)
         throw Error{SORSVD_ERR_PARAMETER, "parameter: sor_svd requires q == 0; use sor_svd_power"};
     if (d->single_pass) throw Error{SORSVD_ERR_UNSUPPORTED, "single_pass (m_approx) is not implemented in this build"};
-    if (d->dtype != SORSVD_F64) throw Error{SORSVD_ERR_UNSUPPORTED, "only SORSVD_F64 is implemented in this build"};
-    if (d->ell > 256) throw Error{SORSVD_ERR_UNSUPPORTED, "ell > 256 not supported in FP64"};
+    if (d->dtype != SORSVD_F64 && d->dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
+    if (d->dtype == SORSVD_F32 && (d->lda % 4))
+        throw Error{SORSVD_ERR_SHAPE, "shape: fp32 A needs lda % 4 == 0 (16-byte rows for TMA)"};
+    if (d->ell > 256) throw Error{SORSVD_ERR_UNSUPPORTED, "ell > 256 is not supported yet (core SVD / QR limit)"};
 }
 
 // Core device-side call. dOmega: n x ell dense (or null: drawn on the host).
-void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const double* dA, const double* dOmega, double* dU,
+void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const double* dOmega, double* dU,
                 double* dS, double* dV, sorsvd_stats* st) {
     validate(d);
     SorProblem P{};
-    P.A = dA;
+    P.dtype = d->dtype;
+    P.A = d->dtype == SORSVD_F64 ? static_cast<const double*>(dA) : nullptr;
+    P.Af = d->dtype == SORSVD_F32 ? static_cast<const float*>(dA) : nullptr;
+    P.Np32 = npad32(d->ell);
     P.m = d->m;
     P.n = d->n;
     P.lda = d->lda;
@@ -1122,10 +1283,14 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const double* dA, const dou
     const int launches0 = c->launches;
     int launches = 0;
     auto enqueue_all = [&]() {
-        // T2 <- Omega (padded)
-        CK(cudaMemsetAsync(b.T2, 0, (size_t)P.n * P.Np * 8, c->stream));
-        CK(cudaMemcpy2DAsync(b.T2, (size_t)P.Np * 8, om, (size_t)P.ell * 8, (size_t)P.ell * 8, (size_t)P.n,
-                             cudaMemcpyDeviceToDevice, c->stream));
+        // T2 <- Omega (padded; rounded to fp32 for the TF32 passes)
+        if (P.dtype == SORSVD_F32) {
+            cast_to_f32(c, om, P.ell, b.T2f, P.Np32, P.n, P.ell, c->stream);
+        } else {
+            CK(cudaMemsetAsync(b.T2, 0, (size_t)P.n * P.Np * 8, c->stream));
+            CK(cudaMemcpy2DAsync(b.T2, (size_t)P.Np * 8, om, (size_t)P.ell * 8, (size_t)P.ell * 8, (size_t)P.n,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+        }
         enqueue_sor(c, P, b, p1, p2, pg, timing);
         CK(cudaMemcpy2DAsync(dU, (size_t)P.k * 8, b.Uo, (size_t)P.Np * 8, (size_t)P.k * 8, (size_t)P.m,
                              cudaMemcpyDeviceToDevice, c->stream));
@@ -1177,7 +1342,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const double* dA, const dou
         st->passes = passes;
         st->method = d->q == 0 ? SORSVD_SOR : SORSVD_SOR_POWER;
         st->flops_passes = 2.0 * (double)d->m * d->n * d->ell * passes;
-        st->bytes_passes = (double)d->m * d->n * 8.0 * passes;
+        st->bytes_passes = (double)d->m * d->n * (d->dtype == SORSVD_F32 ? 4.0 : 8.0) * passes;
         st->launches = launches;
         int sw = 0;
         CK(cudaMemcpy(&sw, b.sweeps, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1537,7 +1702,7 @@ int sorsvd_sor_svd_power_device(sorsvd_ctx* c, const sorsvd_desc* d, const void*
     if (!c) return SORSVD_ERR_PARAMETER;
     return guarded(c, [&] {
         if (!dA || !dU || !dSigma || !dV) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
-        sor_device(c, d, static_cast<const double*>(dA), dOmega, dU, dSigma, dV, st);
+        sor_device(c, d, dA, dOmega, dU, dSigma, dV, st);
     });
 }
 
@@ -1547,10 +1712,11 @@ int sorsvd_sor_svd_power(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, con
     return guarded(c, [&] {
         validate(d);
         if (!A || !U || !sigma || !V) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
-        const size_t abytes = (size_t)d->m * d->lda * 8;
+        const size_t esz = d->dtype == SORSVD_F32 ? 4 : 8;
+        const size_t abytes = (size_t)d->m * d->lda * esz;
         cudaEvent_t e0 = c->ev_h[0], e1 = c->ev_h[1], e2 = c->ev_h[2], e3 = c->ev_h[3];
         CK(cudaEventRecord(e0, c->stream));
-        double* dA = dbuf(c, "hostA", (size_t)d->m * d->lda);
+        double* dA = dbuf(c, "hostA", (abytes + 7) / 8);
         CK(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, c->stream));
         const double* dOm = nullptr;
         if (omega && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
@@ -1745,6 +1911,42 @@ int sorsvd_pass_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int64_t 
         const int l0 = c->launches;
         CK(cudaEventRecord(c->ev_a, c->stream));
         for (int r = 0; r < reps; ++r) run_gemm(c, g, c->stream);
+        CK(cudaEventRecord(c->ev_b, c->stream));
+        CK(cudaEventSynchronize(c->ev_b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+        if (ms_avg) *ms_avg = ms / std::max(reps, 1);
+        if (launches_per_pass) *launches_per_pass = (c->launches - l0) / std::max(reps, 1);
+    });
+}
+
+int sorsvd_matmul_f32_device(sorsvd_ctx* c, int32_t ta, int64_t M, int64_t K, int32_t N, const float* dA, int64_t lda,
+                             const float* dB, int64_t ldb, float* dC, int64_t ldc) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (M < 1 || K < 1 || N < 1) throw Error{SORSVD_ERR_SHAPE, "shape: matmul dims must be positive"};
+        const int Np = npad32(N);
+        float* Bp = reinterpret_cast<float*>(dbuf(c, "mmBf", (size_t)K * Np / 2 + 1, true));
+        float* Cp = reinterpret_cast<float*>(dbuf(c, "mmCf", (size_t)M * Np / 2 + 1));
+        CK(cudaMemcpy2DAsync(Bp, (size_t)Np * 4, dB, (size_t)ldb * 4, (size_t)N * 4, (size_t)K,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        run_tc_gemm(c, ta != 0, dA, lda, M, K, Bp, Np, Np, Cp, Np, c->stream);
+        CK(cudaMemcpy2DAsync(dC, (size_t)ldc * 4, Cp, (size_t)Np * 4, (size_t)N * 4, (size_t)M,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sorsvd_pass_f32_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell, const float* dA,
+                           const float* dX, float* dT, int32_t reps, double* ms_avg, int32_t* launches_per_pass) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        const int Np = npad32(ell);
+        const int64_t M = ta ? n : m, K = ta ? m : n;
+        run_tc_gemm(c, ta != 0, dA, lda, M, K, dX, Np, Np, dT, Np, c->stream);  // warm-up
+        const int l0 = c->launches;
+        CK(cudaEventRecord(c->ev_a, c->stream));
+        for (int r = 0; r < reps; ++r) run_tc_gemm(c, ta != 0, dA, lda, M, K, dX, Np, Np, dT, Np, c->stream);
         CK(cudaEventRecord(c->ev_b, c->stream));
         CK(cudaEventSynchronize(c->ev_b));
         float ms;
