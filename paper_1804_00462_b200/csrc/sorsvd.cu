@@ -1226,11 +1226,11 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     record_stage(c, timing, 5);
 }
 
-std::string sor_key(const SorProblem& P, const void* dOmega, const void* dU, const void* dS, const void* dV) {
-    char buf[512];
-    snprintf(buf, sizeof buf, "sor:%p:%lld:%lld:%lld:%d:%d:%d:%p:%p:%p:%p",
-             P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m,
-             (long long)P.n, (long long)P.lda, P.k, P.ell, P.q, dOmega, dU, dS, dV);
+std::string sor_key(const SorProblem& P) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "sor:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.dtype,
+             P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m, (long long)P.n,
+             (long long)P.lda, P.k, P.ell, P.q);
     return buf;
 }
 
@@ -1269,14 +1269,18 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     P.m_global = d->m_global > 0 ? d->m_global : d->m;
     QrPlan *p1, *p2, *pg;
     SorBuffers b = prepare_sor(c, P, &p1, &p2, &pg);
-    const double* om = dOmega;
-    if (!om || !(d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+    // Omega and the outputs stay outside the captured graph (so the graph is
+    // keyed on A alone): Omega is staged into a context buffer before the
+    // launch, U / sigma / V are copied out after it.
+    double* om_in = dbuf(c, "omega_in", (size_t)P.n * P.ell);
+    if (dOmega && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+        CK(cudaMemcpyAsync(om_in, dOmega, (size_t)P.n * P.ell * 8, cudaMemcpyDeviceToDevice, c->stream));
+    } else {
         c->host_omega.resize((size_t)P.n * P.ell);
         sorsvd_host::gaussian_fill(c->host_omega.data(), (uint64_t)P.n * P.ell, d->seed, 0);
-        double* dom = dbuf(c, "omega_up", (size_t)P.n * P.ell);
-        CK(cudaMemcpyAsync(dom, c->host_omega.data(), (size_t)P.n * P.ell * 8, cudaMemcpyHostToDevice, c->stream));
-        om = dom;
+        CK(cudaMemcpyAsync(om_in, c->host_omega.data(), (size_t)P.n * P.ell * 8, cudaMemcpyHostToDevice, c->stream));
     }
+    const double* om = om_in;
     const bool timing = (d->flags & SORSVD_FLAG_STAGE_TIMES) != 0;
     const bool use_graph = !timing && !(d->flags & SORSVD_FLAG_NO_GRAPH) && !getenv("SORSVD_NO_GRAPH");
     CK(cudaEventRecord(c->ev_a, c->stream));
@@ -1292,6 +1296,8 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
                                  cudaMemcpyDeviceToDevice, c->stream));
         }
         enqueue_sor(c, P, b, p1, p2, pg, timing);
+    };
+    auto copy_out = [&]() {
         CK(cudaMemcpy2DAsync(dU, (size_t)P.k * 8, b.Uo, (size_t)P.Np * 8, (size_t)P.k * 8, (size_t)P.m,
                              cudaMemcpyDeviceToDevice, c->stream));
         CK(cudaMemcpy2DAsync(dV, (size_t)P.k * 8, b.Vo, (size_t)P.Np * 8, (size_t)P.k * 8, (size_t)P.n,
@@ -1299,9 +1305,10 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         CK(cudaMemcpyAsync(dS, b.Sk, (size_t)P.k * 8, cudaMemcpyDeviceToDevice, c->stream));
     };
     if (use_graph) {
-        const std::string key = sor_key(P, om, dU, dS, dV);
+        const std::string key = sor_key(P);
         auto it = c->graphs.find(key);
         if (it == c->graphs.end()) {
+            if (c->graphs.size() >= 32) invalidate_graphs(c);  // bound the cache (keys carry A's address)
             // warm-up run outside capture sets kernel attributes
             enqueue_all();
             CK(cudaStreamSynchronize(c->stream));
@@ -1332,6 +1339,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         enqueue_all();
         launches = c->launches - launches0;
     }
+    copy_out();
     CK(cudaEventRecord(c->ev_b, c->stream));
     if (st) {
         CK(cudaEventSynchronize(c->ev_b));
