@@ -312,6 +312,13 @@ def main():
     flops_step = 2.0 * m_global * n * ell * passes
     value = flops_step / (ms_per_step * 1e-3) / 1e9
 
+    # ---- per-stage device times of one extra call (no graph, STAGE_TIMES) ----
+    fs = P.sor_svd_power(A, k, scfg, omega=omega, ctx=ctx, m_global=m_global, stage_times=True)
+    stages = {key: round(fs.stats[key], 4) for key in ("ms_total", "ms_passes", "ms_qr", "ms_project", "ms_svd",
+                                                        "ms_basis")}
+    stages["jacobi_sweeps"] = fs.stats["jacobi_sweeps"]
+    stages["note"] = "un-graphed call with per-stage CUDA events; passes = the 2q+2 sketch passes"
+
     # ---- roofline of the dominant kernel (the A-streaming pass) ----
     import ctypes
     f32 = cfg.get("dtype") == "f32"
@@ -445,7 +452,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32/tf32" if f32 else "f64",
                 "data": "synthetic", "config": workload, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk,
+                "gpu_launches": launches, "clocks": clk, "stages_ms": stages,
                 "wall_s_timed_region": t_wall, "ms_steps": [round(x, 4) for x in ms_steps]}
         print(json.dumps(line), flush=True)
     if dist:
