@@ -203,12 +203,12 @@ def main():
     k = ell = cfg["k"]
     q = cfg["q"]
     passes = 2 * q + 3
+    from paper_1804_00462_b200.dist import row_partition
     if cfg["scaling"] == "weak":
         m_local, m_global = cfg["m"], cfg["m"] * world
     else:
         m_global = cfg["m"]
-        base, extra = divmod(m_global, world)
-        m_local = base + (1 if rank < extra else 0)
+        m_local = row_partition(m_global, world, rank)[1]
     n = cfg["n"]
     workload = dict(workload=cfg["desc"], m=m_global, n=n, k=k, ell=ell, q=q, passes=passes,
                     rows_per_rank=m_local, parallelism=f"row-sharded x{world}" if world > 1 else "single GPU",
@@ -252,17 +252,12 @@ def main():
 
     device = torch.device("cuda", local_rank)
     torch.cuda.set_device(device)
+    from paper_1804_00462_b200 import dist as D
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
-        idbuf = torch.zeros(128, dtype=torch.uint8, device=device)
-        if rank == 0:
-            idbuf.copy_(torch.frombuffer(bytearray(P.Context.nccl_unique_id()), dtype=torch.uint8).to(device))
-        dist.broadcast(idbuf, 0)
-        ctx = P.Context(local_rank, rank=rank, world=world, nccl_id=bytes(idbuf.cpu().numpy().tobytes()))
-    else:
-        ctx = P.Context(local_rank)
+    ctx = D.make_context(dist, local_rank, rank, world, device)
     stream = torch.cuda.current_stream(device)
     ctx.set_stream(stream.cuda_stream)
 
@@ -303,11 +298,7 @@ def main():
     clocks.recording = False
     clk = clocks.stop()
     ms_steps = [a.elapsed_time(b) for a, b in ev]
-    ms_total = sum(ms_steps)
-    if dist:
-        tt = torch.tensor([ms_total], device=device, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_total = float(tt.item())
+    ms_total = D.max_over_ranks(dist, sum(ms_steps), device)
     ms_per_step = ms_total / args.steps
     flops_step = 2.0 * m_global * n * ell * passes
     value = flops_step / (ms_per_step * 1e-3) / 1e9
@@ -417,11 +408,7 @@ def main():
         t0 = time.perf_counter()
         for i in range(args.steps):
             P.sor_svd_power(a_np, k, hcfg, ctx=ctx, m_global=m_global)
-        el = time.perf_counter() - t0
-        if dist:
-            tt = torch.tensor([el], device=device, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            el = float(tt.item())
+        el = D.max_over_ranks(dist, time.perf_counter() - t0, device)
         e2e = {"value": flops_step / (el / args.steps) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(m_local * n * esz + n * ell * 8),
                "d2h_bytes_per_step": int((m_local + n) * k * 8 + k * 8),

@@ -101,6 +101,13 @@ int sorsvd_ctx_create(int device, sorsvd_ctx** out);
 int sorsvd_nccl_unique_id(void* out128);
 int sorsvd_ctx_create_dist(int device, int rank, int world, const void* unique_id128, sorsvd_ctx** out);
 void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
+/* In-process emulation of `world` ranks on one device (tests): one context
+ * per rank, each driven by its own host thread; collectives become host
+ * barriers plus device sums. Same schedule as the NCCL path, graphs off. */
+typedef struct sorsvd_emu_group sorsvd_emu_group;
+int sorsvd_emu_group_create(int world, sorsvd_emu_group** out);
+void sorsvd_emu_group_destroy(sorsvd_emu_group* group);
+int sorsvd_ctx_create_emulated(int device, int rank, sorsvd_emu_group* group, sorsvd_ctx** out);
 const char* sorsvd_last_error(const sorsvd_ctx* ctx);
 /* Bind the context to a caller stream (cudaStream_t, may be 0 for the
  * context's own stream). */

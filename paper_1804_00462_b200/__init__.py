@@ -31,7 +31,7 @@ from . import _capi as C
 
 __all__ = [
     "SketchMethod", "SketchConfig", "LowRankApprox", "FlopVariant", "RpcaConfig", "RpcaResult", "Context",
-    "ShapeError", "ParameterError", "NumericalError", "CudaError", "NcclError", "UnsupportedError",
+    "ShapeError", "ParameterError", "NumericalError", "CudaError", "NcclError", "UnsupportedError", "EmuGroup",
     "sor_svd_power", "sor_svd", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
     "flop_estimate", "validate_sketch", "thin_qr", "full_svd", "matmul", "default_context", "version",
 ]
@@ -149,9 +149,13 @@ class Context:
     Multi-GPU: Context(device, rank=r, world=w, nccl_id=bytes) with the id from
     Context.nccl_unique_id() on rank 0, broadcast by the caller."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                 emu_group: Optional["EmuGroup"] = None):
         h = ctypes.c_void_p()
-        if world > 1:
+        if emu_group is not None:
+            world = emu_group.world
+            _check(C.lib().sorsvd_ctx_create_emulated(device, rank, emu_group.handle, ctypes.byref(h)))
+        elif world > 1:
             if nccl_id is None or len(nccl_id) != 128:
                 raise ParameterError("parameter: world > 1 needs the 128-byte NCCL unique id")
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -187,6 +191,22 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class EmuGroup:
+    """In-process emulation of `world` ranks on one GPU (one Context and one
+    host thread per rank); the multi-GPU schedule with host-barrier collectives."""
+
+    def __init__(self, world: int):
+        h = ctypes.c_void_p()
+        _check(C.lib().sorsvd_emu_group_create(world, ctypes.byref(h)))
+        self.handle = h
+        self.world = world
+
+    def close(self):
+        if getattr(self, "handle", None):
+            C.lib().sorsvd_emu_group_destroy(self.handle)
+            self.handle = None
 
 
 _default = {}

@@ -63,6 +63,9 @@ SIGNATURES = [
     ("sorsvd_nccl_unique_id", c_i32, [c_vp]),
     ("sorsvd_ctx_create_dist", c_i32, [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, ctypes.POINTER(c_vp)]),
     ("sorsvd_ctx_destroy", None, [c_vp]),
+    ("sorsvd_emu_group_create", c_i32, [ctypes.c_int, ctypes.POINTER(c_vp)]),
+    ("sorsvd_emu_group_destroy", None, [c_vp]),
+    ("sorsvd_ctx_create_emulated", c_i32, [ctypes.c_int, ctypes.c_int, c_vp, ctypes.POINTER(c_vp)]),
     ("sorsvd_last_error", ctypes.c_char_p, [c_vp]),
     ("sorsvd_set_stream", c_i32, [c_vp, c_vp]),
     ("sorsvd_ctx_rank", c_i32, [c_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),

@@ -14,6 +14,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -144,6 +146,31 @@ struct GraphEntry {
 
 }  // namespace
 
+// In-process multi-rank emulation on one device: `world` contexts (one host
+// thread each) share a group; the collectives become a host barrier plus
+// device sums in fixed rank order. Exercises the multi-GPU schedule (sharded
+// passes, cross-rank TSQR tree, all-reduce placement) on a single GPU; CUDA
+// graphs are disabled for emulated contexts (host barriers cannot be captured).
+struct sorsvd_emu_group {
+    int world = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long generation = 0;
+    std::vector<void*> bufs;  // per-rank buffer registered for the current collective
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
 struct sorsvd_ctx {
     int device = 0;
     int rank = 0, world = 1;
@@ -157,6 +184,7 @@ struct sorsvd_ctx {
     std::map<std::string, std::unique_ptr<QrPlan>> plans;
     std::map<std::string, GraphEntry> graphs;
     ncclComm_t comm = nullptr;
+    sorsvd_emu_group* emu = nullptr;  // in-process multi-rank emulation (tests)
     int launches = 0;
     bool capturing = false;
     std::vector<double> host_omega;
@@ -1091,10 +1119,62 @@ SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan**
     return b;
 }
 
-void allreduce_sum(sorsvd_ctx* c, double* buf, size_t count, cudaStream_t s) {
-    if (c->world <= 1) return;
-    NCK(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, s));
+__global__ void emu_sum_kernel(void* const* bufs, int world, size_t count, int f32) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+        if (f32) {
+            float acc = 0.f;
+            for (int r = 0; r < world; ++r) acc += static_cast<float*>(bufs[r])[i];
+            for (int r = 0; r < world; ++r) static_cast<float*>(bufs[r])[i] = acc;
+        } else {
+            double acc = 0.0;
+            for (int r = 0; r < world; ++r) acc += static_cast<double*>(bufs[r])[i];
+            for (int r = 0; r < world; ++r) static_cast<double*>(bufs[r])[i] = acc;
+        }
+    }
 }
+
+// Sum-all-reduce of a device buffer across ranks (NCCL, or the emulation group).
+void comm_allreduce(sorsvd_ctx* c, void* buf, size_t count, bool f32, cudaStream_t s) {
+    if (c->world <= 1) return;
+    if (c->comm) {
+        NCK(nccl().AllReduce(buf, buf, count, f32 ? ncclFloat : ncclDouble, ncclSum, c->comm, s));
+        return;
+    }
+    if (!c->emu) throw Error{SORSVD_ERR_INTERNAL, "multi-rank context without a communicator"};
+    sorsvd_emu_group* g = c->emu;
+    CK(cudaStreamSynchronize(s));
+    g->bufs[c->rank] = buf;
+    g->barrier();
+    if (c->rank == 0) {
+        void** dp = nullptr;
+        CK(cudaMalloc(&dp, sizeof(void*) * g->world));
+        CK(cudaMemcpy(dp, g->bufs.data(), sizeof(void*) * g->world, cudaMemcpyHostToDevice));
+        emu_sum_kernel<<<std::min<size_t>(cdiv(count, 256), (size_t)c->num_sms * 4), 256, 0, s>>>(dp, g->world, count,
+                                                                                                    f32 ? 1 : 0);
+        check_launch(c);
+        CK(cudaStreamSynchronize(s));
+        CK(cudaFree(dp));
+    }
+    g->barrier();
+}
+
+// All-gather of `count` doubles per rank into recv (rank r at r*count).
+void comm_allgather(sorsvd_ctx* c, const double* send, double* recv, size_t count, cudaStream_t s) {
+    if (c->comm) {
+        NCK(nccl().AllGather(send, recv, count, ncclDouble, c->comm, s));
+        return;
+    }
+    sorsvd_emu_group* g = c->emu;
+    CK(cudaStreamSynchronize(s));
+    g->bufs[c->rank] = const_cast<double*>(send);
+    g->barrier();
+    for (int r = 0; r < g->world; ++r)
+        CK(cudaMemcpyAsync(recv + (size_t)r * count, g->bufs[r], count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    g->barrier();
+}
+
+void allreduce_sum(sorsvd_ctx* c, double* buf, size_t count, cudaStream_t s) { comm_allreduce(c, buf, count, false, s); }
 
 void record_stage(sorsvd_ctx* c, bool timing, int idx) {
     if (timing) CK(cudaEventRecord(c->ev_st[idx], c->stream));
@@ -1110,7 +1190,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         if (P.dtype == SORSVD_F32) {  // TF32 tensor-core passes (tc_gemm_f32.cuh)
             run_tc_gemm(c, false, P.Af, P.lda, P.m, P.n, b.T2f, P.Np32, P.Np32, b.T1f, P.Np32, s);
             run_tc_gemm(c, true, P.Af, P.lda, P.n, P.m, b.T1f, P.Np32, P.Np32, b.T2f, P.Np32, s);
-            if (c->world > 1) NCK(nccl().AllReduce(b.T2f, b.T2f, (size_t)P.n * P.Np32, ncclFloat, ncclSum, c->comm, s));
+            comm_allreduce(c, b.T2f, (size_t)P.n * P.Np32, true, s);
             continue;
         }
         GemmCall g1;  // T1 = A * T2     (sketch.hpp:95)
@@ -1150,7 +1230,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         qr_factor(c, p1, b.T1, Np, b.Q1, Np, false, s);
         const int L1 = (int)p1->nodes.size() - 1;
         double* Rg = dbuf(c, "Rg", (size_t)c->world * ell * ell);
-        NCK(nccl().AllGather(p1->R[L1], Rg, (size_t)ell * ell, ncclDouble, c->comm, s));
+        comm_allgather(c, p1->R[L1], Rg, (size_t)ell * ell, s);
         qr_factor(c, pg, nullptr, 0, nullptr, 0, true, s, Rg);
         qr_formq(c, pg, nullptr, 0, nullptr, 0, nullptr, s, true);
         const double* Cg = qr_leaf_factors(pg, false) + (size_t)c->rank * ell * Np;
@@ -1282,7 +1362,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     }
     const double* om = om_in;
     const bool timing = (d->flags & SORSVD_FLAG_STAGE_TIMES) != 0;
-    const bool use_graph = !timing && !(d->flags & SORSVD_FLAG_NO_GRAPH) && !getenv("SORSVD_NO_GRAPH");
+    const bool use_graph = !timing && !c->emu && !(d->flags & SORSVD_FLAG_NO_GRAPH) && !getenv("SORSVD_NO_GRAPH");
     CK(cudaEventRecord(c->ev_a, c->stream));
     const int launches0 = c->launches;
     int launches = 0;
@@ -1656,6 +1736,35 @@ int sorsvd_ctx_create_dist(int device, int rank, int world, const void* unique_i
             std::memcpy(&id, unique_id128, sizeof(id));
             NCK(nccl().CommInitRank(&c->comm, world, id, rank));
         }
+    });
+    if (rc != SORSVD_OK) {
+        delete c;
+        *out = nullptr;
+        return rc;
+    }
+    *out = c;
+    return SORSVD_OK;
+}
+
+int sorsvd_emu_group_create(int world, sorsvd_emu_group** out) {
+    if (!out || world < 1) return SORSVD_ERR_PARAMETER;
+    auto* g = new sorsvd_emu_group();
+    g->world = world;
+    g->bufs.assign(world, nullptr);
+    *out = g;
+    return SORSVD_OK;
+}
+
+void sorsvd_emu_group_destroy(sorsvd_emu_group* g) { delete g; }
+
+int sorsvd_ctx_create_emulated(int device, int rank, sorsvd_emu_group* g, sorsvd_ctx** out) {
+    if (!out || !g || rank < 0 || rank >= g->world) return SORSVD_ERR_PARAMETER;
+    auto* c = new sorsvd_ctx();
+    int rc = guarded(nullptr, [&] {
+        ctx_init(c, device);
+        c->rank = rank;
+        c->world = g->world;
+        c->emu = g;
     });
     if (rc != SORSVD_OK) {
         delete c;

@@ -1,0 +1,106 @@
+"""GPU (single device): the row-sharded multi-GPU schedule, emulated in one
+process — G contexts in one EmuGroup, one host thread each, every rank
+holding a contiguous row block of A. Checks the sharded
+result (U row blocks, replicated sigma and V) against the oracle on the full
+matrix, and that every rank returns the same sigma and V."""
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import sorsvd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_sharded(P, torch, A, k, cfg, world, dtype=None):
+    m = A.shape[0]
+    g = P.EmuGroup(world)
+    base, extra = divmod(m, world)
+    bounds = []
+    r0 = 0
+    for r in range(world):
+        cnt = base + (1 if r < extra else 0)
+        bounds.append((r0, r0 + cnt))
+        r0 += cnt
+    ctxs = [P.Context(0, rank=r, emu_group=g) for r in range(world)]
+    out = [None] * world
+    err = [None] * world
+
+    def work(r):
+        try:
+            a, b = bounds[r]
+            blk = torch.from_numpy(np.ascontiguousarray(A[a:b])).cuda()
+            if dtype is not None:
+                blk = blk.to(dtype)
+            out[r] = P.sor_svd_power(blk, k, cfg, ctx=ctxs[r], m_global=m)
+            torch.cuda.synchronize()
+        except Exception as e:  # surface in the main thread
+            err[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    for c in ctxs:
+        c.close()
+    g.close()
+    u = np.vstack([o.u.cpu().numpy() for o in out])
+    return out, u
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_00462_b200 as P
+    return P, torch
+
+
+@pytest.mark.parametrize("world,m,n,k,q", [(2, 3000, 800, 20, 1), (4, 6000, 500, 32, 0), (3, 2999, 700, 16, 2),
+                                           (8, 8000, 400, 10, 1)])
+def test_sharded_matches_oracle(env, world, m, n, k, q):
+    P, torch = env
+    A = O.gen_lowrank_decay(m, n, 40, lambda j: 2.0 ** (-j / 4), 1e-3, m + world)
+    cfg = O.SketchConfig(k, q, 11)
+    base, ds, dl = O.perturbation_floor(A, k, cfg)
+    out, u = _run_sharded(P, torch, A, k, P.SketchConfig(k, q, 11), world)
+    s0 = out[0].sigma.cpu().numpy()
+    v0 = out[0].v.cpu().numpy()
+    for o in out[1:]:  # replicated parts agree across ranks
+        np.testing.assert_array_equal(o.sigma.cpu().numpy(), s0)
+        np.testing.assert_array_equal(o.v.cpu().numpy(), v0)
+    es = O.sigma_rel_err(s0, base.sigma)
+    assert np.all(es <= np.maximum(1e-10, 10 * np.maximum.accumulate(ds))), es
+    lr = O.lowrank_rel_diff(u, s0, v0, base.u, base.sigma, base.v)
+    assert lr <= max(1e-9, 10 * dl), lr
+
+
+def test_sharded_c2_shape_householder_tree(env):
+    """Ill-conditioned sketch (C2-like, q = 1): CholeskyQR2 is rejected, the
+    cross-rank Householder TSQR tree (all-gather of R factors) runs."""
+    P, torch = env
+    A = O.gen_c2(2, n=1000)
+    cfg = O.SketchConfig(40, 1, 5)
+    base, ds, dl = O.perturbation_floor(A, 40, cfg)
+    out, u = _run_sharded(P, torch, A, 40, P.SketchConfig(40, 1, 5), 4)
+    s0 = out[0].sigma.cpu().numpy()
+    env_ = np.maximum.accumulate(ds)
+    jd = int(np.searchsorted(env_, 1e-10))
+    es = O.sigma_rel_err(s0, base.sigma)
+    assert jd >= 10 and np.all(es[:jd] <= np.maximum(1e-10, 10 * env_[:jd])), es[:jd]
+
+
+def test_sharded_fp32(env):
+    P, torch = env
+    A = O.gen_lowrank_decay(8000, 1024, 64, lambda j: 10.0 ** (-j / 32.0), 1e-3, 9).astype(np.float32)
+    cfg = O.SketchConfig(64, 1, 3)
+    base = O.sor_svd_power(A.astype(np.float64), 64, cfg)
+    out, u = _run_sharded(P, torch, A, 64, P.SketchConfig(64, 1, 3), 2, dtype=torch.float32)
+    s0 = out[0].sigma.cpu().numpy()
+    assert O.sigma_rel_err(s0, base.sigma)[:32].max() <= 3e-3
