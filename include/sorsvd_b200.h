@@ -69,7 +69,7 @@ typedef struct sorsvd_desc {
     int32_t k;        /* target rank */
     int32_t ell;      /* sketch size, k <= ell < min(m_global, n) */
     int32_t q;        /* power iterations */
-    int32_t single_pass; /* SketchConfig::single_pass (not supported yet -> SORSVD_ERR_UNSUPPORTED) */
+    int32_t single_pass; /* SketchConfig::single_pass: M_approx core, 2q+2 passes (sketch.hpp:100-104) */
     uint64_t seed;    /* Omega = gaussian_matrix(n, ell, seed) unless OMEGA_GIVEN */
     int32_t dtype;    /* sorsvd_dtype of A (SORSVD_F64 only in this build) */
     uint32_t flags;

@@ -35,6 +35,8 @@
 #include "tc_gemm_f32.cuh"
 #include "cholqr_f64.cuh"
 #include "cqr_f64.cuh"
+#include "mapprox_f64.cuh"
+#include <cfloat>
 
 using namespace sorsvd_dev;
 
@@ -1072,6 +1074,8 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
 // ------------------------------------------------------------- pipeline ----
 struct SorBuffers {
     double *T1, *T2, *Q1, *Q2, *Y, *Mk, *Uk, *Vk, *Sk, *Uo, *Vo;
+    double *T2pre = nullptr, *Lhs = nullptr, *Core = nullptr, *Uc = nullptr, *Vc = nullptr, *Sc = nullptr,
+           *Pinv = nullptr;  // single_pass (m_approx)
     float *T1f = nullptr, *T2f = nullptr, *Q2f = nullptr, *Yf = nullptr;  // FP32 path
     int* sweeps;
 };
@@ -1085,6 +1089,7 @@ struct SorProblem {
     int Np;            // FP64 padded width (npad)
     int Np32;          // FP32 padded width for the tcgen05 passes (npad32)
     int64_t m_global;
+    bool single_pass;
 };
 
 SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan** p2, QrPlan** pg) {
@@ -1102,6 +1107,15 @@ SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan**
     b.Uo = dbuf(c, "Uo", (size_t)P.m * Np);
     b.Vo = dbuf(c, "Vo", (size_t)P.n * Np);
     b.sweeps = reinterpret_cast<int*>(dbuf(c, "sweeps", 1));
+    if (P.single_pass) {
+        b.T2pre = dbuf(c, "T2pre", (size_t)P.n * Np);
+        b.Lhs = dbuf(c, "Lhs", (size_t)Np * Np);
+        b.Core = dbuf(c, "Core", (size_t)Np * Np);
+        b.Uc = dbuf(c, "Uc", (size_t)Np * Np);
+        b.Vc = dbuf(c, "Vc", (size_t)Np * Np);
+        b.Sc = dbuf(c, "Sc", (size_t)Np);
+        b.Pinv = dbuf(c, "Pinv", (size_t)Np * Np);
+    }
     if (P.dtype == SORSVD_F32) {
         auto fbuf = [&](const char* nm, size_t count) { return reinterpret_cast<float*>(dbuf(c, nm, count / 2 + 2, true)); };
         b.T1f = fbuf("T1f", (size_t)P.m * P.Np32);
@@ -1180,6 +1194,45 @@ void record_stage(sorsvd_ctx* c, bool timing, int idx) {
     if (timing) CK(cudaEventRecord(c->ev_st[idx], c->stream));
 }
 
+// M_approx = (Q1^T T1) pinv(Q2^T T2pre)   (sketch.hpp:54-58,100-101; dense.hpp:138-157).
+// No pass over A: the single-pass variant trades the projection for the
+// pseudo-inverse correction of the ell x ell core.
+void enqueue_m_approx(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, cudaStream_t s) {
+    const int Np = P.Np, ell = P.ell;
+    GemmCall g;  // lhs = Q1^T T1 (row-sharded operands: summed over ranks)
+    g.ta = true;
+    g.A = b.Q1;
+    g.lda = Np;
+    g.M = ell;
+    g.K = P.m;
+    g.B = b.T1;
+    g.ldb = Np;
+    g.N = Np;
+    g.C = b.Lhs;
+    g.ldc = Np;
+    run_gemm(c, g, s);
+    allreduce_sum(c, b.Lhs, (size_t)ell * Np, s);
+    GemmCall h;  // core = Q2^T W (replicated operands)
+    h.ta = true;
+    h.A = b.Q2;
+    h.lda = Np;
+    h.M = ell;
+    h.K = P.n;
+    h.B = b.T2pre;
+    h.ldb = Np;
+    h.N = Np;
+    h.C = b.Core;
+    h.ldc = Np;
+    run_gemm(c, h, s);
+    run_jacobi(c, ell, b.Core, Np, b.Uc, Np, b.Sc, b.Vc, Np, b.sweeps, s);
+    const dim3 grid((unsigned)cdiv(ell, 128), (unsigned)ell);
+    const double tol = (double)ell * DBL_EPSILON;  // pseudo_inverse default cutoff (dense.hpp:155-157)
+    small_gemm_kernel<<<grid, 128, 0, s>>>(b.Vc, Np, b.Uc, Np, true, b.Sc, tol, b.Pinv, Np, ell);
+    check_launch(c);
+    small_gemm_kernel<<<grid, 128, 0, s>>>(b.Lhs, Np, b.Pinv, Np, false, nullptr, 0.0, b.Mk, Np, ell);
+    check_launch(c);
+}
+
 // Enqueue one sor_svd_power on c->stream (T2 must already hold Omega, padded).
 void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, QrPlan* pg,
                  bool timing) {
@@ -1187,6 +1240,12 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     const int Np = P.Np, ell = P.ell;
     record_stage(c, timing, 0);
     for (int i = 0; i <= P.q; ++i) {
+        if (P.single_pass && i == P.q) {  // t2_pre: the row sketch entering the last iteration (sketch.hpp:94)
+            if (P.dtype == SORSVD_F32)
+                cast_to_f64(c, b.T2f, P.Np32, b.T2pre, Np, P.n, ell, s);
+            else
+                CK(cudaMemcpyAsync(b.T2pre, b.T2, (size_t)P.n * Np * 8, cudaMemcpyDeviceToDevice, s));
+        }
         if (P.dtype == SORSVD_F32) {  // TF32 tensor-core passes (tc_gemm_f32.cuh)
             run_tc_gemm(c, false, P.Af, P.lda, P.m, P.n, b.T2f, P.Np32, P.Np32, b.T1f, P.Np32, s);
             run_tc_gemm(c, true, P.Af, P.lda, P.n, P.m, b.T1f, P.Np32, P.Np32, b.T2f, P.Np32, s);
@@ -1242,6 +1301,9 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     CK(cudaEventRecord(c->ev_join, c->side));
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     record_stage(c, timing, 2);
+    if (P.single_pass) {
+        enqueue_m_approx(c, P, b, s);
+    } else {
     // M = Q1^T (A Q2)   (sketch.hpp:100-102)
     if (P.dtype == SORSVD_F32) {
         cast_to_f32(c, b.Q2, Np, b.Q2f, P.Np32, P.n, ell, s);
@@ -1273,6 +1335,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         h.ldc = Np;
         run_gemm(c, h, s);
         allreduce_sum(c, b.Mk, (size_t)ell * Np, s);
+    }
     }
     record_stage(c, timing, 3);
     // truncated_svd(M, k)   (sketch.hpp:103)
@@ -1308,7 +1371,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
 
 std::string sor_key(const SorProblem& P) {
     char buf[256];
-    snprintf(buf, sizeof buf, "sor:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.dtype,
+    snprintf(buf, sizeof buf, "sor:%d:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.dtype, (int)P.single_pass,
              P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m, (long long)P.n,
              (long long)P.lda, P.k, P.ell, P.q);
     return buf;
@@ -1323,7 +1386,6 @@ void validate(const sorsvd_desc* d) {
         throw Error{SORSVD_ERR_PARAMETER, e};
     if ((d->flags & SORSVD_FLAG_BASIC) && d->q != 0)
         throw Error{SORSVD_ERR_PARAMETER, "parameter: sor_svd requires q == 0; use sor_svd_power"};
-    if (d->single_pass) throw Error{SORSVD_ERR_UNSUPPORTED, "single_pass (m_approx) is not implemented in this build"};
     if (d->dtype != SORSVD_F64 && d->dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
     if (d->dtype == SORSVD_F32 && (d->lda % 4))
         throw Error{SORSVD_ERR_SHAPE, "shape: fp32 A needs lda % 4 == 0 (16-byte rows for TMA)"};
@@ -1347,6 +1409,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     P.q = d->q;
     P.Np = npad(d->ell);
     P.m_global = d->m_global > 0 ? d->m_global : d->m;
+    P.single_pass = d->single_pass != 0;
     QrPlan *p1, *p2, *pg;
     SorBuffers b = prepare_sor(c, P, &p1, &p2, &pg);
     // Omega and the outputs stay outside the captured graph (so the graph is
@@ -1426,7 +1489,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
         st->ms_total = ms;
-        const int passes = 2 * d->q + 3;
+        const int passes = d->single_pass ? 2 * d->q + 2 : 2 * d->q + 3;  // sketch.hpp:104
         st->passes = passes;
         st->method = d->q == 0 ? SORSVD_SOR : SORSVD_SOR_POWER;
         st->flops_passes = 2.0 * (double)d->m * d->n * d->ell * passes;

@@ -60,6 +60,19 @@ def main():
         g[name + "_u"], g[name + "_s"], g[name + "_v"] = f.u, f.sigma, f.v
         meta[name] = dict(m=m, n=n, k=k, ell=ell, q=q, seed=seed, passes=f.passes, method=f.method)
         cases.append(name)
+    # single_pass = true (sketch.hpp:54-58,100-104): M_approx core, 2q+2 passes
+    sp_cases = []
+    for (m, n, k, ell, q, seed, aseed) in [(60, 40, 5, 8, 0, 21, 6), (80, 50, 6, 10, 1, 22, 7), (50, 90, 4, 6, 2, 23, 8)]:
+        name = f"sp_{m}x{n}_k{k}_l{ell}_q{q}"
+        x = O.gaussian_matrix(m, 6, O.sub_seed(aseed, 1))
+        y = O.gaussian_matrix(n, 6, O.sub_seed(aseed, 2))
+        e = O.gaussian_matrix(m, n, O.sub_seed(aseed, 3))
+        A = x @ y.T + 1e-3 * e
+        f = Ref.sor_svd_power(A, k, O.SketchConfig(ell, q, seed, single_pass=True))
+        g[name + "_A"] = A
+        g[name + "_u"], g[name + "_s"], g[name + "_v"] = f.u, f.sigma, f.v
+        meta[name] = dict(m=m, n=n, k=k, ell=ell, q=q, seed=seed, passes=f.passes, method=f.method, single_pass=True)
+        sp_cases.append(name)
     # rank-1: 100 x 80, k = 1, ell = 4
     uu = O.gaussian_matrix(100, 1, 91)
     vv = O.gaussian_matrix(80, 1, 92)
@@ -82,7 +95,7 @@ def main():
                            converged=rr.converged, mu0=rr.mu0, ell=10, q=1, seed=5, lam=float(cfg.lam))
     np.savez_compressed(os.path.join(OUT, "golden_ref.npz"), **g)
     with open(os.path.join(OUT, "golden_meta.json"), "w") as fh:
-        json.dump({"cases": cases, "meta": meta, "blas": Ref and O.ref_lib().ref_blas_config().decode()}, fh, indent=1)
+        json.dump({"cases": cases, "sp_cases": sp_cases, "meta": meta, "blas": Ref and O.ref_lib().ref_blas_config().decode()}, fh, indent=1)
     print("wrote", len(g), "arrays")
 
 

@@ -227,6 +227,39 @@ def test_ell_greater_than_k(P):
     _check_parity(f, base.sigma, base.u, base.v, ds, dl)
 
 
+@pytest.mark.parametrize("m,n,k,ell,q", [(400, 300, 10, 10, 0), (300, 400, 10, 14, 2), (2001, 1500, 50, 60, 1),
+                                         (1000, 1000, 20, 20, 0), (64, 1000, 8, 8, 1)])
+def test_single_pass_vs_oracle(P, m, n, k, ell, q):
+    # single_pass = true: M_approx = Q1^T T1 pinv(Q2^T T2_pre) (sketch.hpp:54-58,100-104)
+    A = O.gen_lowrank_decay(m, n, 40, lambda j: 2.0 ** (-j / 4), 1e-3, m + 3 * n)
+    cfg = O.SketchConfig(ell, q, 29, single_pass=True)
+    base, ds, dl = O.perturbation_floor(A, k, cfg)
+    f = P.sor_svd_power(A, k, P.SketchConfig(ell, q, 29, single_pass=True))
+    assert f.passes == 2 * q + 2 and base.passes == 2 * q + 2
+    _check_parity(f, base.sigma, base.u, base.v, ds, dl)
+
+
+def test_single_pass_golden(P, golden):
+    g, meta = golden
+    for name in meta.get("sp_cases", []):
+        md = meta["meta"][name]
+        A = g[name + "_A"]
+        f = P.sor_svd_power(A, md["k"], P.SketchConfig(md["ell"], md["q"], md["seed"], single_pass=True))
+        assert f.passes == md["passes"]
+        _, ds, dl = O.perturbation_floor(A, md["k"], O.SketchConfig(md["ell"], md["q"], md["seed"], single_pass=True))
+        _check_parity(f, g[name + "_s"], g[name + "_u"], g[name + "_v"], ds, dl)
+
+
+def test_single_pass_device_f32(P):
+    import torch
+    A = O.gen_lowrank_decay(3000, 2000, 64, lambda j: 10.0 ** (-j / 64.0), 1e-3, 77)
+    cfg = O.SketchConfig(64, 1, 5, single_pass=True)
+    base = O.sor_svd_power(A.astype(np.float32).astype(np.float64), 64, cfg)
+    f = P.sor_svd_power(torch.from_numpy(A.astype(np.float32)).cuda(), 64, P.SketchConfig(64, 1, 5, single_pass=True))
+    es = O.sigma_rel_err(f.sigma.cpu().numpy(), base.sigma)
+    assert es.max() <= 3e-3, es.max()
+
+
 def test_errors(P):
     A = np.ones((10, 8))
     with pytest.raises(P.ParameterError):
@@ -241,8 +274,6 @@ def test_errors(P):
         P.sor_svd(A, 1, P.SketchConfig(2, 1, 1))         # sor_svd requires q == 0
     with pytest.raises(P.ParameterError):
         P.sor_svd_power(np.ones((1, 8)), 1, P.SketchConfig(1, 0, 1))
-    with pytest.raises(P.UnsupportedError):
-        P.sor_svd_power(A, 2, P.SketchConfig(3, 0, 1, single_pass=True))
     # the context survives errors
     f = P.sor_svd_power(O.gaussian_matrix(10, 8, 1), 2, P.SketchConfig(3, 0, 1))
     assert np.all(np.isfinite(f.sigma))

@@ -69,6 +69,20 @@ def test_sor_svd_power_port_matches_reference_golden(golden):
         assert O.lowrank_rel_diff(f.u, f.sigma, f.v, g[name + "_u"], g[name + "_s"], g[name + "_v"]) <= max(1e-10, 10 * dl), name
 
 
+def test_single_pass_port_matches_reference_golden(golden):
+    # m_approx + pseudo_inverse (sketch.hpp:54-58, dense.hpp:138-157), 2q+2 passes
+    g, meta = golden
+    assert len(meta["sp_cases"]) == 3
+    for name in meta["sp_cases"]:
+        md = meta["meta"][name]
+        cfg = O.SketchConfig(md["ell"], md["q"], md["seed"], single_pass=True)
+        f = O.sor_svd_power(g[name + "_A"], md["k"], cfg)
+        assert f.passes == md["passes"] == 2 * md["q"] + 2
+        _, ds, dl = O.perturbation_floor(g[name + "_A"], md["k"], cfg)
+        assert np.all(O.sigma_rel_err(f.sigma, g[name + "_s"]) <= np.maximum(1e-11, 10 * ds)), name
+        assert O.lowrank_rel_diff(f.u, f.sigma, f.v, g[name + "_u"], g[name + "_s"], g[name + "_v"]) <= max(1e-10, 10 * dl), name
+
+
 def test_rank1_exact(golden):
     # rank-1 100x80, k=1, ell=4 -> error <= 1e-10
     g, _ = golden
