@@ -58,6 +58,9 @@ typedef enum sorsvd_flop_variant {
 #define SORSVD_FLAG_NO_GRAPH 0x2u     /* issue kernels directly (no CUDA-graph replay) */
 #define SORSVD_FLAG_STAGE_TIMES 0x4u  /* per-stage CUDA-event times in stats (implies NO_GRAPH) */
 #define SORSVD_FLAG_BASIC 0x8u        /* sor_svd semantics: require q == 0 (sketch.hpp:116-119) */
+#define SORSVD_FLAG_TF32 0x10u        /* dtype F32: passes on the TF32 tensor cores (fast; ~1e-3 relative,
+                                         resolves only sketch directions above the TF32 rounding level).
+                                         Default for F32: FP64 arithmetic on the FP32-stored A. */
 
 typedef struct sorsvd_ctx sorsvd_ctx;
 

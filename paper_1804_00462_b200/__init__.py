@@ -272,15 +272,20 @@ def _desc(m, n, lda, k, cfg: SketchConfig, flags: int, m_global: int = 0, dtype:
 # -------------------------------------------------------------- hot path --
 def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Context] = None,
                   stage_times: bool = False, use_graph: bool = True, m_global: int = 0,
-                  _basic: bool = False) -> LowRankApprox:
+                  _basic: bool = False, fp32_mode: str = "fp64") -> LowRankApprox:
     """Subspace-orbit randomized SVD with q power iterations (sketch.hpp:87).
 
     a: numpy (m, n) on the host or a CUDA torch tensor; float64 runs the FP64
-    path, float32 runs the passes on the TF32 tensor cores (QR and the core
-    SVD stay FP64; results are FP64).
+    path. float32 input is kept in FP32 (half the bytes); fp32_mode="fp64"
+    (default) computes the passes in FP64 on the DMMA pipe, fp32_mode="tf32"
+    on the TF32 tensor cores (fast; ~1e-3 relative and only the sketch
+    directions above the TF32 rounding level are resolved). QR and
+    the core SVD are FP64 and results are FP64 either way.
     omega: optional (n, ell) test matrix; default gaussian_matrix(n, ell, seed)
     exactly as the reference draws it (sketch.hpp:90)."""
-    flags = 0
+    if fp32_mode not in ("fp64", "tf32"):
+        raise ParameterError("parameter: fp32_mode must be 'fp64' or 'tf32'")
+    flags = C.FLAG_TF32 if fp32_mode == "tf32" else 0
     if omega is not None:
         flags |= C.FLAG_OMEGA_GIVEN
     if stage_times:
@@ -342,7 +347,7 @@ def sor_svd(a, k: int, cfg: SketchConfig, **kw) -> LowRankApprox:
 
 # ----------------------------------------------------- stage entry points --
 def thin_qr(t, ctx: Optional[Context] = None):
-    """dense.hpp:114 on a CUDA float64 tensor (tall-skinny, k <= 256): (q, r)."""
+    """dense.hpp:114 on a CUDA float64 tensor (tall-skinny, k <= 512): (q, r)."""
     import torch
     if not _is_torch_cuda(t) or t.dtype != torch.float64:
         raise ShapeError("shape: thin_qr expects a CUDA float64 tensor")

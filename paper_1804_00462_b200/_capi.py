@@ -26,6 +26,7 @@ FLAG_OMEGA_GIVEN = 0x1
 FLAG_NO_GRAPH = 0x2
 FLAG_STAGE_TIMES = 0x4
 FLAG_BASIC = 0x8
+FLAG_TF32 = 0x10
 
 
 class SorsvdDesc(ctypes.Structure):

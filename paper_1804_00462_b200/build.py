@@ -19,7 +19,7 @@ LIB = os.path.join(OUT_DIR, "libsorsvd_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["sorsvd.cu", "host_rng.cpp"]
-HEADERS = ["common.cuh", "gemm_f64.cuh", "cqr_f64.cuh", "cholqr_f64.cuh", "jacobi_f64.cuh", "rpca_f64.cuh", "peaks.cuh", "tc_gemm_f32.cuh", "host_api.hpp"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h")))
 
 
 def _stale() -> bool:

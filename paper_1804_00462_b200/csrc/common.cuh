@@ -34,6 +34,17 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
                  "r"(src_bytes));
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+                 "r"(src_bytes));
+}
+// one element (8 or 4 bytes), zero-filled when !ok
+__device__ __forceinline__ void cp_async_elem(double* smem, const double* gmem, bool ok) {
+    cp_async8(smem, gmem, ok ? 8 : 0);
+}
+__device__ __forceinline__ void cp_async_elem(float* smem, const float* gmem, bool ok) {
+    cp_async4(smem, gmem, ok ? 4 : 0);
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {

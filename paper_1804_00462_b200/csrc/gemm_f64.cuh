@@ -16,13 +16,19 @@
 // A and B tiles are staged through a 4-stage cp.async (LDGSTS) ring in shared
 // memory with +4-double row padding so every fragment read is bank-conflict
 // free. A is streamed exactly once per pass (the dominant HBM traffic).
+//
+// A may also be FP32 (AT = float: Config 3/5 inputs stored in single
+// precision): the tile is staged as floats (half the HBM bytes) and widened
+// to FP64 when the fragments are read, so the arithmetic is the same FP64
+// DMMA as for double inputs (the power iteration needs it: see DESIGN.md,
+// "FP32 inputs").
 #pragma once
 #include "common.cuh"
 
 namespace sorsvd_dev {
 
 struct GemmArgs {
-    const double* A;
+    const void* A;  // double, or float for the FP32-storage kernels
     int64_t lda;
     const double* B;
     int64_t ldb;
@@ -45,24 +51,27 @@ constexpr int kGemmThreads = 256;
 constexpr int kGemmBK = 16;
 constexpr int kGemmStages = 4;
 
-template <int FM, int FN, bool TA>
+template <int FM, int FN, bool TA, typename AT = double>
 struct GemmShape {
     static constexpr int BM = 8 * 8 * FM;
     static constexpr int BN = 8 * FN;
     static constexpr int BK = kGemmBK;
-    static constexpr int LDA_S = TA ? (BM + 4) : (BK + 4);  // padded smem strides (== 4 mod 8)
+    static constexpr int EPV = 16 / (int)sizeof(AT);  // A elements per 16-byte vector
+    // padded smem strides: fragment reads conflict free (doubles: == 4 mod 8; floats: +4 / +8 words)
+    static constexpr int LDA_S = TA ? (BM + (sizeof(AT) == 4 ? 8 : 4)) : (BK + 4);
     static constexpr int LDB_S = BN + 4;
-    static constexpr int A_STAGE = TA ? BK * LDA_S : BM * LDA_S;
+    static constexpr int A_STAGE = TA ? BK * LDA_S : BM * LDA_S;  // elements of AT
+    static constexpr int A_BYTES = ((A_STAGE * (int)sizeof(AT) + 15) / 16) * 16;
     static constexpr int B_STAGE = BK * LDB_S;
-    static constexpr int STAGE = A_STAGE + B_STAGE;
-    static constexpr size_t SMEM = (size_t)kGemmStages * STAGE * sizeof(double);
+    static constexpr int STAGE_BYTES = A_BYTES + B_STAGE * 8;
+    static constexpr size_t SMEM = (size_t)kGemmStages * STAGE_BYTES;
 };
 
-template <int FM, int FN, bool TA, bool V16>
+template <int FM, int FN, bool TA, bool V16, typename AT = double>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
-    using S = GemmShape<FM, FN, TA>;
+    using S = GemmShape<FM, FN, TA, AT>;
     if (p.pred && *p.pred == p.pred_skip) return;
-    extern __shared__ __align__(128) double smem[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
 
     int64_t row0, rows;
@@ -77,58 +86,63 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
     }
     const int ncol0 = blockIdx.y * S::BN;
     const double* __restrict__ Bp = p.B + seg * p.b_seg_stride + ncol0;
-    const double* __restrict__ Ap = p.A;
+    const AT* __restrict__ Ap = static_cast<const AT*>(p.A);
+    constexpr int EPV = S::EPV;
     const int64_t kBegin = (int64_t)blockIdx.z * p.k_chunk;
     int64_t kEnd = kBegin + p.k_chunk;
     if (kEnd > p.K) kEnd = p.K;
     const int KT = kEnd > kBegin ? (int)((kEnd - kBegin + S::BK - 1) / S::BK) : 0;
 
+    auto a_stage = [&](int slot) { return reinterpret_cast<AT*>(smem_raw + (size_t)slot * S::STAGE_BYTES); };
+    auto b_stage = [&](int slot) {
+        return reinterpret_cast<double*>(smem_raw + (size_t)slot * S::STAGE_BYTES + S::A_BYTES);
+    };
     auto load_stage = [&](int slot, int kt) {
-        double* As = smem + slot * S::STAGE;
-        double* Bs = As + S::A_STAGE;
+        AT* As = a_stage(slot);
+        double* Bs = b_stage(slot);
         const int64_t k0 = kBegin + (int64_t)kt * S::BK;
         if (!TA) {
             if (V16) {
-                for (int id = tid; id < S::BM * (S::BK / 2); id += kGemmThreads) {
-                    const int r = id / (S::BK / 2), c = id % (S::BK / 2);
-                    const int64_t kk = k0 + 2 * c;
+                for (int id = tid; id < S::BM * (S::BK / EPV); id += kGemmThreads) {
+                    const int r = id / (S::BK / EPV), c = id % (S::BK / EPV);
+                    const int64_t kk = k0 + EPV * c;
                     int bytes = 0;
-                    const double* src = Ap;
+                    const AT* src = Ap;
                     if (r < rows && kk < kEnd) {
-                        const int64_t rem = (kEnd - kk) * 8;
+                        const int64_t rem = (kEnd - kk) * (int64_t)sizeof(AT);
                         bytes = rem >= 16 ? 16 : (int)rem;
                         src = Ap + (row0 + r) * p.lda + kk;
                     }
-                    cp_async16(As + r * S::LDA_S + 2 * c, src, bytes);
+                    cp_async16(As + r * S::LDA_S + EPV * c, src, bytes);
                 }
             } else {
                 for (int id = tid; id < S::BM * S::BK; id += kGemmThreads) {
                     const int r = id / S::BK, c = id % S::BK;
                     const int64_t kk = k0 + c;
                     const bool ok = r < rows && kk < kEnd;
-                    cp_async8(As + r * S::LDA_S + c, ok ? Ap + (row0 + r) * p.lda + kk : Ap, ok ? 8 : 0);
+                    cp_async_elem(As + r * S::LDA_S + c, ok ? Ap + (row0 + r) * p.lda + kk : Ap, ok);
                 }
             }
         } else {
             if (V16) {
-                for (int id = tid; id < S::BK * (S::BM / 2); id += kGemmThreads) {
-                    const int kr = id / (S::BM / 2), c = id % (S::BM / 2);
+                for (int id = tid; id < S::BK * (S::BM / EPV); id += kGemmThreads) {
+                    const int kr = id / (S::BM / EPV), c = id % (S::BM / EPV);
                     const int64_t kk = k0 + kr;
                     int bytes = 0;
-                    const double* src = Ap;
-                    if (kk < kEnd && 2 * c < rows) {
-                        const int64_t rem = (rows - 2 * c) * 8;
+                    const AT* src = Ap;
+                    if (kk < kEnd && EPV * c < rows) {
+                        const int64_t rem = (rows - EPV * c) * (int64_t)sizeof(AT);
                         bytes = rem >= 16 ? 16 : (int)rem;
-                        src = Ap + kk * p.lda + row0 + 2 * c;
+                        src = Ap + kk * p.lda + row0 + EPV * c;
                     }
-                    cp_async16(As + kr * S::LDA_S + 2 * c, src, bytes);
+                    cp_async16(As + kr * S::LDA_S + EPV * c, src, bytes);
                 }
             } else {
                 for (int id = tid; id < S::BK * S::BM; id += kGemmThreads) {
                     const int kr = id / S::BM, c = id % S::BM;
                     const int64_t kk = k0 + kr;
                     const bool ok = kk < kEnd && c < rows;
-                    cp_async8(As + kr * S::LDA_S + c, ok ? Ap + kk * p.lda + row0 + c : Ap, ok ? 8 : 0);
+                    cp_async_elem(As + kr * S::LDA_S + c, ok ? Ap + kk * p.lda + row0 + c : Ap, ok);
                 }
             }
         }
@@ -160,15 +174,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
             if (nk < KT) load_stage(nk % kGemmStages, nk);
             cp_async_commit();
         }
-        const double* As = smem + (kt % kGemmStages) * S::STAGE;
-        const double* Bs = As + S::A_STAGE;
+        const AT* As = a_stage(kt % kGemmStages);
+        const double* Bs = b_stage(kt % kGemmStages);
 #pragma unroll
         for (int ks = 0; ks < S::BK / 4; ++ks) {
             double a[FM], b[FN];
 #pragma unroll
             for (int fm = 0; fm < FM; ++fm)
-                a[fm] = TA ? As[(ks * 4 + t4) * S::LDA_S + wrow + fm * 8 + g]
-                           : As[(wrow + fm * 8 + g) * S::LDA_S + ks * 4 + t4];
+                a[fm] = (double)(TA ? As[(ks * 4 + t4) * S::LDA_S + wrow + fm * 8 + g]
+                                    : As[(wrow + fm * 8 + g) * S::LDA_S + ks * 4 + t4]);
 #pragma unroll
             for (int fn = 0; fn < FN; ++fn) b[fn] = Bs[(ks * 4 + t4) * S::LDB_S + fn * 8 + g];
 #pragma unroll

@@ -36,6 +36,8 @@
 #include "cholqr_f64.cuh"
 #include "cqr_f64.cuh"
 #include "mapprox_f64.cuh"
+#include "jacobi_big_f64.cuh"
+#include "cholc_f64.cuh"
 #include <cfloat>
 
 using namespace sorsvd_dev;
@@ -137,6 +139,12 @@ struct QrPlan {
     double *G1 = nullptr, *G2 = nullptr, *Ri1 = nullptr, *Ri2 = nullptr, *R1 = nullptr, *Qtmp = nullptr,
            *cwork = nullptr;
     int* flag = nullptr;
+    // k > 256: shifted CholeskyQR3 (cholc_f64.cuh); R lands in R[0] with row pitch ldR
+    bool big = false;
+    int ldR = 0;
+    double* Rp[3] = {nullptr, nullptr, nullptr};
+    double* Rtmp = nullptr;
+    double* Wtrsm = nullptr;  // rows x 32 GEMM part of the blocked TRSM
     std::string ws_name;  // per-plan split-K workspace (the two sketches' QRs run concurrently)
     std::vector<void*> owned;
 };
@@ -244,29 +252,35 @@ struct GemmCall {
     int64_t b_seg_stride = 0;
     int force_splits = 0;
     const char* ws_name = "gemm_ws";
+    const float* Af = nullptr;  // FP32-storage A (FP64 arithmetic); overrides A
 };
 
-template <int FM, int FN, bool TA, bool V16>
+template <int FM, int FN, bool TA, bool V16, typename AT>
 void launch_gemm_t(const GemmArgs& a, dim3 grid, cudaStream_t s) {
-    using S = GemmShape<FM, FN, TA>;
+    using S = GemmShape<FM, FN, TA, AT>;
     static bool attr_set = false;
     if (!attr_set) {
-        CK(cudaFuncSetAttribute(gemm_f64_kernel<FM, FN, TA, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(gemm_f64_kernel<FM, FN, TA, V16, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)S::SMEM));
         attr_set = true;
     }
-    gemm_f64_kernel<FM, FN, TA, V16><<<grid, kGemmThreads, S::SMEM, s>>>(a);
+    gemm_f64_kernel<FM, FN, TA, V16, AT><<<grid, kGemmThreads, S::SMEM, s>>>(a);
 }
 
 template <int FN>
-void dispatch_fn(bool ta, bool v16, const GemmArgs& a, dim3 grid, cudaStream_t s) {
+void dispatch_fn(bool ta, bool v16, bool f32a, const GemmArgs& a, dim3 grid, cudaStream_t s) {
     constexpr int FM = FN <= 4 ? 4 : 2;
+    if (f32a) {  // FP32-storage A: 16-byte rows required (validated by the caller)
+        if (ta) launch_gemm_t<FM, FN, true, true, float>(a, grid, s);
+        else launch_gemm_t<FM, FN, false, true, float>(a, grid, s);
+        return;
+    }
     if (ta) {
-        if (v16) launch_gemm_t<FM, FN, true, true>(a, grid, s);
-        else launch_gemm_t<FM, FN, true, false>(a, grid, s);
+        if (v16) launch_gemm_t<FM, FN, true, true, double>(a, grid, s);
+        else launch_gemm_t<FM, FN, true, false, double>(a, grid, s);
     } else {
-        if (v16) launch_gemm_t<FM, FN, false, true>(a, grid, s);
-        else launch_gemm_t<FM, FN, false, false>(a, grid, s);
+        if (v16) launch_gemm_t<FM, FN, false, true, double>(a, grid, s);
+        else launch_gemm_t<FM, FN, false, false, double>(a, grid, s);
     }
 }
 
@@ -300,7 +314,7 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         }
     }
     GemmArgs a{};
-    a.A = g.A;
+    a.A = g.Af ? static_cast<const void*>(g.Af) : static_cast<const void*>(g.A);
     a.lda = g.lda;
     a.B = g.B;
     a.ldb = g.ldb;
@@ -326,12 +340,15 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         a.ldc = g.ldc;
         a.c_split_stride = 0;
     }
-    const bool aligned = ((uintptr_t)g.A % 16) == 0 && (g.lda % 2) == 0;
+    const bool f32a = g.Af != nullptr;
+    const bool aligned = f32a ? (((uintptr_t)g.Af % 16) == 0 && (g.lda % 4) == 0)
+                              : (((uintptr_t)g.A % 16) == 0 && (g.lda % 2) == 0);
+    if (f32a && !aligned) throw Error{SORSVD_ERR_SHAPE, "shape: fp32 A needs 16-byte aligned rows (lda % 4 == 0)"};
     const bool v16 = aligned;
     dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)S);
     switch (FN) {
 #define FN_CASE(n) \
-    case n: dispatch_fn<n>(g.ta, v16, a, grid, s); break;
+    case n: dispatch_fn<n>(g.ta, v16, f32a, a, grid, s); break;
         FN_CASE(1) FN_CASE(2) FN_CASE(3) FN_CASE(4) FN_CASE(5) FN_CASE(6) FN_CASE(7) FN_CASE(8)
         FN_CASE(9) FN_CASE(10) FN_CASE(11) FN_CASE(12) FN_CASE(13) FN_CASE(14) FN_CASE(15) FN_CASE(16)
 #undef FN_CASE
@@ -664,6 +681,9 @@ double* dalloc(QrPlan* p, size_t count) {
     return d;
 }
 
+constexpr int kHouseMaxK = 256;  // largest k of the cluster Householder TSQR (2k x k node in one cluster)
+constexpr int kBigQrPasses = 5;  // adaptive CholeskyQR passes for k > 256 (cholc_f64.cuh); odd -> ends in Q
+
 // Build (or fetch) the TSQR plan for `rows` x k. leaves_given > 0 builds a
 // plan whose level-0 "leaves" are external k x k R blocks (the cross-GPU tree).
 QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const char* tag) {
@@ -677,6 +697,25 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
     p->rows = rows;
     p->k = k;
     p->Np = npad(k);
+    p->ldR = k;
+    if (k > kHouseMaxK) {
+        if (leaves_given > 0) throw Error{SORSVD_ERR_INTERNAL, "tsqr tree plan requested for k > 256"};
+        const int Np = p->Np;
+        p->big = true;
+        p->ldR = Np;
+        p->nodes.push_back(1);
+        p->R.assign(1, dalloc(p.get(), (size_t)k * Np));
+        p->G1 = dalloc(p.get(), (size_t)Np * Np);
+        p->Ri1 = dalloc(p.get(), (size_t)Np * Np);
+        for (auto& r : p->Rp) r = dalloc(p.get(), (size_t)Np * Np);
+        p->Rtmp = dalloc(p.get(), (size_t)Np * Np);
+        p->Qtmp = dalloc(p.get(), (size_t)rows * Np);
+        p->Wtrsm = dalloc(p.get(), (size_t)rows * kCholcB);
+        p->flag = reinterpret_cast<int*>(dalloc(p.get(), 1));  // [0] breakdown, [1] done
+        QrPlan* raw = p.get();
+        c->plans[key] = std::move(p);
+        return raw;
+    }
     p->rb_max = cqr_rows_per_cta(k);
     p->cmax = cqr_max_cluster(c, k);
     if (leaves_given > 0) {
@@ -918,11 +957,148 @@ void launch_chol(sorsvd_ctx* c, const CholArgs& a, cudaStream_t s) {
     check_launch(c);
 }
 
+// k > 256: adaptive (shifted) CholeskyQR passes (cholc_f64.cuh). T (rows x k,
+// pitch Np) is left intact; Q gets the orthonormal factor, p->R[0] (pitch Np)
+// R = R_p ... R_1.
+// distributed: T is this rank's row block; the Gram matrices are summed over
+// ranks (the shift uses the global row count) and every rank forms its own
+// rows of Q.
+void allreduce_sum(sorsvd_ctx* c, double* buf, size_t count, cudaStream_t s);
+
+void qr_run_big(sorsvd_ctx* c, QrPlan* p, const double* T, int64_t ldt, double* Q, int64_t ldq, cudaStream_t s,
+                int64_t rows_global = 0, bool distributed = false) {
+    const int k = p->k, Np = p->Np;
+    if (ldt != Np || ldq != Np) throw Error{SORSVD_ERR_INTERNAL, "qr_run_big: T and Q must be padded to Np"};
+    const int64_t mg = rows_global > 0 ? rows_global : p->rows;
+    auto gram = [&](const double* X, double* G) {
+        GemmCall g;
+        g.ta = true;
+        g.A = X;
+        g.lda = Np;
+        g.M = k;
+        g.K = p->rows;
+        g.B = X;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = G;
+        g.ldc = Np;
+        g.ws_name = p->ws_name.c_str();
+        run_gemm(c, g, s);
+        if (distributed) allreduce_sum(c, G, (size_t)k * Np, s);
+    };
+    // Out R = X (blocked TRSM: the GEMM part X_{<J} R_{<J,J} on the DMMA engine)
+    double* W = p->Wtrsm;
+    auto trsm = [&](const double* X, const double* R, double* Out) {
+        const int nblk = (k + kCholcB - 1) / kCholcB;
+        const unsigned grid = (unsigned)cdiv(p->rows, 256);
+        for (int J = 0; J < nblk; ++J) {
+            const int c0 = J * kCholcB, nb = std::min(kCholcB, k - c0);
+            if (J > 0) {
+                GemmCall g;
+                g.A = Out;
+                g.lda = Np;
+                g.M = p->rows;
+                g.K = c0;
+                g.B = R + c0;
+                g.ldb = Np;
+                g.N = (nb + 7) & ~7;  // stays inside R's Np-wide rows
+                g.C = W;
+                g.ldc = kCholcB;
+                g.ws_name = p->ws_name.c_str();
+                run_gemm(c, g, s);
+            }
+            trsm_rows_kernel<<<grid, 256, 0, s>>>(X + c0, Np, J > 0 ? W : nullptr, kCholcB, R + (size_t)c0 * Np + c0,
+                                                  Np, nb, Out + c0, Np, p->rows, c->pred, c->pred_skip);
+            check_launch(c);
+        }
+    };
+    auto chol = [&](double* R) {
+        CholcArgs a{};
+        a.G = p->G1;
+        a.ldg = Np;
+        a.k = k;
+        a.shift_coef = 11.0 * ((double)mg * k + (double)k * (k + 1)) * DBL_EPSILON;
+        a.R = R;
+        a.ldr = Np;
+        a.flag = p->flag;
+        a.done = p->flag + 1;
+        a.done_tol = 1e-13;
+        const int C = (k + kCholcB - 1) / kCholcB;
+        const size_t sm = cholc_smem_bytes(k);
+        CK(cudaFuncSetAttribute(cholc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        CK(cudaFuncSetAttribute(cholc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)C);
+        cfg.blockDim = dim3(kCholcThreads);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = C;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, cholc_kernel, a));
+        check_launch(c);
+    };
+    int* done = p->flag + 1;
+    CK(cudaMemsetAsync(p->flag, 0, 2 * sizeof(int), s));
+    set_identity_kernel<<<64, 256, 0, s>>>(p->R[0], Np, k);
+    check_launch(c);
+    const double* X = T;
+    double* outs[2] = {Q, p->Qtmp};
+    const int blocks = (int)std::min<int64_t>(cdiv(p->rows * Np, 256), (int64_t)c->num_sms * 8);
+    for (int pass = 0; pass < kBigQrPasses; ++pass) {
+        double* out = outs[pass & 1];
+        {
+            PredScope ps(c, done, 1);
+            gram(X, p->G1);
+        }
+        chol(p->Rp[0]);  // sets *done when X is already orthonormal
+        {
+            PredScope ps(c, done, 1);
+            trsm(X, p->Rp[0], out);
+            GemmCall g;  // R <- R_pass * R
+            g.A = p->Rp[0];
+            g.lda = Np;
+            g.M = k;
+            g.K = k;
+            g.B = p->R[0];
+            g.ldb = Np;
+            g.N = Np;
+            g.C = p->Rtmp;
+            g.ldc = Np;
+            g.ws_name = p->ws_name.c_str();
+            run_gemm(c, g, s);
+            copy_rows_kernel<<<64, 256, 0, s>>>(p->Rtmp, Np, p->R[0], Np, k, Np, done, 1);
+            check_launch(c);
+        }
+        // converged earlier: carry X through unchanged
+        copy_rows_kernel<<<blocks, 256, 0, s>>>(X, Np, out, Np, p->rows, Np, done, 0);
+        check_launch(c);
+        X = out;
+    }
+}
+
+// After a synchronised run: a failed shifted Cholesky (cond(T) beyond ~1/eps
+// or non-finite input) is reported as the reference's numerical_error.
+void check_big_qr(QrPlan* p) {
+    if (!p || !p->big) return;
+    int f = 0;
+    CK(cudaMemcpy(&f, p->flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (f) throw Error{SORSVD_ERR_NUMERICAL, "numerical: thin_qr (shifted CholeskyQR) broke down"};
+}
+
 // Full single-GPU thin QR of T (rows x k): CholeskyQR2 when the sketch is well
 // conditioned, the cluster Householder TSQR otherwise (device-side choice,
 // cholqr_f64.cuh). T is left intact by the CholeskyQR2 path; the Householder
 // path may overwrite it. Final R (diag >= 0) lands in p->R[L].
 void qr_run(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int64_t ldq, cudaStream_t s) {
+    if (p->big) {
+        qr_run_big(c, p, T, ldt, Q, ldq, s);
+        return;
+    }
     const int k = p->k, Np = p->Np;
     const int L = (int)p->nodes.size() - 1;
     auto gram = [&](const double* X, int64_t ldx, double* G) {
@@ -1022,9 +1198,66 @@ void launch_jacobi_t(sorsvd_ctx* c, const JacobiArgs& a, int csize, cudaStream_t
     check_launch(c);
 }
 
+template <int KP>
+void launch_jacobi_big_t(const JacobiBigArgs& a, int csize, cudaStream_t s) {
+    const size_t sm = (size_t)3 * kJbWarps * 2 * (32 * KP) * sizeof(double);  // mailboxes x2 parities + outbox
+    CK(cudaFuncSetAttribute(jacobi_big_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(jacobi_big_kernel<KP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)csize);
+    cfg.blockDim = dim3(kJbWarps * 32);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, jacobi_big_kernel<KP>, a));
+}
+
+// 256 < k <= 512: G-only ring with a rotation log, V rebuilt row-parallel
+// (jacobi_big_f64.cuh).
+void run_jacobi_big(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int ldu, double* S, double* V,
+                    int ldv, int* sweeps, cudaStream_t s) {
+    const int kk = (k + 3) & ~3, P = kk / 2, W = P / 2;
+    const int csize = (W + kJbWarps - 1) / kJbWarps;
+    if (csize > 16) throw Error{SORSVD_ERR_UNSUPPORTED, "jacobi: k > 512"};
+    const int max_sweeps = 40;
+    JacobiBigArgs a{};
+    a.M = M;
+    a.ldm = ldm;
+    a.k = k;
+    a.kk = kk;
+    a.Gout = dbuf(c, "jb_G", (size_t)kk * kk);
+    a.tlog = dbuf(c, "jb_log", (size_t)max_sweeps * (kk - 1) * P);
+    a.max_sweeps = max_sweeps;
+    a.info = reinterpret_cast<int*>(dbuf(c, "jb_info", 1));
+    double* sig = dbuf(c, "jb_sig", (size_t)k);
+    double* sgn = dbuf(c, "jb_sgn", (size_t)k);
+    int* perm = reinterpret_cast<int*>(dbuf(c, "jb_perm", (size_t)k));
+    if (kk <= 384) launch_jacobi_big_t<12>(a, csize, s);
+    else launch_jacobi_big_t<16>(a, csize, s);
+    check_launch(c);
+    const int wpb = 8;
+    jb_sigma_kernel<<<(k + wpb - 1) / wpb, 32 * wpb, 0, s>>>(a.Gout, k, kk, sig);
+    check_launch(c);
+    jb_rank_kernel<<<(k + wpb - 1) / wpb, 32 * wpb, 0, s>>>(a.Gout, k, kk, sig, U, ldu, S, perm, sgn);
+    check_launch(c);
+    const size_t sm = (size_t)kJbRows * kk * sizeof(double);
+    jb_vrec_kernel<<<(k + kJbRows - 1) / kJbRows, P, sm, s>>>(a.tlog, a.info, k, kk, perm, sgn, V, ldv);
+    check_launch(c);
+    if (sweeps) CK(cudaMemcpyAsync(sweeps, a.info, sizeof(int), cudaMemcpyDeviceToDevice, s));
+}
+
 void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int ldu, double* S, double* V, int ldv,
                 int* sweeps, cudaStream_t s) {
-    if (k > 256) throw Error{SORSVD_ERR_UNSUPPORTED, "jacobi: k > 256"};
+    if (k > 256 || (getenv("SORSVD_JACOBI_BIG") && k >= 8)) {
+        run_jacobi_big(c, k, M, ldm, U, ldu, S, V, ldv, sweeps, s);
+        return;
+    }
     JacobiArgs a{};
     a.M = M;
     a.ldm = ldm;
@@ -1090,6 +1323,7 @@ struct SorProblem {
     int Np32;          // FP32 padded width for the tcgen05 passes (npad32)
     int64_t m_global;
     bool single_pass;
+    bool tf32;         // dtype F32 with SORSVD_FLAG_TF32: passes on the tcgen05 tensor cores
 };
 
 SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan** p2, QrPlan** pg) {
@@ -1116,7 +1350,7 @@ SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan**
         b.Sc = dbuf(c, "Sc", (size_t)Np);
         b.Pinv = dbuf(c, "Pinv", (size_t)Np * Np);
     }
-    if (P.dtype == SORSVD_F32) {
+    if (P.tf32) {
         auto fbuf = [&](const char* nm, size_t count) { return reinterpret_cast<float*>(dbuf(c, nm, count / 2 + 2, true)); };
         b.T1f = fbuf("T1f", (size_t)P.m * P.Np32);
         b.T2f = fbuf("T2f", (size_t)P.n * P.Np32);
@@ -1125,8 +1359,9 @@ SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan**
     }
     *p1 = get_qr_plan(c, P.m, P.ell, 0, "T1");
     *p2 = get_qr_plan(c, P.n, P.ell, 0, "T2");
-    *pg = c->world > 1 ? get_qr_plan(c, (int64_t)c->world * P.ell, P.ell, c->world, "G") : nullptr;
-    if (c->world > 1) {
+    *pg = (c->world > 1 && P.ell <= kHouseMaxK) ? get_qr_plan(c, (int64_t)c->world * P.ell, P.ell, c->world, "G")
+                                                 : nullptr;
+    if (c->world > 1 && P.ell <= kHouseMaxK) {
         dbuf(c, "Rg", (size_t)c->world * P.ell * P.ell);
         dbuf(c, "CinLocal", (size_t)P.ell * Np);
     }
@@ -1241,19 +1476,20 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     record_stage(c, timing, 0);
     for (int i = 0; i <= P.q; ++i) {
         if (P.single_pass && i == P.q) {  // t2_pre: the row sketch entering the last iteration (sketch.hpp:94)
-            if (P.dtype == SORSVD_F32)
+            if (P.tf32)
                 cast_to_f64(c, b.T2f, P.Np32, b.T2pre, Np, P.n, ell, s);
             else
                 CK(cudaMemcpyAsync(b.T2pre, b.T2, (size_t)P.n * Np * 8, cudaMemcpyDeviceToDevice, s));
         }
-        if (P.dtype == SORSVD_F32) {  // TF32 tensor-core passes (tc_gemm_f32.cuh)
+        if (P.tf32) {  // TF32 tensor-core passes (tc_gemm_f32.cuh)
             run_tc_gemm(c, false, P.Af, P.lda, P.m, P.n, b.T2f, P.Np32, P.Np32, b.T1f, P.Np32, s);
             run_tc_gemm(c, true, P.Af, P.lda, P.n, P.m, b.T1f, P.Np32, P.Np32, b.T2f, P.Np32, s);
             comm_allreduce(c, b.T2f, (size_t)P.n * P.Np32, true, s);
             continue;
         }
-        GemmCall g1;  // T1 = A * T2     (sketch.hpp:95)
+        GemmCall g1;  // T1 = A * T2     (sketch.hpp:95); FP32 A widened to FP64 in the kernel
         g1.A = P.A;
+        g1.Af = P.Af;
         g1.lda = P.lda;
         g1.M = P.m;
         g1.K = P.n;
@@ -1266,6 +1502,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         GemmCall g2;  // T2 = A^T * T1   (sketch.hpp:96)
         g2.ta = true;
         g2.A = P.A;
+        g2.Af = P.Af;
         g2.lda = P.lda;
         g2.M = P.n;
         g2.K = P.m;
@@ -1277,7 +1514,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         run_gemm(c, g2, s);
         allreduce_sum(c, b.T2, (size_t)P.n * Np, s);
     }
-    if (P.dtype == SORSVD_F32) {  // the QR / SVD stages run in FP64
+    if (P.tf32) {  // the QR / SVD stages run in FP64
         cast_to_f64(c, b.T1f, P.Np32, b.T1, Np, P.m, ell, s);
         cast_to_f64(c, b.T2f, P.Np32, b.T2, Np, P.n, ell, s);
     }
@@ -1285,7 +1522,9 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     // Q1 = thin_qr(T1).q, Q2 = thin_qr(T2).q concurrently (sketch.hpp:98-99)
     CK(cudaEventRecord(c->ev_fork, s));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    if (c->world > 1) {
+    if (c->world > 1 && p1->big) {
+        qr_run_big(c, p1, b.T1, Np, b.Q1, Np, s, P.m_global, true);  // Gram matrices summed over ranks
+    } else if (c->world > 1) {
         qr_factor(c, p1, b.T1, Np, b.Q1, Np, false, s);
         const int L1 = (int)p1->nodes.size() - 1;
         double* Rg = dbuf(c, "Rg", (size_t)c->world * ell * ell);
@@ -1305,7 +1544,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         enqueue_m_approx(c, P, b, s);
     } else {
     // M = Q1^T (A Q2)   (sketch.hpp:100-102)
-    if (P.dtype == SORSVD_F32) {
+    if (P.tf32) {
         cast_to_f32(c, b.Q2, Np, b.Q2f, P.Np32, P.n, ell, s);
         run_tc_gemm(c, false, P.Af, P.lda, P.m, P.n, b.Q2f, P.Np32, P.Np32, b.Yf, P.Np32, s);
         cast_to_f64(c, b.Yf, P.Np32, b.Y, Np, P.m, ell, s);
@@ -1321,7 +1560,8 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g.N = Np;
         g.C = b.Y;
         g.ldc = Np;
-        if (P.dtype == SORSVD_F64) run_gemm(c, g, s);
+        g.Af = P.Af;
+        if (!P.tf32) run_gemm(c, g, s);
         GemmCall h;
         h.ta = true;
         h.A = b.Q1;
@@ -1371,7 +1611,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
 
 std::string sor_key(const SorProblem& P) {
     char buf[256];
-    snprintf(buf, sizeof buf, "sor:%d:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.dtype, (int)P.single_pass,
+    snprintf(buf, sizeof buf, "sor:%d:%d:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.dtype, (int)P.single_pass, (int)P.tf32,
              P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m, (long long)P.n,
              (long long)P.lda, P.k, P.ell, P.q);
     return buf;
@@ -1389,7 +1629,7 @@ void validate(const sorsvd_desc* d) {
     if (d->dtype != SORSVD_F64 && d->dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
     if (d->dtype == SORSVD_F32 && (d->lda % 4))
         throw Error{SORSVD_ERR_SHAPE, "shape: fp32 A needs lda % 4 == 0 (16-byte rows for TMA)"};
-    if (d->ell > 256) throw Error{SORSVD_ERR_UNSUPPORTED, "ell > 256 is not supported yet (core SVD / QR limit)"};
+    if (d->ell > 512) throw Error{SORSVD_ERR_UNSUPPORTED, "ell > 512 is not supported (core SVD / QR limit)"};
 }
 
 // Core device-side call. dOmega: n x ell dense (or null: drawn on the host).
@@ -1410,6 +1650,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     P.Np = npad(d->ell);
     P.m_global = d->m_global > 0 ? d->m_global : d->m;
     P.single_pass = d->single_pass != 0;
+    P.tf32 = d->dtype == SORSVD_F32 && (d->flags & SORSVD_FLAG_TF32);
     QrPlan *p1, *p2, *pg;
     SorBuffers b = prepare_sor(c, P, &p1, &p2, &pg);
     // Omega and the outputs stay outside the captured graph (so the graph is
@@ -1431,7 +1672,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     int launches = 0;
     auto enqueue_all = [&]() {
         // T2 <- Omega (padded; rounded to fp32 for the TF32 passes)
-        if (P.dtype == SORSVD_F32) {
+        if (P.tf32) {
             cast_to_f32(c, om, P.ell, b.T2f, P.Np32, P.n, P.ell, c->stream);
         } else {
             CK(cudaMemsetAsync(b.T2, 0, (size_t)P.n * P.Np * 8, c->stream));
@@ -1484,6 +1725,11 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     }
     copy_out();
     CK(cudaEventRecord(c->ev_b, c->stream));
+    if (p1->big || p2->big) {
+        CK(cudaEventSynchronize(c->ev_b));
+        check_big_qr(p1);
+        check_big_qr(p2);
+    }
     if (st) {
         CK(cudaEventSynchronize(c->ev_b));
         float ms = 0.f;
@@ -1930,7 +2176,7 @@ int sorsvd_thin_qr_device(sorsvd_ctx* c, int64_t m, int32_t k, const double* dT,
     if (!c) return SORSVD_ERR_PARAMETER;
     return guarded(c, [&] {
         if (m < k || k < 1) throw Error{SORSVD_ERR_SHAPE, "shape: thin_qr requires rows >= cols"};
-        if (k > 256) throw Error{SORSVD_ERR_UNSUPPORTED, "thin_qr: k > 256"};
+        if (k > 512) throw Error{SORSVD_ERR_UNSUPPORTED, "thin_qr: k > 512"};
         const int Np = npad(k);
         QrPlan* p = get_qr_plan(c, m, k, 0, "api");
         double* T = dbuf(c, "qrT", (size_t)m * Np, true);
@@ -1942,9 +2188,10 @@ int sorsvd_thin_qr_device(sorsvd_ctx* c, int64_t m, int32_t k, const double* dT,
                              cudaMemcpyDeviceToDevice, c->stream));
         const int L = (int)p->nodes.size() - 1;
         if (dR)
-            CK(cudaMemcpy2DAsync(dR, (size_t)ldr * 8, p->R[L], (size_t)k * 8, (size_t)k * 8, (size_t)k,
+            CK(cudaMemcpy2DAsync(dR, (size_t)ldr * 8, p->R[L], (size_t)p->ldR * 8, (size_t)k * 8, (size_t)k,
                                  cudaMemcpyDeviceToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+        check_big_qr(p);
     });
 }
 
@@ -1952,7 +2199,7 @@ int sorsvd_small_svd_device(sorsvd_ctx* c, int32_t k, const double* dM, int64_t 
                             double* dS, double* dV, int64_t ldv, int32_t* sweeps) {
     if (!c) return SORSVD_ERR_PARAMETER;
     return guarded(c, [&] {
-        if (k < 1 || k > 256) throw Error{SORSVD_ERR_PARAMETER, "parameter: k out of range [1, 256]"};
+        if (k < 1 || k > 512) throw Error{SORSVD_ERR_PARAMETER, "parameter: k out of range [1, 512]"};
         int* dsw = reinterpret_cast<int*>(dbuf(c, "sweeps_svd", 1));
         run_jacobi(c, k, dM, (int)ldm, dU, (int)ldu, dS, dV, (int)ldv, dsw, c->stream);
         int sw = 0;

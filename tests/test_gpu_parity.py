@@ -52,7 +52,7 @@ def test_matmul_skinny(P, torch_mod, M, K, N, ta):
 
 
 @pytest.mark.parametrize("m,k", [(50, 10), (2, 1), (1000, 20), (4000, 100), (300, 112), (25344, 10), (9000, 37),
-                                 (1500, 128), (2000, 256)])
+                                 (1500, 128), (2000, 256), (3000, 300), (2000, 512), (20000, 384)])
 def test_thin_qr_vs_oracle(P, torch_mod, m, k):
     t = O.gaussian_matrix(m, k, m * 7 + k)
     q_ref, r_ref = O.thin_qr(t)
@@ -67,6 +67,23 @@ def test_thin_qr_vs_oracle(P, torch_mod, m, k):
     np.testing.assert_allclose(r, r_ref, atol=1e-11 * np.abs(r_ref).max())
 
 
+@pytest.mark.parametrize("cond_exp", [6, 12])
+def test_thin_qr_k512_ill_conditioned(P, torch_mod, cond_exp):
+    # k > 256 runs shifted CholeskyQR3; graded columns up to cond 1e12
+    m, k = 6000, 512
+    u0, _ = np.linalg.qr(O.gaussian_matrix(m, k, 3))
+    v0, _ = np.linalg.qr(O.gaussian_matrix(k, k, 4))
+    t = (u0 * 10.0 ** (-cond_exp * np.arange(k) / (k - 1))) @ v0.T
+    q, r = P.thin_qr(torch_mod.from_numpy(t).cuda())
+    q, r = q.cpu().numpy(), r.cpu().numpy()
+    assert np.abs(q.T @ q - np.eye(k)).max() < 1e-13
+    assert np.abs(q @ r - t).max() < 1e-13 * np.abs(t).max() * np.sqrt(m)
+    assert np.all(np.diag(r) > 0) and np.allclose(np.tril(r, -1), 0)
+    q_ref, r_ref = O.thin_qr(t)
+    # the leading columns are well determined; compare R (sign-fixed) relative to its scale
+    np.testing.assert_allclose(r, r_ref, atol=1e-10 * np.abs(r_ref).max())
+
+
 def test_thin_qr_rank_deficient(P, torch_mod):
     t = O.gaussian_matrix(500, 8, 3)
     t[:, 5] = 0.0
@@ -77,7 +94,7 @@ def test_thin_qr_rank_deficient(P, torch_mod):
     assert np.abs(q @ r.cpu().numpy() - t).max() < 1e-12
 
 
-@pytest.mark.parametrize("k", [1, 2, 5, 20, 33, 100, 112, 128, 256])
+@pytest.mark.parametrize("k", [1, 2, 5, 20, 33, 100, 112, 128, 256, 257, 300, 384, 511, 512])
 def test_small_svd_vs_oracle(P, torch_mod, k):
     mm = O.gaussian_matrix(k, k, 1000 + k)
     u_ref, s_ref, v_ref = O.full_svd(mm)
@@ -105,6 +122,36 @@ def test_small_svd_graded(P, torch_mod):
     _, s, _, _ = P.full_svd(torch_mod.from_numpy(mm).cuda())
     s_ref = np.linalg.svd(mm, compute_uv=False)
     np.testing.assert_allclose(s.cpu().numpy()[:40], s_ref[:40], rtol=1e-9)
+
+
+@pytest.mark.parametrize("k", [8, 37, 100])
+def test_small_svd_big_kernel_forced(P, torch_mod, k, monkeypatch):
+    # the k > 256 path (G-only ring + rotation log + row-parallel V rebuild)
+    # forced on small k must agree with the reference SVD just the same
+    monkeypatch.setenv("SORSVD_JACOBI_BIG", "1")
+    mm = O.gaussian_matrix(k, k, 5000 + k)
+    u_ref, s_ref, v_ref = O.full_svd(mm)
+    u, s, v, sweeps = P.full_svd(torch_mod.from_numpy(mm).cuda())
+    u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+    np.testing.assert_allclose(s, s_ref, rtol=1e-12, atol=1e-14 * s_ref[0])
+    assert np.abs(u.T @ u - np.eye(k)).max() < 1e-13
+    assert np.abs(v.T @ v - np.eye(k)).max() < 1e-13
+    assert np.abs((u * s) @ v.T - mm).max() < 1e-13 * s_ref[0] * k
+    assert 1 <= sweeps <= 40
+
+
+def test_small_svd_graded_k512(P, torch_mod):
+    # the Config 5 core spectrum (sigma_j = 1/j) at k = 512
+    k = 512
+    u0, _ = np.linalg.qr(O.gaussian_matrix(k, k, 11))
+    v0, _ = np.linalg.qr(O.gaussian_matrix(k, k, 12))
+    sig = 1.0 / np.arange(1, k + 1)
+    mm = (u0 * sig) @ v0.T
+    u, s, v, sweeps = P.full_svd(torch_mod.from_numpy(mm).cuda())
+    s_ref = np.linalg.svd(mm, compute_uv=False)
+    np.testing.assert_allclose(s.cpu().numpy(), s_ref, rtol=1e-11)
+    u, v = u.cpu().numpy(), v.cpu().numpy()
+    assert np.abs((u * s.cpu().numpy()) @ v.T - mm).max() < 1e-13 * k
 
 
 # ----------------------------------------------------- sor_svd_power parity --
@@ -216,6 +263,79 @@ def test_config3_scaled_k256(P):
     base, ds, dl = O.perturbation_floor(A, 256, cfg, trials=1)
     f = P.sor_svd_power(A, 256, P.SketchConfig(256, 1, 31))
     _check_parity(f, base.sigma, base.u, base.v, ds, dl)
+
+
+def _check_parity_banded(f, base, ds, dl):
+    """The C2 protocol (test_config2_full): per-sigma 10x the floor envelope
+    where the reference is determined (floor <= 1e-10), 100x on the
+    transition band (floor <= 1e-6), low-rank parity on the determined part."""
+    env = np.maximum.accumulate(ds)
+    jd = int(np.searchsorted(env, 1e-10))
+    jt = int(np.searchsorted(env, 1e-6))
+    es = O.sigma_rel_err(np.asarray(f.sigma), base.sigma)
+    assert np.all(es[:jd] <= np.maximum(1e-10, 10 * env[:jd])), es[:jd]
+    assert np.all(es[jd:jt] <= 100 * env[jd:jt]), (es[jd:jt].max(), env[jd:jt].max())
+    if jd > 0:
+        lr = O.lowrank_rel_diff(f.u[:, :jd], f.sigma[:jd], f.v[:, :jd], base.u[:, :jd], base.sigma[:jd],
+                                base.v[:, :jd])
+        assert lr <= max(1e-9, 10 * dl), lr
+    return jd, jt
+
+
+def test_k512_fp64_vs_oracle(P):
+    # BASELINE config 5 has k = 512: adaptive shifted CholeskyQR + the rotation-log Jacobi, FP64.
+    # The sketch's condition number is 512^3 ~ 1.3e8, so the trailing sigmas are only defined
+    # up to the rounding history of thin_qr: the floor here also includes two Householder runs
+    # on row / column permutations of the sketches (equally valid reference executions, which
+    # drift 4-8x further than the 1e-16-input floor). CholeskyQR's span error carries an extra
+    # ~sqrt(k) (DESIGN.md, "k > 256"): measured 3-4x that Householder spread.
+    A = O.gen_lowrank_decay(4096, 3000, 512, lambda j: 1.0 / j, 1e-6, 5)
+    cfg = O.SketchConfig(512, 1, 41)
+    base, ds, dl = O.perturbation_floor(A, 512, cfg, trials=1, qr_variants=2)
+    f = P.sor_svd_power(A, 512, P.SketchConfig(512, 1, 41))
+    env = np.maximum.accumulate(ds)
+    es = O.sigma_rel_err(f.sigma, base.sigma)
+    lim = np.maximum(1e-10, 10 * env)
+    assert np.all(es <= lim), (es.max(), int(np.argmax(es / lim)))
+    jd = int(np.searchsorted(env, 1e-11))
+    assert jd >= 64, jd
+    lr = O.lowrank_rel_diff(f.u[:, :jd], f.sigma[:jd], f.v[:, :jd], base.u[:, :jd], base.sigma[:jd],
+                            base.v[:, :jd])
+    assert lr <= max(1e-9, 10 * dl), lr
+
+
+def _c5_scaled():
+    # Config 5 distributions (s_j = 1/j, q = 2, k = 512) at m = n = 8192. The noise std is
+    # scaled by sqrt(131072/8192) so ||E||_2 ~ 0.07 as at full size: the spectrum is 1/j
+    # down to the noise floor (j ~ 14), as in the full-size Config 5.
+    m = n = 8192
+    return O.gen_lowrank_decay(m, n, 512, lambda j: 1.0 / j, 4e-4, 55).astype(np.float32)
+
+
+def test_config5_scaled_fp32(P):
+    # FP32-stored A, FP64 passes (the default fp32_mode): FP64 parity against the oracle
+    # on the same rounded A
+    import torch
+    A = _c5_scaled()
+    cfg = O.SketchConfig(512, 2, 61)
+    base, ds, dl = O.perturbation_floor(A.astype(np.float64), 512, cfg, trials=1)
+    f = P.sor_svd_power(torch.from_numpy(A).cuda(), 512, P.SketchConfig(512, 2, 61))
+    assert f.passes == 7
+    es = O.sigma_rel_err(f.sigma.cpu().numpy(), base.sigma)
+    assert np.all(es <= np.maximum(1e-10, 10 * np.maximum.accumulate(ds))), (es.max(), ds.max())
+
+
+def test_config5_scaled_tf32_resolution(P):
+    # fp32_mode="tf32": every pass rounds to TF32 (2^-11), so after 2q+1 = 5 passes a sketch
+    # direction j is resolved only while (sigma_j/sigma_1)^5 stays well above that level
+    # (DESIGN.md "FP32 inputs"): the leading sigmas agree to ~1e-3, the tail does not.
+    import torch
+    A = _c5_scaled()
+    base = O.sor_svd_power(A.astype(np.float64), 512, O.SketchConfig(512, 2, 61))
+    f = P.sor_svd_power(torch.from_numpy(A).cuda(), 512, P.SketchConfig(512, 2, 61), fp32_mode="tf32")
+    es = O.sigma_rel_err(f.sigma.cpu().numpy(), base.sigma)
+    assert es[:4].max() <= 3e-3, es[:4]
+    assert np.all(np.diff(f.sigma.cpu().numpy()) <= 0)
 
 
 def test_ell_greater_than_k(P):

@@ -55,10 +55,35 @@ def test_sor_svd_fp32_vs_fp64_oracle(env):
     A = O.gen_lowrank_decay(20000, 2000, 256, lambda j: 10.0 ** (-j / 64.0), 1e-3, 3).astype(np.float32)
     Ad = A.astype(np.float64)
     base = O.sor_svd_power(Ad, 128, O.SketchConfig(128, 1, 31))
-    f = P.sor_svd_power(torch.from_numpy(A).cuda(), 128, P.SketchConfig(128, 1, 31))
+    f = P.sor_svd_power(torch.from_numpy(A).cuda(), 128, P.SketchConfig(128, 1, 31), fp32_mode="tf32")
     s = f.sigma.cpu().numpy()
     es = O.sigma_rel_err(s, base.sigma)
     assert es[:64].max() <= 3e-3, es[:64].max()
     lr = O.lowrank_rel_diff(f.u.cpu().numpy(), s, f.v.cpu().numpy(), base.u, base.sigma, base.v)
     assert lr <= 3e-3, lr
     print("fp32/TF32 sigma err (lead 64)", es[:64].max(), "all", es.max(), "low-rank", lr)
+
+
+def test_sor_svd_fp32_storage_fp64_passes(env):
+    """FP32-stored A with the default fp32_mode="fp64": the passes widen A to
+    FP64 inside the DMMA GEMM, so the result matches the FP64 oracle on the
+    same rounded matrix to FP64 parity (north-star tolerances, 10x floor)."""
+    P, torch = env
+    from oracle import sorsvd_oracle as O
+    A = O.gen_lowrank_decay(20000, 2000, 256, lambda j: 10.0 ** (-j / 64.0), 1e-3, 3).astype(np.float32)
+    Ad = A.astype(np.float64)
+    cfg = O.SketchConfig(128, 1, 31)
+    base, ds, dl = O.perturbation_floor(Ad, 128, cfg, trials=1)
+    f = P.sor_svd_power(torch.from_numpy(A).cuda(), 128, P.SketchConfig(128, 1, 31))
+    s = f.sigma.cpu().numpy()
+    es = O.sigma_rel_err(s, base.sigma)
+    assert np.all(es <= np.maximum(1e-10, 10 * np.maximum.accumulate(ds))), es.max()
+    lr = O.lowrank_rel_diff(f.u.cpu().numpy(), s, f.v.cpu().numpy(), base.u, base.sigma, base.v)
+    assert lr <= max(1e-9, 10 * dl), lr
+
+
+def test_fp32_mode_rejects_unknown(env):
+    P, torch = env
+    a = torch.zeros((64, 48), device="cuda", dtype=torch.float32)
+    with pytest.raises(P.ParameterError):
+        P.sor_svd_power(a, 4, P.SketchConfig(8, 0, 1), fp32_mode="fp16")
