@@ -39,9 +39,17 @@ CONFIGS = {
     # BASELINE.json configs[2], fp64 variant
     "c3": dict(m=200000, n=20000, k=256, q=1, scaling="strong",
                desc="C3 fp64 m=200000 n=20000 k=ell=256 q=1, A = X diag(10^(-j/64)) Y^T + N(0,1e-6)"),
-    # BASELINE.json configs[2], fp32 variant (TF32 tensor-core passes, FP64 QR/SVD)
-    "c3f32": dict(m=200000, n=20000, k=256, q=1, scaling="strong", dtype="f32",
-                  desc="C3 fp32 m=200000 n=20000 k=ell=256 q=1 (TF32 tcgen05 passes), same A rounded to fp32"),
+    # BASELINE.json configs[2], fp32 variant: A stored in FP32, passes in FP64 arithmetic (default fp32_mode)
+    "c3f32": dict(m=200000, n=20000, k=256, q=1, scaling="strong", dtype="f32", mode="fp64",
+                  desc="C3 fp32 m=200000 n=20000 k=ell=256 q=1, same A rounded to fp32 (FP64 DMMA passes)"),
+    # the same on the TF32 tensor cores (fp32_mode="tf32")
+    "c3tf32": dict(m=200000, n=20000, k=256, q=1, scaling="strong", dtype="f32", mode="tf32",
+                   desc="C3 fp32 m=200000 n=20000 k=ell=256 q=1 (TF32 tcgen05 passes), same A rounded to fp32"),
+    # BASELINE.json configs[4]: 68.7 GB FP32 matrix, FP64 arithmetic
+    "c5": dict(m=131072, n=131072, k=512, q=2, scaling="strong", dtype="f32", mode="fp64",
+               desc="C5 fp32 m=n=131072 k=ell=512 q=2, A = X diag(1/j) Y^T + N(0,1e-8) (FP64 DMMA passes)"),
+    "c5tf32": dict(m=131072, n=131072, k=512, q=2, scaling="strong", dtype="f32", mode="tf32",
+                   desc="C5 fp32 m=n=131072 k=ell=512 q=2 (TF32 tcgen05 passes; leading sigmas only)"),
 }
 
 
@@ -69,14 +77,32 @@ def make_matrix(cfg_name, m_local, n, rank, world, device):
         r = min(m_local, n)
         s = 1.0 / torch.arange(1, r + 1, device=device, dtype=f64) ** 2
         return (u[:, :r] * s) @ v[:, :r].T
-    if cfg_name in ("c3", "c3f32"):
+    if cfg_name in ("c5", "c5tf32"):
+        mg = CONFIGS["c5"]["m"]
+        g.manual_seed(1000 + rank)
+        x = torch.randn(m_local, 512, generator=g, device=device, dtype=f64) / math.sqrt(mg)
+        g.manual_seed(2000)
+        y = torch.randn(n, 512, generator=g, device=device, dtype=f64) / math.sqrt(n)
+        s = 1.0 / torch.arange(1, 513, device=device, dtype=f64)
+        a = torch.empty(m_local, n, device=device, dtype=torch.float32)
+        g.manual_seed(3000 + rank)
+        step = 4096
+        ys = (y * s).T.contiguous()
+        for i in range(0, m_local, step):
+            j = min(m_local, i + step)
+            blk = x[i:j] @ ys
+            blk += 1e-4 * torch.randn(j - i, n, generator=g, device=device, dtype=f64)
+            a[i:j] = blk.to(torch.float32)
+            del blk
+        return a
+    if cfg_name in ("c3", "c3f32", "c3tf32"):
         mg = CONFIGS["c3"]["m"]
         g.manual_seed(1000 + rank)
         x = torch.randn(m_local, 256, generator=g, device=device, dtype=f64) / math.sqrt(mg)
         g.manual_seed(2000)
         y = torch.randn(n, 256, generator=g, device=device, dtype=f64) / math.sqrt(n)
         s = 10.0 ** (-torch.arange(1, 257, device=device, dtype=f64) / 64.0)
-        a = torch.empty(m_local, n, device=device, dtype=torch.float32 if cfg_name == "c3f32" else f64)
+        a = torch.empty(m_local, n, device=device, dtype=torch.float32 if cfg_name != "c3" else f64)
         g.manual_seed(3000 + rank)
         step = 8192
         for i in range(0, m_local, step):
@@ -227,6 +253,11 @@ def main():
         elif args.config == "c2":
             a = O.gen_c2(2, n=n, m=cfg["m"])
             sample = "full C2 instance"
+        elif args.config.startswith("c5"):
+            a = O.gen_lowrank_decay(16384, 16384, 512, lambda j: 1.0 / j, 4e-4, 5).astype(np.float32).astype(np.float64)
+            sample = ("16384x16384 instance of the C5 distribution (k=512, q=2, noise scaled to keep ||E|| ~ 0.07); "
+                      "the metric is per-flop, extrapolated linearly in m*n*k*passes")
+            n = 16384
         else:
             a = O.gen_lowrank_decay(20000, n, 256, lambda j: 10.0 ** (-j / 64.0), 1e-3, 3)
             sample = "row-block sample 20000x20000 of the C3 distribution (same n, k, q)"
@@ -269,8 +300,10 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
     scfg = P.SketchConfig(ell=ell, q=q, seed=7)
 
+    fp32_mode = cfg.get("mode", "fp64")
+
     def call():
-        return P.sor_svd_power(A, k, scfg, omega=omega, ctx=ctx, m_global=m_global)
+        return P.sor_svd_power(A, k, scfg, omega=omega, ctx=ctx, m_global=m_global, fp32_mode=fp32_mode)
 
     def barrier():
         if dist:
@@ -304,7 +337,8 @@ def main():
     value = flops_step / (ms_per_step * 1e-3) / 1e9
 
     # ---- per-stage device times of one extra call (no graph, STAGE_TIMES) ----
-    fs = P.sor_svd_power(A, k, scfg, omega=omega, ctx=ctx, m_global=m_global, stage_times=True)
+    fs = P.sor_svd_power(A, k, scfg, omega=omega, ctx=ctx, m_global=m_global, stage_times=True,
+                         fp32_mode=fp32_mode)
     stages = {key: round(fs.stats[key], 4) for key in ("ms_total", "ms_passes", "ms_qr", "ms_project", "ms_svd",
                                                         "ms_basis")}
     stages["jacobi_sweeps"] = fs.stats["jacobi_sweeps"]
@@ -313,6 +347,7 @@ def main():
     # ---- roofline of the dominant kernel (the A-streaming pass) ----
     import ctypes
     f32 = cfg.get("dtype") == "f32"
+    tf32 = f32 and fp32_mode == "tf32"
     esz = 4 if f32 else 8
     pk = ctypes.c_double()
     hb = ctypes.c_double()
@@ -326,7 +361,7 @@ def main():
         except Exception:
             mp = {}
     hbm_peak = mp.get("hbm_gbs", 6650.0)
-    if f32:
+    if tf32:
         # TF32 peak: a plain library GEMM (cuBLAS TF32, 8192^3) measured live, like the bf16 entry
         torch.backends.cuda.matmul.allow_tf32 = True
         xa = torch.randn(8192, 8192, device=device, dtype=torch.float32)
@@ -351,10 +386,11 @@ def main():
     else:
         tensor_peak = fp64_peak
         peak_src = "live FP64 DMMA burst (sorsvd_measure_peaks); MEASURED_PEAKS.json has no FP64 entry"
-        Np = (ell + 7) // 8 * 8 if ell <= 128 else (ell + 127) // 128 * 128
+        Np = (ell + 7) // 8 * 8 if ell <= 128 else (ell + 127) // 128 * 128  # npad()
         tdt = torch.float64
-        pass_fn = P._capi.lib().sorsvd_pass_device
-        kname = "gemm_f64_kernel (DMMA m8n8k4, cp.async ring)"
+        pass_fn = P._capi.lib().sorsvd_pass_f32a_device if f32 else P._capi.lib().sorsvd_pass_device
+        kname = ("gemm_f64_kernel<float A> (FP32 tile widened to FP64, DMMA m8n8k4)" if f32
+                 else "gemm_f64_kernel (DMMA m8n8k4, cp.async ring)")
     X = torch.zeros(n, Np, dtype=tdt, device=device)
     X[:, :ell] = omega.to(tdt)
     T = torch.zeros(m_local, Np, dtype=tdt, device=device)
@@ -403,11 +439,11 @@ def main():
         torch.cuda.empty_cache()
         hcfg = P.SketchConfig(ell=ell, q=q, seed=7)
         for _ in range(max(1, min(args.warmup, 2))):
-            P.sor_svd_power(a_np, k, hcfg, ctx=ctx, m_global=m_global)
+            P.sor_svd_power(a_np, k, hcfg, ctx=ctx, m_global=m_global, fp32_mode=fp32_mode)
         barrier()
         t0 = time.perf_counter()
         for i in range(args.steps):
-            P.sor_svd_power(a_np, k, hcfg, ctx=ctx, m_global=m_global)
+            P.sor_svd_power(a_np, k, hcfg, ctx=ctx, m_global=m_global, fp32_mode=fp32_mode)
         el = D.max_over_ranks(dist, time.perf_counter() - t0, device)
         e2e = {"value": flops_step / (el / args.steps) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(m_local * n * esz + n * ell * 8),
@@ -422,22 +458,27 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         if a_np is None:
             a_np = A.cpu().numpy()
-        if args.config in ("c3", "c3f32"):
+        if args.config in ("c3", "c3f32", "c3tf32"):
             a_cpu = np.ascontiguousarray(a_np[:20000], dtype=np.float64)
             sample = "row-block sample 20000x20000 of the C3 matrix (same n, k, q)"
+        elif args.config.startswith("c5"):
+            a_cpu = np.ascontiguousarray(a_np[:16384, :16384], dtype=np.float64)
+            sample = ("16384x16384 block of the C5 matrix (k=512, q=2); per-flop rate, extrapolated linearly "
+                      "in m*n*k*passes")
         else:
             a_cpu = a_np
             sample = f"full {args.config.upper()} instance"
         times, cores, kind = cpu_reference(a_cpu, k, ell, q, 7, 3, min_seconds=10.0)
         sec = statistics.median(times)
-        cpu = {"value": 2.0 * a_cpu.shape[0] * n * ell * passes / sec / 1e9, "unit": "GFLOP/s", "cores": cores,
+        cpu = {"value": 2.0 * a_cpu.shape[0] * a_cpu.shape[1] * ell * passes / sec / 1e9, "unit": "GFLOP/s",
+               "cores": cores,
                "kind": kind, "sample": f"{sample}; median of {len(times)} calls ({sum(times):.1f}s)",
                "ms_per_call": sec * 1e3}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32/tf32" if f32 else "f64",
+                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": ("f32/tf32" if tf32 else "f32 storage, f64 arithmetic") if f32 else "f64",
                 "data": "synthetic", "config": workload, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "stages_ms": stages,
                 "wall_s_timed_region": t_wall, "ms_steps": [round(x, 4) for x in ms_steps]}

@@ -197,6 +197,12 @@ int sorsvd_pass_f32_device(sorsvd_ctx* ctx, int32_t ta, int64_t m, int64_t n, in
                            const float* dA, const float* dX, float* dT, int32_t reps, double* ms_avg,
                            int32_t* launches_per_pass);
 
+/* FP32-stored A with FP64 arithmetic (the default F32 sor path): dX / dT are
+ * FP64 with the sorsvd_pass_device padding. */
+int sorsvd_pass_f32a_device(sorsvd_ctx* ctx, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell,
+                            const float* dA, const double* dX, double* dT, int32_t reps, double* ms_avg,
+                            int32_t* launches_per_pass);
+
 /* ---- host helpers mirroring random.hpp / sketch.hpp ----------------------- */
 uint64_t sorsvd_sub_seed(uint64_t seed, uint64_t stream);                    /* random.hpp:24 */
 int sorsvd_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out, int nthreads); /* random.hpp:60 */

@@ -86,6 +86,8 @@ SIGNATURES = [
                                    ctypes.POINTER(c_i32)]),
     ("sorsvd_pass_f32_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_dp,
                                        ctypes.POINTER(c_i32)]),
+    ("sorsvd_pass_f32a_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_dp,
+                                        ctypes.POINTER(c_i32)]),
     ("sorsvd_sub_seed", c_u64, [c_u64, c_u64]),
     ("sorsvd_gaussian_matrix", c_i32, [c_i64, c_i64, c_u64, c_dp, ctypes.c_int]),
     ("sorsvd_flop_estimate", ctypes.c_longlong, [ctypes.c_longlong] * 5 + [ctypes.c_int]),

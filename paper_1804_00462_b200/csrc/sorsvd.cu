@@ -2318,14 +2318,16 @@ int sorsvd_measure_peaks(sorsvd_ctx* c, double* fp64_tflops, double* hbm_read_gb
 
 // One A-streaming pass (T = A X or T = A^T X) launched `reps` times between
 // CUDA events on the context stream; X/T are padded (ldx = ldt = npad(ell)).
-int sorsvd_pass_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell, const double* dA,
-                       const double* dX, double* dT, int32_t reps, double* ms_avg, int32_t* launches_per_pass) {
+static int pass_device_impl(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell,
+                            const double* dA, const float* dAf, const double* dX, double* dT, int32_t reps,
+                            double* ms_avg, int32_t* launches_per_pass) {
     if (!c) return SORSVD_ERR_PARAMETER;
     return guarded(c, [&] {
         const int Np = npad(ell);
         GemmCall g;
         g.ta = ta != 0;
-        g.A = static_cast<const double*>(dA);
+        g.A = dA;
+        g.Af = dAf;
         g.lda = lda;
         g.M = ta ? n : m;
         g.K = ta ? m : n;
@@ -2345,6 +2347,17 @@ int sorsvd_pass_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int64_t 
         if (ms_avg) *ms_avg = ms / std::max(reps, 1);
         if (launches_per_pass) *launches_per_pass = (c->launches - l0) / std::max(reps, 1);
     });
+}
+
+int sorsvd_pass_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell, const double* dA,
+                       const double* dX, double* dT, int32_t reps, double* ms_avg, int32_t* launches_per_pass) {
+    return pass_device_impl(c, ta, m, n, lda, ell, dA, nullptr, dX, dT, reps, ms_avg, launches_per_pass);
+}
+
+int sorsvd_pass_f32a_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell,
+                            const float* dA, const double* dX, double* dT, int32_t reps, double* ms_avg,
+                            int32_t* launches_per_pass) {
+    return pass_device_impl(c, ta, m, n, lda, ell, nullptr, dA, dX, dT, reps, ms_avg, launches_per_pass);
 }
 
 int sorsvd_matmul_f32_device(sorsvd_ctx* c, int32_t ta, int64_t M, int64_t K, int32_t N, const float* dA, int64_t lda,
