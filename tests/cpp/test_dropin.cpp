@@ -46,6 +46,16 @@ int main() {
     LowRankApprox r2 = sor_svd_power(p, 10, cfg), g2 = cuda::sor_svd_power(p, 10, cfg);
     std::printf("polydecay sigma max rel err %.3e\n", max_rel(g2.sigma, r2.sigma));
     fails += !(max_rel(g2.sigma, r2.sigma) <= 1e-8);
+    // single-pass core (sketch.hpp:54-58): M_approx, 2q+2 passes
+    cfg.ell = 12;
+    cfg.q = 1;
+    cfg.seed = 5;
+    cfg.single_pass = true;
+    LowRankApprox r3 = sor_svd_power(a, 10, cfg), g3 = cuda::sor_svd_power(a, 10, cfg);
+    std::printf("single_pass sigma max rel err %.3e, passes %d/%d\n", max_rel(g3.sigma, r3.sigma), g3.passes,
+                r3.passes);
+    fails += !(max_rel(g3.sigma, r3.sigma) <= 1e-10) + (g3.passes != r3.passes);
+    cfg.single_pass = false;
     // error behaviour mirrors the reference exceptions
     try {
         cfg.ell = 400;
