@@ -42,6 +42,12 @@ struct CqrArgs {
     int root_sign;        // apply diag(R) >= 0 (dense.hpp:127-132)
     const int* pred;      // optional: no-op when *pred == pred_skip (CholeskyQR2 accepted)
     int pred_skip;
+    // compact-WY mode (cqr_kernel only): skip the in-kernel form-Q; write the
+    // unit-lower Householder vectors V into qout, tau and the root signs out.
+    // Q is then formed by wy_tfactor_kernel + two DMMA GEMMs (sorsvd.cu).
+    int wy;
+    double* tau_out;
+    double* sgn_out;
 };
 
 // shared-memory layout (doubles): A[ld*k] | red[2*RW] | S[RW] | tau[k] | sgn[k]
@@ -257,6 +263,25 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
     }
     __syncthreads();  // R is read from A before form-Q overwrites it
 
+    if (a.wy) {
+        // V[gi][c] = 1 on the diagonal, v_c below it, 0 above
+        // (a reflector with tau = 0 is the identity: its column is written as 0 so
+        //  that I - V T V^T needs no entry for it)
+        for (int e = tid; e < nr * k; e += blockDim.x) {
+            const int i = e / k, c = e - i * k;
+            const int gi = lr0 + i;
+            const double v = gi > c ? A[(size_t)c * ld + i] : (gi == c ? 1.0 : 0.0);
+            a.qout[(row0 + lr0 + i) * a.ldq + c] = tau[c] != 0.0 ? v : 0.0;
+        }
+        if (r == 0)
+            for (int c = tid; c < k; c += blockDim.x) {
+                a.tau_out[c] = tau[c];
+                a.sgn_out[c] = sgn[c];
+            }
+        cl.sync();  // peers are done reading this CTA's reduction buffers
+        return;
+    }
+
     // ------------------------------------------------------------ form Q --
     // Q = H_0 ... H_{k-1} [I; 0] in place (dorg2r order). Step j applies H_j to
     // the columns c > j, and in the same pass accumulates step j-1's dots
@@ -358,6 +383,38 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
         const int i = e / k, c = e - i * k;
         a.qout[(row0 + lr0 + i) * a.ldq + c] = sgn[c] * A[(size_t)c * ld + i];
     }
+}
+
+// Compact WY for the explicit Q of a single-block QR (LAPACK dlarft + dorgqr
+// as GEMMs). With V the unit-lower Householder vectors (zero columns where
+// tau = 0), H_0 ... H_{k-1} = I - V T V^T with T upper triangular and
+//   T^{-1} = diag(1/tau) + strictly_upper(V^T V)
+// (1 on the diagonal where tau = 0), so T comes from one triangular inverse
+// (trinv_kernel) instead of dlarft's k-step recurrence, and
+//   Q = (I - V T V^T)[:, :k] diag(sgn) = E diag(sgn) - V X,  X = T V1^T diag(sgn)
+// (V1 = top k x k block of V): two DMMA GEMMs plus a diagonal fix-up.
+// wy_prep_kernel forms U = T^{-1} and B = V1^T diag(sgn) (both k x ld, zero padded).
+__global__ void wy_prep_kernel(const double* __restrict__ G, int ldg, const double* __restrict__ tau,
+                               const double* __restrict__ sgn, const double* __restrict__ V, int64_t ldv, int k,
+                               double* __restrict__ U, double* __restrict__ B, int ld, const int* pred, int pred_skip) {
+    if (pred && *pred == pred_skip) return;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+        const int i = e / k, j = e - i * k;
+        double u = 0.0;
+        if (j > i) u = G[(size_t)i * ldg + j];
+        else if (j == i) u = tau[i] != 0.0 ? 1.0 / tau[i] : 1.0;
+        U[(size_t)i * ld + j] = u;
+        // B[l][c] = V[c][l] sgn[c] for l <= c  (V1 is unit lower triangular)
+        const int l = i, c = j;
+        B[(size_t)l * ld + c] = l <= c ? V[(size_t)c * ldv + l] * sgn[c] : 0.0;
+    }
+}
+
+// Q(c, c) += sgn[c] for c < k (the E diag(sgn) term of the compact-WY Q).
+__global__ void wy_diag_kernel(double* __restrict__ Q, int64_t ldq, const double* __restrict__ sgn, int k,
+                               const int* pred, int pred_skip) {
+    if (pred && *pred == pred_skip) return;
+    for (int c = threadIdx.x; c < k; c += blockDim.x) Q[(size_t)c * ldq + c] += sgn[c];
 }
 
 // Register-resident variant: thread t owns column c = t % k over a chunk of

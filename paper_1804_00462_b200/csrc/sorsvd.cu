@@ -145,6 +145,7 @@ struct QrPlan {
     double* Rp[3] = {nullptr, nullptr, nullptr};
     double* Rtmp = nullptr;
     double* Wtrsm = nullptr;  // rows x 32 GEMM part of the blocked TRSM
+    double *wy_tau = nullptr, *wy_sgn = nullptr;  // compact-WY Q of a single-block Householder QR
     std::string ws_name;  // per-plan split-K workspace (the two sketches' QRs run concurrently)
     std::vector<void*> owned;
 };
@@ -621,7 +622,7 @@ void launch_cqr(sorsvd_ctx* c, const CqrArgs& a0, int nblocks, int rows_max, int
     CqrArgs a = a0;
     a.pred = c->pred;
     a.pred_skip = c->pred_skip;
-    const RegCfg rc = getenv("SORSVD_CQR_SMEM") ? RegCfg{} : cqr_reg_choose(a.k, rows_max, kCqrMaxCluster);
+    const RegCfg rc = (getenv("SORSVD_CQR_SMEM") || a.wy) ? RegCfg{} : cqr_reg_choose(a.k, rows_max, kCqrMaxCluster);
     if (rc.ch) {
         const int Rb = (int)cdiv(rows_max, rc.csize);
         switch (rc.ch) {
@@ -724,7 +725,8 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
         // the per-reflector latency (cluster reduction) dominates, so the
         // fewest tree levels win: leaves as large as either kernel can hold
         const int64_t reg_cap = getenv("SORSVD_CQR_SMEM") ? 0 : cqr_reg_capacity(k, kCqrMaxCluster);
-        const int64_t leaf_max = std::max<int64_t>(reg_cap, (int64_t)p->cmax * p->rb_max);
+        int64_t leaf_max = std::max<int64_t>(reg_cap, (int64_t)p->cmax * p->rb_max);
+        if (getenv("SORSVD_QR_LEAF_CTA")) leaf_max = std::max<int64_t>(p->rb_max, 2 * k);  // experiment
         p->P = (int)std::max<int64_t>(1, cdiv(rows, leaf_max));
         const int64_t base = rows / p->P, extra = rows % p->P;
         int64_t r = 0;
@@ -801,6 +803,8 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
         p->cwork = dalloc(p.get(), (size_t)k * k);
         p->Qtmp = dalloc(p.get(), (size_t)rows * Np);
         p->flag = reinterpret_cast<int*>(dalloc(p.get(), 1));
+        p->wy_tau = dalloc(p.get(), (size_t)k);
+        p->wy_sgn = dalloc(p.get(), (size_t)k);
     }
     QrPlan* raw = p.get();
     c->plans[key] = std::move(p);
@@ -817,17 +821,75 @@ void qr_factor(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int6
     if (!Rleaves) {
         CqrArgs a{};
         const bool direct = (L == 0 && root_sign);
+        // one block, explicit Q wanted: factor only, then Q by compact WY (two GEMMs)
+        const bool wy = direct && k >= 48 && p->wy_tau && !getenv("SORSVD_NO_WY");  // small k: in-kernel form-Q wins
         a.in = T;
         a.ldi = ldt;
-        a.qout = direct ? Q : T;
-        a.ldq = direct ? ldq : ldt;
+        a.qout = wy ? p->Qtmp : (direct ? Q : T);
+        a.ldq = wy ? p->Np : (direct ? ldq : ldt);
         a.row0 = p->d_row0;
         a.rows = p->d_rows;
         a.k = k;
         a.R = p->R[0];
         a.ldr = k;
         a.root_sign = (L == 0 && root_sign) ? 1 : 0;
+        a.wy = wy ? 1 : 0;
+        a.tau_out = p->wy_tau;
+        a.sgn_out = p->wy_sgn;
         launch_cqr(c, a, p->P, p->max_leaf_rows, p->cmax, p->rb_max, s);
+        if (wy) {
+            const int Np = p->Np;
+            GemmCall g;  // G = V^T V
+            g.ta = true;
+            g.A = p->Qtmp;
+            g.lda = Np;
+            g.M = k;
+            g.K = p->rows;
+            g.B = p->Qtmp;
+            g.ldb = Np;
+            g.N = Np;
+            g.C = p->G2;
+            g.ldc = Np;
+            g.ws_name = p->ws_name.c_str();
+            run_gemm(c, g, s);
+            // U = T^{-1} (into Ri1), B = V1^T diag(sgn) (into Ri2); T = U^{-1} (into R1... via trinv)
+            wy_prep_kernel<<<16, 256, 0, s>>>(p->G2, Np, p->wy_tau, p->wy_sgn, p->Qtmp, Np, k, p->Ri1, p->Ri2, Np,
+                                              c->pred, c->pred_skip);
+            check_launch(c);
+            const int wpb = 4;
+            trinv_kernel<<<(k + wpb - 1) / wpb, 32 * wpb, (size_t)wpb * k * sizeof(double), s>>>(
+                p->Ri1, Np, k, p->G1, Np, c->pred, c->pred_skip);
+            check_launch(c);
+            {
+                GemmCall x;  // X = T B  (k x Np) into Ri1 (U is no longer needed)
+                x.A = p->G1;
+                x.lda = Np;
+                x.M = k;
+                x.K = k;
+                x.B = p->Ri2;
+                x.ldb = Np;
+                x.N = Np;
+                x.C = p->Ri1;
+                x.ldc = Np;
+                x.ws_name = p->ws_name.c_str();
+                run_gemm(c, x, s);
+            }
+            GemmCall h;  // Q = -V X  (+ E diag(sgn) below)
+            h.A = p->Qtmp;
+            h.lda = Np;
+            h.M = p->rows;
+            h.K = k;
+            h.B = p->Ri1;
+            h.ldb = Np;
+            h.N = Np;
+            h.C = Q;
+            h.ldc = ldq;
+            h.alpha = -1.0;
+            h.ws_name = p->ws_name.c_str();
+            run_gemm(c, h, s);
+            wy_diag_kernel<<<1, 128, 0, s>>>(Q, ldq, p->wy_sgn, k, c->pred, c->pred_skip);
+            check_launch(c);
+        }
     }
     for (int l = 1; l <= L; ++l) {
         const double* Rin = (l == 1 && Rleaves) ? Rleaves : p->R[l - 1];
