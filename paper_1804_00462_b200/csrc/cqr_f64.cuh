@@ -48,6 +48,7 @@ struct CqrArgs {
     int wy;
     double* tau_out;
     double* sgn_out;
+    long long* prof;  // optional (tools): per-step clock64 stamps of CTA 0 / warp 0 / lane 0
 };
 
 // shared-memory layout (doubles): A[ld*k] | red[2*RW] | S[RW] | tau[k] | sgn[k]
@@ -151,9 +152,13 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
         const int i0 = max(0, j + 1 - lr0);  // local rows with global index > j
         const int jo = j - lr0;
         const bool owner = jo >= 0 && jo < nr;
+        const bool prof = a.prof && r == 0 && tid == 0 && b == 0;
+        if (prof) a.prof[j * 6 + 0] = clock64();
         cl.sync();
+        if (prof) a.prof[j * 6 + 1] = clock64();
         for (int idx = tid; idx < 2 + 2 * nt; idx += blockDim.x) S[idx] = csum((int)(P - red), idx);
         __syncthreads();
+        if (prof) a.prof[j * 6 + 2] = clock64();
         const double ss = S[0], alpha = S[1];
         double t = 0.0, beta = alpha, scal = 0.0;
         if (ss != 0.0) {
@@ -197,6 +202,7 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
             }
         }
         __syncthreads();
+        if (prof) a.prof[j * 6 + 3] = clock64();
         // fused pass over the remaining trailing columns c > j+1
         if (nt > 1) {
             const double* xn = A + (size_t)(j + 1) * ld;  // next reflector (updated, unscaled)
@@ -242,6 +248,7 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
                 }
             }
         }
+        if (prof) a.prof[j * 6 + 4] = clock64();
         // (no barrier here: the next step starts with cl.sync)
     }
     __syncthreads();

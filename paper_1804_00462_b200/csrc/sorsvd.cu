@@ -183,6 +183,7 @@ struct sorsvd_emu_group {
 };
 
 struct sorsvd_ctx {
+    long long* cqr_prof = nullptr;  // tools only (SORSVD_CQR_PROF)
     int device = 0;
     int rank = 0, world = 1;
     int num_sms = 148;
@@ -622,6 +623,12 @@ void launch_cqr(sorsvd_ctx* c, const CqrArgs& a0, int nblocks, int rows_max, int
     CqrArgs a = a0;
     a.pred = c->pred;
     a.pred_skip = c->pred_skip;
+    if (getenv("SORSVD_CQR_PROF")) {  // tools/prof_cqr.py: per-step clock stamps
+        static long long* dprof = nullptr;
+        if (!dprof) CK(cudaMalloc(&dprof, 6 * 512 * sizeof(long long)));
+        a.prof = dprof;
+        c->cqr_prof = dprof;
+    }
     const RegCfg rc = (getenv("SORSVD_CQR_SMEM") || a.wy) ? RegCfg{} : cqr_reg_choose(a.k, rows_max, kCqrMaxCluster);
     if (rc.ch) {
         const int Rb = (int)cdiv(rows_max, rc.csize);
@@ -1335,7 +1342,8 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
     const int KP = kp <= 1 ? 1 : kp <= 2 ? 2 : kp <= 4 ? 4 : 8;
     const int P = ((k + 1) & ~1) / 2;
     if (k <= 32 && jacobi_cta_smem_bytes(k) <= 212 * 1024) {
-        // small k: one CTA, G and V in shared memory (no cluster barrier needed)
+        // small k: one CTA, G and V in shared memory (no cluster barrier needed;
+        // measured 4x slower than the cluster ring at k = 100)
         const int warps = std::min(P, 32);
         const size_t sm = jacobi_cta_smem_bytes(k);
         CK(cudaFuncSetAttribute(jacobi_cta_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -2254,6 +2262,21 @@ int sorsvd_thin_qr_device(sorsvd_ctx* c, int64_t m, int32_t k, const double* dT,
                                  cudaMemcpyDeviceToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         check_big_qr(p);
+        if (c->cqr_prof) {  // SORSVD_CQR_PROF: average per-step phase lengths of the last cqr launch
+            std::vector<long long> h(6 * 512);
+            CK(cudaMemcpy(h.data(), c->cqr_prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+            double ph[5] = {0, 0, 0, 0, 0};
+            int n = 0;
+            for (int j = 1; j + 1 < k; ++j, ++n) {
+                ph[0] += (double)(h[j * 6 + 1] - h[j * 6 + 0]);        // cluster barrier
+                ph[1] += (double)(h[j * 6 + 2] - h[j * 6 + 1]);        // payload sum + barrier
+                ph[2] += (double)(h[j * 6 + 3] - h[j * 6 + 2]);        // beta/tau, owner column, barrier
+                ph[3] += (double)(h[j * 6 + 4] - h[j * 6 + 3]);        // fused pass (warp 0)
+                ph[4] += (double)(h[(j + 1) * 6 + 0] - h[j * 6 + 0]);  // whole step
+            }
+            fprintf(stderr, "[cqr prof] k=%d cycles/step: cl.sync %.0f csum %.0f owner %.0f fused %.0f total %.0f\n", k,
+                    ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, ph[4] / n);
+        }
     });
 }
 
