@@ -45,6 +45,17 @@ struct GemmArgs {
     double alpha;
     const int* pred;  // optional device flag: the launch is a no-op when *pred == pred_skip
     int pred_skip;
+    // stream-K (grid underfilled by whole tiles): CTA c runs segments
+    // [sk_cta_seg[c], sk_cta_seg[c+1]) of the (tile, k-range) list; a segment
+    // covering a whole tile writes C directly, partial ones go to slot g of
+    // `sk_ws` (BM x BN each) and streamk_fixup_kernel sums them in slot order
+    const int* sk_cta_seg;
+    const int* sk_seg_tile;
+    const int* sk_seg_k0;  // in BK units
+    const int* sk_seg_k1;
+    int sk_units;          // BK units per tile
+    int sk_gy;             // column chunks per row tile
+    double* sk_ws;
 };
 
 constexpr int kGemmThreads = 256;
@@ -67,30 +78,17 @@ struct GemmShape {
     static constexpr size_t SMEM = (size_t)kGemmStages * STAGE_BYTES;
 };
 
-template <int FM, int FN, bool TA, bool V16, typename AT = double>
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
+// One output tile (rows [row0, row0+rows), columns [ncol0, ncol0+BN)) over the
+// K range [kBegin, kEnd); the result goes to Cbase + (row_base + r) * ldc.
+template <int FM, int FN, bool TA, bool V16, typename AT>
+__device__ __forceinline__ void gemm_tile(const GemmArgs& p, unsigned char* smem_raw, int64_t row0, int64_t rows,
+                                          int seg, int ncol0, int64_t kBegin, int64_t kEnd, double* Cbase,
+                                          int64_t row_base, int64_t ldc) {
     using S = GemmShape<FM, FN, TA, AT>;
-    if (p.pred && *p.pred == p.pred_skip) return;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-
-    int64_t row0, rows;
-    int seg = 0;
-    if (p.tile_row0) {
-        row0 = p.tile_row0[blockIdx.x];
-        rows = p.tile_rows[blockIdx.x];
-        seg = p.tile_seg[blockIdx.x];
-    } else {
-        row0 = (int64_t)blockIdx.x * S::BM;
-        rows = p.M - row0 < S::BM ? p.M - row0 : S::BM;
-    }
-    const int ncol0 = blockIdx.y * S::BN;
     const double* __restrict__ Bp = p.B + seg * p.b_seg_stride + ncol0;
     const AT* __restrict__ Ap = static_cast<const AT*>(p.A);
     constexpr int EPV = S::EPV;
-    const int64_t kBegin = (int64_t)blockIdx.z * p.k_chunk;
-    int64_t kEnd = kBegin + p.k_chunk;
-    if (kEnd > p.K) kEnd = p.K;
     const int KT = kEnd > kBegin ? (int)((kEnd - kBegin + S::BK - 1) / S::BK) : 0;
 
     auto a_stage = [&](int slot) { return reinterpret_cast<AT*>(smem_raw + (size_t)slot * S::STAGE_BYTES); };
@@ -192,18 +190,83 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
         }
     }
     cp_async_wait<0>();
+    __syncthreads();  // the smem ring may be reused by the next segment
 
-    double* Cp = p.C + (int64_t)blockIdx.z * p.c_split_stride + ncol0;
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
         const int r = wrow + fm * 8 + g;
         if (r < rows) {
-            double* crow = Cp + (row0 + r) * p.ldc + 2 * t4;
+            double* crow = Cbase + (row_base + r) * ldc + 2 * t4;
 #pragma unroll
             for (int fn = 0; fn < FN; ++fn)
                 *reinterpret_cast<double2*>(crow + fn * 8) =
                     make_double2(p.alpha * acc[fm][fn][0], p.alpha * acc[fm][fn][1]);
         }
+    }
+}
+
+
+template <int FM, int FN, bool TA, bool V16, typename AT = double>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
+    using S = GemmShape<FM, FN, TA, AT>;
+    if (p.pred && *p.pred == p.pred_skip) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    if (p.sk_cta_seg) {  // stream-K
+        const int g0 = p.sk_cta_seg[blockIdx.x], g1 = p.sk_cta_seg[blockIdx.x + 1];
+        for (int gs = g0; gs < g1; ++gs) {
+            const int tile = p.sk_seg_tile[gs];
+            const int mt = tile / p.sk_gy, nt = tile - mt * p.sk_gy;
+            const int64_t row0 = (int64_t)mt * S::BM;
+            const int64_t rows = p.M - row0 < S::BM ? p.M - row0 : S::BM;
+            const int ku0 = p.sk_seg_k0[gs], ku1 = p.sk_seg_k1[gs];
+            const int64_t kBegin = (int64_t)ku0 * S::BK;
+            const int64_t kEnd = min((int64_t)ku1 * S::BK, p.K);
+            if (ku0 == 0 && ku1 == p.sk_units)  // whole tile: straight to C
+                gemm_tile<FM, FN, TA, V16, AT>(p, smem_raw, row0, rows, 0, nt * S::BN, kBegin, kEnd,
+                                               p.C + nt * S::BN, row0, p.ldc);
+            else
+                gemm_tile<FM, FN, TA, V16, AT>(p, smem_raw, row0, rows, 0, nt * S::BN, kBegin, kEnd,
+                                               p.sk_ws + (size_t)gs * S::BM * S::BN, 0, S::BN);
+        }
+        return;
+    }
+    int64_t row0, rows;
+    int seg = 0;
+    if (p.tile_row0) {
+        row0 = p.tile_row0[blockIdx.x];
+        rows = p.tile_rows[blockIdx.x];
+        seg = p.tile_seg[blockIdx.x];
+    } else {
+        row0 = (int64_t)blockIdx.x * S::BM;
+        rows = p.M - row0 < S::BM ? p.M - row0 : S::BM;
+    }
+    const int64_t kBegin = (int64_t)blockIdx.z * p.k_chunk;
+    const int64_t kEnd = min(kBegin + p.k_chunk, p.K);
+    const int ncol0 = blockIdx.y * S::BN;
+    gemm_tile<FM, FN, TA, V16, AT>(p, smem_raw, row0, rows, seg, ncol0, kBegin, kEnd,
+                                   p.C + (int64_t)blockIdx.z * p.c_split_stride + ncol0, row0, p.ldc);
+}
+
+// Stream-K fix-up: every tile split over several segments gets the sum of
+// its partial slots in slot order (deterministic). One CTA-stride loop over
+// (tile, row, col) of the split tiles only.
+__global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* __restrict__ tile_seg0,
+                                     const int* __restrict__ split_tiles, int nsplit, int BM, int BN, int gy,
+                                     int64_t M, double* __restrict__ C, int64_t ldc, const int* pred, int pred_skip) {
+    if (pred && *pred == pred_skip) return;
+    const int64_t per = (int64_t)BM * BN;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nsplit * per;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int st = (int)(e / per);
+        const int64_t w = e - (int64_t)st * per;
+        const int tile = split_tiles[st];
+        const int r = (int)(w / BN), col = (int)(w - (int64_t)r * BN);
+        const int mt = tile / gy, nt = tile - mt * gy;
+        const int64_t row = (int64_t)mt * BM + r;
+        if (row >= M) continue;
+        double acc = 0.0;
+        for (int gs = tile_seg0[tile]; gs < tile_seg0[tile + 1]; ++gs) acc += ws[(size_t)gs * per + w];
+        C[row * ldc + (int64_t)nt * BN + col] = acc;
     }
 }
 

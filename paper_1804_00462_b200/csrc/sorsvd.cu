@@ -195,6 +195,11 @@ struct sorsvd_ctx {
     std::map<std::string, Buf> bufs;
     std::map<std::string, std::unique_ptr<QrPlan>> plans;
     std::map<std::string, GraphEntry> graphs;
+    struct SkTable {
+        std::vector<int*> dev;  // cta_seg, seg_tile, seg_k0, seg_k1, tile_seg0, split_tiles
+        int nsplit = 0, nseg = 0;
+    };
+    std::map<std::string, SkTable> sk_tables;  // stream-K segment tables, by shape
     ncclComm_t comm = nullptr;
     sorsvd_emu_group* emu = nullptr;  // in-process multi-rank emulation (tests)
     int launches = 0;
@@ -315,6 +320,19 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
             }
         }
     }
+    // stream-K when whole tiles x splits leave SMs idle: equal BK-unit shares per
+    // CTA across tile boundaries, partial tiles summed by streamk_fixup_kernel
+    bool streamk = false;
+    const int64_t units = cdiv(g.K, kGemmBK);
+    const int64_t tiles = gx * gy;
+    if (!g.tile_row0 && g.force_splits == 0 && !getenv("SORSVD_NO_STREAMK") && tiles < (int64_t)c->num_sms &&
+        units >= 64) {
+        const int64_t n = c->num_sms;
+        const double sk_cost = (double)cdiv(tiles * units, n) * kGemmBK + 2 * 96.0 + 0.02 * 3 * g.M * g.N / (double)n;
+        const double cur_cost = (double)cdiv(tiles * S, n) * ((double)g.K / S + 96.0) +
+                                (S > 1 ? 0.02 * S * g.M * g.N / (double)n : 0.0);
+        streamk = sk_cost < 0.95 * cur_cost;
+    }
     GemmArgs a{};
     a.A = g.Af ? static_cast<const void*>(g.Af) : static_cast<const void*>(g.A);
     a.lda = g.lda;
@@ -342,12 +360,71 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         a.ldc = g.ldc;
         a.c_split_stride = 0;
     }
+    std::vector<int> sk_split_tiles_h;
+    const int* sk_tile_seg0 = nullptr;
+    const int* sk_split_tiles = nullptr;
+    if (streamk) {
+        const int n = c->num_sms;
+        const int64_t T = tiles * units;
+        char key[128];
+        snprintf(key, sizeof key, "%lld:%lld:%d:%d", (long long)tiles, (long long)units, n, (int)gy);
+        auto it = c->sk_tables.find(key);
+        if (it == c->sk_tables.end()) {
+            if (c->capturing) throw Error{SORSVD_ERR_INTERNAL, "stream-K table creation during capture"};
+            std::vector<int> cta_seg{0}, seg_tile, seg_k0, seg_k1, tile_seg0(tiles + 1, 0), split;
+            for (int cc = 0; cc < n; ++cc) {
+                int64_t u0 = cc * T / n, u1 = (cc + 1) * T / n;
+                while (u0 < u1) {
+                    const int64_t t = u0 / units, k0 = u0 - t * units, k1 = std::min<int64_t>(units, k0 + (u1 - u0));
+                    seg_tile.push_back((int)t);
+                    seg_k0.push_back((int)k0);
+                    seg_k1.push_back((int)k1);
+                    u0 += k1 - k0;
+                }
+                cta_seg.push_back((int)seg_tile.size());
+            }
+            for (size_t q = 0; q < seg_tile.size(); ++q) tile_seg0[seg_tile[q] + 1]++;
+            for (int64_t t = 0; t < tiles; ++t) {
+                if (tile_seg0[t + 1] > 1) split.push_back((int)t);
+                tile_seg0[t + 1] += tile_seg0[t];
+            }
+            auto up = [&](const std::vector<int>& v) {
+                int* d = nullptr;
+                CK(cudaMalloc(&d, std::max<size_t>(v.size(), 1) * sizeof(int)));
+                if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+                return d;
+            };
+            sorsvd_ctx::SkTable t;
+            t.dev = {up(cta_seg), up(seg_tile), up(seg_k0), up(seg_k1), up(tile_seg0), up(split)};
+            t.nsplit = (int)split.size();
+            t.nseg = (int)seg_tile.size();
+            it = c->sk_tables.emplace(key, t).first;
+        }
+        const std::vector<int*>& tab = it->second.dev;
+        a.sk_cta_seg = tab[0];
+        a.sk_seg_tile = tab[1];
+        a.sk_seg_k0 = tab[2];
+        a.sk_seg_k1 = tab[3];
+        sk_tile_seg0 = tab[4];
+        sk_split_tiles = tab[5];
+        a.sk_units = (int)units;
+        a.sk_gy = (int)gy;
+        const int BN = g.N <= 128 ? g.N : 128;
+        a.sk_ws = dbuf(c, std::string(g.ws_name) + "_sk", (size_t)it->second.nseg * BM * BN);
+        sk_split_tiles_h.resize((size_t)it->second.nsplit);
+    }
     const bool f32a = g.Af != nullptr;
     const bool aligned = f32a ? (((uintptr_t)g.Af % 16) == 0 && (g.lda % 4) == 0)
                               : (((uintptr_t)g.A % 16) == 0 && (g.lda % 2) == 0);
     if (f32a && !aligned) throw Error{SORSVD_ERR_SHAPE, "shape: fp32 A needs 16-byte aligned rows (lda % 4 == 0)"};
     const bool v16 = aligned;
     dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)S);
+    if (streamk) {
+        grid = dim3((unsigned)c->num_sms, 1, 1);
+        a.C = g.C;
+        a.ldc = g.ldc;
+        a.c_split_stride = 0;
+    }
     switch (FN) {
 #define FN_CASE(n) \
     case n: dispatch_fn<n>(g.ta, v16, f32a, a, grid, s); break;
@@ -357,6 +434,18 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         default: throw Error{SORSVD_ERR_INTERNAL, "gemm: FN"};
     }
     check_launch(c);
+    if (streamk) {
+        const int nsplit = (int)sk_split_tiles_h.size();
+        if (nsplit > 0) {
+            const int BN = g.N <= 128 ? g.N : 128;
+            const int64_t work = (int64_t)nsplit * BM * BN;
+            streamk_fixup_kernel<<<(int)std::min<int64_t>(cdiv(work, 256), (int64_t)c->num_sms * 8), 256, 0, s>>>(
+                a.sk_ws, sk_tile_seg0, sk_split_tiles, nsplit, BM, BN, (int)gy, g.M, g.C, g.ldc, c->pred,
+                c->pred_skip);
+            check_launch(c);
+        }
+        return;
+    }
     if (S > 1) {
         if (g.ldc % 2) throw Error{SORSVD_ERR_INTERNAL, "gemm: odd ldc with splits"};
         const int64_t count2 = g.M * g.ldc / 2;
@@ -2170,6 +2259,8 @@ void sorsvd_ctx_destroy(sorsvd_ctx* c) {
     cudaEventDestroy(c->ev_b);
     for (auto& e : c->ev_st) cudaEventDestroy(e);
     for (auto& e : c->ev_h) cudaEventDestroy(e);
+    for (auto& kv : c->sk_tables)
+        for (int* d : kv.second.dev) cudaFree(d);
     cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->own_stream);
     delete c;
