@@ -254,19 +254,20 @@ __global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* _
                                      const int* __restrict__ split_tiles, int nsplit, int BM, int BN, int gy,
                                      int64_t M, double* __restrict__ C, int64_t ldc, const int* pred, int pred_skip) {
     if (pred && *pred == pred_skip) return;
-    const int64_t per = (int64_t)BM * BN;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nsplit * per;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int st = (int)(e / per);
-        const int64_t w = e - (int64_t)st * per;
+    const int per = BM * BN;  // one tile's elements (< 2^31)
+    // grid.y = split tile index, grid.x strides over the tile's elements (32-bit index math)
+    for (int st = blockIdx.y; st < nsplit; st += gridDim.y) {
         const int tile = split_tiles[st];
-        const int r = (int)(w / BN), col = (int)(w - (int64_t)r * BN);
         const int mt = tile / gy, nt = tile - mt * gy;
-        const int64_t row = (int64_t)mt * BM + r;
-        if (row >= M) continue;
-        double acc = 0.0;
-        for (int gs = tile_seg0[tile]; gs < tile_seg0[tile + 1]; ++gs) acc += ws[(size_t)gs * per + w];
-        C[row * ldc + (int64_t)nt * BN + col] = acc;
+        const int g0 = tile_seg0[tile], g1 = tile_seg0[tile + 1];
+        for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < per; w += gridDim.x * blockDim.x) {
+            const int r = w / BN, col = w - r * BN;
+            const int64_t row = (int64_t)mt * BM + r;
+            if (row >= M) continue;
+            double acc = 0.0;
+            for (int gs = g0; gs < g1; ++gs) acc += ws[(size_t)gs * per + w];
+            C[row * ldc + (int64_t)nt * BN + col] = acc;
+        }
     }
 }
 

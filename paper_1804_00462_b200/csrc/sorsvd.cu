@@ -438,8 +438,9 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         const int nsplit = (int)sk_split_tiles_h.size();
         if (nsplit > 0) {
             const int BN = g.N <= 128 ? g.N : 128;
-            const int64_t work = (int64_t)nsplit * BM * BN;
-            streamk_fixup_kernel<<<(int)std::min<int64_t>(cdiv(work, 256), (int64_t)c->num_sms * 8), 256, 0, s>>>(
+            const dim3 fgrid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)BM * BN, 256), 16)),
+                             (unsigned)std::min(nsplit, 65535));
+            streamk_fixup_kernel<<<fgrid, 256, 0, s>>>(
                 a.sk_ws, sk_tile_seg0, sk_split_tiles, nsplit, BM, BN, (int)gy, g.M, g.C, g.ldc, c->pred,
                 c->pred_skip);
             check_launch(c);
@@ -952,7 +953,7 @@ void qr_factor(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int6
             wy_prep_kernel<<<16, 256, 0, s>>>(p->G2, Np, p->wy_tau, p->wy_sgn, p->Qtmp, Np, k, p->Ri1, p->Ri2, Np,
                                               c->pred, c->pred_skip);
             check_launch(c);
-            const int wpb = 4;
+            const int wpb = 4;  // (a shared-memory staged variant measured slower: issue bound on the shuffles)
             trinv_kernel<<<(k + wpb - 1) / wpb, 32 * wpb, (size_t)wpb * k * sizeof(double), s>>>(
                 p->Ri1, Np, k, p->G1, Np, c->pred, c->pred_skip);
             check_launch(c);
