@@ -45,6 +45,10 @@ CONFIGS = {
     # the same on the TF32 tensor cores (fp32_mode="tf32")
     "c3tf32": dict(m=200000, n=20000, k=256, q=1, scaling="strong", dtype="f32", mode="tf32",
                    desc="C3 fp32 m=200000 n=20000 k=ell=256 q=1 (TF32 tcgen05 passes), same A rounded to fp32"),
+    # BASELINE.json configs[3]: inexact-ALM RPCA, SOR-SVD (k = 10, q = 1) per iteration; one step = one solve
+    "c4": dict(m=25344, n=300, k=10, q=1, scaling="weak", kind="rpca",
+               desc="C4 RPCA fp64 25344x300 (176x144 frames), D = X Y^T (rank 5) + 10% sparse U[-50,50], "
+                    "lambda = 1/sqrt(m), tol 1e-7, max 100 iterations, SOR-SVD k=10 q=1 per iteration"),
     # BASELINE.json configs[4]: 68.7 GB FP32 matrix, FP64 arithmetic
     "c5": dict(m=131072, n=131072, k=512, q=2, scaling="strong", dtype="f32", mode="fp64",
                desc="C5 fp32 m=n=131072 k=ell=512 q=2, A = X diag(1/j) Y^T + N(0,1e-8) (FP64 DMMA passes)"),
@@ -77,6 +81,18 @@ def make_matrix(cfg_name, m_local, n, rank, world, device):
         r = min(m_local, n)
         s = 1.0 / torch.arange(1, r + 1, device=device, dtype=f64) ** 2
         return (u[:, :r] * s) @ v[:, :r].T
+    if cfg_name == "c4":
+        g.manual_seed(1000 + rank)
+        x = torch.randn(m_local, 5, generator=g, device=device, dtype=f64)
+        g.manual_seed(2000)
+        y = torch.randn(n, 5, generator=g, device=device, dtype=f64)
+        d = x @ y.T
+        g.manual_seed(3000 + rank)
+        nnz = int(round(0.1 * m_local * n))
+        idx = torch.randperm(m_local * n, generator=g, device=device)[:nnz]
+        vals = -50.0 + 100.0 * torch.rand(nnz, generator=g, device=device, dtype=f64)
+        d.view(-1)[idx] += vals
+        return d
     if cfg_name in ("c5", "c5tf32"):
         mg = CONFIGS["c5"]["m"]
         g.manual_seed(1000 + rank)
@@ -210,6 +226,131 @@ def cpu_sample(cfg_name, a_dev, cfg):
     return a_dev.cpu().numpy(), f"full {cfg_name.upper()} instance"
 
 
+# ---------------------------------------------------------------- C4 -----
+def _rpca_flops(m, n, ell, q, iterations):
+    """SOR-SVD flops of a solve: 2*m*n*ell*(2q+3) per iteration (the metric's numerator)."""
+    return 2.0 * m * n * ell * (2 * q + 3) * iterations
+
+
+def run_rpca(args, cfg, D, ctx, dist, rank, world, local_rank, device, stream, m_global, workload):
+    """Config 4: one step = one inexact-ALM solve on the device-resident D (mu0
+    estimated on the device), L2 flushed between steps; e2e = the host-buffer
+    API (H2D of D, D2H of L and S inside the timed region)."""
+    import numpy as np
+    import torch
+    import paper_1804_00462_b200 as P
+    from paper_1804_00462_b200 import dist as Dm
+    m, n = D.shape
+    ell, q = cfg["k"], cfg["q"]
+    rcfg = P.RpcaConfig(lam=1.0 / math.sqrt(max(m_global, n)), mu0=0.0, ell=ell, q=q, seed=9, max_iter=100)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    for _ in range(max(args.warmup, 0)):
+        r = P.rpca_alm(D, rcfg, ctx=ctx)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks.recording = True
+    t_wall = time.perf_counter()
+    iters = []
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        r = P.rpca_alm(D, rcfg, ctx=ctx)
+        ev[i][1].record(stream)
+        iters.append(r.iterations)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    clocks.recording = False
+    clk = clocks.stop()
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    ms_per_step = Dm.max_over_ranks(dist, sum(ms_steps), device) / args.steps
+    it = iters[-1]
+    flops = _rpca_flops(m_global, n, ell, q, it)
+    value = flops / (ms_per_step * 1e-3) / 1e9
+    # HBM roofline of an iteration: 2q+3 passes over D (8 B/entry each) + the fused
+    # update (read D, Y; write S, Y, W: 40 B/entry); the dominant traffic
+    mp = {}
+    mp_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp_path):
+        try:
+            mp = json.load(open(mp_path))
+        except Exception:
+            mp = {}
+    hbm_peak = mp.get("hbm_gbs", 6650.0)
+    bytes_iter = 8.0 * m * n * (2 * q + 3) + 40.0 * m * n
+    achieved = bytes_iter * it / (ms_per_step * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "traffic": None, "kernel": "whole RPCA iteration (2q+3 A-passes + fused rpca_update_kernel)",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "bytes_per_iteration": bytes_iter,
+            "ms_per_iteration": ms_per_step / it}
+    # e2e: host buffers through the public API
+    e2e = None
+    if not args.no_e2e:
+        dh = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+        dh.copy_(D)
+        d_np = dh.numpy()
+        P.rpca_alm(d_np, rcfg, ctx=ctx)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            P.rpca_alm(d_np, rcfg, ctx=ctx)
+        el = Dm.max_over_ranks(dist, time.perf_counter() - t0, device) / args.steps
+        e2e = {"value": flops / el / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(8 * m * n),
+               "d2h_bytes_per_step": int(2 * 8 * m * n), "ms_per_step": el * 1e3,
+               "path": "sorsvd_rpca_alm (host D in, host L and S out)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        _prefer_avx512_blas()
+        from oracle import sorsvd_oracle as O
+        O.Ref.set_threads(os.cpu_count() or 1)
+        d_cpu = D.cpu().numpy()
+        t0 = time.perf_counter()
+        rr = O.Ref.rpca_alm(d_cpu, O.RpcaConfig(lam=rcfg.lam, mu0=r.mu0, ell=ell, q=q, seed=9, max_iter=100))
+        sec = time.perf_counter() - t0
+        cpu = {"value": _rpca_flops(m, n, ell, q, rr.iterations) / sec / 1e9, "unit": "GFLOP/s",
+               "cores": os.cpu_count(), "kind": "reference",
+               "sample": f"full C4 solve ({rr.iterations} iterations, same mu0), {sec:.1f}s",
+               "ms_per_call": sec * 1e3, "iterations": rr.iterations}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": dict(workload, iterations=it, rank_l=r.rank_l, nnz_s=r.nnz_s, rel_error=r.rel_error),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(r.stats.get("launches", 0)),
+                "clocks": clk, "wall_s_timed_region": t_wall, "ms_steps": [round(x, 4) for x in ms_steps]}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_rpca_reference(args, cfg, workload, O):
+    """--impl reference for C4: the compiled reference's sor_svd_power inside the
+    SPEC.md:386-398 loop (oracle/_ref) on all host cores, same distribution."""
+    import numpy as np
+    O.Ref.set_threads(os.cpu_count() or 1)
+    D, _, _ = O.gen_c4(4, m=cfg["m"], n=cfg["n"])
+    rc = O.RpcaConfig(lam=1.0 / math.sqrt(max(D.shape)), mu0=0.0, ell=cfg["k"], q=cfg["q"], seed=9, max_iter=100)
+    times, its = [], 0
+    for i in range(max(args.steps, 1)):
+        t0 = time.perf_counter()
+        rr = O.Ref.rpca_alm(D, rc)
+        times.append(time.perf_counter() - t0)
+        its = rr.iterations
+    sec = sum(times) / len(times)
+    val = _rpca_flops(D.shape[0], D.shape[1], cfg["k"], cfg["q"], its) / sec / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": 1,
+            "steps": len(times), "warmup": 0, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(workload, iterations=its),
+            "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",
+                             "sample": "full C4 solve"},
+            "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ------------------------------------------------------------------ main --
 def main():
     ap = argparse.ArgumentParser()
@@ -253,6 +394,8 @@ def main():
         elif args.config == "c2":
             a = O.gen_c2(2, n=n, m=cfg["m"])
             sample = "full C2 instance"
+        elif args.config == "c4":
+            return run_rpca_reference(args, cfg, workload, O)
         elif args.config.startswith("c5"):
             a = O.gen_lowrank_decay(16384, 16384, 512, lambda j: 1.0 / j, 4e-4, 5).astype(np.float32).astype(np.float64)
             sample = ("16384x16384 instance of the C5 distribution (k=512, q=2, noise scaled to keep ||E|| ~ 0.07); "
@@ -296,6 +439,8 @@ def main():
     A = make_matrix(args.config, m_local, n, rank, world, device)
     torch.cuda.synchronize()
     log(f"[rank {rank}] generated {m_local}x{n} fp64 in {time.perf_counter() - t_gen:.1f}s")
+    if cfg.get("kind") == "rpca":
+        return run_rpca(args, cfg, A, ctx, dist, rank, world, local_rank, device, stream, m_global, workload)
     omega = torch.from_numpy(P.gaussian_matrix(n, ell, 7)).to(device)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
     scfg = P.SketchConfig(ell=ell, q=q, seed=7)

@@ -168,4 +168,45 @@ __global__ void nnz_partials_kernel(const double* __restrict__ x, int64_t m, int
     }
 }
 
+// ---- sigma_1 by repeated squaring of the small Gram matrix (mu0 estimate) ----
+// x[i] *= 1 / max|x| over the first `rows` rows (rows x ld, cols valid), one CTA.
+__global__ void scale_by_maxabs_kernel(double* __restrict__ X, int rows, int cols, int ld) {
+    __shared__ double red[32];
+    double mx = 0.0;
+    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+        const int i = e / cols, j = e - i * cols;
+        mx = fmax(mx, fabs(X[(size_t)i * ld + j]));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double s = red[0] > 0.0 ? 1.0 / red[0] : 0.0;
+    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+        const int i = e / cols, j = e - i * cols;
+        X[(size_t)i * ld + j] *= s;
+    }
+}
+
+// At[j][i] = A[i][j] for i < m, j < n (At row pitch ldt).
+__global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                                 double* __restrict__ At, int64_t ldt) {
+    __shared__ double tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r, j = j0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < m && j < n) ? A[i * lda + j] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t j = j0 + r, i = i0 + threadIdx.x;
+        if (j < n && i < m) At[j * ldt + i] = tile[threadIdx.x][r];
+    }
+}
+
 }  // namespace sorsvd_dev

@@ -1931,6 +1931,134 @@ double device_sumsq(sorsvd_ctx* c, const double* x, int64_t m, int64_t n, int64_
     return h[0];
 }
 
+// sigma_1(A) when min(m, n) <= 1024: G = A^T A (or A A^T), 12 squarings (each
+// rescaled by its max entry) give P ~ G^(4096), whose range is the top
+// eigenspace to working precision; a Rayleigh-Ritz step on span(P Omega)
+// (16 columns: QR, Q^T G Q, Jacobi) gives lambda_1 = sigma_1^2 to ~eps
+// relative. ~25 launches instead of a subspace iteration on A whose step
+// count depends on sigma_2 / sigma_1.
+double estimate_sigma1_gram(sorsvd_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda) {
+    const bool tall = m >= n;
+    const int s = (int)(tall ? n : m);
+    const int Np = npad(s);
+    double* G = dbuf(c, "est_G", (size_t)Np * Np, true);
+    double* P0 = dbuf(c, "est_P0", (size_t)Np * Np, true);
+    double* P1 = dbuf(c, "est_P1", (size_t)Np * Np, true);
+    cudaStream_t st = c->stream;
+    if (tall) {
+        // G = A^T A: TN with B = A needs B padded to Np columns -> copy A's rows? use A^T A via TN on A
+        // directly when n is already a multiple of 8 and lda == n, else stage A padded.
+        const double* Ap = A;
+        int64_t ldp = lda;
+        if (lda % 2 || n % 8 || lda != n) {
+            double* Ad = dbuf(c, "est_Apad", (size_t)m * Np, true);
+            CK(cudaMemcpy2DAsync(Ad, (size_t)Np * 8, A, (size_t)lda * 8, (size_t)n * 8, (size_t)m,
+                                 cudaMemcpyDeviceToDevice, st));
+            Ap = Ad;
+            ldp = Np;
+        }
+        GemmCall g;
+        g.ta = true;
+        g.A = Ap;
+        g.lda = ldp;
+        g.M = s;
+        g.K = m;
+        g.B = Ap;
+        g.ldb = ldp;
+        g.N = Np;
+        g.C = G;
+        g.ldc = Np;
+        g.ws_name = "est_ws";
+        run_gemm(c, g, st);
+    } else {
+        // G = A A^T: NN with B = A^T (staged transposed, padded)
+        double* At = dbuf(c, "est_At", (size_t)n * Np, true);
+        dim3 tb(32, 8), tg((unsigned)cdiv(m, 32), (unsigned)cdiv(n, 32));
+        transpose_kernel<<<tg, tb, 0, st>>>(A, lda, m, n, At, Np);
+        check_launch(c);
+        GemmCall g;
+        g.A = A;
+        g.lda = lda;
+        g.M = s;
+        g.K = n;
+        g.B = At;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = G;
+        g.ldc = Np;
+        g.ws_name = "est_ws";
+        run_gemm(c, g, st);
+    }
+    CK(cudaMemcpyAsync(P0, G, (size_t)s * Np * 8, cudaMemcpyDeviceToDevice, st));
+    double* cur = P0;
+    double* nxt = P1;
+    for (int it = 0; it < 12; ++it) {
+        scale_by_maxabs_kernel<<<1, 1024, 0, st>>>(cur, s, s, Np);
+        check_launch(c);
+        GemmCall g;
+        g.A = cur;
+        g.lda = Np;
+        g.M = s;
+        g.K = s;
+        g.B = cur;
+        g.ldb = Np;
+        g.N = Np;
+        g.C = nxt;
+        g.ldc = Np;
+        g.ws_name = "est_ws";
+        run_gemm(c, g, st);
+        std::swap(cur, nxt);
+    }
+    scale_by_maxabs_kernel<<<1, 1024, 0, st>>>(cur, s, s, Np);
+    check_launch(c);
+    // Rayleigh-Ritz on span(G^(4096) Omega), b = 16 columns: the Ritz value is
+    // exact to working precision unless lambda_17 / lambda_1 > ~0.99
+    const int b = std::min(16, s);
+    const int Nb = npad(b);
+    double* Om = dbuf(c, "est_Om", (size_t)s * Nb, true);
+    double* X = dbuf(c, "est_X2", (size_t)s * Nb, true);
+    double* Qb = dbuf(c, "est_Qb", (size_t)s * Nb, true);
+    double* GQ = dbuf(c, "est_GQ", (size_t)s * Nb, true);
+    double* H = dbuf(c, "est_H", (size_t)b * Nb, true);
+    double* Uh = dbuf(c, "est_Uh", (size_t)b * b);
+    double* Vh = dbuf(c, "est_Vh", (size_t)b * b);
+    double* Sh = dbuf(c, "est_Sh", (size_t)b);
+    int* sw = reinterpret_cast<int*>(dbuf(c, "est_sw2", 1));
+    {
+        std::vector<double> h((size_t)s * b);
+        sorsvd_host::gaussian_fill(h.data(), h.size(), 0x5eed5eedULL, 0);
+        CK(cudaMemcpy2DAsync(Om, (size_t)Nb * 8, h.data(), (size_t)b * 8, (size_t)b * 8, (size_t)s,
+                             cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    auto mm = [&](bool ta, const double* Am, int64_t ldam, int64_t M, int64_t K, const double* Bm, double* Cm) {
+        GemmCall g;
+        g.ta = ta;
+        g.A = Am;
+        g.lda = ldam;
+        g.M = M;
+        g.K = K;
+        g.B = Bm;
+        g.ldb = Nb;
+        g.N = Nb;
+        g.C = Cm;
+        g.ldc = Nb;
+        g.ws_name = "est_ws";
+        run_gemm(c, g, st);
+    };
+    mm(false, cur, Np, s, s, Om, X);   // X = P Omega
+    QrPlan* pq = get_qr_plan(c, s, b, 0, "est_b");
+    qr_run(c, pq, X, Nb, Qb, Nb, st);  // Q = orth(X)
+    mm(false, G, Np, s, s, Qb, GQ);    // G Q
+    mm(true, Qb, Nb, b, s, GQ, H);     // H = Q^T G Q  (b x b, symmetric PSD)
+    run_jacobi(c, b, H, Nb, Uh, b, Sh, Vh, b, sw, st);
+    double h = 0.0;
+    CK(cudaMemcpyAsync(&h, Sh, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!std::isfinite(h) || h < 0.0) throw Error{SORSVD_ERR_NUMERICAL, "numerical: sigma_1 estimate not finite"};
+    return std::sqrt(h);
+}
+
 // sigma_1(A) for mu0 = 1.25/||D||_2: block subspace iteration
 // with re-orthonormalisation (TSQR each step) and a Rayleigh-Ritz value from
 // the Jacobi SVD of R(A X); iterates until the Ritz value is stationary to
@@ -2018,7 +2146,10 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
         return;
     }
     double mu = d->mu0;
-    if (!(mu > 0.0)) mu = 1.25 / estimate_sigma1(c, dD, m, n, ldd, d->seed ^ 0x5bd1e995ULL);
+    if (!(mu > 0.0))
+        mu = 1.25 / (std::min(m, n) <= 1024 && !getenv("SORSVD_SIGMA1_SUBSPACE")
+                         ? estimate_sigma1_gram(c, dD, m, n, ldd)
+                         : estimate_sigma1(c, dD, m, n, ldd, d->seed ^ 0x5bd1e995ULL));
     r.mu0 = mu;
     const double mu_bar = (d->mu_bar_factor > 0 ? d->mu_bar_factor : 1e7) * mu;
     CK(cudaMemsetAsync(S, 0, (size_t)m * n * 8, c->stream));

@@ -443,9 +443,24 @@ def test_rpca_zero_input(P):
     assert r.iterations == 1 and r.converged and np.all(r.l == 0) and np.all(r.s == 0)
 
 
-def test_rpca_mu0_estimate(P):
-    D, _, _ = O.gen_c4(4, m=1000, n=120)
-    r = P.rpca_alm(D, P.RpcaConfig(lam=1 / np.sqrt(1000), mu0=0.0, ell=10, q=1, seed=2, max_iter=100))
+@pytest.mark.parametrize("m,n", [(1000, 120), (120, 1000), (25344, 300)])
+def test_rpca_mu0_estimate(P, m, n):
+    # mu0 = 1.25 / sigma_1(D): Gram squaring + Rayleigh-Ritz on the device
+    D, _, _ = O.gen_c4(4, m=m, n=n)
+    r = P.rpca_alm(D, P.RpcaConfig(lam=1 / np.sqrt(max(m, n)), mu0=0.0, ell=10, q=1, seed=2, max_iter=100))
     exact = 1.25 / O.norm_spectral(D)
-    assert abs(r.mu0 - exact) <= 1e-9 * exact
+    assert abs(r.mu0 - exact) <= 1e-12 * exact, (r.mu0, exact)
     assert r.converged
+
+
+def test_rpca_mu0_estimate_clustered_top(P):
+    # nearly degenerate top singular values (plain power iteration would stall)
+    m, n = 800, 200
+    u, _ = np.linalg.qr(O.gaussian_matrix(m, n, 1))
+    v, _ = np.linalg.qr(O.gaussian_matrix(n, n, 2))
+    sig = np.linspace(1.0, 0.2, n)
+    sig[1] = 1.0 - 1e-9
+    sig[2] = 1.0 - 2e-6
+    D = (u * sig) @ v.T
+    r = P.rpca_alm(D, P.RpcaConfig(lam=1 / np.sqrt(m), mu0=0.0, ell=10, q=1, seed=2, max_iter=3))
+    assert abs(r.mu0 - 1.25) <= 1e-12 * 1.25, r.mu0
