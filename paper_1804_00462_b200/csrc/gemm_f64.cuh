@@ -272,14 +272,29 @@ __global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* _
 }
 
 // out[i] = sum_{s<S} ws[s*stride + i], fixed summation order (deterministic).
+// The partial loads are issued 8 at a time ahead of the (ordered) adds: with
+// many splits and few outputs (K = m reductions) the loop is L2-latency bound.
 __global__ void reduce_splits_kernel(const double* __restrict__ ws, int64_t count2, int S, int64_t stride,
                                      double* __restrict__ out, const int* pred, int pred_skip) {
     if (pred && *pred == pred_skip) return;
     const int64_t n2 = count2;
+    const double2* __restrict__ w2 = reinterpret_cast<const double2*>(ws);
+    const int64_t st2 = stride / 2;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
-        double2 acc = reinterpret_cast<const double2*>(ws)[i];
-        for (int s = 1; s < S; ++s) {
-            const double2 v = reinterpret_cast<const double2*>(ws + s * stride)[i];
+        double2 acc = w2[i];
+        int s = 1;
+        for (; s + 8 <= S; s += 8) {
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = w2[(int64_t)(s + u) * st2 + i];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                acc.x += v[u].x;
+                acc.y += v[u].y;
+            }
+        }
+        for (; s < S; ++s) {
+            const double2 v = w2[(int64_t)s * st2 + i];
             acc.x += v.x;
             acc.y += v.y;
         }

@@ -37,9 +37,12 @@ struct RpcaArgs {
     double mu, mu_next, eps;  // eps = lambda / mu
     double* partial;          // per-block residual^2 partials
     int mode;                 // 0 = ALM update, 1 = write L only
+    const int* pred;          // optional: no-op when *pred == pred_skip (iteration after convergence)
+    int pred_skip;
 };
 
 __global__ void __launch_bounds__(kRpcaThreads) rpca_update_kernel(RpcaArgs a) {
+    if (a.pred && *a.pred == a.pred_skip) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
     const int64_t i0 = (int64_t)blockIdx.y * 64 + (warp >> 1) * 16;
     const int64_t j0 = (int64_t)blockIdx.x * 64 + (warp & 1) * 32;
@@ -111,7 +114,9 @@ __global__ void __launch_bounds__(kRpcaThreads) rpca_update_kernel(RpcaArgs a) {
 }
 
 // Deterministic single-block reduction of partials: out[0] = sum, (sqrt into out[1]).
-__global__ void sum_partials_kernel(const double* __restrict__ p, int64_t n, double* out) {
+__global__ void sum_partials_kernel(const double* __restrict__ p, int64_t n, double* out, const int* pred = nullptr,
+                                    int pred_skip = 0) {
+    if (pred && *pred == pred_skip) return;
     __shared__ double red[32];
     double t = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) t += p[i];
@@ -123,6 +128,24 @@ __global__ void sum_partials_kernel(const double* __restrict__ p, int64_t n, dou
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
         out[0] = s;
         out[1] = sqrt(s);
+    }
+}
+
+// Stopping test of iteration `it` on the device, so that the
+// host can enqueue several iterations ahead: st[0] = done flag (sticky), st[1]
+// = iterations executed, st[2] = error flag; rel[0] = this iteration's
+// ||D - L - S||_F / ||D||_F. Predicated like the iteration itself.
+__global__ void rpca_check_kernel(const double* __restrict__ tot, double dnorm, double tol, int it, int* st,
+                                  double* rel, const int* pred, int pred_skip) {
+    if (pred && *pred == pred_skip) return;
+    const double r = sqrt(tot[0]) / dnorm;
+    rel[0] = r;
+    st[1] = it + 1;
+    if (!isfinite(r)) {
+        st[2] = 1;
+        st[0] = 1;
+    } else if (r < tol) {
+        st[0] = 1;
     }
 }
 
@@ -169,25 +192,26 @@ __global__ void nnz_partials_kernel(const double* __restrict__ x, int64_t m, int
 }
 
 // ---- sigma_1 by repeated squaring of the small Gram matrix (mu0 estimate) ----
-// x[i] *= 1 / max|x| over the first `rows` rows (rows x ld, cols valid), one CTA.
-__global__ void scale_by_maxabs_kernel(double* __restrict__ X, int rows, int cols, int ld) {
-    __shared__ double red[32];
-    double mx = 0.0;
-    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+// *mx = max |X| over rows x cols (non-negative doubles order like their bits);
+// *mx must be 0 on entry. Grid-stride, one atomic per warp.
+__global__ void maxabs_kernel(const double* __restrict__ X, int rows, int cols, int ld,
+                              unsigned long long* __restrict__ mx) {
+    double m = 0.0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
         const int i = e / cols, j = e - i * cols;
-        mx = fmax(mx, fabs(X[(size_t)i * ld + j]));
+        m = fmax(m, fabs(X[(size_t)i * ld + j]));
     }
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (threadIdx.x == 0) red[0] = v;
-    }
-    __syncthreads();
-    const double s = red[0] > 0.0 ? 1.0 / red[0] : 0.0;
-    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(mx, (unsigned long long)__double_as_longlong(m));
+}
+
+// X *= 1 / *mx, then *mx = 0 for the next use (the last block to finish resets it
+// is not needed: each use gets its own slot).
+__global__ void scale_by_kernel(double* __restrict__ X, int rows, int cols, int ld,
+                                const unsigned long long* __restrict__ mx) {
+    const double m = __longlong_as_double((long long)*mx);
+    const double s = m > 0.0 ? 1.0 / m : 0.0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
         const int i = e / cols, j = e - i * cols;
         X[(size_t)i * ld + j] *= s;
     }

@@ -1769,11 +1769,12 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     record_stage(c, timing, 5);
 }
 
-std::string sor_key(const SorProblem& P) {
-    char buf[256];
+std::string sor_key(const SorProblem& P, const int* pred = nullptr) {
+    char buf[320];
     snprintf(buf, sizeof buf, "sor:%d:%d:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.dtype, (int)P.single_pass, (int)P.tf32,
              P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m, (long long)P.n,
              (long long)P.lda, P.k, P.ell, P.q);
+    if (pred) snprintf(buf + strlen(buf), sizeof buf - strlen(buf), ":pred%p", (const void*)pred);
     return buf;
 }
 
@@ -1992,9 +1993,17 @@ double estimate_sigma1_gram(sorsvd_ctx* c, const double* A, int64_t m, int64_t n
     CK(cudaMemcpyAsync(P0, G, (size_t)s * Np * 8, cudaMemcpyDeviceToDevice, st));
     double* cur = P0;
     double* nxt = P1;
-    for (int it = 0; it < 12; ++it) {
-        scale_by_maxabs_kernel<<<1, 1024, 0, st>>>(cur, s, s, Np);
+    unsigned long long* mx = reinterpret_cast<unsigned long long*>(dbuf(c, "est_mx", 16));
+    CK(cudaMemsetAsync(mx, 0, 16 * sizeof(unsigned long long), st));
+    const int sg = (int)std::min<int64_t>(cdiv((int64_t)s * s, 256), 2 * c->num_sms);
+    auto rescale = [&](int slot) {
+        maxabs_kernel<<<sg, 256, 0, st>>>(cur, s, s, Np, mx + slot);
         check_launch(c);
+        scale_by_kernel<<<sg, 256, 0, st>>>(cur, s, s, Np, mx + slot);
+        check_launch(c);
+    };
+    for (int it = 0; it < 12; ++it) {
+        rescale(it);
         GemmCall g;
         g.A = cur;
         g.lda = Np;
@@ -2009,8 +2018,7 @@ double estimate_sigma1_gram(sorsvd_ctx* c, const double* A, int64_t m, int64_t n
         run_gemm(c, g, st);
         std::swap(cur, nxt);
     }
-    scale_by_maxabs_kernel<<<1, 1024, 0, st>>>(cur, s, s, Np);
-    check_launch(c);
+    rescale(12);
     // Rayleigh-Ritz on span(G^(4096) Omega), b = 16 columns: the Ritz value is
     // exact to working precision unless lambda_17 / lambda_1 > ~0.99
     const int b = std::min(16, s);
@@ -2158,66 +2166,100 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
     const int64_t nblk = (int64_t)grid.x * grid.y;
     double* part = dbuf(c, "rp_part", (size_t)nblk);
     double* tot = dbuf(c, "rp_tot", 2);
-    std::vector<double> hsig(ell);
-    double mu_last = mu;
+    // Iterations are enqueued kBatch at a time without a host round trip: the
+    // stopping test runs on the device (rpca_check_kernel) and every kernel of
+    // an iteration after convergence is predicated off, so the result is the
+    // same as stopping on the host. mu follows its data-independent schedule
+    // (min(rho mu, mu_bar)); each in-flight iteration has its own
+    // U / sigma / V slot so the last executed one survives for the final L.
+    constexpr int kBatch = 4;
+    double* Us = dbuf(c, "rp_Us", (size_t)kBatch * m * ell);
+    double* Vs = dbuf(c, "rp_Vs", (size_t)kBatch * n * ell);
+    double* sigs = dbuf(c, "rp_sigs", (size_t)kBatch * ell);
+    int* stf = reinterpret_cast<int*>(dbuf(c, "rp_state", 2));  // [0] done, [1] iterations, [2] error
+    double* rels = dbuf(c, "rp_rel", 1);
+    CK(cudaMemsetAsync(stf, 0, 4 * sizeof(int), c->stream));
+    std::vector<double> mus;
+    mus.push_back(mu);
     int it = 0;
     double rel = 0.0;
     int rank = 0;
     bool conv = false;
+    int executed = 0;
     while (it < d->max_iter) {
-        sorsvd_desc sd{};
-        sd.m = m;
-        sd.n = n;
-        sd.lda = it == 0 ? ldd : n;
-        sd.k = ell;
-        sd.ell = ell;
-        sd.q = d->q;
-        sd.seed = d->seed + (uint64_t)it;
-        sd.dtype = SORSVD_F64;
-        sd.flags = d->flags & SORSVD_FLAG_NO_GRAPH;
-        sor_device(c, &sd, it == 0 ? dD : W, nullptr, U, sig, V, nullptr);
-        const double mu_next = std::min(d->rho * mu, mu_bar);
-        RpcaArgs a{};
-        a.D = dD;
-        a.ldd = ldd;
-        a.S = S;
-        a.Y = Y;
-        a.W = W;
-        a.ldx = n;
-        a.U = U;
-        a.ldu = ell;
-        a.V = V;
-        a.ldv = ell;
-        a.sig = sig;
-        a.m = m;
-        a.n = n;
-        a.k = ell;
-        a.mu = mu;
-        a.mu_next = mu_next;
-        a.eps = lambda / mu;
-        a.partial = part;
-        a.mode = 0;
-        rpca_update_kernel<<<grid, kRpcaThreads, 0, c->stream>>>(a);
-        check_launch(c);
-        sum_partials_kernel<<<1, 1024, 0, c->stream>>>(part, nblk, tot);
-        check_launch(c);
-        double h[2];
-        CK(cudaMemcpyAsync(h, tot, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(hsig.data(), sig, ell * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        const int nb = std::min(kBatch, d->max_iter - it);
+        for (int bi = 0; bi < nb; ++bi) {
+            const int j = it + bi;
+            while ((int)mus.size() <= j + 1) mus.push_back(std::min(d->rho * mus.back(), mu_bar));
+            double* Uj = Us + (size_t)(j % kBatch) * m * ell;
+            double* Vj = Vs + (size_t)(j % kBatch) * n * ell;
+            double* sj = sigs + (size_t)(j % kBatch) * ell;
+            PredScope ps(c, stf, 1);  // everything below is skipped once stf[0] == 1
+            sorsvd_desc sd{};
+            sd.m = m;
+            sd.n = n;
+            sd.lda = j == 0 ? ldd : n;
+            sd.k = ell;
+            sd.ell = ell;
+            sd.q = d->q;
+            sd.seed = d->seed + (uint64_t)j;
+            sd.dtype = SORSVD_F64;
+            sd.flags = d->flags & SORSVD_FLAG_NO_GRAPH;
+            sor_device(c, &sd, j == 0 ? dD : W, nullptr, Uj, sj, Vj, nullptr);
+            RpcaArgs a{};
+            a.D = dD;
+            a.ldd = ldd;
+            a.S = S;
+            a.Y = Y;
+            a.W = W;
+            a.ldx = n;
+            a.U = Uj;
+            a.ldu = ell;
+            a.V = Vj;
+            a.ldv = ell;
+            a.sig = sj;
+            a.m = m;
+            a.n = n;
+            a.k = ell;
+            a.mu = mus[j];
+            a.mu_next = mus[j + 1];
+            a.eps = lambda / mus[j];
+            a.partial = part;
+            a.mode = 0;
+            a.pred = stf;
+            a.pred_skip = 1;
+            rpca_update_kernel<<<grid, kRpcaThreads, 0, c->stream>>>(a);
+            check_launch(c);
+            sum_partials_kernel<<<1, 1024, 0, c->stream>>>(part, nblk, tot, stf, 1);
+            check_launch(c);
+            rpca_check_kernel<<<1, 1, 0, c->stream>>>(tot, dnorm, d->tol, j, stf, rels, stf, 1);
+            check_launch(c);
+        }
+        int hst[3];
+        CK(cudaMemcpyAsync(hst, stf, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&rel, rels, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        mu_last = mu;
-        rank = 0;
-        const double z0 = std::max(hsig[0] - 1.0 / mu, 0.0);
-        for (int j = 0; j < ell; ++j)
-            if (std::max(hsig[j] - 1.0 / mu, 0.0) > 1e-8 * z0) ++rank;
-        mu = mu_next;
-        ++it;
-        rel = std::sqrt(h[0]) / dnorm;
-        if (!std::isfinite(rel)) throw Error{SORSVD_ERR_NUMERICAL, "numerical: rpca produced a non-finite iterate"};
-        if (rel < d->tol) {
+        executed = hst[1];
+        if (hst[2]) throw Error{SORSVD_ERR_NUMERICAL, "numerical: rpca produced a non-finite iterate"};
+        if (hst[0]) {
             conv = true;
             break;
         }
+        it += nb;
+    }
+    it = executed;
+    // rank of the last executed iteration's shrunk spectrum
+    const int fl = it - 1;
+    U = Us + (size_t)(fl % kBatch) * m * ell;
+    V = Vs + (size_t)(fl % kBatch) * n * ell;
+    sig = sigs + (size_t)(fl % kBatch) * ell;
+    std::vector<double> hsig(ell);
+    CK(cudaMemcpy(hsig.data(), sig, ell * sizeof(double), cudaMemcpyDeviceToHost));
+    const double mu_last = mus[fl];
+    {
+        const double z0 = std::max(hsig[0] - 1.0 / mu_last, 0.0);
+        for (int jj = 0; jj < ell; ++jj)
+            if (std::max(hsig[jj] - 1.0 / mu_last, 0.0) > 1e-8 * z0) ++rank;
     }
     if (dL) {
         RpcaArgs a{};
