@@ -56,6 +56,8 @@ struct GemmArgs {
     int sk_units;          // BK units per tile
     int sk_gy;             // column chunks per row tile
     double* sk_ws;
+    int gy_fused;          // > 0: blockIdx.x = row_tile * gy_fused + column chunk (chunks of a row tile
+                           // run back to back, so A's tile is served from L2 the second time)
 };
 
 constexpr int kGemmThreads = 256;
@@ -237,12 +239,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
         rows = p.tile_rows[blockIdx.x];
         seg = p.tile_seg[blockIdx.x];
     } else {
-        row0 = (int64_t)blockIdx.x * S::BM;
+        const int mt = p.gy_fused > 0 ? (int)(blockIdx.x / p.gy_fused) : (int)blockIdx.x;
+        row0 = (int64_t)mt * S::BM;
         rows = p.M - row0 < S::BM ? p.M - row0 : S::BM;
     }
     const int64_t kBegin = (int64_t)blockIdx.z * p.k_chunk;
     const int64_t kEnd = min(kBegin + p.k_chunk, p.K);
-    const int ncol0 = blockIdx.y * S::BN;
+    const int ncol0 = (p.gy_fused > 0 ? (int)(blockIdx.x % p.gy_fused) : (int)blockIdx.y) * S::BN;
     gemm_tile<FM, FN, TA, V16, AT>(p, smem_raw, row0, rows, seg, ncol0, kBegin, kEnd,
                                    p.C + (int64_t)blockIdx.z * p.c_split_stride + ncol0, row0, p.ldc);
 }

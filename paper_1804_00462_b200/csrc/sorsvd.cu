@@ -419,6 +419,10 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
     if (f32a && !aligned) throw Error{SORSVD_ERR_SHAPE, "shape: fp32 A needs 16-byte aligned rows (lda % 4 == 0)"};
     const bool v16 = aligned;
     dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)S);
+    if (!g.tile_row0 && gy > 1) {
+        a.gy_fused = (int)gy;
+        grid = dim3((unsigned)(gx * gy), 1, (unsigned)S);
+    }
     if (streamk) {
         grid = dim3((unsigned)c->num_sms, 1, 1);
         a.C = g.C;
