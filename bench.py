@@ -46,7 +46,7 @@ CONFIGS = {
     "c3tf32": dict(m=200000, n=20000, k=256, q=1, scaling="strong", dtype="f32", mode="tf32",
                    desc="C3 fp32 m=200000 n=20000 k=ell=256 q=1 (TF32 tcgen05 passes), same A rounded to fp32"),
     # BASELINE.json configs[3]: inexact-ALM RPCA, SOR-SVD (k = 10, q = 1) per iteration; one step = one solve
-    "c4": dict(m=25344, n=300, k=10, q=1, scaling="weak", kind="rpca",
+    "c4": dict(m=25344, n=300, k=10, q=1, scaling="strong", kind="rpca",
                desc="C4 RPCA fp64 25344x300 (176x144 frames), D = X Y^T (rank 5) + 10% sparse U[-50,50], "
                     "lambda = 1/sqrt(m), tol 1e-7, max 100 iterations, SOR-SVD k=10 q=1 per iteration"),
     # BASELINE.json configs[4]: 68.7 GB FP32 matrix, FP64 arithmetic
@@ -247,7 +247,7 @@ def run_rpca(args, cfg, D, ctx, dist, rank, world, local_rank, device, stream, m
     clocks = ClockSampler(local_rank)
     clocks.start()
     for _ in range(max(args.warmup, 0)):
-        r = P.rpca_alm(D, rcfg, ctx=ctx)
+        r = P.rpca_alm(D, rcfg, ctx=ctx, m_global=m_global)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks.recording = True
@@ -256,7 +256,7 @@ def run_rpca(args, cfg, D, ctx, dist, rank, world, local_rank, device, stream, m
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record(stream)
-        r = P.rpca_alm(D, rcfg, ctx=ctx)
+        r = P.rpca_alm(D, rcfg, ctx=ctx, m_global=m_global)
         ev[i][1].record(stream)
         iters.append(r.iterations)
     torch.cuda.synchronize()
@@ -290,10 +290,10 @@ def run_rpca(args, cfg, D, ctx, dist, rank, world, local_rank, device, stream, m
         dh = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
         dh.copy_(D)
         d_np = dh.numpy()
-        P.rpca_alm(d_np, rcfg, ctx=ctx)
+        P.rpca_alm(d_np, rcfg, ctx=ctx, m_global=m_global)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            P.rpca_alm(d_np, rcfg, ctx=ctx)
+            P.rpca_alm(d_np, rcfg, ctx=ctx, m_global=m_global)
         el = Dm.max_over_ranks(dist, time.perf_counter() - t0, device) / args.steps
         e2e = {"value": flops / el / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(8 * m * n),
                "d2h_bytes_per_step": int(2 * 8 * m * n), "ms_per_step": el * 1e3,

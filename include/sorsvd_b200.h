@@ -143,6 +143,7 @@ typedef struct sorsvd_rpca_desc {
     uint64_t seed;        /* iteration it uses seed + it */
     uint32_t flags;
     int32_t pad_;
+    int64_t m_global;     /* multi-GPU: total rows (m = this rank's row block); <= 0 -> m */
 } sorsvd_rpca_desc;
 
 typedef struct sorsvd_rpca_result {

@@ -414,8 +414,12 @@ def rpca_default_config(m: int, n: int, ell: int = 10, q: int = 1, seed: int = 0
                       max_iter=500, ell=ell, q=q, seed=seed)
 
 
-def rpca_alm(x, cfg: RpcaConfig, ctx: Optional[Context] = None, want_l: bool = True) -> RpcaResult:
-    """Inexact ALM RPCA with SOR-SVD per iteration."""
+def rpca_alm(x, cfg: RpcaConfig, ctx: Optional[Context] = None, want_l: bool = True,
+             m_global: int = 0) -> RpcaResult:
+    """Inexact ALM RPCA with SOR-SVD per iteration.
+    Multi-GPU: x is this rank's row block of D, m_global the total rows; L and
+    S come back row-sharded, the scalars (iterations, rel_error, rank, nnz)
+    are global."""
     res = C.RpcaRes()
     if _is_torch_cuda(x):
         import torch
@@ -423,7 +427,7 @@ def rpca_alm(x, cfg: RpcaConfig, ctx: Optional[Context] = None, want_l: bool = T
         _torch_stream(ctx, x)
         m, n = x.shape
         d = C.RpcaDesc(m, n, x.stride(0), cfg.lam, cfg.mu0, cfg.mu_bar_factor, cfg.rho, cfg.tol, cfg.max_iter,
-                       cfg.ell, cfg.q, C.F64, cfg.seed & (2**64 - 1), 0, 0)
+                       cfg.ell, cfg.q, C.F64, cfg.seed & (2**64 - 1), 0, 0, m_global)
         s = torch.empty((m, n), dtype=torch.float64, device=x.device)
         l = torch.empty((m, n), dtype=torch.float64, device=x.device) if want_l else None
         _check(C.lib().sorsvd_rpca_alm_device(ctx.handle, ctypes.byref(d), x.data_ptr(),
@@ -434,7 +438,7 @@ def rpca_alm(x, cfg: RpcaConfig, ctx: Optional[Context] = None, want_l: bool = T
         ctx = ctx or default_context(0)
         m, n = x.shape
         d = C.RpcaDesc(m, n, n, cfg.lam, cfg.mu0, cfg.mu_bar_factor, cfg.rho, cfg.tol, cfg.max_iter, cfg.ell,
-                       cfg.q, C.F64, cfg.seed & (2**64 - 1), 0, 0)
+                       cfg.q, C.F64, cfg.seed & (2**64 - 1), 0, 0, m_global)
         s = np.empty((m, n))
         l = np.empty((m, n)) if want_l else None
         _check(C.lib().sorsvd_rpca_alm(ctx.handle, ctypes.byref(d), x.ctypes.data_as(C.c_dp),

@@ -49,7 +49,7 @@ class RpcaDesc(ctypes.Structure):
     _fields_ = [("m", c_i64), ("n", c_i64), ("ldd", c_i64), ("lam", ctypes.c_double), ("mu0", ctypes.c_double),
                 ("mu_bar_factor", ctypes.c_double), ("rho", ctypes.c_double), ("tol", ctypes.c_double),
                 ("max_iter", c_i32), ("ell", c_i32), ("q", c_i32), ("dtype", c_i32), ("seed", c_u64),
-                ("flags", c_u32), ("pad_", c_i32)]
+                ("flags", c_u32), ("pad_", c_i32), ("m_global", c_i64)]
 
 
 class RpcaRes(ctypes.Structure):

@@ -1930,6 +1930,7 @@ double device_sumsq(sorsvd_ctx* c, const double* x, int64_t m, int64_t n, int64_
     check_launch(c);
     sum_partials_kernel<<<1, 1024, 0, c->stream>>>(part, blocks, tot);
     check_launch(c);
+    comm_allreduce(c, tot, 1, false, c->stream);  // multi-rank: sum over the row blocks
     double h[2];
     CK(cudaMemcpyAsync(h, tot, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1943,7 +1944,7 @@ double device_sumsq(sorsvd_ctx* c, const double* x, int64_t m, int64_t n, int64_
 // relative. ~25 launches instead of a subspace iteration on A whose step
 // count depends on sigma_2 / sigma_1.
 double estimate_sigma1_gram(sorsvd_ctx* c, const double* A, int64_t m, int64_t n, int64_t lda) {
-    const bool tall = m >= n;
+    const bool tall = m >= n || c->world > 1;  // row-sharded D: G = sum_r D_r^T D_r
     const int s = (int)(tall ? n : m);
     const int Np = npad(s);
     double* G = dbuf(c, "est_G", (size_t)Np * Np, true);
@@ -1975,6 +1976,7 @@ double estimate_sigma1_gram(sorsvd_ctx* c, const double* A, int64_t m, int64_t n
         g.ldc = Np;
         g.ws_name = "est_ws";
         run_gemm(c, g, st);
+        comm_allreduce(c, G, (size_t)s * Np, false, st);
     } else {
         // G = A A^T: NN with B = A^T (staged transposed, padded)
         double* At = dbuf(c, "est_At", (size_t)n * Np, true);
@@ -2137,7 +2139,9 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
     if (const char* e = sorsvd_host::validate_sketch(m, n, d->ell, d->ell, d->q)) throw Error{SORSVD_ERR_PARAMETER, e};
     if (d->dtype != SORSVD_F64) throw Error{SORSVD_ERR_UNSUPPORTED, "only SORSVD_F64 is implemented"};
     const int ell = d->ell;
-    const double lambda = d->lambda > 0 ? d->lambda : 1.0 / std::sqrt((double)std::max(m, n));
+    const int64_t mg = d->m_global > 0 ? d->m_global : m;
+    if (c->world == 1 && mg != m) throw Error{SORSVD_ERR_SHAPE, "shape: m_global != m on a single-rank context"};
+    const double lambda = d->lambda > 0 ? d->lambda : 1.0 / std::sqrt((double)std::max(mg, n));
     CK(cudaEventRecord(c->ev_h[2], c->stream));
     const int launches0 = c->launches;
     double* S = dSout ? dSout : dbuf(c, "rp_S", (size_t)m * n);
@@ -2158,10 +2162,14 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
         return;
     }
     double mu = d->mu0;
-    if (!(mu > 0.0))
-        mu = 1.25 / (std::min(m, n) <= 1024 && !getenv("SORSVD_SIGMA1_SUBSPACE")
+    if (!(mu > 0.0)) {
+        const bool gram = c->world > 1 ? n <= 1024 : std::min(m, n) <= 1024;
+        if (c->world > 1 && !gram)
+            throw Error{SORSVD_ERR_UNSUPPORTED, "multi-rank rpca with n > 1024 needs mu0 passed in"};
+        mu = 1.25 / (gram && !getenv("SORSVD_SIGMA1_SUBSPACE")
                          ? estimate_sigma1_gram(c, dD, m, n, ldd)
                          : estimate_sigma1(c, dD, m, n, ldd, d->seed ^ 0x5bd1e995ULL));
+    }
     r.mu0 = mu;
     const double mu_bar = (d->mu_bar_factor > 0 ? d->mu_bar_factor : 1e7) * mu;
     CK(cudaMemsetAsync(S, 0, (size_t)m * n * 8, c->stream));
@@ -2209,6 +2217,7 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
             sd.seed = d->seed + (uint64_t)j;
             sd.dtype = SORSVD_F64;
             sd.flags = d->flags & SORSVD_FLAG_NO_GRAPH;
+            sd.m_global = mg;
             sor_device(c, &sd, j == 0 ? dD : W, nullptr, Uj, sj, Vj, nullptr);
             RpcaArgs a{};
             a.D = dD;
@@ -2236,6 +2245,7 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
             check_launch(c);
             sum_partials_kernel<<<1, 1024, 0, c->stream>>>(part, nblk, tot, stf, 1);
             check_launch(c);
+            comm_allreduce(c, tot, 1, false, c->stream);  // residual over all row blocks
             rpca_check_kernel<<<1, 1, 0, c->stream>>>(tot, dnorm, d->tol, j, stf, rels, stf, 1);
             check_launch(c);
         }
@@ -2292,6 +2302,16 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
     CK(cudaStreamSynchronize(c->stream));
     long long nnz = 0;
     for (auto v : hn) nnz += (long long)v;
+    if (c->world > 1) {  // global count (exact in double below 2^53)
+        double* dn = dbuf(c, "rp_nnz_g", 1);
+        const double hv = (double)nnz;
+        CK(cudaMemcpyAsync(dn, &hv, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        comm_allreduce(c, dn, 1, false, c->stream);
+        double tot_nnz = 0.0;
+        CK(cudaMemcpyAsync(&tot_nnz, dn, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        nnz = (long long)tot_nnz;
+    }
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->ev_h[2], c->ev_h[3]));
     r.iterations = it;

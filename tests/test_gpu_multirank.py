@@ -104,3 +104,70 @@ def test_sharded_fp32(env):
     out, u = _run_sharded(P, torch, A, 64, P.SketchConfig(64, 1, 3), 2, dtype=torch.float32)
     s0 = out[0].sigma.cpu().numpy()
     assert O.sigma_rel_err(s0, base.sigma)[:32].max() <= 3e-3
+
+
+def _rpca_sharded(P, torch, D, cfg, world):
+    m = D.shape[0]
+    g = P.EmuGroup(world)
+    base, extra = divmod(m, world)
+    bounds, r0 = [], 0
+    for r in range(world):
+        cnt = base + (1 if r < extra else 0)
+        bounds.append((r0, r0 + cnt))
+        r0 += cnt
+    ctxs = [P.Context(0, rank=r, emu_group=g) for r in range(world)]
+    out, err = [None] * world, [None] * world
+
+    def work(r):
+        try:
+            a, b = bounds[r]
+            blk = torch.from_numpy(np.ascontiguousarray(D[a:b])).cuda()
+            out[r] = P.rpca_alm(blk, cfg, ctx=ctxs[r], m_global=m)
+            torch.cuda.synchronize()
+        except Exception as e:
+            err[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    for c in ctxs:
+        c.close()
+    g.close()
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rpca_sharded_matches_single(env, world):
+    # Config 4 row-sharded: elementwise work local, the residual,
+    # ||D||_F, the sigma_1 Gram and ||S||_0 summed over ranks
+    P, torch = env
+    D, L0, S0 = O.gen_c4(4, m=3000, n=150)
+    cfg = P.RpcaConfig(lam=1 / np.sqrt(3000), mu0=0.0, ell=10, q=1, seed=9, max_iter=100)
+    one = P.rpca_alm(torch.from_numpy(D).cuda(), cfg)
+    out = _rpca_sharded(P, torch, D, cfg, world)
+    for o in out:
+        assert o.iterations == one.iterations and o.rank_l == one.rank_l and o.nnz_s == one.nnz_s
+        assert abs(o.mu0 - one.mu0) <= 1e-12 * one.mu0
+    l = np.vstack([o.l.cpu().numpy() for o in out])
+    s = np.vstack([o.s.cpu().numpy() for o in out])
+    l1, s1 = one.l.cpu().numpy(), one.s.cpu().numpy()
+    assert np.linalg.norm(l - l1) <= 1e-9 * np.linalg.norm(l1)
+    assert np.linalg.norm(s - s1) <= 1e-9 * np.linalg.norm(s1)
+
+
+def test_sharded_k300_gram_qr(env):
+    # k > 256 across ranks: the CholeskyQR Gram matrices are all-reduced
+    P, torch = env
+    A = O.gen_lowrank_decay(3000, 1200, 300, lambda j: 1.0 / j, 1e-6, 12)
+    cfg = O.SketchConfig(300, 1, 5)
+    base, ds, _ = O.perturbation_floor(A, 300, cfg, trials=1, qr_variants=2)
+    out, u = _run_sharded(P, torch, A, 300, P.SketchConfig(300, 1, 5), 2)
+    s = out[0].sigma.cpu().numpy()
+    es = O.sigma_rel_err(s, base.sigma)
+    assert np.all(es <= np.maximum(1e-10, 10 * np.maximum.accumulate(ds))), es.max()
+    assert np.array_equal(s, out[1].sigma.cpu().numpy())
