@@ -61,14 +61,18 @@ struct GemmArgs {
 };
 
 constexpr int kGemmThreads = 256;
-constexpr int kGemmBK = 16;
-constexpr int kGemmStages = 4;
+// K depth per smem stage and ring depth: the wide tiles (FM = 2, N up to 128)
+// take BK = 32 with 3 stages (half the barriers per flop; <= 212 KB), the
+// narrow-N tiles (FM = 4) BK = 16 with 4 stages.
+__host__ __device__ constexpr int gemm_bk(int FM) { return FM >= 4 ? 16 : 32; }
+__host__ __device__ constexpr int gemm_stages(int FM) { return FM >= 4 ? 4 : 3; }
 
 template <int FM, int FN, bool TA, typename AT = double>
 struct GemmShape {
     static constexpr int BM = 8 * 8 * FM;
     static constexpr int BN = 8 * FN;
-    static constexpr int BK = kGemmBK;
+    static constexpr int BK = gemm_bk(FM);
+    static constexpr int STAGES = gemm_stages(FM);
     static constexpr int EPV = 16 / (int)sizeof(AT);  // A elements per 16-byte vector
     // padded smem strides: fragment reads conflict free (doubles: == 4 mod 8; floats: +4 / +8 words)
     static constexpr int LDA_S = TA ? (BM + (sizeof(AT) == 4 ? 8 : 4)) : (BK + 4);
@@ -77,7 +81,7 @@ struct GemmShape {
     static constexpr int A_BYTES = ((A_STAGE * (int)sizeof(AT) + 15) / 16) * 16;
     static constexpr int B_STAGE = BK * LDB_S;
     static constexpr int STAGE_BYTES = A_BYTES + B_STAGE * 8;
-    static constexpr size_t SMEM = (size_t)kGemmStages * STAGE_BYTES;
+    static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES;
 };
 
 // One output tile (rows [row0, row0+rows), columns [ncol0, ncol0+BN)) over the
@@ -161,21 +165,21 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& p, unsigned char* smem
         for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
-    for (int s = 0; s < kGemmStages - 1; ++s) {
+    for (int s = 0; s < S::STAGES - 1; ++s) {
         if (s < KT) load_stage(s, s);
         cp_async_commit();
     }
     const int wrow = warp * 8 * FM;
     for (int kt = 0; kt < KT; ++kt) {
-        cp_async_wait<kGemmStages - 2>();
+        cp_async_wait<S::STAGES - 2>();
         __syncthreads();
         {
-            const int nk = kt + kGemmStages - 1;
-            if (nk < KT) load_stage(nk % kGemmStages, nk);
+            const int nk = kt + S::STAGES - 1;
+            if (nk < KT) load_stage(nk % S::STAGES, nk);
             cp_async_commit();
         }
-        const AT* As = a_stage(kt % kGemmStages);
-        const double* Bs = b_stage(kt % kGemmStages);
+        const AT* As = a_stage(kt % S::STAGES);
+        const double* Bs = b_stage(kt % S::STAGES);
 #pragma unroll
         for (int ks = 0; ks < S::BK / 4; ++ks) {
             double a[FM], b[FN];

@@ -291,6 +291,11 @@ void dispatch_fn(bool ta, bool v16, bool f32a, const GemmArgs& a, dim3 grid, cud
     }
 }
 
+int gemm_bk_for(int N) {
+    const int FN = N <= 128 ? N / 8 : 16;
+    return gemm_bk(FN <= 4 ? 4 : 2);
+}
+
 int gemm_bm_for(int N) {
     const int FN = N <= 128 ? N / 8 : 16;
     return 64 * (FN <= 4 ? 4 : 2);
@@ -323,12 +328,13 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
     // stream-K when whole tiles x splits leave SMs idle: equal BK-unit shares per
     // CTA across tile boundaries, partial tiles summed by streamk_fixup_kernel
     bool streamk = false;
-    const int64_t units = cdiv(g.K, kGemmBK);
+    const int BK = gemm_bk_for(g.N);
+    const int64_t units = cdiv(g.K, BK);
     const int64_t tiles = gx * gy;
     if (!g.tile_row0 && g.force_splits == 0 && !getenv("SORSVD_NO_STREAMK") && tiles < (int64_t)c->num_sms &&
         units >= 64) {
         const int64_t n = c->num_sms;
-        const double sk_cost = (double)cdiv(tiles * units, n) * kGemmBK + 2 * 96.0 + 0.02 * 3 * g.M * g.N / (double)n;
+        const double sk_cost = (double)cdiv(tiles * units, n) * BK + 2 * 96.0 + 0.02 * 3 * g.M * g.N / (double)n;
         const double cur_cost = (double)cdiv(tiles * S, n) * ((double)g.K / S + 96.0) +
                                 (S > 1 ? 0.02 * S * g.M * g.N / (double)n : 0.0);
         streamk = sk_cost < 0.95 * cur_cost;
@@ -347,8 +353,8 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
     a.tile_seg = g.tile_seg;
     a.pred = c->pred;
     a.pred_skip = c->pred_skip;
-    const int64_t kchunk = cdiv(cdiv(g.K, S), kGemmBK) * kGemmBK;
-    a.k_chunk = std::max<int64_t>(kchunk, kGemmBK);
+    const int64_t kchunk = cdiv(cdiv(g.K, S), BK) * BK;
+    a.k_chunk = std::max<int64_t>(kchunk, BK);
     double* ws = nullptr;
     if (S > 1) {
         ws = dbuf(c, g.ws_name, (size_t)S * g.M * g.ldc);
