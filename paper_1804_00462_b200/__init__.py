@@ -269,6 +269,18 @@ def _desc(m, n, lda, k, cfg: SketchConfig, flags: int, m_global: int = 0, dtype:
                         flags, m_global)
 
 
+def _host_out(shape):
+    """float64 numpy array for a host-API result. Page-locked (from torch's
+    caching host allocator) when torch is importable, so the device-to-host
+    copy runs at full PCIe rate instead of through the driver's pageable
+    staging; a plain numpy array otherwise."""
+    try:
+        import torch
+        return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    except Exception:
+        return np.empty(shape)
+
+
 # -------------------------------------------------------------- hot path --
 def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Context] = None,
                   stage_times: bool = False, use_graph: bool = True, m_global: int = 0,
@@ -322,9 +334,9 @@ def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Contex
         ctx = ctx or default_context(0)
         m, n = a.shape
         d = _desc(m, n, n, k, cfg, flags, m_global, C.F32 if a.dtype == np.float32 else C.F64)
-        u = np.empty((m, k))
-        s = np.empty((k,))
-        v = np.empty((n, k))
+        u = _host_out((m, k))
+        s = _host_out((k,))
+        v = _host_out((n, k))
         om_p = None
         if omega is not None:
             om = np.ascontiguousarray(omega, dtype=np.float64)
@@ -439,8 +451,8 @@ def rpca_alm(x, cfg: RpcaConfig, ctx: Optional[Context] = None, want_l: bool = T
         m, n = x.shape
         d = C.RpcaDesc(m, n, n, cfg.lam, cfg.mu0, cfg.mu_bar_factor, cfg.rho, cfg.tol, cfg.max_iter, cfg.ell,
                        cfg.q, C.F64, cfg.seed & (2**64 - 1), 0, 0, m_global)
-        s = np.empty((m, n))
-        l = np.empty((m, n)) if want_l else None
+        s = _host_out((m, n))
+        l = _host_out((m, n)) if want_l else None
         _check(C.lib().sorsvd_rpca_alm(ctx.handle, ctypes.byref(d), x.ctypes.data_as(C.c_dp),
                                        l.ctypes.data_as(C.c_dp) if l is not None else None,
                                        s.ctypes.data_as(C.c_dp), ctypes.byref(res)), ctx.handle)
