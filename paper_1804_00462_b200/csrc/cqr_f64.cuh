@@ -221,17 +221,24 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
                     for (int q = 0; q < 4; ++q)
                         if (g.on[q]) g.y[q][jo] -= dd[q];
                 }
+                // all loads of a row before any store: the four column pointers
+                // may alias as far as the compiler knows, and a load->FMA->store
+                // chain per column serialises on the shared-memory latency
+#pragma unroll 2
                 for (int i = i0 + lane; i < nr; i += 32) {
                     const double vi = scal * x[i];
                     const double xi = (i >= i0n) ? xn[i] : 0.0;
+                    double yv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) yv[q] = g.y[q][i];  // off columns alias column c0 (readable)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        if (g.on[q]) {
-                            const double yv = fma(-dd[q], vi, g.y[q][i]);
-                            g.y[q][i] = yv;
-                            sn[q] = fma(xi, yv, sn[q]);
-                        }
+                        yv[q] = fma(-dd[q], vi, yv[q]);
+                        sn[q] = fma(xi, yv[q], sn[q]);
                     }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (g.on[q]) g.y[q][i] = yv[q];
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) sn[q] = warp_sum(sn[q]);
@@ -352,17 +359,21 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
             }
             __syncwarp();  // row j is read by another lane in the dot below
             if (next) {
+#pragma unroll 2
                 for (int i = i0n + lane; i < nr; i += 32) {
                     const double vi = (lr0 + i > j) ? v[i] : 0.0;
                     const double wn = vn[i];
+                    double yv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) yv[q] = g.y[q][i];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        if (g.on[q]) {
-                            const double yv = fma(-dd[q], vi, g.y[q][i]);
-                            g.y[q][i] = yv;
-                            sn[q] = fma(wn, yv, sn[q]);
-                        }
+                        yv[q] = fma(-dd[q], vi, yv[q]);
+                        sn[q] = fma(wn, yv[q], sn[q]);
                     }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (g.on[q]) g.y[q][i] = yv[q];
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) sn[q] = warp_sum(sn[q]);
@@ -373,11 +384,15 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
                         if (g.on[q]) Pn[c0 + q * nw - j] = sn[q] + (ownern ? g.y[q][jon] : 0.0);
                 }
             } else if (reduce) {
+#pragma unroll 2
                 for (int i = i0 + lane; i < nr; i += 32) {
                     const double vi = v[i];
+                    double yv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) yv[q] = g.y[q][i];
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        if (g.on[q]) g.y[q][i] = fma(-dd[q], vi, g.y[q][i]);
+                        if (g.on[q]) g.y[q][i] = fma(-dd[q], vi, yv[q]);
                 }
             }
         }

@@ -101,10 +101,40 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& p, unsigned char* smem
     auto b_stage = [&](int slot) {
         return reinterpret_cast<double*>(smem_raw + (size_t)slot * S::STAGE_BYTES + S::A_BYTES);
     };
+    // Interior stages (whole row tile, whole BK slab, 16-byte rows) take the
+    // fast path: every thread's A chunks sit in one fixed column of the tile
+    // (CPR chunks per tile row divides the 256 threads), so the global source
+    // is a per-tile base plus a per-stage offset plus a constant stride, and
+    // no bounds arithmetic is issued inside the DMMA loop's stage refill.
+    constexpr int CPR = (TA ? S::BM : S::BK) / EPV;           // 16-byte chunks per smem tile row
+    constexpr int RSTEP = kGemmThreads / CPR;                  // tile rows between a thread's chunks
+    constexpr int NA = (TA ? S::BK : S::BM) / RSTEP;           // chunks per thread
+    static_assert(kGemmThreads % CPR == 0 && (TA ? S::BK : S::BM) % RSTEP == 0, "A chunk map");
+    const bool full_rows = V16 && rows == S::BM;
+    const int ac = tid % CPR, ar0 = tid / CPR;
+    const AT* __restrict__ abase =
+        TA ? Ap + (int64_t)ar0 * p.lda + row0 + EPV * ac : Ap + (row0 + ar0) * p.lda + EPV * ac;
+    const int64_t astride = (int64_t)RSTEP * p.lda;
+    const int asoff = ar0 * S::LDA_S + EPV * ac;
     auto load_stage = [&](int slot, int kt) {
         AT* As = a_stage(slot);
         double* Bs = b_stage(slot);
         const int64_t k0 = kBegin + (int64_t)kt * S::BK;
+        if (full_rows && k0 + S::BK <= kEnd) {
+            const AT* src = abase + (TA ? k0 * p.lda : k0);
+#pragma unroll
+            for (int i = 0; i < NA; ++i) cp_async16(As + asoff + i * RSTEP * S::LDA_S, src + i * astride, 16);
+            const double* bsrc = Bp + k0 * p.ldb;
+#pragma unroll
+            for (int i = 0; i < (S::BK * (S::BN / 2) + kGemmThreads - 1) / kGemmThreads; ++i) {
+                const int id = tid + i * kGemmThreads;
+                if (id < S::BK * (S::BN / 2)) {
+                    const int kr = id / (S::BN / 2), c = id - kr * (S::BN / 2);
+                    cp_async16(Bs + kr * S::LDB_S + 2 * c, bsrc + (int64_t)kr * p.ldb + 2 * c, 16);
+                }
+            }
+            return;
+        }
         if (!TA) {
             if (V16) {
                 for (int id = tid; id < S::BM * (S::BK / EPV); id += kGemmThreads) {

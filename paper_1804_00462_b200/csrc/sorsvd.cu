@@ -338,6 +338,7 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         const double cur_cost = (double)cdiv(tiles * S, n) * ((double)g.K / S + 96.0) +
                                 (S > 1 ? 0.02 * S * g.M * g.N / (double)n : 0.0);
         streamk = sk_cost < 0.95 * cur_cost;
+        if (const char* e = getenv("SORSVD_STREAMK")) streamk = atoi(e) != 0;  // experiments
     }
     GemmArgs a{};
     a.A = g.Af ? static_cast<const void*>(g.Af) : static_cast<const void*>(g.A);
