@@ -73,6 +73,9 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_inv_kernel(CholArgs a) {
             s_piv[0] = r;
             pmax = fmax(pmax, d);
             pmin = fmin(pmin, d);
+            // the pass-1 pivot gate is monotone (pmin only falls, pmax only rises):
+            // reject as soon as it fails instead of after the whole factorisation
+            if (a.pass == 1 && !(pmin > 1e-14 * pmax)) s_bad = 1;
         }
         __syncthreads();
         if (s_bad) break;  // not positive definite: reject early (uniform: shared flag)

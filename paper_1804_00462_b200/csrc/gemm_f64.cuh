@@ -285,14 +285,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
 }
 
 // Stream-K fix-up: every tile split over several segments gets the sum of
-// its partial slots in slot order (deterministic). One CTA-stride loop over
-// (tile, row, col) of the split tiles only.
+// its partial slots in slot order (deterministic: 0 + s_0 + s_1 + ...).
+// grid.y = split tile, grid.x covers the tile's elements one per thread; the
+// slot loads are issued 16 ahead of the ordered adds, since a tile split over
+// ~100 segments (a K = m reduction onto one tile) is otherwise a chain of
+// dependent L2 round trips.
 __global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* __restrict__ tile_seg0,
                                      const int* __restrict__ split_tiles, int nsplit, int BM, int BN, int gy,
                                      int64_t M, double* __restrict__ C, int64_t ldc, const int* pred, int pred_skip) {
     if (pred && *pred == pred_skip) return;
     const int per = BM * BN;  // one tile's elements (< 2^31)
-    // grid.y = split tile index, grid.x strides over the tile's elements (32-bit index math)
     for (int st = blockIdx.y; st < nsplit; st += gridDim.y) {
         const int tile = split_tiles[st];
         const int mt = tile / gy, nt = tile - mt * gy;
@@ -301,8 +303,17 @@ __global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* _
             const int r = w / BN, col = w - r * BN;
             const int64_t row = (int64_t)mt * BM + r;
             if (row >= M) continue;
+            const double* src = ws + (size_t)g0 * per + w;
             double acc = 0.0;
-            for (int gs = g0; gs < g1; ++gs) acc += ws[(size_t)gs * per + w];
+            int gs = g0;
+            for (; gs + 16 <= g1; gs += 16, src += (size_t)16 * per) {
+                double v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) v[u] = __ldcg(src + (size_t)u * per);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) acc += v[u];
+            }
+            for (; gs < g1; ++gs, src += per) acc += __ldcg(src);
             C[row * ldc + (int64_t)nt * BN + col] = acc;
         }
     }

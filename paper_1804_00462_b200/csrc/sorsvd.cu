@@ -260,6 +260,10 @@ struct GemmCall {
     int force_splits = 0;
     const char* ws_name = "gemm_ws";
     const float* Af = nullptr;  // FP32-storage A (FP64 arithmetic); overrides A
+    // stream-K is taken when its modelled cost is below sk_bias x split-K's; the
+    // A-streaming passes with one column chunk use 1.0 (measured: C2 pass
+    // 145 -> 137 us), everything else keeps the margin its numerics were pinned with
+    double sk_bias = 0.95;
 };
 
 template <int FM, int FN, bool TA, bool V16, typename AT>
@@ -337,7 +341,7 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         const double sk_cost = (double)cdiv(tiles * units, n) * BK + 2 * 96.0 + 0.02 * 3 * g.M * g.N / (double)n;
         const double cur_cost = (double)cdiv(tiles * S, n) * ((double)g.K / S + 96.0) +
                                 (S > 1 ? 0.02 * S * g.M * g.N / (double)n : 0.0);
-        streamk = sk_cost < 0.95 * cur_cost;
+        streamk = sk_cost < g.sk_bias * cur_cost;
         if (const char* e = getenv("SORSVD_STREAMK")) streamk = atoi(e) != 0;  // experiments
     }
     GemmArgs a{};
@@ -449,8 +453,7 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         const int nsplit = (int)sk_split_tiles_h.size();
         if (nsplit > 0) {
             const int BN = g.N <= 128 ? g.N : 128;
-            const dim3 fgrid((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)BM * BN, 256), 16)),
-                             (unsigned)std::min(nsplit, 65535));
+            const dim3 fgrid((unsigned)cdiv((int64_t)BM * BN, 256), (unsigned)std::min(nsplit, 65535));
             streamk_fixup_kernel<<<fgrid, 256, 0, s>>>(
                 a.sk_ws, sk_tile_seg0, sk_split_tiles, nsplit, BM, BN, (int)gy, g.M, g.C, g.ldc, c->pred,
                 c->pred_skip);
@@ -1669,6 +1672,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g1.N = Np;
         g1.C = b.T1;
         g1.ldc = Np;
+        g1.sk_bias = Np <= 128 ? 1.0 : 0.95;
         run_gemm(c, g1, s);
         GemmCall g2;  // T2 = A^T * T1   (sketch.hpp:96)
         g2.ta = true;
@@ -1682,6 +1686,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g2.N = Np;
         g2.C = b.T2;
         g2.ldc = Np;
+        g2.sk_bias = Np <= 128 ? 1.0 : 0.95;
         run_gemm(c, g2, s);
         allreduce_sum(c, b.T2, (size_t)P.n * Np, s);
     }
@@ -1732,6 +1737,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g.C = b.Y;
         g.ldc = Np;
         g.Af = P.Af;
+        g.sk_bias = Np <= 128 ? 1.0 : 0.95;
         if (!P.tf32) run_gemm(c, g, s);
         GemmCall h;
         h.ta = true;
@@ -2717,6 +2723,7 @@ static int pass_device_impl(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int
         g.N = Np;
         g.C = dT;
         g.ldc = Np;
+        g.sk_bias = Np <= 128 ? 1.0 : 0.95;  // as the sketch passes of enqueue_sor
         run_gemm(c, g, c->stream);  // warm-up (sizes the split workspace)
         const int l0 = c->launches;
         CK(cudaEventRecord(c->ev_a, c->stream));
