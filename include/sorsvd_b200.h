@@ -128,6 +128,22 @@ int sorsvd_sor_svd_power_device(sorsvd_ctx* ctx, const sorsvd_desc* desc, const 
                                 const double* dOmega, double* dU, double* dSigma, double* dV,
                                 sorsvd_stats* stats);
 
+/* ---- baselines: r_svd (sketch.hpp:124) / tsr_svd (sketch.hpp:139) -----------
+ * Same descriptor; desc.k is ignored (all ell triplets are returned: U m x ell,
+ * sigma ell, V n x ell), single_pass and BASIC are ignored, tsr ignores q.
+ * r_svd: Omega = gaussian_matrix(n, ell, seed) unless OMEGA_GIVEN; passes 2q+2.
+ * tsr_svd: Psi1 = gaussian_matrix(n, ell, seed), Psi2 = gaussian_matrix(m, ell,
+ * seed ^ 1) unless OMEGA_GIVEN (then both must be given); passes 1 (the two
+ * sketches are two launches over A in this build). Single rank; no TF32. */
+int sorsvd_r_svd(sorsvd_ctx* ctx, const sorsvd_desc* desc, const void* A, const double* omega, double* U,
+                 double* sigma, double* V, sorsvd_stats* stats);
+int sorsvd_r_svd_device(sorsvd_ctx* ctx, const sorsvd_desc* desc, const void* dA, const double* dOmega,
+                        double* dU, double* dSigma, double* dV, sorsvd_stats* stats);
+int sorsvd_tsr_svd(sorsvd_ctx* ctx, const sorsvd_desc* desc, const void* A, const double* psi1, const double* psi2,
+                   double* U, double* sigma, double* V, sorsvd_stats* stats);
+int sorsvd_tsr_svd_device(sorsvd_ctx* ctx, const sorsvd_desc* desc, const void* dA, const double* dPsi1,
+                          const double* dPsi2, double* dU, double* dSigma, double* dV, sorsvd_stats* stats);
+
 /* ---- RPCA by inexact ALM --------------- */
 typedef struct sorsvd_rpca_desc {
     int64_t m, n, ldd;

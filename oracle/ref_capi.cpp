@@ -135,6 +135,31 @@ int ref_sor_svd_power(std::int64_t m, std::int64_t n, const double* a, int k, in
     });
 }
 
+// sketch.hpp:124 (r_svd) / :139 (tsr_svd): all ell triplets, U m x ell, V n x ell
+int ref_r_svd(std::int64_t m, std::int64_t n, const double* a, int ell, int q, std::uint64_t seed, double* u,
+              double* sigma, double* v, int* passes, int* method) {
+    return guarded([&] {
+        auto r = sorsvd::r_svd(wrap(m, n, a), ell, q, seed);
+        put(r.u, u);
+        std::memcpy(sigma, r.sigma.data(), r.sigma.size() * sizeof(double));
+        put(r.v, v);
+        *passes = r.passes;
+        *method = (int)r.method;
+    });
+}
+
+int ref_tsr_svd(std::int64_t m, std::int64_t n, const double* a, int ell, std::uint64_t seed, double* u,
+                double* sigma, double* v, int* passes, int* method) {
+    return guarded([&] {
+        auto r = sorsvd::tsr_svd(wrap(m, n, a), ell, seed);
+        put(r.u, u);
+        std::memcpy(sigma, r.sigma.data(), r.sigma.size() * sizeof(double));
+        put(r.v, v);
+        *passes = r.passes;
+        *method = (int)r.method;
+    });
+}
+
 // sketch.hpp:178
 long long ref_flop_estimate(long long m, long long n, long long ell, long long k, long long q,
                             int variant) {

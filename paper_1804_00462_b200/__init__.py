@@ -4,6 +4,9 @@ Mirrors the reference C++ API (/root/reference/proj/include/sorsvd):
 
     sor_svd_power(a, k, cfg)  -> LowRankApprox      sketch.hpp:87
     sor_svd(a, k, cfg)        -> LowRankApprox      sketch.hpp:116
+    r_svd(a, ell, q, seed)    -> LowRankApprox      sketch.hpp:124 (baseline)
+    tsr_svd(a, ell, seed)     -> LowRankApprox      sketch.hpp:139 (baseline)
+    truncate(x, k)                                  sketch.hpp:152
     SketchConfig / LowRankApprox / SketchMethod      sketch.hpp:13-48
     flop_estimate / FlopVariant                      sketch.hpp:176-196
     gaussian_matrix / sub_seed                       random.hpp:24,60
@@ -32,7 +35,7 @@ from . import _capi as C
 __all__ = [
     "SketchMethod", "SketchConfig", "LowRankApprox", "FlopVariant", "RpcaConfig", "RpcaResult", "Context",
     "ShapeError", "ParameterError", "NumericalError", "CudaError", "NcclError", "UnsupportedError", "EmuGroup",
-    "sor_svd_power", "sor_svd", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
+    "sor_svd_power", "sor_svd", "r_svd", "tsr_svd", "truncate", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
     "flop_estimate", "validate_sketch", "thin_qr", "full_svd", "matmul", "default_context", "version",
 ]
 
@@ -282,6 +285,69 @@ def _host_out(shape):
 
 
 # -------------------------------------------------------------- hot path --
+def _decompose(kind: str, a, k: int, cfg: SketchConfig, flags: int, omega, psi2, ctx, m_global: int = 0):
+    """One call of sor_svd_power ("sor"), r_svd ("rsvd") or tsr_svd ("tsr")
+    through the host-buffer or device entry point; returns (stats, u, sigma, v)."""
+    host_fn = {"sor": "sorsvd_sor_svd_power", "rsvd": "sorsvd_r_svd", "tsr": "sorsvd_tsr_svd"}[kind]
+    if omega is not None:
+        flags |= C.FLAG_OMEGA_GIVEN
+    st = C.SorsvdStats()
+    if _is_torch_cuda(a):
+        import torch
+        if a.dtype not in (torch.float64, torch.float32) or a.dim() != 2 or a.stride(1) != 1:
+            raise ShapeError("shape: device input must be a row-major float64 or float32 matrix")
+        ctx = ctx or default_context(a.device.index or 0)
+        _torch_stream(ctx, a)
+        m, n = a.shape
+        lda = a.stride(0)
+        d = _desc(m, n, lda, k, cfg, flags, m_global, C.F32 if a.dtype == torch.float32 else C.F64)
+        u = torch.empty((m, k), dtype=torch.float64, device=a.device)
+        s = torch.empty((k,), dtype=torch.float64, device=a.device)
+        v = torch.empty((n, k), dtype=torch.float64, device=a.device)
+        ptrs = []
+        keep = []
+        for x, rows in ((omega, n), (psi2, m)):
+            if x is None:
+                ptrs.append(None)
+                continue
+            t = torch.as_tensor(x, dtype=torch.float64, device=a.device).contiguous()
+            if tuple(t.shape) != (rows, cfg.ell):
+                raise ShapeError("shape: test matrix must be (rows, ell)")
+            keep.append(t)
+            ptrs.append(t.data_ptr())
+        fn = getattr(C.lib(), host_fn + "_device")
+        args = [ctx.handle, ctypes.byref(d), a.data_ptr(), ptrs[0]] + ([ptrs[1]] if kind == "tsr" else [])
+        _check(fn(*args, u.data_ptr(), s.data_ptr(), v.data_ptr(), ctypes.byref(st)), ctx.handle)
+    else:
+        a = np.asarray(a)
+        a = np.ascontiguousarray(a, dtype=np.float32 if a.dtype == np.float32 else np.float64)
+        if a.ndim != 2:
+            raise ShapeError("shape: input must be a matrix")
+        ctx = ctx or default_context(0)
+        m, n = a.shape
+        d = _desc(m, n, n, k, cfg, flags, m_global, C.F32 if a.dtype == np.float32 else C.F64)
+        u = _host_out((m, k))
+        s = _host_out((k,))
+        v = _host_out((n, k))
+        ptrs = []
+        keep = []
+        for x, rows in ((omega, n), (psi2, m)):
+            if x is None:
+                ptrs.append(None)
+                continue
+            t = np.ascontiguousarray(x, dtype=np.float64)
+            if t.shape != (rows, cfg.ell):
+                raise ShapeError("shape: test matrix must be (rows, ell)")
+            keep.append(t)
+            ptrs.append(t.ctypes.data_as(C.c_dp))
+        fn = getattr(C.lib(), host_fn)
+        args = [ctx.handle, ctypes.byref(d), a.ctypes.data_as(ctypes.c_void_p), ptrs[0]] + (
+            [ptrs[1]] if kind == "tsr" else [])
+        _check(fn(*args, u.ctypes.data_as(C.c_dp), s.ctypes.data_as(C.c_dp), v.ctypes.data_as(C.c_dp),
+                  ctypes.byref(st)), ctx.handle)
+    return st, u, s, v
+
+
 def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Context] = None,
                   stage_times: bool = False, use_graph: bool = True, m_global: int = 0,
                   _basic: bool = False, fp32_mode: str = "fp64") -> LowRankApprox:
@@ -298,54 +364,13 @@ def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Contex
     if fp32_mode not in ("fp64", "tf32"):
         raise ParameterError("parameter: fp32_mode must be 'fp64' or 'tf32'")
     flags = C.FLAG_TF32 if fp32_mode == "tf32" else 0
-    if omega is not None:
-        flags |= C.FLAG_OMEGA_GIVEN
     if stage_times:
         flags |= C.FLAG_STAGE_TIMES
     if not use_graph:
         flags |= C.FLAG_NO_GRAPH
     if _basic:
         flags |= C.FLAG_BASIC
-    st = C.SorsvdStats()
-    if _is_torch_cuda(a):
-        import torch
-        if a.dtype not in (torch.float64, torch.float32) or a.dim() != 2 or a.stride(1) != 1:
-            raise ShapeError("shape: device input must be a row-major float64 or float32 matrix")
-        ctx = ctx or default_context(a.device.index or 0)
-        _torch_stream(ctx, a)
-        m, n = a.shape
-        lda = a.stride(0)
-        d = _desc(m, n, lda, k, cfg, flags, m_global, C.F32 if a.dtype == torch.float32 else C.F64)
-        u = torch.empty((m, k), dtype=torch.float64, device=a.device)
-        s = torch.empty((k,), dtype=torch.float64, device=a.device)
-        v = torch.empty((n, k), dtype=torch.float64, device=a.device)
-        om_ptr = None
-        if omega is not None:
-            om = torch.as_tensor(omega, dtype=torch.float64, device=a.device).contiguous()
-            om_ptr = om.data_ptr()
-        _check(C.lib().sorsvd_sor_svd_power_device(ctx.handle, ctypes.byref(d), a.data_ptr(), om_ptr,
-                                                   u.data_ptr(), s.data_ptr(), v.data_ptr(), ctypes.byref(st)),
-               ctx.handle)
-    else:
-        a = np.asarray(a)
-        a = np.ascontiguousarray(a, dtype=np.float32 if a.dtype == np.float32 else np.float64)
-        if a.ndim != 2:
-            raise ShapeError("shape: input must be a matrix")
-        ctx = ctx or default_context(0)
-        m, n = a.shape
-        d = _desc(m, n, n, k, cfg, flags, m_global, C.F32 if a.dtype == np.float32 else C.F64)
-        u = _host_out((m, k))
-        s = _host_out((k,))
-        v = _host_out((n, k))
-        om_p = None
-        if omega is not None:
-            om = np.ascontiguousarray(omega, dtype=np.float64)
-            if om.shape != (n, cfg.ell):
-                raise ShapeError("shape: omega must be n x ell")
-            om_p = om.ctypes.data_as(C.c_dp)
-        _check(C.lib().sorsvd_sor_svd_power(ctx.handle, ctypes.byref(d), a.ctypes.data_as(ctypes.c_void_p), om_p,
-                                            u.ctypes.data_as(C.c_dp), s.ctypes.data_as(C.c_dp),
-                                            v.ctypes.data_as(C.c_dp), ctypes.byref(st)), ctx.handle)
+    st, u, s, v = _decompose("sor", a, k, cfg, flags, omega, None, ctx, m_global)
     method = SketchMethod.sor if cfg.q == 0 else SketchMethod.sor_power
     return LowRankApprox(u, s, v, method, st.passes, cfg.ell, cfg.q, cfg.seed, st.as_dict())
 
@@ -355,6 +380,37 @@ def sor_svd(a, k: int, cfg: SketchConfig, **kw) -> LowRankApprox:
     if cfg.q != 0:
         raise ParameterError("parameter: sor_svd requires q == 0; use sor_svd_power")
     return sor_svd_power(a, k, cfg, _basic=True, **kw)
+
+
+def r_svd(a, ell: int, q: int, seed: int, omega=None, ctx: Optional[Context] = None,
+          use_graph: bool = True) -> LowRankApprox:
+    """One-sided randomized SVD baseline (sketch.hpp:124-136): all ell triplets,
+    passes 2q+2. omega (n, ell) defaults to gaussian_matrix(n, ell, seed)."""
+    cfg = SketchConfig(ell=ell, q=q, seed=seed)
+    flags = 0 if use_graph else C.FLAG_NO_GRAPH
+    st, u, s, v = _decompose("rsvd", a, ell, cfg, flags, omega, None, ctx)
+    return LowRankApprox(u, s, v, SketchMethod.rsvd, st.passes, ell, q, seed, st.as_dict())
+
+
+def tsr_svd(a, ell: int, seed: int, psi1=None, psi2=None, ctx: Optional[Context] = None,
+            use_graph: bool = True) -> LowRankApprox:
+    """Two-sided randomized SVD baseline (sketch.hpp:139-149): Psi1 (n, ell) from
+    seed, Psi2 (m, ell) from seed ^ 1 unless both are given; pseudo-inverse core;
+    all ell triplets, passes 1."""
+    if (psi1 is None) != (psi2 is None):
+        raise ParameterError("parameter: give both psi1 and psi2 or neither")
+    cfg = SketchConfig(ell=ell, q=0, seed=seed)
+    flags = 0 if use_graph else C.FLAG_NO_GRAPH
+    st, u, s, v = _decompose("tsr", a, ell, cfg, flags, psi1, psi2, ctx)
+    return LowRankApprox(u, s, v, SketchMethod.tsr, st.passes, ell, 0, seed, st.as_dict())
+
+
+def truncate(x: LowRankApprox, k: int) -> LowRankApprox:
+    """sketch.hpp:152-160: the leading k triplets (views of the same storage)."""
+    if k < 1 or k > len(x.sigma):
+        raise ParameterError("truncate rank out of range")
+    return LowRankApprox(x.u[:, :k], x.sigma[:k], x.v[:, :k], x.method, x.passes, x.ell, x.q, x.seed,
+                         dict(x.stats))
 
 
 # ----------------------------------------------------- stage entry points --

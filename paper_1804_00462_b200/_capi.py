@@ -74,6 +74,14 @@ SIGNATURES = [
                                      ctypes.POINTER(SorsvdStats)]),
     ("sorsvd_sor_svd_power_device", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_vp, c_vp, c_vp, c_vp, c_vp,
                                             ctypes.POINTER(SorsvdStats)]),
+    ("sorsvd_r_svd", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_vp, c_dp, c_dp, c_dp, c_dp,
+                             ctypes.POINTER(SorsvdStats)]),
+    ("sorsvd_r_svd_device", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_vp, c_vp, c_vp, c_vp, c_vp,
+                                    ctypes.POINTER(SorsvdStats)]),
+    ("sorsvd_tsr_svd", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_vp, c_dp, c_dp, c_dp, c_dp, c_dp,
+                               ctypes.POINTER(SorsvdStats)]),
+    ("sorsvd_tsr_svd_device", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                      ctypes.POINTER(SorsvdStats)]),
     ("sorsvd_rpca_alm", c_i32, [c_vp, ctypes.POINTER(RpcaDesc), c_dp, c_dp, c_dp, ctypes.POINTER(RpcaRes)]),
     ("sorsvd_rpca_alm_device", c_i32, [c_vp, ctypes.POINTER(RpcaDesc), c_vp, c_vp, c_vp, ctypes.POINTER(RpcaRes)]),
     ("sorsvd_thin_qr_device", c_i32, [c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]),

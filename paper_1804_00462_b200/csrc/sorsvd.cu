@@ -205,6 +205,7 @@ struct sorsvd_ctx {
     int launches = 0;
     bool capturing = false;
     std::vector<double> host_omega;
+    std::vector<double> host_psi2;  // tsr_svd's second test matrix (host draw)
     const int* pred = nullptr;  // predication of every launch (CholeskyQR2 vs Householder)
     int pred_skip = 0;
 };
@@ -1483,6 +1484,7 @@ struct SorBuffers {
     double *T1, *T2, *Q1, *Q2, *Y, *Mk, *Uk, *Vk, *Sk, *Uo, *Vo;
     double *T2pre = nullptr, *Lhs = nullptr, *Core = nullptr, *Uc = nullptr, *Vc = nullptr, *Sc = nullptr,
            *Pinv = nullptr;  // single_pass (m_approx)
+    double *Psi2 = nullptr, *Y2 = nullptr;  // tsr_svd: second test matrix (m x Np) and row sketch (n x Np)
     float *T1f = nullptr, *T2f = nullptr, *Q2f = nullptr, *Yf = nullptr;  // FP32 path
     int* sweeps;
 };
@@ -1498,6 +1500,7 @@ struct SorProblem {
     int64_t m_global;
     bool single_pass;
     bool tf32;         // dtype F32 with SORSVD_FLAG_TF32: passes on the tcgen05 tensor cores
+    int method = SORSVD_SOR_POWER;  // SORSVD_RSVD / SORSVD_TSR: the baselines of sketch.hpp:124-149
 };
 
 SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan** p2, QrPlan** pg) {
@@ -1515,7 +1518,11 @@ SorBuffers prepare_sor(sorsvd_ctx* c, const SorProblem& P, QrPlan** p1, QrPlan**
     b.Uo = dbuf(c, "Uo", (size_t)P.m * Np);
     b.Vo = dbuf(c, "Vo", (size_t)P.n * Np);
     b.sweeps = reinterpret_cast<int*>(dbuf(c, "sweeps", 1));
-    if (P.single_pass) {
+    if (P.method == SORSVD_TSR) {
+        b.Psi2 = dbuf(c, "Psi2", (size_t)P.m * Np);
+        b.Y2 = dbuf(c, "Y2", (size_t)P.n * Np);
+    }
+    if (P.single_pass || P.method == SORSVD_TSR) {
         b.T2pre = dbuf(c, "T2pre", (size_t)P.n * Np);
         b.Lhs = dbuf(c, "Lhs", (size_t)Np * Np);
         b.Core = dbuf(c, "Core", (size_t)Np * Np);
@@ -1786,9 +1793,111 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     record_stage(c, timing, 5);
 }
 
+__global__ void transpose_pad_kernel(const double* __restrict__ src, int64_t lds, int k, double* __restrict__ dst,
+                                     int ldd) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ldd * ldd; e += gridDim.x * blockDim.x) {
+        const int i = e / ldd, j = e - i * ldd;
+        dst[e] = (i < k && j < k) ? src[(int64_t)j * lds + i] : 0.0;
+    }
+}
+
+// One skinny GEMM C = op(A) B over the whole A (the sketch passes of the baselines).
+void pass_gemm(sorsvd_ctx* c, const SorProblem& P, bool ta, const double* B, double* C, cudaStream_t s) {
+    GemmCall g;
+    g.ta = ta;
+    g.A = P.A;
+    g.Af = P.Af;
+    g.lda = P.lda;
+    g.M = ta ? P.n : P.m;
+    g.K = ta ? P.m : P.n;
+    g.B = B;
+    g.ldb = P.Np;
+    g.N = P.Np;
+    g.C = C;
+    g.ldc = P.Np;
+    g.sk_bias = P.Np <= 128 ? 1.0 : 0.95;
+    run_gemm(c, g, s);
+}
+
+// U = Q1 Uk (m x Np), V = Q2 Vk (n x Np)   (sketch.hpp:105,107 / :135 / :147)
+void enqueue_basis(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, cudaStream_t s) {
+    for (int h = 0; h < 2; ++h) {
+        GemmCall g;
+        g.A = h ? b.Q2 : b.Q1;
+        g.lda = P.Np;
+        g.M = h ? P.n : P.m;
+        g.K = P.ell;
+        g.B = h ? b.Vk : b.Uk;
+        g.ldb = P.Np;
+        g.N = P.Np;
+        g.C = h ? b.Vo : b.Uo;
+        g.ldc = P.Np;
+        run_gemm(c, g, s);
+    }
+}
+
+// r_svd (sketch.hpp:124-136): Y = (A A^T)^q A Omega, Qy = thin_qr(Y).q,
+// B = Qy^T A, full_svd(B), U = Qy U_B. T2 holds Omega on entry.
+// full_svd of the ell x n B (dense.hpp:65) runs as B^T = A^T Qy = Qb Rb
+// (one more TN pass + a thin QR), then the ell x ell one-sided Jacobi on
+// Rb^T = U_B S (Vj)^T, so U_B comes out of the Jacobi kernel with the
+// reference sign canonicalisation (dense.hpp:80-95) and V = Qb Vj.
+void enqueue_rsvd(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, bool timing) {
+    cudaStream_t s = c->stream;
+    record_stage(c, timing, 0);
+    pass_gemm(c, P, false, b.T2, b.T1, s);  // Y = A Omega        (:127)
+    for (int i = 0; i < P.q; ++i) {         // Y = A (A^T Y)      (:128)
+        pass_gemm(c, P, true, b.T1, b.T2, s);
+        pass_gemm(c, P, false, b.T2, b.T1, s);
+    }
+    record_stage(c, timing, 1);
+    qr_run(c, p1, b.T1, P.Np, b.Q1, P.Np, s);  // Qy = thin_qr(Y).q   (:129)
+    record_stage(c, timing, 2);
+    pass_gemm(c, P, true, b.Q1, b.T2, s);      // B^T = A^T Qy       (:130)
+    qr_run(c, p2, b.T2, P.Np, b.Q2, P.Np, s);  // B^T = Qb Rb
+    const int L = (int)p2->nodes.size() - 1;
+    transpose_pad_kernel<<<std::min(cdiv((int64_t)P.Np * P.Np, 256), (int64_t)c->num_sms), 256, 0, s>>>(
+        p2->R[L], p2->ldR, P.ell, b.Mk, P.Np);  // Rb^T = B Qb
+    check_launch(c);
+    record_stage(c, timing, 3);
+    run_jacobi(c, P.ell, b.Mk, P.Np, b.Uk, P.Np, b.Sk, b.Vk, P.Np, b.sweeps, s);  // full_svd(B)   (:131)
+    record_stage(c, timing, 4);
+    enqueue_basis(c, P, b, s);  // U = Qy U_B (:132), V = Qb Vj
+    record_stage(c, timing, 5);
+}
+
+// tsr_svd (sketch.hpp:139-149): Y1 = A Psi1, Y2 = A^T Psi2 (Psi2 from seed^1),
+// Q1 = thin_qr(Y1).q, Q2 = thin_qr(Y2).q, B = m_approx(Q1, Y1, Q2, Psi1),
+// full_svd(B), U = Q1 U_B, V = Q2 V_B. T2 holds Psi1, b.Psi2 holds Psi2.
+// The two sketches are two launches over A here (the reference counts the
+// pair as its one pass, sketch.hpp:148).
+void enqueue_tsr(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, bool timing) {
+    cudaStream_t s = c->stream;
+    record_stage(c, timing, 0);
+    pass_gemm(c, P, false, b.T2, b.T1, s);   // Y1 = A Psi1     (:143)
+    pass_gemm(c, P, true, b.Psi2, b.Y2, s);  // Y2 = A^T Psi2   (:144)
+    record_stage(c, timing, 1);
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    qr_run(c, p1, b.T1, P.Np, b.Q1, P.Np, s);        // (:145)
+    qr_run(c, p2, b.Y2, P.Np, b.Q2, P.Np, c->side);  // (:146)
+    CK(cudaEventRecord(c->ev_join, c->side));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    record_stage(c, timing, 2);
+    SorBuffers bb = b;
+    bb.T2pre = b.T2;  // m_approx's W is Psi1 itself (:147)
+    enqueue_m_approx(c, P, bb, s);
+    record_stage(c, timing, 3);
+    run_jacobi(c, P.ell, b.Mk, P.Np, b.Uk, P.Np, b.Sk, b.Vk, P.Np, b.sweeps, s);  // full_svd(B)  (:148)
+    record_stage(c, timing, 4);
+    enqueue_basis(c, P, b, s);
+    record_stage(c, timing, 5);
+}
+
 std::string sor_key(const SorProblem& P, const int* pred = nullptr) {
     char buf[320];
-    snprintf(buf, sizeof buf, "sor:%d:%d:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.dtype, (int)P.single_pass, (int)P.tf32,
+    snprintf(buf, sizeof buf, "sor%d:%d:%d:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.method, P.dtype, (int)P.single_pass,
+             (int)P.tf32,
              P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m, (long long)P.n,
              (long long)P.lda, P.k, P.ell, P.q);
     if (pred) snprintf(buf + strlen(buf), sizeof buf - strlen(buf), ":pred%p", (const void*)pred);
@@ -1812,9 +1921,16 @@ void validate(const sorsvd_desc* d) {
 
 // Core device-side call. dOmega: n x ell dense (or null: drawn on the host).
 void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const double* dOmega, double* dU,
-                double* dS, double* dV, sorsvd_stats* st) {
+                double* dS, double* dV, sorsvd_stats* st, int method = SORSVD_SOR_POWER,
+                const double* dPsi2 = nullptr) {
     validate(d);
+    const bool baseline = method == SORSVD_RSVD || method == SORSVD_TSR;
+    if (baseline) {
+        if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "r_svd / tsr_svd: single-rank only in this build"};
+        if (d->flags & SORSVD_FLAG_TF32) throw Error{SORSVD_ERR_UNSUPPORTED, "r_svd / tsr_svd: no TF32 mode"};
+    }
     SorProblem P{};
+    P.method = method;
     P.dtype = d->dtype;
     P.A = d->dtype == SORSVD_F64 ? static_cast<const double*>(dA) : nullptr;
     P.Af = d->dtype == SORSVD_F32 ? static_cast<const float*>(dA) : nullptr;
@@ -1827,10 +1943,22 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     P.q = d->q;
     P.Np = npad(d->ell);
     P.m_global = d->m_global > 0 ? d->m_global : d->m;
-    P.single_pass = d->single_pass != 0;
+    P.single_pass = d->single_pass != 0 && !baseline;
     P.tf32 = d->dtype == SORSVD_F32 && (d->flags & SORSVD_FLAG_TF32);
     QrPlan *p1, *p2, *pg;
     SorBuffers b = prepare_sor(c, P, &p1, &p2, &pg);
+    double* psi2_in = nullptr;
+    if (method == SORSVD_TSR) {  // Psi2 = gaussian_matrix(m, ell, seed ^ 1)   (sketch.hpp:142)
+        psi2_in = dbuf(c, "psi2_in", (size_t)P.m * P.ell);
+        if (dPsi2 && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+            CK(cudaMemcpyAsync(psi2_in, dPsi2, (size_t)P.m * P.ell * 8, cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            c->host_psi2.resize((size_t)P.m * P.ell);
+            sorsvd_host::gaussian_fill(c->host_psi2.data(), (uint64_t)P.m * P.ell, d->seed ^ 1ULL, 0);
+            CK(cudaMemcpyAsync(psi2_in, c->host_psi2.data(), (size_t)P.m * P.ell * 8, cudaMemcpyHostToDevice,
+                               c->stream));
+        }
+    }
     // Omega and the outputs stay outside the captured graph (so the graph is
     // keyed on A alone): Omega is staged into a context buffer before the
     // launch, U / sigma / V are copied out after it.
@@ -1857,7 +1985,16 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
             CK(cudaMemcpy2DAsync(b.T2, (size_t)P.Np * 8, om, (size_t)P.ell * 8, (size_t)P.ell * 8, (size_t)P.n,
                                  cudaMemcpyDeviceToDevice, c->stream));
         }
-        enqueue_sor(c, P, b, p1, p2, pg, timing);
+        if (method == SORSVD_TSR) {
+            CK(cudaMemsetAsync(b.Psi2, 0, (size_t)P.m * P.Np * 8, c->stream));
+            CK(cudaMemcpy2DAsync(b.Psi2, (size_t)P.Np * 8, psi2_in, (size_t)P.ell * 8, (size_t)P.ell * 8,
+                                 (size_t)P.m, cudaMemcpyDeviceToDevice, c->stream));
+            enqueue_tsr(c, P, b, p1, p2, timing);
+        } else if (method == SORSVD_RSVD) {
+            enqueue_rsvd(c, P, b, p1, p2, timing);
+        } else {
+            enqueue_sor(c, P, b, p1, p2, pg, timing);
+        }
     };
     auto copy_out = [&]() {
         CK(cudaMemcpy2DAsync(dU, (size_t)P.k * 8, b.Uo, (size_t)P.Np * 8, (size_t)P.k * 8, (size_t)P.m,
@@ -1913,11 +2050,14 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
         st->ms_total = ms;
-        const int passes = d->single_pass ? 2 * d->q + 2 : 2 * d->q + 3;  // sketch.hpp:104
+        const int passes = method == SORSVD_RSVD ? 2 * d->q + 2                       // sketch.hpp:134
+                           : method == SORSVD_TSR ? 1                                  // sketch.hpp:148
+                           : d->single_pass     ? 2 * d->q + 2 : 2 * d->q + 3;        // sketch.hpp:104
         st->passes = passes;
-        st->method = d->q == 0 ? SORSVD_SOR : SORSVD_SOR_POWER;
-        st->flops_passes = 2.0 * (double)d->m * d->n * d->ell * passes;
-        st->bytes_passes = (double)d->m * d->n * (d->dtype == SORSVD_F32 ? 4.0 : 8.0) * passes;
+        st->method = baseline ? method : d->q == 0 ? SORSVD_SOR : SORSVD_SOR_POWER;
+        const int launched = method == SORSVD_TSR ? 2 : passes;  // tsr: A Psi1 and A^T Psi2 are two sweeps here
+        st->flops_passes = 2.0 * (double)d->m * d->n * d->ell * launched;
+        st->bytes_passes = (double)d->m * d->n * (d->dtype == SORSVD_F32 ? 4.0 : 8.0) * launched;
         st->launches = launches;
         int sw = 0;
         CK(cudaMemcpy(&sw, b.sweeps, sizeof(int), cudaMemcpyDeviceToHost));
@@ -2504,10 +2644,10 @@ int sorsvd_sor_svd_power_device(sorsvd_ctx* c, const sorsvd_desc* d, const void*
     });
 }
 
-int sorsvd_sor_svd_power(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const double* omega, double* U,
-                         double* sigma, double* V, sorsvd_stats* st) {
-    if (!c) return SORSVD_ERR_PARAMETER;
-    return guarded(c, [&] {
+// Host-buffer call of one of the decompositions: A (and the given test
+// matrices) uploaded, U / sigma / V downloaded, all inside the timed call.
+static void host_call(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const double* omega, const double* psi2,
+                      double* U, double* sigma, double* V, sorsvd_stats* st, int method) {
         validate(d);
         if (!A || !U || !sigma || !V) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
         const size_t esz = d->dtype == SORSVD_F32 ? 4 : 8;
@@ -2522,12 +2662,18 @@ int sorsvd_sor_svd_power(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, con
             CK(cudaMemcpyAsync(p, omega, (size_t)d->n * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
             dOm = p;
         }
+        const double* dPsi2 = nullptr;
+        if (psi2 && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+            double* p = dbuf(c, "hostPsi2", (size_t)d->m * d->ell);
+            CK(cudaMemcpyAsync(p, psi2, (size_t)d->m * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
+            dPsi2 = p;
+        }
         CK(cudaEventRecord(e1, c->stream));
         double* dU = dbuf(c, "hostU", (size_t)d->m * d->k);
         double* dS = dbuf(c, "hostS", (size_t)d->k);
         double* dV = dbuf(c, "hostV", (size_t)d->n * d->k);
         sorsvd_stats local{};
-        sor_device(c, d, dA, dOm, dU, dS, dV, &local);
+        sor_device(c, d, dA, dOm, dU, dS, dV, &local, method, dPsi2);
         CK(cudaEventRecord(e2, c->stream));
         CK(cudaMemcpyAsync(U, dU, (size_t)d->m * d->k * 8, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(V, dV, (size_t)d->n * d->k * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -2540,6 +2686,66 @@ int sorsvd_sor_svd_power(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, con
         local.ms_h2d = h2d;
         local.ms_d2h = d2h;
         if (st) *st = local;
+}
+
+int sorsvd_sor_svd_power(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const double* omega, double* U,
+                         double* sigma, double* V, sorsvd_stats* st) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] { host_call(c, d, A, omega, nullptr, U, sigma, V, st, SORSVD_SOR_POWER); });
+}
+
+// r_svd / tsr_svd take (ell, q, seed) / (ell, seed): the descriptor is
+// normalised to k = ell (all ell triplets are returned, sketch.hpp:122,139),
+// q = 0 for tsr and no single-pass core.
+static sorsvd_desc baseline_desc(const sorsvd_desc* d, int method) {
+    if (!d) throw Error{SORSVD_ERR_PARAMETER, "parameter: null descriptor"};
+    sorsvd_desc e = *d;
+    e.k = e.ell;
+    e.single_pass = 0;
+    e.flags &= ~SORSVD_FLAG_BASIC;
+    if (method == SORSVD_TSR) e.q = 0;
+    return e;
+}
+
+int sorsvd_r_svd(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const double* omega, double* U, double* sigma,
+                 double* V, sorsvd_stats* st) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        const sorsvd_desc e = baseline_desc(d, SORSVD_RSVD);
+        host_call(c, &e, A, omega, nullptr, U, sigma, V, st, SORSVD_RSVD);
+    });
+}
+
+int sorsvd_r_svd_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const double* dOmega, double* dU,
+                        double* dSigma, double* dV, sorsvd_stats* st) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        const sorsvd_desc e = baseline_desc(d, SORSVD_RSVD);
+        if (!dA || !dU || !dSigma || !dV) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        sor_device(c, &e, dA, dOmega, dU, dSigma, dV, st, SORSVD_RSVD);
+    });
+}
+
+int sorsvd_tsr_svd(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const double* psi1, const double* psi2,
+                   double* U, double* sigma, double* V, sorsvd_stats* st) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        const sorsvd_desc e = baseline_desc(d, SORSVD_TSR);
+        if ((e.flags & SORSVD_FLAG_OMEGA_GIVEN) && (!psi1 || !psi2))
+            throw Error{SORSVD_ERR_PARAMETER, "parameter: OMEGA_GIVEN needs both psi1 and psi2"};
+        host_call(c, &e, A, psi1, psi2, U, sigma, V, st, SORSVD_TSR);
+    });
+}
+
+int sorsvd_tsr_svd_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const double* dPsi1,
+                          const double* dPsi2, double* dU, double* dSigma, double* dV, sorsvd_stats* st) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        const sorsvd_desc e = baseline_desc(d, SORSVD_TSR);
+        if (!dA || !dU || !dSigma || !dV) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        if ((e.flags & SORSVD_FLAG_OMEGA_GIVEN) && (!dPsi1 || !dPsi2))
+            throw Error{SORSVD_ERR_PARAMETER, "parameter: OMEGA_GIVEN needs both psi1 and psi2"};
+        sor_device(c, &e, dA, dPsi1, dU, dSigma, dV, st, SORSVD_TSR, dPsi2);
     });
 }
 

@@ -56,6 +56,28 @@ int main() {
                 r3.passes);
     fails += !(max_rel(g3.sigma, r3.sigma) <= 1e-10) + (g3.passes != r3.passes);
     cfg.single_pass = false;
+    // baselines (sketch.hpp:124, :139): all ell triplets
+    LowRankApprox r4 = r_svd(a, 12, 1, 9), g4 = cuda::r_svd(a, 12, 1, 9);
+    LowRankApprox r5 = tsr_svd(a, 12, 9), g5 = cuda::tsr_svd(a, 12, 9);
+    std::printf("r_svd sigma max rel err %.3e (passes %d/%d), tsr_svd %.3e (passes %d/%d)\n",
+                max_rel(std::vector<double>(g4.sigma.begin(), g4.sigma.begin() + 10),
+                        std::vector<double>(r4.sigma.begin(), r4.sigma.begin() + 10)),
+                g4.passes, r4.passes,
+                max_rel(std::vector<double>(g5.sigma.begin(), g5.sigma.begin() + 10),
+                        std::vector<double>(r5.sigma.begin(), r5.sigma.begin() + 10)),
+                g5.passes, r5.passes);
+    fails += (g4.passes != r4.passes) + (g5.passes != r5.passes) + (g4.method != r4.method) +
+             (g5.method != r5.method) + (g4.u.cols() != 12) + (g5.v.cols() != 12);
+    fails += !(max_rel(std::vector<double>(g4.sigma.begin(), g4.sigma.begin() + 10),
+                       std::vector<double>(r4.sigma.begin(), r4.sigma.begin() + 10)) <= 1e-10);
+    fails += !(max_rel(std::vector<double>(g5.sigma.begin(), g5.sigma.begin() + 10),
+                       std::vector<double>(r5.sigma.begin(), r5.sigma.begin() + 10)) <= 1e-10);
+    try {
+        cuda::r_svd(p, 300, 0, 1);
+        ++fails;
+    } catch (const parameter_error& e) {
+        std::printf("parameter_error: %s\n", e.what());
+    }
     // error behaviour mirrors the reference exceptions
     try {
         cfg.ell = 400;

@@ -73,6 +73,21 @@ def main():
         g[name + "_u"], g[name + "_s"], g[name + "_v"] = f.u, f.sigma, f.v
         meta[name] = dict(m=m, n=n, k=k, ell=ell, q=q, seed=seed, passes=f.passes, method=f.method, single_pass=True)
         sp_cases.append(name)
+    # baselines r_svd (sketch.hpp:124) and tsr_svd (sketch.hpp:139): all ell triplets
+    bl_cases = []
+    for (kind, m, n, ell, q, seed, aseed) in [("rsvd", 60, 40, 8, 0, 31, 9), ("rsvd", 70, 50, 10, 1, 32, 10),
+                                               ("rsvd", 40, 90, 6, 2, 33, 11), ("tsr", 60, 40, 8, 0, 34, 12),
+                                               ("tsr", 50, 80, 10, 0, 35, 13), ("tsr", 129, 65, 16, 0, 36, 14)]:
+        name = f"{kind}_{m}x{n}_l{ell}_q{q}"
+        x = O.gaussian_matrix(m, 6, O.sub_seed(aseed, 1))
+        y = O.gaussian_matrix(n, 6, O.sub_seed(aseed, 2))
+        e = O.gaussian_matrix(m, n, O.sub_seed(aseed, 3))
+        A = x @ y.T + 1e-3 * e
+        f = Ref.r_svd(A, ell, q, seed) if kind == "rsvd" else Ref.tsr_svd(A, ell, seed)
+        g[name + "_A"] = A
+        g[name + "_u"], g[name + "_s"], g[name + "_v"] = f.u, f.sigma, f.v
+        meta[name] = dict(kind=kind, m=m, n=n, ell=ell, q=q, seed=seed, passes=f.passes, method=f.method)
+        bl_cases.append(name)
     # rank-1: 100 x 80, k = 1, ell = 4
     uu = O.gaussian_matrix(100, 1, 91)
     vv = O.gaussian_matrix(80, 1, 92)
@@ -95,7 +110,7 @@ def main():
                            converged=rr.converged, mu0=rr.mu0, ell=10, q=1, seed=5, lam=float(cfg.lam))
     np.savez_compressed(os.path.join(OUT, "golden_ref.npz"), **g)
     with open(os.path.join(OUT, "golden_meta.json"), "w") as fh:
-        json.dump({"cases": cases, "sp_cases": sp_cases, "meta": meta, "blas": Ref and O.ref_lib().ref_blas_config().decode()}, fh, indent=1)
+        json.dump({"cases": cases, "sp_cases": sp_cases, "bl_cases": bl_cases, "meta": meta, "blas": Ref and O.ref_lib().ref_blas_config().decode()}, fh, indent=1)
     print("wrote", len(g), "arrays")
 
 

@@ -83,6 +83,33 @@ def test_single_pass_port_matches_reference_golden(golden):
         assert O.lowrank_rel_diff(f.u, f.sigma, f.v, g[name + "_u"], g[name + "_s"], g[name + "_v"]) <= max(1e-10, 10 * dl), name
 
 
+@pytest.mark.parametrize("kind", ["rsvd", "tsr"])
+def test_baselines_port_match_reference_golden(golden, kind):
+    # r_svd (sketch.hpp:124-136) and tsr_svd (sketch.hpp:139-149) restated in numpy vs the compiled reference
+    g, meta = golden
+    names = [n for n in meta["bl_cases"] if meta["meta"][n]["kind"] == kind]
+    assert len(names) == 3
+    for name in names:
+        md = meta["meta"][name]
+        A = g[name + "_A"]
+        f = O.r_svd(A, md["ell"], md["q"], md["seed"]) if kind == "rsvd" else O.tsr_svd(A, md["ell"], md["seed"])
+        assert f.passes == md["passes"] == (2 * md["q"] + 2 if kind == "rsvd" else 1)
+        assert f.method == md["method"] == (O.RSVD if kind == "rsvd" else O.TSR)
+        _, ds, dl = O.baseline_floor(kind, A, md["ell"], md["q"], md["seed"], include_reference=False)
+        assert np.all(O.sigma_rel_err(f.sigma, g[name + "_s"]) <= np.maximum(1e-11, 10 * ds)), name
+        assert O.lowrank_rel_diff(f.u, f.sigma, f.v, g[name + "_u"], g[name + "_s"], g[name + "_v"]) <= max(1e-10, 10 * dl), name
+
+
+def test_truncate_rules():
+    a = O.gaussian_matrix(30, 20, 3)
+    f = O.r_svd(a, 6, 0, 1)
+    t = O.truncate(f, 4)
+    assert t.u.shape == (30, 4) and t.v.shape == (20, 4) and np.array_equal(t.sigma, f.sigma[:4])
+    for k in (0, 7):
+        with pytest.raises(O.ParameterError):
+            O.truncate(f, k)
+
+
 def test_rank1_exact(golden):
     # rank-1 100x80, k=1, ell=4 -> error <= 1e-10
     g, _ = golden
