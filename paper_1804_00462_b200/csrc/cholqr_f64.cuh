@@ -22,6 +22,7 @@
 namespace sorsvd_dev {
 
 constexpr int kCholThreads = 1024;
+constexpr size_t kCholSmemBytes = 200 * 1024;  // dynamic shared memory of chol_inv_kernel
 
 struct CholArgs {
     const double* G;   // k x ldg symmetric (upper part used)
@@ -46,7 +47,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_inv_kernel(CholArgs a) {
     __shared__ double s_piv[2];
     const int k = a.k, tid = threadIdx.x;
     if (a.pass == 2 && *a.flag != 0) return;  // pass 1 already rejected
-    const bool in_smem = (size_t)k * k * sizeof(double) <= 200 * 1024;
+    const bool in_smem = (size_t)k * k * sizeof(double) <= kCholSmemBytes;
     double* L = in_smem ? smc : a.work;  // row-major k x k, lower triangle holds R^T
     if (tid == 0) s_bad = 0;
     double dev = 0.0;
@@ -82,12 +83,15 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_inv_kernel(CholArgs a) {
         const double r = s_piv[0];
         for (int i = j + 1 + tid; i < k; i += blockDim.x) L[(size_t)i * k + j] /= r;
         __syncthreads();
-        const int nt = k - j - 1;
-        for (int e = tid; e < nt * nt; e += blockDim.x) {
-            const int ii = e / nt, jj = e - ii * nt;
-            if (jj <= ii) {
-                const int i = j + 1 + ii, c = j + 1 + jj;
-                L[(size_t)i * k + c] = fma(-L[(size_t)i * k + j], L[(size_t)c * k + j], L[(size_t)i * k + c]);
+        // trailing rank-1 update of the lower triangle: one warp per row, lanes
+        // across its columns (no per-element index division; each element still
+        // sees the same fma sequence over j, so the factor is unchanged)
+        {
+            const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+            for (int i = j + 1 + warp; i < k; i += nw) {
+                double* Li = L + (size_t)i * k;
+                const double lij = Li[j];
+                for (int c = j + 1 + lane; c <= i; c += 32) Li[c] = fma(-lij, L[(size_t)c * k + j], Li[c]);
             }
         }
         __syncthreads();
@@ -104,13 +108,22 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_inv_kernel(CholArgs a) {
             const int i = e / k, c = e - i * k;
             a.Rf[(size_t)i * a.ldf + c] = c >= i ? L[(size_t)c * k + i] : 0.0;
         }
-    // R = L^T (upper). Rinv column c solves R x = e_c by back substitution (one thread per column).
+    // R = L^T (upper). Rinv column c solves R x = e_c by back substitution (one thread per column);
+    // the partial solution stays in shared memory (xs, column-interleaved) rather than being
+    // re-read from global memory, same operation order as before.
+    double* xs = in_smem ? smc + (size_t)k * k : nullptr;
+    const bool xs_ok = in_smem && ((size_t)k * k + (size_t)k * k) * sizeof(double) <= kCholSmemBytes;
     for (int c = tid; c < k; c += blockDim.x) {
         // x_i for i <= c, from i = c down to 0: x_i = (delta_ic - sum_{l=i+1..c} R_il x_l) / R_ii, R_il = L[l][i]
         for (int i = c; i >= 0; --i) {
             double s = (i == c) ? 1.0 : 0.0;
-            for (int l = i + 1; l <= c; ++l) s = fma(-L[(size_t)l * k + i], a.Rinv[(size_t)l * a.ldr + c], s);
-            a.Rinv[(size_t)i * a.ldr + c] = s / L[(size_t)i * k + i];
+            if (xs_ok)
+                for (int l = i + 1; l <= c; ++l) s = fma(-L[(size_t)l * k + i], xs[(size_t)l * k + c], s);
+            else
+                for (int l = i + 1; l <= c; ++l) s = fma(-L[(size_t)l * k + i], a.Rinv[(size_t)l * a.ldr + c], s);
+            const double x = s / L[(size_t)i * k + i];
+            if (xs_ok) xs[(size_t)i * k + c] = x;
+            a.Rinv[(size_t)i * a.ldr + c] = x;
         }
         for (int i = c + 1; i < k; ++i) a.Rinv[(size_t)i * a.ldr + c] = 0.0;
     }

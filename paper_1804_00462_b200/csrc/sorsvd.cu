@@ -1125,7 +1125,9 @@ struct PredScope {
 };
 
 void launch_chol(sorsvd_ctx* c, const CholArgs& a, cudaStream_t s) {
-    const size_t sm = (size_t)a.k * a.k * sizeof(double) <= 200 * 1024 ? (size_t)a.k * a.k * sizeof(double) : 0;
+    // the factor in shared memory when it fits, plus the back-substitution columns when both fit
+    const size_t kk8 = (size_t)a.k * a.k * sizeof(double);
+    const size_t sm = 2 * kk8 <= kCholSmemBytes ? 2 * kk8 : kk8 <= kCholSmemBytes ? kk8 : 0;
     CK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(sm, 1)));
     chol_inv_kernel<<<1, kCholThreads, sm, s>>>(a);
     check_launch(c);
