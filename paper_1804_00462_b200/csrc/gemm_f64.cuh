@@ -320,7 +320,7 @@ __global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* _
 }
 
 // out[i] = sum_{s<S} ws[s*stride + i], fixed summation order (deterministic).
-// The partial loads are issued 8 at a time ahead of the (ordered) adds: with
+// The partial loads are issued 16 at a time ahead of the (ordered) adds: with
 // many splits and few outputs (K = m reductions) the loop is L2-latency bound.
 __global__ void reduce_splits_kernel(const double* __restrict__ ws, int64_t count2, int S, int64_t stride,
                                      double* __restrict__ out, const int* pred, int pred_skip) {
@@ -331,12 +331,12 @@ __global__ void reduce_splits_kernel(const double* __restrict__ ws, int64_t coun
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
         double2 acc = w2[i];
         int s = 1;
-        for (; s + 8 <= S; s += 8) {
-            double2 v[8];
+        for (; s + 16 <= S; s += 16) {
+            double2 v[16];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = w2[(int64_t)(s + u) * st2 + i];
+            for (int u = 0; u < 16; ++u) v[u] = w2[(int64_t)(s + u) * st2 + i];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 16; ++u) {
                 acc.x += v[u].x;
                 acc.y += v[u].y;
             }

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <string>
 #include <vector>
@@ -169,16 +170,24 @@ struct sorsvd_emu_group {
     int arrived = 0;
     long generation = 0;
     std::vector<void*> bufs;  // per-rank buffer registered for the current collective
+    bool broken = false;      // a rank failed: its peers must not wait for it forever
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
+        if (broken) throw Error{SORSVD_ERR_INTERNAL, "emulated group: a peer rank failed"};
         const long gen = generation;
         if (++arrived == world) {
             arrived = 0;
             ++generation;
             cv.notify_all();
         } else {
-            cv.wait(lk, [&] { return generation != gen; });
+            cv.wait(lk, [&] { return generation != gen || broken; });
+            if (generation == gen) throw Error{SORSVD_ERR_INTERNAL, "emulated group: a peer rank failed"};
         }
+    }
+    void poison() {
+        std::lock_guard<std::mutex> lk(mu);
+        broken = true;
+        cv.notify_all();
     }
 };
 
@@ -228,11 +237,42 @@ double* dbuf(sorsvd_ctx* c, const std::string& name, size_t count, bool zero = f
         b.p = nullptr;
         CK(cudaMalloc(&b.p, bytes));
         b.bytes = bytes;
+        // the zero fill runs on the legacy stream, which does not order with the
+        // context's non-blocking streams: wait for it here (allocation is rare)
         CK(cudaMemset(b.p, 0, bytes));
+        CK(cudaStreamSynchronize(0));
     } else if (zero) {
         CK(cudaMemsetAsync(b.p, 0, bytes, c->stream));
     }
     return static_cast<double*>(b.p);
+}
+
+// Kernel attributes are process-wide (per device), and contexts may live on
+// several host threads (one per emulated rank, or a caller's thread pool):
+// every kernel that takes dynamic shared memory is opened up ONCE to the
+// device's opt-in maximum (plus non-portable cluster sizes where it needs
+// them), instead of being set to each launch's size right before the launch,
+// which another thread could undo in between (a launch failure, or a
+// different occupancy answer and so a different cluster shape on one rank).
+std::mutex g_attr_mu;
+
+template <typename... Args>
+void allow_smem(void (*fn)(Args...), bool cluster = false) {
+    static std::set<std::pair<const void*, int>> done;  // guarded by g_attr_mu
+    thread_local std::set<std::pair<const void*, int>> seen;  // this thread's fast path
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const std::pair<const void*, int> key{reinterpret_cast<const void*>(fn), dev};
+    if (seen.count(key)) return;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    seen.insert(key);
+    if (!done.insert(key).second) return;
+    int mx = 0;
+    CK(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, fn));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes));
+    if (cluster) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
 void check_launch(sorsvd_ctx* c) {
@@ -270,12 +310,7 @@ struct GemmCall {
 template <int FM, int FN, bool TA, bool V16, typename AT>
 void launch_gemm_t(const GemmArgs& a, dim3 grid, cudaStream_t s) {
     using S = GemmShape<FM, FN, TA, AT>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(gemm_f64_kernel<FM, FN, TA, V16, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)S::SMEM));
-        attr_set = true;
-    }
+    allow_smem(gemm_f64_kernel<FM, FN, TA, V16, AT>);
     gemm_f64_kernel<FM, FN, TA, V16, AT><<<grid, kGemmThreads, S::SMEM, s>>>(a);
 }
 
@@ -321,9 +356,14 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         const int64_t base = gx * gy;
         const int64_t maxS = std::max<int64_t>(1, std::min<int64_t>(512, g.K / 128));
         double best = 1e300;
+        // tiny outputs (Gram matrices of the CholeskyQR gates, C1 / C4 shapes): the split
+        // reduction is a chain of dependent L2 round trips (16 partials per trip in
+        // reduce_splits_kernel), ~48 K-rows each, not a bandwidth term
+        const double trip = (g.M * g.N <= 4096) ? 3.0 : 0.0;  // 16 partials per trip
         for (int64_t cand = 1; cand <= maxS; ++cand) {
             const double waves = (double)cdiv(base * cand, c->num_sms);
-            const double cost = waves * ((double)g.K / cand + 96.0) + (cand > 1 ? 0.02 * cand * g.M * g.N / (double)c->num_sms : 0.0);
+            const double cost = waves * ((double)g.K / cand + 96.0) +
+                                (cand > 1 ? 0.02 * cand * g.M * g.N / (double)c->num_sms + trip * cand : 0.0);
             if (cost < best * 0.999) {
                 best = cost;
                 S = (int)cand;
@@ -336,8 +376,11 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
     const int BK = gemm_bk_for(g.N);
     const int64_t units = cdiv(g.K, BK);
     const int64_t tiles = gx * gy;
+    // tiny outputs keep split-K: a stream-K tile spread over ~all SMs has a fix-up that is
+    // a chain of ~num_sms / 16 dependent L2 round trips per element
+    const bool tiny_out = g.M * g.N <= 4096;
     if (!g.tile_row0 && g.force_splits == 0 && !getenv("SORSVD_NO_STREAMK") && tiles < (int64_t)c->num_sms &&
-        units >= 64) {
+        units >= 64 && !tiny_out) {
         const int64_t n = c->num_sms;
         const double sk_cost = (double)cdiv(tiles * units, n) * BK + 2 * 96.0 + 0.02 * 3 * g.M * g.N / (double)n;
         const double cur_cost = (double)cdiv(tiles * S, n) * ((double)g.K / S + 96.0) +
@@ -510,11 +553,7 @@ inline int npad32(int ell) { return ell <= 256 ? ((ell + 31) / 32) * 32 : ((ell 
 template <int BN, bool TA>
 void launch_tc_t(const CUtensorMap& ma, const CUtensorMap& mb, const TcArgs& a, dim3 grid, cudaStream_t s) {
     using S = TcShape<BN>;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(tc_gemm_tf32_kernel<BN, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-        attr = true;
-    }
+    allow_smem(tc_gemm_tf32_kernel<BN, TA>);
     tc_gemm_tf32_kernel<BN, TA><<<grid, kTcThreads, S::SMEM, s>>>(ma, mb, a);
 }
 
@@ -611,12 +650,14 @@ int cqr_rows_per_cta(int k) {
 }
 
 int cqr_max_cluster(sorsvd_ctx* c, int k) {
-    static std::map<int, int> cache;
-    auto it = cache.find(k);
-    if (it != cache.end()) return it->second;
+    static std::map<int, int> cache;  // guarded by g_attr_mu (process-wide, shared by all contexts)
+    {
+        std::lock_guard<std::mutex> lk(g_attr_mu);
+        auto it = cache.find(k);
+        if (it != cache.end()) return it->second;
+    }
     const size_t sm = cqr_smem_bytes(cqr_rows_per_cta(k), k);
-    CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    allow_smem(cqr_kernel, true);
     int best = 1;
     for (int cs = kCqrMaxCluster; cs >= 1; cs /= 2) {
         cudaLaunchConfig_t cfg{};
@@ -638,8 +679,9 @@ int cqr_max_cluster(sorsvd_ctx* c, int k) {
         cudaGetLastError();
     }
     (void)c;
-    cache[k] = best;
-    return best;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    cache.emplace(k, best);
+    return cache[k];
 }
 
 struct RegCfg {
@@ -702,8 +744,7 @@ int64_t cqr_reg_capacity(int k, int cmax) {
 template <int CH>
 void launch_cqr_reg_t(sorsvd_ctx* c, const CqrArgs& a, int nblocks, const RegCfg& rc, int Rb, cudaStream_t s) {
     const size_t sm = cqr_reg_smem_bytes(Rb, a.k, CH);
-    CK(cudaFuncSetAttribute(cqr_reg_kernel<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(cqr_reg_kernel<CH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    allow_smem(cqr_reg_kernel<CH>, true);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(nblocks * rc.csize));
     cfg.blockDim = dim3((unsigned)rc.threads);
@@ -749,8 +790,7 @@ void launch_cqr(sorsvd_ctx* c, const CqrArgs& a0, int nblocks, int rows_max, int
     const int csize = (int)std::min<int64_t>(cmax_smem, cdiv(rows_max, rb_smem));
     const int Rb = (int)cdiv(rows_max, csize);
     const size_t sm = cqr_smem_bytes(Rb, a.k);
-    CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(cqr_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    allow_smem(cqr_kernel, true);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(nblocks * csize));
     cfg.blockDim = dim3(kCqrThreads);
@@ -790,6 +830,7 @@ double* dalloc(QrPlan* p, size_t count) {
     double* d = nullptr;
     CK(cudaMalloc(&d, std::max<size_t>(count, 1) * sizeof(double)));
     CK(cudaMemset(d, 0, std::max<size_t>(count, 1) * sizeof(double)));
+    CK(cudaStreamSynchronize(0));  // legacy-stream fill vs the non-blocking streams (see dbuf)
     p->owned.push_back(d);
     return d;
 }
@@ -1128,8 +1169,10 @@ void launch_chol(sorsvd_ctx* c, const CholArgs& a, cudaStream_t s) {
     // the factor in shared memory when it fits, plus the back-substitution columns when both fit
     const size_t kk8 = (size_t)a.k * a.k * sizeof(double);
     const size_t sm = 2 * kk8 <= kCholSmemBytes ? 2 * kk8 : kk8 <= kCholSmemBytes ? kk8 : 0;
-    CK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(sm, 1)));
-    chol_inv_kernel<<<1, kCholThreads, sm, s>>>(a);
+    allow_smem(chol_inv_kernel);
+    // small k: fewer threads (cheaper barriers); the per-element operation order is unchanged
+    const int threads = a.k <= 16 ? 128 : a.k <= 48 ? 256 : kCholThreads;
+    chol_inv_kernel<<<1, threads, sm, s>>>(a);
     check_launch(c);
 }
 
@@ -1201,8 +1244,7 @@ void qr_run_big(sorsvd_ctx* c, QrPlan* p, const double* T, int64_t ldt, double* 
         a.done_tol = 1e-13;
         const int C = (k + kCholcB - 1) / kCholcB;
         const size_t sm = cholc_smem_bytes(k);
-        CK(cudaFuncSetAttribute(cholc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        CK(cudaFuncSetAttribute(cholc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        allow_smem(cholc_kernel, true);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)C);
         cfg.blockDim = dim3(kCholcThreads);
@@ -1356,8 +1398,7 @@ const double* qr_leaf_factors(QrPlan* p, bool had_cin) {
 template <int KP>
 void launch_jacobi_t(sorsvd_ctx* c, const JacobiArgs& a, int csize, cudaStream_t s) {
     const size_t sm = jacobi_smem_bytes(a.k, a.ppc);
-    CK(cudaFuncSetAttribute(jacobi_cluster_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(jacobi_cluster_kernel<KP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    allow_smem(jacobi_cluster_kernel<KP>, true);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)csize);
     cfg.blockDim = dim3((unsigned)(32 * a.ppc));
@@ -1377,8 +1418,7 @@ void launch_jacobi_t(sorsvd_ctx* c, const JacobiArgs& a, int csize, cudaStream_t
 template <int KP>
 void launch_jacobi_big_t(const JacobiBigArgs& a, int csize, cudaStream_t s) {
     const size_t sm = (size_t)3 * kJbWarps * 2 * (32 * KP) * sizeof(double);  // mailboxes x2 parities + outbox
-    CK(cudaFuncSetAttribute(jacobi_big_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(cudaFuncSetAttribute(jacobi_big_kernel<KP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    allow_smem(jacobi_big_kernel<KP>, true);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)csize);
     cfg.blockDim = dim3(kJbWarps * 32);
@@ -1453,7 +1493,7 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
         // measured 4x slower than the cluster ring at k = 100)
         const int warps = std::min(P, 32);
         const size_t sm = jacobi_cta_smem_bytes(k);
-        CK(cudaFuncSetAttribute(jacobi_cta_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        allow_smem(jacobi_cta_kernel<1, 1>);
         jacobi_cta_kernel<1, 1><<<1, 32 * warps, sm, s>>>(a);
         check_launch(c);
         return;
@@ -1721,7 +1761,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     } else {
         qr_run(c, p1, b.T1, Np, b.Q1, Np, s);
     }
-    qr_run(c, p2, b.T2, Np, b.Q2, Np, c->side);
+    qr_run(c, p2, b.T2, Np, b.Q2, Np, getenv("SORSVD_NO_SIDE") ? s : c->side);
     CK(cudaEventRecord(c->ev_join, c->side));
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     record_stage(c, timing, 2);
@@ -2493,6 +2533,7 @@ int guarded(sorsvd_ctx* c, F&& f) {
         f();
         return SORSVD_OK;
     } catch (const Error& e) {
+        if (c && c->emu) c->emu->poison();  // release peers blocked in a collective
         return fail(c, e);
     } catch (const std::bad_alloc&) {
         return fail(c, Error{SORSVD_ERR_OOM, "host allocation failed"});

@@ -1,6 +1,6 @@
 """Summarise an ncu --metrics gpu__time_duration.sum --csv launch list: per-kernel count / total / share
 of the LAST `--calls` fraction (default: second half = the second of two identical calls)."""
-import csv, sys
+import csv, re, sys
 from collections import OrderedDict
 rows = list(csv.reader(open(sys.argv[1])))
 for i, r in enumerate(rows):
@@ -8,7 +8,7 @@ for i, r in enumerate(rows):
         hdr = r; start = i + 1; break
 idx = {h: i for i, h in enumerate(hdr)}
 ks = [(r[idx['Kernel Name']], float(r[idx['Metric Value']])) for r in rows[start:]
-      if r[idx['Metric Name']] == 'gpu__time_duration.sum' and 'sorsvd_dev' in r[idx['Kernel Name']]]
+      if r[idx['Metric Name']] == 'gpu__time_duration.sum' and not re.search(r'\bat(_cuda_detail)?::', r[idx['Kernel Name']])]
 ks = ks[len(ks) // 2:] if '--all' not in sys.argv else ks
 agg = OrderedDict()
 for n, t in ks:
