@@ -128,6 +128,22 @@ int sorsvd_sor_svd_power_device(sorsvd_ctx* ctx, const sorsvd_desc* desc, const 
                                 const double* dOmega, double* dU, double* dSigma, double* dV,
                                 sorsvd_stats* stats);
 
+/* ---- batched trials (the Monte-Carlo loop of bounds.hpp:262-379) -------------
+ * `trials` independent sor_svd_power calls on the same A, trial t drawn from
+ * seeds[t] (or desc.seed + t when seeds is NULL, the harness's convention,
+ * bounds.hpp:288), or from omegas (trials x n x ell) with OMEGA_GIVEN. Every
+ * pass over A serves all trials in one launch. Outputs are stacked per trial:
+ * U trials x m x k, sigma trials x k, V trials x n x k. Each trial matches the
+ * single call with its seed to the parity tolerances (not bitwise: the wider
+ * passes sum in a different order). Single rank; ell <= 256; no TF32, no
+ * single_pass. */
+int sorsvd_sor_svd_power_batch(sorsvd_ctx* ctx, const sorsvd_desc* desc, int32_t trials, const uint64_t* seeds,
+                               const void* A, const double* omegas, double* U, double* sigma, double* V,
+                               sorsvd_stats* stats);
+int sorsvd_sor_svd_power_batch_device(sorsvd_ctx* ctx, const sorsvd_desc* desc, int32_t trials,
+                                      const uint64_t* seeds, const void* dA, const double* dOmegas, double* dU,
+                                      double* dSigma, double* dV, sorsvd_stats* stats);
+
 /* ---- baselines: r_svd (sketch.hpp:124) / tsr_svd (sketch.hpp:139) -----------
  * Same descriptor; desc.k is ignored (all ell triplets are returned: U m x ell,
  * sigma ell, V n x ell), single_pass and BASIC are ignored, tsr ignores q.

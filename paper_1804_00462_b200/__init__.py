@@ -35,7 +35,7 @@ from . import _capi as C
 __all__ = [
     "SketchMethod", "SketchConfig", "LowRankApprox", "FlopVariant", "RpcaConfig", "RpcaResult", "Context",
     "ShapeError", "ParameterError", "NumericalError", "CudaError", "NcclError", "UnsupportedError", "EmuGroup",
-    "sor_svd_power", "sor_svd", "r_svd", "tsr_svd", "truncate", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
+    "sor_svd_power", "sor_svd", "sor_svd_power_batch", "r_svd", "tsr_svd", "truncate", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
     "flop_estimate", "validate_sketch", "thin_qr", "full_svd", "matmul", "default_context", "version",
 ]
 
@@ -373,6 +373,65 @@ def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Contex
     st, u, s, v = _decompose("sor", a, k, cfg, flags, omega, None, ctx, m_global)
     method = SketchMethod.sor if cfg.q == 0 else SketchMethod.sor_power
     return LowRankApprox(u, s, v, method, st.passes, cfg.ell, cfg.q, cfg.seed, st.as_dict())
+
+
+def sor_svd_power_batch(a, k: int, cfg: SketchConfig, trials: int, seeds=None, omegas=None,
+                        ctx: Optional[Context] = None) -> list:
+    """`trials` independent sor_svd_power calls on one A (the Monte-Carlo loop of
+    bounds.hpp:262-379): trial t uses seeds[t], default cfg.seed + t
+    (bounds.hpp:288), or omegas[t] (trials, n, ell). Every pass over A serves
+    all trials in one launch. Returns one LowRankApprox per trial."""
+    if trials < 1:
+        raise ParameterError("parameter: trials must be positive")
+    seed_list = [(cfg.seed + t) & (2**64 - 1) for t in range(trials)] if seeds is None else \
+        [int(x) & (2**64 - 1) for x in seeds]
+    if len(seed_list) != trials:
+        raise ShapeError("shape: need one seed per trial")
+    sarr = (C.c_u64 * trials)(*seed_list)
+    flags = C.FLAG_OMEGA_GIVEN if omegas is not None else 0
+    st = C.SorsvdStats()
+    if _is_torch_cuda(a):
+        import torch
+        if a.dtype not in (torch.float64, torch.float32) or a.dim() != 2 or a.stride(1) != 1:
+            raise ShapeError("shape: device input must be a row-major float64 or float32 matrix")
+        ctx = ctx or default_context(a.device.index or 0)
+        _torch_stream(ctx, a)
+        m, n = a.shape
+        d = _desc(m, n, a.stride(0), k, cfg, flags, 0, C.F32 if a.dtype == torch.float32 else C.F64)
+        u = torch.empty((trials, m, k), dtype=torch.float64, device=a.device)
+        s = torch.empty((trials, k), dtype=torch.float64, device=a.device)
+        v = torch.empty((trials, n, k), dtype=torch.float64, device=a.device)
+        om = None
+        if omegas is not None:
+            om = torch.as_tensor(omegas, dtype=torch.float64, device=a.device).contiguous()
+            if tuple(om.shape) != (trials, n, cfg.ell):
+                raise ShapeError("shape: omegas must be (trials, n, ell)")
+        _check(C.lib().sorsvd_sor_svd_power_batch_device(ctx.handle, ctypes.byref(d), trials, sarr, a.data_ptr(),
+                                                         om.data_ptr() if om is not None else None, u.data_ptr(),
+                                                         s.data_ptr(), v.data_ptr(), ctypes.byref(st)), ctx.handle)
+    else:
+        a = np.asarray(a)
+        a = np.ascontiguousarray(a, dtype=np.float32 if a.dtype == np.float32 else np.float64)
+        ctx = ctx or default_context(0)
+        m, n = a.shape
+        d = _desc(m, n, n, k, cfg, flags, 0, C.F32 if a.dtype == np.float32 else C.F64)
+        u = _host_out((trials, m, k))
+        s = _host_out((trials, k))
+        v = _host_out((trials, n, k))
+        om_p = None
+        if omegas is not None:
+            om = np.ascontiguousarray(omegas, dtype=np.float64)
+            if om.shape != (trials, n, cfg.ell):
+                raise ShapeError("shape: omegas must be (trials, n, ell)")
+            om_p = om.ctypes.data_as(C.c_dp)
+        _check(C.lib().sorsvd_sor_svd_power_batch(ctx.handle, ctypes.byref(d), trials, sarr,
+                                                  a.ctypes.data_as(ctypes.c_void_p), om_p, u.ctypes.data_as(C.c_dp),
+                                                  s.ctypes.data_as(C.c_dp), v.ctypes.data_as(C.c_dp),
+                                                  ctypes.byref(st)), ctx.handle)
+    method = SketchMethod.sor if cfg.q == 0 else SketchMethod.sor_power
+    stats = st.as_dict()
+    return [LowRankApprox(u[t], s[t], v[t], method, st.passes, cfg.ell, cfg.q, seed_list[t], dict(stats))
+            for t in range(trials)]
 
 
 def sor_svd(a, k: int, cfg: SketchConfig, **kw) -> LowRankApprox:

@@ -74,6 +74,10 @@ SIGNATURES = [
                                      ctypes.POINTER(SorsvdStats)]),
     ("sorsvd_sor_svd_power_device", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_vp, c_vp, c_vp, c_vp, c_vp,
                                             ctypes.POINTER(SorsvdStats)]),
+    ("sorsvd_sor_svd_power_batch", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_i32, ctypes.POINTER(c_u64), c_vp,
+                                           c_dp, c_dp, c_dp, c_dp, ctypes.POINTER(SorsvdStats)]),
+    ("sorsvd_sor_svd_power_batch_device", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_i32, ctypes.POINTER(c_u64),
+                                                  c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(SorsvdStats)]),
     ("sorsvd_r_svd", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_vp, c_dp, c_dp, c_dp, c_dp,
                              ctypes.POINTER(SorsvdStats)]),
     ("sorsvd_r_svd_device", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_vp, c_vp, c_vp, c_vp, c_vp,

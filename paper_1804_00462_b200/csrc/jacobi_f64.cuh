@@ -439,3 +439,4 @@ __host__ __device__ inline size_t jacobi_cta_smem_bytes(int k) {
 }
 
 }  // namespace sorsvd_dev
+

@@ -197,6 +197,8 @@ struct sorsvd_ctx {
     int rank = 0, world = 1;
     int num_sms = 148;
     cudaStream_t own_stream = nullptr, stream = nullptr, side = nullptr;
+    std::vector<cudaStream_t> tstreams;  // batched trials (created on first use)
+    std::vector<cudaEvent_t> tevents;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_a = nullptr, ev_b = nullptr;
     cudaEvent_t ev_st[8] = {};
     cudaEvent_t ev_h[4] = {};
@@ -2116,6 +2118,200 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     }
 }
 
+// ------------------------------------------------------- batched trials ----
+// T independent sor_svd_power calls on one A (bounds.hpp:262-379 runs one per
+// Monte-Carlo trial, seed + t) sharing every pass over A: the T test matrices
+// sit side by side as the columns of one n x (T Np) operand, so each of the
+// 2q+2 sketch passes and the projection pass is ONE launch over A for all
+// trials (A read once, a T-times wider and better-fed DMMA tile). The
+// per-trial QRs, core SVDs and basis products are latency-bound chains; they
+// run on up to kTrialStreams streams side by side.
+constexpr int kTrialStreams = 8;
+
+void ensure_trial_streams(sorsvd_ctx* c, int n) {
+    while ((int)c->tstreams.size() < n) {
+        cudaStream_t t;
+        cudaEvent_t e;
+        CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->tstreams.push_back(t);
+        c->tevents.push_back(e);
+    }
+}
+
+void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_t* seeds, const void* dA,
+                  const double* dOmegas, double* dU, double* dS, double* dV, sorsvd_stats* st) {
+    validate(d);
+    if (trials < 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: trials must be positive"};
+    if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "batched trials: single-rank only in this build"};
+    if (d->flags & SORSVD_FLAG_TF32) throw Error{SORSVD_ERR_UNSUPPORTED, "batched trials: no TF32 mode"};
+    if (d->single_pass) throw Error{SORSVD_ERR_UNSUPPORTED, "batched trials: single_pass not supported"};
+    if (d->ell > kHouseMaxK) throw Error{SORSVD_ERR_UNSUPPORTED, "batched trials: ell <= 256"};
+    SorProblem P{};
+    P.dtype = d->dtype;
+    P.A = d->dtype == SORSVD_F64 ? static_cast<const double*>(dA) : nullptr;
+    P.Af = d->dtype == SORSVD_F32 ? static_cast<const float*>(dA) : nullptr;
+    P.m = d->m;
+    P.n = d->n;
+    P.lda = d->lda;
+    P.k = d->k;
+    P.ell = d->ell;
+    P.q = d->q;
+    P.Np = npad(d->ell);
+    P.m_global = P.m;
+    const int Np = P.Np, ell = P.ell, k = P.k;
+    const int64_t m = P.m, n = P.n;
+    const int Wt = trials * Np;                       // the trials' columns side by side
+    const int W = Wt <= 128 ? Wt : ((Wt + 127) / 128) * 128;  // padded for the GEMM's column chunks
+    double* X = dbuf(c, "b_X", (size_t)n * W);      // Omega_all, then T2_all, then Q2_all
+    double* T1b = dbuf(c, "b_T1", (size_t)m * W);
+    double* Yb = dbuf(c, "b_Y", (size_t)m * W);
+    double* om_in = dbuf(c, "b_om", (size_t)trials * n * ell);
+    cudaStream_t s = c->stream;
+    // test matrices: gaussian_matrix(n, ell, seed_t) per trial (sketch.hpp:90), or given
+    if (dOmegas && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+        CK(cudaMemcpyAsync(om_in, dOmegas, (size_t)trials * n * ell * 8, cudaMemcpyDeviceToDevice, s));
+    } else {
+        c->host_omega.resize((size_t)trials * n * ell);
+        for (int t = 0; t < trials; ++t)
+            sorsvd_host::gaussian_fill(c->host_omega.data() + (size_t)t * n * ell, (uint64_t)n * ell,
+                                       seeds ? seeds[t] : d->seed + (uint64_t)t, 0);
+        CK(cudaMemcpyAsync(om_in, c->host_omega.data(), (size_t)trials * n * ell * 8, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaEventRecord(c->ev_a, s));
+    const int l0 = c->launches;
+    CK(cudaMemsetAsync(X, 0, (size_t)n * W * 8, s));
+    for (int t = 0; t < trials; ++t)
+        CK(cudaMemcpy2DAsync(X + (size_t)t * Np, (size_t)W * 8, om_in + (size_t)t * n * ell, (size_t)ell * 8,
+                             (size_t)ell * 8, (size_t)n, cudaMemcpyDeviceToDevice, s));
+    auto pass = [&](bool ta, const double* B, double* C) {
+        GemmCall g;
+        g.ta = ta;
+        g.A = P.A;
+        g.Af = P.Af;
+        g.lda = P.lda;
+        g.M = ta ? n : m;
+        g.K = ta ? m : n;
+        g.B = B;
+        g.ldb = W;
+        g.N = W;
+        g.C = C;
+        g.ldc = W;
+        g.sk_bias = W <= 128 ? 1.0 : 0.95;
+        run_gemm(c, g, s);
+    };
+    for (int i = 0; i <= P.q; ++i) {  // sketch.hpp:93-97, all trials per launch
+        pass(false, X, T1b);
+        pass(true, T1b, X);
+    }
+    // per-trial QRs (sketch.hpp:98-99) side by side on the trial streams
+    const int S = std::min(trials, kTrialStreams);
+    ensure_trial_streams(c, S);
+    struct Trial {
+        double *T1, *T2, *Q1, *Q2, *Mk, *Uk, *Vk, *Sk, *Uo, *Vo;
+        int* sweeps;
+        QrPlan *p1, *p2;
+    };
+    std::vector<Trial> tr(trials);
+    for (int t = 0; t < trials; ++t) {
+        const std::string tag = "b" + std::to_string(t) + "_";
+        Trial& x = tr[t];
+        x.T1 = dbuf(c, tag + "T1", (size_t)m * Np);
+        x.T2 = dbuf(c, tag + "T2", (size_t)n * Np);
+        x.Q1 = dbuf(c, tag + "Q1", (size_t)m * Np);
+        x.Q2 = dbuf(c, tag + "Q2", (size_t)n * Np);
+        x.Mk = dbuf(c, tag + "Mk", (size_t)Np * Np);
+        x.Uk = dbuf(c, tag + "Uk", (size_t)Np * Np);
+        x.Vk = dbuf(c, tag + "Vk", (size_t)Np * Np);
+        x.Sk = dbuf(c, tag + "Sk", (size_t)Np);
+        x.Uo = dbuf(c, tag + "Uo", (size_t)m * Np);
+        x.Vo = dbuf(c, tag + "Vo", (size_t)n * Np);
+        x.sweeps = reinterpret_cast<int*>(dbuf(c, tag + "sw", 1));
+        x.p1 = get_qr_plan(c, m, ell, 0, (tag + "T1").c_str());
+        x.p2 = get_qr_plan(c, n, ell, 0, (tag + "T2").c_str());
+    }
+    auto fork = [&]() {
+        CK(cudaEventRecord(c->ev_fork, s));
+        for (int j = 0; j < S; ++j) CK(cudaStreamWaitEvent(c->tstreams[j], c->ev_fork, 0));
+    };
+    auto join = [&]() {
+        for (int j = 0; j < S; ++j) {
+            CK(cudaEventRecord(c->tevents[j], c->tstreams[j]));
+            CK(cudaStreamWaitEvent(s, c->tevents[j], 0));
+        }
+    };
+    fork();
+    for (int t = 0; t < trials; ++t) {
+        cudaStream_t ts = c->tstreams[t % S];
+        Trial& x = tr[t];
+        CK(cudaMemcpy2DAsync(x.T1, (size_t)Np * 8, T1b + (size_t)t * Np, (size_t)W * 8, (size_t)Np * 8, (size_t)m,
+                             cudaMemcpyDeviceToDevice, ts));
+        CK(cudaMemcpy2DAsync(x.T2, (size_t)Np * 8, X + (size_t)t * Np, (size_t)W * 8, (size_t)Np * 8, (size_t)n,
+                             cudaMemcpyDeviceToDevice, ts));
+        qr_run(c, x.p1, x.T1, Np, x.Q1, Np, ts);
+        qr_run(c, x.p2, x.T2, Np, x.Q2, Np, ts);
+        CK(cudaMemcpy2DAsync(X + (size_t)t * Np, (size_t)W * 8, x.Q2, (size_t)Np * 8, (size_t)Np * 8, (size_t)n,
+                             cudaMemcpyDeviceToDevice, ts));
+    }
+    join();
+    pass(false, X, Yb);  // Y_t = A Q2_t for all trials in one launch (sketch.hpp:100-102)
+    fork();
+    for (int t = 0; t < trials; ++t) {
+        cudaStream_t ts = c->tstreams[t % S];
+        Trial& x = tr[t];
+        const std::string ws = "bws" + std::to_string(t % S);
+        GemmCall h;  // M_t = Q1_t^T Y_t
+        h.ta = true;
+        h.A = x.Q1;
+        h.lda = Np;
+        h.M = ell;
+        h.K = m;
+        h.B = Yb + (size_t)t * Np;
+        h.ldb = W;
+        h.N = Np;
+        h.C = x.Mk;
+        h.ldc = Np;
+        h.ws_name = ws.c_str();
+        run_gemm(c, h, ts);
+        run_jacobi(c, ell, x.Mk, Np, x.Uk, Np, x.Sk, x.Vk, Np, x.sweeps, ts);  // sketch.hpp:103
+        for (int hh = 0; hh < 2; ++hh) {  // U = Q1 Ut_k, V = Q2 Vt_k   (sketch.hpp:105,107)
+            GemmCall g;
+            g.A = hh ? x.Q2 : x.Q1;
+            g.lda = Np;
+            g.M = hh ? n : m;
+            g.K = ell;
+            g.B = hh ? x.Vk : x.Uk;
+            g.ldb = Np;
+            g.N = Np;
+            g.C = hh ? x.Vo : x.Uo;
+            g.ldc = Np;
+            g.ws_name = ws.c_str();
+            run_gemm(c, g, ts);
+        }
+        CK(cudaMemcpy2DAsync(dU + (size_t)t * m * k, (size_t)k * 8, x.Uo, (size_t)Np * 8, (size_t)k * 8, (size_t)m,
+                             cudaMemcpyDeviceToDevice, ts));
+        CK(cudaMemcpy2DAsync(dV + (size_t)t * n * k, (size_t)k * 8, x.Vo, (size_t)Np * 8, (size_t)k * 8, (size_t)n,
+                             cudaMemcpyDeviceToDevice, ts));
+        CK(cudaMemcpyAsync(dS + (size_t)t * k, x.Sk, (size_t)k * 8, cudaMemcpyDeviceToDevice, ts));
+    }
+    join();
+    CK(cudaEventRecord(c->ev_b, s));
+    if (st) {
+        CK(cudaEventSynchronize(c->ev_b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+        st->ms_total = ms;
+        st->passes = 2 * d->q + 3;
+        st->method = d->q == 0 ? SORSVD_SOR : SORSVD_SOR_POWER;
+        st->flops_passes = 2.0 * (double)m * n * ell * st->passes * trials;
+        st->bytes_passes = (double)m * n * (d->dtype == SORSVD_F32 ? 4.0 : 8.0) * st->passes;  // A read once per pass
+        st->launches = c->launches - l0;
+        int sw = 0;
+        CK(cudaMemcpy(&sw, tr[0].sweeps, sizeof(int), cudaMemcpyDeviceToHost));
+        st->jacobi_sweeps = sw;
+    }
+}
+
 // ----------------------------------------------------------------- RPCA ----
 double device_sumsq(sorsvd_ctx* c, const double* x, int64_t m, int64_t n, int64_t ld) {
     const int blocks = c->num_sms * 4;
@@ -2655,6 +2851,8 @@ void sorsvd_ctx_destroy(sorsvd_ctx* c) {
     for (auto& e : c->ev_h) cudaEventDestroy(e);
     for (auto& kv : c->sk_tables)
         for (int* d : kv.second.dev) cudaFree(d);
+    for (cudaStream_t t : c->tstreams) cudaStreamDestroy(t);
+    for (cudaEvent_t e : c->tevents) cudaEventDestroy(e);
     cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->own_stream);
     delete c;
@@ -2789,6 +2987,59 @@ int sorsvd_tsr_svd_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, c
         if ((e.flags & SORSVD_FLAG_OMEGA_GIVEN) && (!dPsi1 || !dPsi2))
             throw Error{SORSVD_ERR_PARAMETER, "parameter: OMEGA_GIVEN needs both psi1 and psi2"};
         sor_device(c, &e, dA, dPsi1, dU, dSigma, dV, st, SORSVD_TSR, dPsi2);
+    });
+}
+
+int sorsvd_sor_svd_power_batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int32_t trials, const uint64_t* seeds,
+                                      const void* dA, const double* dOmegas, double* dU, double* dSigma, double* dV,
+                                      sorsvd_stats* st) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (!dA || !dU || !dSigma || !dV) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        batch_device(c, d, trials, seeds, dA, dOmegas, dU, dSigma, dV, st);
+    });
+}
+
+int sorsvd_sor_svd_power_batch(sorsvd_ctx* c, const sorsvd_desc* d, int32_t trials, const uint64_t* seeds,
+                               const void* A, const double* omegas, double* U, double* sigma, double* V,
+                               sorsvd_stats* st) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        validate(d);
+        if (trials < 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: trials must be positive"};
+        if (!A || !U || !sigma || !V) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        const size_t esz = d->dtype == SORSVD_F32 ? 4 : 8;
+        const size_t abytes = (size_t)d->m * d->lda * esz;
+        cudaEvent_t e0 = c->ev_h[0], e1 = c->ev_h[1], e2 = c->ev_h[2], e3 = c->ev_h[3];
+        CK(cudaEventRecord(e0, c->stream));
+        double* dA = dbuf(c, "hostA", (abytes + 7) / 8);
+        CK(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, c->stream));
+        const double* dOm = nullptr;
+        const size_t om_n = (size_t)trials * d->n * d->ell;
+        if (omegas && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+            double* p = dbuf(c, "hostOmB", om_n);
+            CK(cudaMemcpyAsync(p, omegas, om_n * 8, cudaMemcpyHostToDevice, c->stream));
+            dOm = p;
+        }
+        CK(cudaEventRecord(e1, c->stream));
+        const size_t un = (size_t)trials * d->m * d->k, vn = (size_t)trials * d->n * d->k, sn = (size_t)trials * d->k;
+        double* dU = dbuf(c, "hostUB", un);
+        double* dS = dbuf(c, "hostSB", sn);
+        double* dV = dbuf(c, "hostVB", vn);
+        sorsvd_stats local{};
+        batch_device(c, d, trials, seeds, dA, dOm, dU, dS, dV, &local);
+        CK(cudaEventRecord(e2, c->stream));
+        CK(cudaMemcpyAsync(U, dU, un * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(V, dV, vn * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(sigma, dS, sn * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaEventRecord(e3, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        float h2d = 0.f, d2h = 0.f;
+        CK(cudaEventElapsedTime(&h2d, e0, e1));
+        CK(cudaEventElapsedTime(&d2h, e2, e3));
+        local.ms_h2d = h2d;
+        local.ms_d2h = d2h;
+        if (st) *st = local;
     });
 }
 

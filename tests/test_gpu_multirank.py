@@ -171,3 +171,42 @@ def test_sharded_k300_gram_qr(env):
     es = O.sigma_rel_err(s, base.sigma)
     assert np.all(es <= np.maximum(1e-10, 10 * np.maximum.accumulate(ds))), es.max()
     assert np.array_equal(s, out[1].sigma.cpu().numpy())
+
+
+def test_sharded_replicated_outputs_deterministic(env):
+    # sigma and V are replicated: bit-identical on every rank and on every repeat, with the
+    # ranks' contexts created fresh each time (first-call allocations included) and all
+    # eight ranks' streams running concurrently on the one device
+    P, torch = env
+    A = O.gen_lowrank_decay(8000, 400, 40, lambda j: 2.0 ** (-j / 4), 1e-3, 8008)
+    ref = None
+    for _ in range(6):
+        out, _ = _run_sharded(P, torch, A, 10, P.SketchConfig(10, 1, 11), 8)
+        for o in out:
+            s, v = o.sigma.cpu().numpy(), o.v.cpu().numpy()
+            if ref is None:
+                ref = (s, v)
+            np.testing.assert_array_equal(s, ref[0])
+            np.testing.assert_array_equal(v, ref[1])
+
+
+def test_concurrent_contexts_thin_qr_deterministic(env):
+    # one context per host thread (the C ABI's threading contract): same input, same bits
+    P, torch = env
+    ctxs = [P.Context(0) for _ in range(8)]
+    u, _ = np.linalg.qr(O.gaussian_matrix(1000, 10, 5))
+    T = torch.from_numpy(u * np.logspace(0, -3, 10)).cuda()
+    for _ in range(5):
+        out = [None] * 8
+
+        def work(r):
+            out[r] = P.thin_qr(T.clone(), ctx=ctxs[r])[0]
+            torch.cuda.synchronize()
+
+        th = [threading.Thread(target=work, args=(r,)) for r in range(8)]
+        [t.start() for t in th]
+        [t.join() for t in th]
+        for o in out[1:]:
+            assert torch.equal(o, out[0])
+    for c in ctxs:
+        c.close()

@@ -112,6 +112,31 @@ def test_small_svd_vs_oracle(P, torch_mod, k):
         np.testing.assert_allclose(v, v_ref, atol=1e-10)
 
 
+@pytest.mark.parametrize("k", [1, 2, 3, 7, 10, 16, 17, 31, 32])
+def test_small_svd_small_k(P, torch_mod, k):
+    # k <= 32 runs the single-CTA Jacobi: against dgesdd on a graded spectrum and with
+    # exact zero columns (rank deficiency)
+    rng = np.random.default_rng(k)
+    u0, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    v0, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    sig = 10.0 ** (-np.arange(k) / 4.0)
+    for mm in ((u0 * sig) @ v0.T, np.hstack([O.gaussian_matrix(k, max(k - 2, 1), k), np.zeros((k, k - max(k - 2, 1)))])):
+        mm = np.ascontiguousarray(mm)
+        u_ref, s_ref, v_ref = O.full_svd(mm)
+        u, s, v, sweeps = P.full_svd(torch_mod.from_numpy(mm).cuda())
+        u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+        assert np.all(np.diff(s) <= 0) and 1 <= sweeps <= 60
+        np.testing.assert_allclose(s, s_ref, rtol=1e-11, atol=1e-14 * s_ref[0])
+        assert np.abs(v.T @ v - np.eye(k)).max() < 1e-13
+        assert np.abs((u * s) @ v.T - mm).max() < 1e-13 * s_ref[0] * k
+        nz = s_ref > 1e-12 * s_ref[0]
+        assert np.abs((u[:, nz].T @ u[:, nz]) - np.eye(int(nz.sum()))).max() < 1e-13
+        gap = np.min(np.abs(np.diff(s_ref[nz]))) if nz.sum() > 1 else 1.0
+        if gap > 1e-6 * s_ref[0]:
+            np.testing.assert_allclose(u[:, nz], u_ref[:, nz], atol=1e-10)
+            np.testing.assert_allclose(v[:, nz], v_ref[:, nz], atol=1e-10)
+
+
 def test_small_svd_graded(P, torch_mod):
     # strongly graded spectrum: one-sided Jacobi keeps relative accuracy
     k = 60
