@@ -198,6 +198,15 @@ int sorsvd_rpca_alm(sorsvd_ctx* ctx, const sorsvd_rpca_desc* desc, const double*
 int sorsvd_rpca_alm_device(sorsvd_ctx* ctx, const sorsvd_rpca_desc* desc, const double* dD, double* dL,
                            double* dS, sorsvd_rpca_result* res);
 
+/* approx_error(a, x, NormKind::frobenius) (sketch.hpp:168-172) on device
+ * buffers: ||A - U diag(sigma) V^T||_F in one fused pass over A (A m x lda,
+ * FP64 or FP32 by dtype; U m x ldu, V n x ldv, first k columns). Multi-rank:
+ * A and U are this rank's row block and the sum of squares is reduced over
+ * ranks. The spectral norm (dgesdd of the m x n difference) is not provided. */
+int sorsvd_approx_error_fro_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const void* dA, int64_t lda, int32_t dtype,
+                                   int32_t k, const double* dU, int64_t ldu, const double* dSigma, const double* dV,
+                                   int64_t ldv, double* err);
+
 /* ---- stage-level entry points (kernel unit tests) ------------------------- */
 /* thin_qr (dense.hpp:114): dT (m x ldt) -> dQ (m x ldq), dR (k x ldr); device. */
 int sorsvd_thin_qr_device(sorsvd_ctx* ctx, int64_t m, int32_t k, const double* dT, int64_t ldt, double* dQ,

@@ -160,6 +160,17 @@ int ref_tsr_svd(std::int64_t m, std::int64_t n, const double* a, int ell, std::u
     });
 }
 
+// sketch.hpp:168-172: approx_error(a, x, kind) on a given factorisation
+int ref_approx_error(std::int64_t m, std::int64_t n, const double* a, int k, const double* u, const double* sigma,
+                     const double* v, int kind, double* out) {
+    return guarded([&] {
+        sorsvd::LowRankApprox x{wrap(m, k, u), std::vector<double>(sigma, sigma + k), wrap(n, k, v),
+                                sorsvd::SketchMethod::sor, 0, k, 0, 0};
+        *out = sorsvd::approx_error(wrap(m, n, a), x, kind == 0 ? sorsvd::NormKind::frobenius
+                                                                : sorsvd::NormKind::spectral);
+    });
+}
+
 // sketch.hpp:178
 long long ref_flop_estimate(long long m, long long n, long long ell, long long k, long long q,
                             int variant) {

@@ -35,7 +35,7 @@ from . import _capi as C
 __all__ = [
     "SketchMethod", "SketchConfig", "LowRankApprox", "FlopVariant", "RpcaConfig", "RpcaResult", "Context",
     "ShapeError", "ParameterError", "NumericalError", "CudaError", "NcclError", "UnsupportedError", "EmuGroup",
-    "sor_svd_power", "sor_svd", "sor_svd_power_batch", "r_svd", "tsr_svd", "truncate", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
+    "sor_svd_power", "sor_svd", "sor_svd_power_batch", "r_svd", "tsr_svd", "truncate", "approx_error", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
     "flop_estimate", "validate_sketch", "thin_qr", "full_svd", "matmul", "default_context", "version",
 ]
 
@@ -462,6 +462,33 @@ def tsr_svd(a, ell: int, seed: int, psi1=None, psi2=None, ctx: Optional[Context]
     flags = 0 if use_graph else C.FLAG_NO_GRAPH
     st, u, s, v = _decompose("tsr", a, ell, cfg, flags, psi1, psi2, ctx)
     return LowRankApprox(u, s, v, SketchMethod.tsr, st.passes, ell, 0, seed, st.as_dict())
+
+
+def approx_error(a, x: LowRankApprox, kind: str = "frobenius", ctx: Optional[Context] = None) -> float:
+    """sketch.hpp:168-172: ||a - reconstruct(x)|| for kind "frobenius", in one fused
+    pass over a on the device (the m x n reconstruction is never formed). The
+    spectral norm needs a dense SVD of the difference and is not provided."""
+    import torch
+    if kind != "frobenius":
+        raise UnsupportedError("approx_error: only the Frobenius norm runs on the device")
+    dev = a.device if _is_torch_cuda(a) else torch.device("cuda", 0)
+    A = a if _is_torch_cuda(a) else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    if A.dtype not in (torch.float64, torch.float32) or A.dim() != 2 or A.stride(1) != 1:
+        raise ShapeError("shape: approx_error expects a row-major float64 or float32 matrix")
+    u = torch.as_tensor(x.u, dtype=torch.float64, device=dev).contiguous()
+    s = torch.as_tensor(x.sigma, dtype=torch.float64, device=dev).contiguous()
+    v = torch.as_tensor(x.v, dtype=torch.float64, device=dev).contiguous()
+    m, n = A.shape
+    if u.shape[0] != m or v.shape[0] != n:
+        raise ShapeError("approx_error: approximation does not match matrix dims")
+    ctx = ctx or default_context(dev.index or 0)
+    _torch_stream(ctx, A)
+    out = ctypes.c_double()
+    _check(C.lib().sorsvd_approx_error_fro_device(ctx.handle, m, n, A.data_ptr(), A.stride(0),
+                                                  C.F32 if A.dtype == torch.float32 else C.F64, s.shape[0],
+                                                  u.data_ptr(), u.shape[1], s.data_ptr(), v.data_ptr(), v.shape[1],
+                                                  ctypes.byref(out)), ctx.handle)
+    return out.value
 
 
 def truncate(x: LowRankApprox, k: int) -> LowRankApprox:

@@ -88,6 +88,8 @@ SIGNATURES = [
                                       ctypes.POINTER(SorsvdStats)]),
     ("sorsvd_rpca_alm", c_i32, [c_vp, ctypes.POINTER(RpcaDesc), c_dp, c_dp, c_dp, ctypes.POINTER(RpcaRes)]),
     ("sorsvd_rpca_alm_device", c_i32, [c_vp, ctypes.POINTER(RpcaDesc), c_vp, c_vp, c_vp, ctypes.POINTER(RpcaRes)]),
+    ("sorsvd_approx_error_fro_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i32, c_i32, c_vp, c_i64, c_vp,
+                                               c_vp, c_i64, c_dp]),
     ("sorsvd_thin_qr_device", c_i32, [c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]),
     ("sorsvd_small_svd_device", c_i32, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64,
                                         ctypes.POINTER(c_i32)]),

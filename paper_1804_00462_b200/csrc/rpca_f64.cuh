@@ -234,3 +234,73 @@ __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int6
 }
 
 }  // namespace sorsvd_dev
+
+namespace sorsvd_dev {
+
+// approx_error(a, x, frobenius) (sketch.hpp:168-172): ||A - U diag(sigma) V^T||_F
+// in ONE pass over A, without forming the m x n reconstruction (the reference
+// materialises reconstruct(x) with a dgemm and then takes norm()). Each 64 x 64
+// tile of U diag(sigma) V^T is built on DMMA fragments (same layout as
+// rpca_update_kernel), subtracted from A in registers and squared; per-block
+// partial sums, reduced in fixed order. A may be FP32-stored (widened).
+template <typename AT>
+__global__ void __launch_bounds__(kRpcaThreads) approx_err_kernel(const AT* __restrict__ A, int64_t lda,
+                                                                 const double* __restrict__ U, int64_t ldu,
+                                                                 const double* __restrict__ sig,
+                                                                 const double* __restrict__ V, int64_t ldv,
+                                                                 int64_t m, int64_t n, int k, double* partial) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+    const int64_t i0 = (int64_t)blockIdx.y * 64 + (warp >> 1) * 16;
+    const int64_t j0 = (int64_t)blockIdx.x * 64 + (warp & 1) * 32;
+    double acc[2][4][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int kk0 = 0; kk0 < k; kk0 += 4) {
+        const int kk = kk0 + t4;
+        const double z = kk < k ? sig[kk] : 0.0;
+        double af[2], bf[4];
+#pragma unroll
+        for (int fm = 0; fm < 2; ++fm) {
+            const int64_t i = i0 + fm * 8 + g;
+            af[fm] = (kk < k && i < m) ? U[i * ldu + kk] * z : 0.0;
+        }
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) {
+            const int64_t j = j0 + fn * 8 + g;
+            bf[fn] = (kk < k && j < n) ? V[j * ldv + kk] : 0.0;
+        }
+#pragma unroll
+        for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+            for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
+    }
+    double res = 0.0;
+#pragma unroll
+    for (int fm = 0; fm < 2; ++fm) {
+        const int64_t i = i0 + fm * 8 + g;
+        if (i >= m) continue;
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t j = j0 + fn * 8 + 2 * t4 + h;
+                if (j >= n) continue;
+                const double r = (double)A[i * lda + j] - acc[fm][fn][h];
+                res = fma(r, r, res);
+            }
+        }
+    }
+    __shared__ double red[kRpcaThreads / 32];
+    res = warp_sum(res);
+    if (lane == 0) red[warp] = res;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kRpcaThreads / 32; ++w) t += red[w];
+        partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+}  // namespace sorsvd_dev

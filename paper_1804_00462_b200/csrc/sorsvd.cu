@@ -3043,6 +3043,37 @@ int sorsvd_sor_svd_power_batch(sorsvd_ctx* c, const sorsvd_desc* d, int32_t tria
     });
 }
 
+// approx_error(a, x, frobenius)   (sketch.hpp:168-172), fused single pass over A
+int sorsvd_approx_error_fro_device(sorsvd_ctx* c, int64_t m, int64_t n, const void* dA, int64_t lda, int32_t dtype,
+                                   int32_t k, const double* dU, int64_t ldu, const double* dSigma, const double* dV,
+                                   int64_t ldv, double* err) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (m < 1 || n < 1 || k < 1 || lda < n || ldu < k || ldv < k)
+            throw Error{SORSVD_ERR_SHAPE, "shape: approx_error: approximation does not match matrix dims"};
+        if (!dA || !dU || !dSigma || !dV || !err) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        if (dtype != SORSVD_F64 && dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
+        const dim3 grid((unsigned)cdiv(n, 64), (unsigned)cdiv(m, 64));
+        const int64_t nblk = (int64_t)grid.x * grid.y;
+        double* part = dbuf(c, "ae_part", (size_t)nblk);
+        double* tot = dbuf(c, "ae_tot", 2);
+        if (dtype == SORSVD_F64)
+            approx_err_kernel<double><<<grid, kRpcaThreads, 0, c->stream>>>(static_cast<const double*>(dA), lda, dU,
+                                                                            ldu, dSigma, dV, ldv, m, n, k, part);
+        else
+            approx_err_kernel<float><<<grid, kRpcaThreads, 0, c->stream>>>(static_cast<const float*>(dA), lda, dU, ldu,
+                                                                           dSigma, dV, ldv, m, n, k, part);
+        check_launch(c);
+        sum_partials_kernel<<<1, 1024, 0, c->stream>>>(part, nblk, tot);
+        check_launch(c);
+        comm_allreduce(c, tot, 1, false, c->stream);  // row-sharded A: sum of squares over ranks
+        double h[2];
+        CK(cudaMemcpyAsync(h, tot, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        *err = sqrt(h[0]);
+    });
+}
+
 int sorsvd_thin_qr_device(sorsvd_ctx* c, int64_t m, int32_t k, const double* dT, int64_t ldt, double* dQ,
                           int64_t ldq, double* dR, int64_t ldr) {
     if (!c) return SORSVD_ERR_PARAMETER;

@@ -120,3 +120,30 @@ def test_truncate_and_errors(P):
         P.r_svd(A, 5, -1, 1)
     with pytest.raises(P.ParameterError):
         P.tsr_svd(A, 5, 1, psi1=O.gaussian_matrix(40, 5, 1))
+
+
+def test_approx_error_frobenius_vs_reference(P, golden):
+    # approx_error(a, x, frobenius) (sketch.hpp:168-172), one fused pass over A on the device,
+    # against the compiled reference evaluated on the same factors
+    import torch
+    g, meta = golden
+    for name in meta["cases"][:3] + ["c1"]:
+        if name == "c1":
+            A, u, s, v = O.gen_c1(1), g["c1_u"], g["c1_s"], g["c1_v"]
+        else:
+            A, u, s, v = g[name + "_A"], g[name + "_u"], g[name + "_s"], g[name + "_v"]
+        x = O.LowRankApprox(u, s, v, 0, 0, len(s), 0, 0)
+        ref = O.Ref.approx_error(A, u, s, v, 0) if O.os.path.exists(O.REF_LIB_PATH) else O.approx_error(A, x)
+        got = P.approx_error(A, x)
+        assert abs(got - ref) <= 1e-10 * ref, (name, got, ref)
+        got_dev = P.approx_error(torch.from_numpy(A).cuda(), x)
+        assert got_dev == got
+    # FP32-stored A: the FP64 oracle on the rounded matrix
+    A = O.gen_lowrank_decay(700, 500, 30, lambda j: 2.0 ** (-j / 3), 1e-3, 4).astype(np.float32)
+    f = P.sor_svd_power(A, 20, P.SketchConfig(24, 1, 2))
+    ref = O.approx_error(A.astype(np.float64), O.LowRankApprox(f.u, f.sigma, f.v, 0, 0, 20, 0, 0))
+    assert abs(P.approx_error(A, f) - ref) <= 1e-10 * ref
+    with pytest.raises(P.UnsupportedError):
+        P.approx_error(A, f, "spectral")
+    with pytest.raises(P.ShapeError):
+        P.approx_error(A[:100], f)

@@ -100,6 +100,17 @@ def test_baselines_port_match_reference_golden(golden, kind):
         assert O.lowrank_rel_diff(f.u, f.sigma, f.v, g[name + "_u"], g[name + "_s"], g[name + "_v"]) <= max(1e-10, 10 * dl), name
 
 
+def test_approx_error_port_vs_reference(ref_available):
+    # sketch.hpp:168-172 on a sor_svd_power result: restatement vs the compiled reference
+    if not ref_available:
+        pytest.skip("oracle/_ref not built")
+    a = O.gen_lowrank_decay(120, 90, 20, lambda j: 2.0 ** (-j / 2), 1e-4, 8)
+    f = O.sor_svd_power(a, 10, O.SketchConfig(12, 1, 3))
+    for kind, code in (("frobenius", 0), ("spectral", 1)):
+        r = O.Ref.approx_error(a, f.u, f.sigma, f.v, code)
+        assert abs(O.approx_error(a, f, kind) - r) <= 1e-12 * r
+
+
 def test_truncate_rules():
     a = O.gaussian_matrix(30, 20, 3)
     f = O.r_svd(a, 6, 0, 1)
