@@ -137,6 +137,26 @@ def test_small_svd_small_k(P, torch_mod, k):
             np.testing.assert_allclose(v[:, nz], v_ref[:, nz], atol=1e-10)
 
 
+@pytest.mark.parametrize("k", [33, 64, 100, 128])
+def test_small_svd_p2p_ring_vs_barrier_ring(P, torch_mod, k, monkeypatch):
+    # 32 < k <= 128 runs the point-to-point ring (st.async + per-slot mbarriers, no cluster
+    # barrier per round); the barrier ring it replaced must give the same spectrum, and the
+    # p2p result is bit-stable across repeats (no timing dependence)
+    mm = torch_mod.from_numpy(np.ascontiguousarray(O.gen_lowrank_decay(k, k, k, lambda j: 1.0 / j ** 2, 0.0, k)))
+    mm = mm.cuda()
+    u1, s1, v1, w1 = P.full_svd(mm)
+    for _ in range(3):
+        u2, s2, v2, _ = P.full_svd(mm)
+        assert torch_mod.equal(s1, s2) and torch_mod.equal(u1, u2) and torch_mod.equal(v1, v2)
+    monkeypatch.setenv("SORSVD_JACOBI_BARRIER", "1")
+    _, s3, _, w3 = P.full_svd(mm)
+    s_ref = np.linalg.svd(mm.cpu().numpy(), compute_uv=False)
+    # dgesdd is accurate to eps * sigma_1 in absolute terms on the tiny tail
+    np.testing.assert_allclose(s1.cpu().numpy(), s_ref, rtol=1e-11, atol=1e-15 * s_ref[0])
+    np.testing.assert_allclose(s1.cpu().numpy(), s3.cpu().numpy(), rtol=2e-11, atol=1e-15 * s_ref[0])
+    assert abs(w1 - w3) <= 1
+
+
 def test_small_svd_graded(P, torch_mod):
     # strongly graded spectrum: one-sided Jacobi keeps relative accuracy
     k = 60
