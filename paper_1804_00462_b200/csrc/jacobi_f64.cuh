@@ -160,8 +160,8 @@ __global__ void jacobi_cluster_kernel(JacobiArgs a) {
                     }
                 }
                 const int nxt = cur ^ 1;
-                double* dT = dstT[nxt];
-                double* dB = dstB[nxt];
+                double* dT = nxt ? dstT[1] : dstT[0];  // selects keep the pointers in registers
+                double* dB = nxt ? dstB[1] : dstB[0];
 #pragma unroll
                 for (int p = 0; p < KP; ++p) {
                     const int i = lane + 32 * p;
