@@ -72,8 +72,63 @@ __global__ void __launch_bounds__(kRpcaThreads) rpca_update_kernel(RpcaArgs a) {
             for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
     }
     double res = 0.0;
+    // each lane's two columns are adjacent: 16-byte loads / stores of D, Y, S, W when the
+    // rows are 16-byte aligned (same arithmetic as the element path)
+    const bool vec = a.mode == 0 && ((a.ldd | a.ldx) & 1) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(a.D) | reinterpret_cast<uintptr_t>(a.S) |
+                       reinterpret_cast<uintptr_t>(a.Y) | reinterpret_cast<uintptr_t>(a.W)) & 15) == 0;
+    if (vec) {
+#pragma unroll
+        for (int fm = 0; fm < 2; ++fm) {
+            const int64_t i = i0 + fm * 8 + g;
+            if (i >= a.m) continue;
+#pragma unroll
+            for (int fn = 0; fn < 4; ++fn) {
+                const int64_t j = j0 + fn * 8 + 2 * t4;
+                if (j + 1 >= a.n) {  // ragged right edge: the element path
+                    for (int h = 0; h < 2 && j + h < a.n; ++h) {
+                        const double l = acc[fm][fn][h];
+                        const double d = a.D[i * a.ldd + j + h];
+                        const double y = a.Y[i * a.ldx + j + h];
+                        const double t = d - l + y / a.mu;
+                        const double sh = fabs(t) - a.eps;
+                        const double sv = sh > 0.0 ? (t > 0.0 ? sh : -sh) : 0.0;
+                        const double r = d - l - sv;
+                        const double yn = y + a.mu * r;
+                        a.S[i * a.ldx + j + h] = sv;
+                        a.Y[i * a.ldx + j + h] = yn;
+                        if (a.W) a.W[i * a.ldx + j + h] = d - sv + yn / a.mu_next;
+                        res = fma(r, r, res);
+                    }
+                    continue;
+                }
+                const double2 d2 = __ldcs(reinterpret_cast<const double2*>(a.D + i * a.ldd + j));
+                const double2 y2 = __ldcs(reinterpret_cast<const double2*>(a.Y + i * a.ldx + j));
+                double sv[2], yn[2], wv[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double l = acc[fm][fn][h];
+                    const double d = h ? d2.y : d2.x;
+                    const double y = h ? y2.y : y2.x;
+                    const double t = d - l + y / a.mu;
+                    const double sh = fabs(t) - a.eps;
+                    sv[h] = sh > 0.0 ? (t > 0.0 ? sh : -sh) : 0.0;
+                    const double r = d - l - sv[h];
+                    yn[h] = y + a.mu * r;
+                    wv[h] = d - sv[h] + yn[h] / a.mu_next;
+                    res = fma(r, r, res);
+                }
+                __stcs(reinterpret_cast<double2*>(a.S + i * a.ldx + j), make_double2(sv[0], sv[1]));
+                __stcs(reinterpret_cast<double2*>(a.Y + i * a.ldx + j), make_double2(yn[0], yn[1]));
+                // W is the next iteration's SOR-SVD input, read by its 2q+3 passes: a normal
+                // store (L2-resident when it fits); D, Y, S are streamed
+                if (a.W) *reinterpret_cast<double2*>(a.W + i * a.ldx + j) = make_double2(wv[0], wv[1]);
+            }
+        }
+    }
 #pragma unroll
     for (int fm = 0; fm < 2; ++fm) {
+        if (vec) break;
         const int64_t i = i0 + fm * 8 + g;
         if (i >= a.m) continue;
 #pragma unroll
