@@ -1510,6 +1510,15 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
     const int kp = (k + 31) / 32;
     const int KP = kp <= 1 ? 1 : kp <= 2 ? 2 : kp <= 4 ? 4 : 8;
     const int P = ((k + 1) & ~1) / 2;
+    if (k > 16 && k <= 32 && !getenv("SORSVD_JACOBI_BARRIER")) {
+        // 16 < k <= 32: the point-to-point ring, one warp per CTA over a P-CTA cluster
+        // (measured C1, k = 20: 0.118 -> 0.087 ms); k <= 16 keeps the single CTA (RPCA's
+        // k = 10 is faster there)
+        const int Pk = ((k + 1) & ~1) / 2;
+        a.ppc = 1;
+        launch_jacobi_p2p_t<2>(c, a, Pk, s);
+        return;
+    }
     if (k <= 32 && jacobi_cta_smem_bytes(k) <= 212 * 1024) {
         // small k: one CTA, G and V in shared memory (no cluster barrier needed;
         // measured 4x slower than the cluster ring at k = 100)

@@ -137,7 +137,7 @@ def test_small_svd_small_k(P, torch_mod, k):
             np.testing.assert_allclose(v[:, nz], v_ref[:, nz], atol=1e-10)
 
 
-@pytest.mark.parametrize("k", [33, 64, 100, 128])
+@pytest.mark.parametrize("k", [17, 20, 31, 32, 33, 64, 100, 128])
 def test_small_svd_p2p_ring_vs_barrier_ring(P, torch_mod, k, monkeypatch):
     # 32 < k <= 128 runs the point-to-point ring (st.async + per-slot mbarriers, no cluster
     # barrier per round); the barrier ring it replaced must give the same spectrum, and the
