@@ -48,6 +48,22 @@ __host__ __device__ inline size_t jacobi_smem_bytes(int k, int ppc) {
     return (2 * (size_t)ppc * slot + 2 * 2 * (size_t)ppc + 4 * (size_t)ppc + 64) * sizeof(double);
 }
 
+
+// Jacobi rotation of a column pair from its Gram entries al = |p|^2, be = |q|^2,
+// ga = p.q: tan = 2 ga sgn(d) / (|d| + sqrt(d^2 + 4 ga^2)), d = be - al (the smaller
+// angle). Computed from two reciprocal square roots (cos 2th = |d| r1,
+// c = sqrt((1 + cos 2th) / 2), s = ga sgn(d) r1 / c) instead of a division, a square
+// root and a reciprocal square root in sequence: a shorter FP64 dependency chain on
+// the critical path of every ring round.
+__device__ __forceinline__ void jac_rotation(double al, double be, double ga, double& c, double& sn) {
+    const double d = be - al;
+    const double r1 = rsqrt(fma(d, d, 4.0 * ga * ga));
+    const double x = fma(0.5 * fabs(d), r1, 0.5);
+    const double r2 = rsqrt(x);
+    c = x * r2;
+    sn = (d < 0.0 ? -ga : ga) * r1 * r2;
+}
+
 template <int KP>
 __global__ void jacobi_cluster_kernel(JacobiArgs a) {
     cgj::cluster_group cl = cgj::this_cluster();
@@ -144,11 +160,8 @@ __global__ void jacobi_cluster_kernel(JacobiArgs a) {
                 }
                 if (ga != 0.0 && ga * ga > tol2 * al * be) {
                     rotated = 1;
-                    // tan of the Jacobi angle (smaller root of t^2 + 2 zeta t - 1 = 0)
-                    const double d = be - al;
-                    const double t = (2.0 * ga * (d < 0.0 ? -1.0 : 1.0)) / (fabs(d) + sqrt(fma(d, d, 4.0 * ga * ga)));
-                    const double c = rsqrt(fma(t, t, 1.0));
-                    const double sn = c * t;
+                    double c, sn;
+                    jac_rotation(al, be, ga, c, sn);
 #pragma unroll
                     for (int p = 0; p < KP; ++p) {
                         const double x = gt[p], y = gb[p];
@@ -351,12 +364,8 @@ __global__ void __launch_bounds__(PPW == 1 ? 1024 : 512, 1) jacobi_cta_kernel(Ja
                 for (int t = 0; t < PPW; ++t) {
                     if (!(act[t] && ga[t] != 0.0 && ga[t] * ga[t] > tol2 * al[t] * be[t])) continue;
                     rotated = 1;
-                    // tan of the Jacobi angle (smaller root of t^2 + 2 zeta t - 1 = 0)
-                    const double d = be[t] - al[t];
-                    const double tt =
-                        (2.0 * ga[t] * (d < 0.0 ? -1.0 : 1.0)) / (fabs(d) + sqrt(fma(d, d, 4.0 * ga[t] * ga[t])));
-                    const double c = rsqrt(fma(tt, tt, 1.0));
-                    const double sn = c * tt;
+                    double c, sn;
+                    jac_rotation(al[t], be[t], ga[t], c, sn);
                     double* Gp = G + (size_t)cp[t] * k;
                     double* Gq = G + (size_t)cq[t] * k;
                     double* Vp = V + (size_t)cp[t] * k;
@@ -596,10 +605,8 @@ __global__ void jacobi_p2p_kernel(JacobiArgs a) {
                 }
                 if (ga != 0.0 && ga * ga > tol2 * al * be) {
                     rotated = 1;
-                    const double d = be - al;
-                    const double t = (2.0 * ga * (d < 0.0 ? -1.0 : 1.0)) / (fabs(d) + sqrt(fma(d, d, 4.0 * ga * ga)));
-                    const double c = rsqrt(fma(t, t, 1.0));
-                    const double sn = c * t;
+                    double c, sn;
+                    jac_rotation(al, be, ga, c, sn);
 #pragma unroll
                     for (int p = 0; p < KP; ++p) {
                         const double x = gt[p], y = gb[p];
