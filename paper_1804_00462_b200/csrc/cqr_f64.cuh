@@ -27,6 +27,9 @@ namespace sorsvd_dev {
 namespace cg = cooperative_groups;
 
 constexpr int kCqrThreads = 512;
+// trailing columns a warp updates per sweep of its rows in the factor's fused pass: the
+// reflector x and the next column xn are read once per group (shared-memory traffic)
+constexpr int kCqrNG = 4;
 constexpr int kCqrSmemBudget = 212 * 1024;
 
 struct CqrArgs {
@@ -207,18 +210,18 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
         if (nt > 1) {
             const double* xn = A + (size_t)(j + 1) * ld;  // next reflector (updated, unscaled)
             const int ntn = nt - 1;
-            for (int c0 = first_owned(j + 2); c0 < k; c0 += 4 * nw) {
-                ColGroup<4> g(A, ld, c0, nw, k);
-                double dd[4], sn[4];
+            for (int c0 = first_owned(j + 2); c0 < k; c0 += kCqrNG * nw) {
+                ColGroup<kCqrNG> g(A, ld, c0, nw, k);
+                double dd[kCqrNG], sn[kCqrNG];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kCqrNG; ++q) {
                     const int c = c0 + q * nw;
                     dd[q] = g.on[q] ? (S[2 + nt + (c - j - 1)] + scal * S[2 + (c - j - 1)]) * t : 0.0;
                     sn[q] = 0.0;
                 }
                 if (owner && lane == 0) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
+                    for (int q = 0; q < kCqrNG; ++q)
                         if (g.on[q]) g.y[q][jo] -= dd[q];
                 }
                 // all loads of a row before any store: the four column pointers
@@ -228,24 +231,24 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
                 for (int i = i0 + lane; i < nr; i += 32) {
                     const double vi = scal * x[i];
                     const double xi = (i >= i0n) ? xn[i] : 0.0;
-                    double yv[4];
+                    double yv[kCqrNG];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) yv[q] = g.y[q][i];  // off columns alias column c0 (readable)
+                    for (int q = 0; q < kCqrNG; ++q) yv[q] = g.y[q][i];  // off columns alias column c0 (readable)
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
+                    for (int q = 0; q < kCqrNG; ++q) {
                         yv[q] = fma(-dd[q], vi, yv[q]);
                         sn[q] = fma(xi, yv[q], sn[q]);
                     }
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
+                    for (int q = 0; q < kCqrNG; ++q)
                         if (g.on[q]) g.y[q][i] = yv[q];
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) sn[q] = warp_sum(sn[q]);
+                for (int q = 0; q < kCqrNG; ++q) sn[q] = warp_sum(sn[q]);
                 __syncwarp();
                 if (lane == 0) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
+                    for (int q = 0; q < kCqrNG; ++q) {
                         if (g.on[q]) {
                             const int c = c0 + q * nw;
                             Pn[2 + (c - j - 2)] = sn[q];
