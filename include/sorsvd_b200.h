@@ -207,6 +207,17 @@ int sorsvd_approx_error_fro_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const 
                                    int32_t k, const double* dU, int64_t ldu, const double* dSigma, const double* dV,
                                    int64_t ldv, double* err);
 
+/* ---- SORD matrix files ----------------------------------------
+ * "SORD", u32 version = 1, u64 rows, u64 cols, then rows*cols little-endian
+ * float64, row-major. The loader streams the file into device memory through two
+ * pinned staging buffers (the disk read of one chunk overlaps the copy of the
+ * other; the host never holds the matrix), optionally rounding to FP32 on the
+ * device (dtype SORSVD_F32, e.g. a 137 GB FP64 file into 68.7 GB of HBM). */
+int sorsvd_sord_header(const char* path, int64_t* rows, int64_t* cols);
+int sorsvd_load_sord_device(sorsvd_ctx* ctx, const char* path, void* dA, int64_t lda, int32_t dtype);
+int sorsvd_save_sord_device(sorsvd_ctx* ctx, const char* path, const double* dA, int64_t rows, int64_t cols,
+                            int64_t lda);
+
 /* ---- stage-level entry points (kernel unit tests) ------------------------- */
 /* thin_qr (dense.hpp:114): dT (m x ldt) -> dQ (m x ldq), dR (k x ldr); device. */
 int sorsvd_thin_qr_device(sorsvd_ctx* ctx, int64_t m, int32_t k, const double* dT, int64_t ldt, double* dQ,

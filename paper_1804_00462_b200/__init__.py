@@ -35,7 +35,7 @@ from . import _capi as C
 __all__ = [
     "SketchMethod", "SketchConfig", "LowRankApprox", "FlopVariant", "RpcaConfig", "RpcaResult", "Context",
     "ShapeError", "ParameterError", "NumericalError", "CudaError", "NcclError", "UnsupportedError", "EmuGroup",
-    "sor_svd_power", "sor_svd", "sor_svd_power_batch", "r_svd", "tsr_svd", "truncate", "approx_error", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
+    "sor_svd_power", "sor_svd", "sor_svd_power_batch", "r_svd", "tsr_svd", "truncate", "approx_error", "sord_header", "load_sord", "save_sord", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
     "flop_estimate", "validate_sketch", "thin_qr", "full_svd", "matmul", "default_context", "version",
 ]
 
@@ -489,6 +489,40 @@ def approx_error(a, x: LowRankApprox, kind: str = "frobenius", ctx: Optional[Con
                                                   u.data_ptr(), u.shape[1], s.data_ptr(), v.data_ptr(), v.shape[1],
                                                   ctypes.byref(out)), ctx.handle)
     return out.value
+
+
+def sord_header(path: str):
+    """(rows, cols) of a SORD matrix file (no GPU needed)."""
+    r, c = C.c_i64(), C.c_i64()
+    _check(C.lib().sorsvd_sord_header(path.encode(), ctypes.byref(r), ctypes.byref(c)))
+    return r.value, c.value
+
+
+def load_sord(path: str, device: int = 0, dtype=None, ctx: Optional[Context] = None):
+    """Stream a SORD file into a CUDA tensor (float64, or float32 rounded on
+    the device) without holding the matrix on the host."""
+    import torch
+    dtype = dtype or torch.float64
+    if dtype not in (torch.float64, torch.float32):
+        raise ParameterError("parameter: dtype must be float64 or float32")
+    rows, cols = sord_header(path)
+    out = torch.empty((rows, cols), dtype=dtype, device=torch.device("cuda", device))
+    ctx = ctx or default_context(device)
+    _torch_stream(ctx, out)
+    _check(C.lib().sorsvd_load_sord_device(ctx.handle, path.encode(), out.data_ptr(), cols,
+                                           C.F32 if dtype == torch.float32 else C.F64), ctx.handle)
+    return out
+
+
+def save_sord(path: str, a, ctx: Optional[Context] = None) -> None:
+    """Write a CUDA float64 matrix as a SORD file, streamed through pinned buffers."""
+    import torch
+    if not _is_torch_cuda(a) or a.dtype != torch.float64 or a.dim() != 2 or a.stride(1) != 1:
+        raise ShapeError("shape: save_sord expects a row-major CUDA float64 matrix")
+    ctx = ctx or default_context(a.device.index or 0)
+    _torch_stream(ctx, a)
+    _check(C.lib().sorsvd_save_sord_device(ctx.handle, path.encode(), a.data_ptr(), a.shape[0], a.shape[1],
+                                           a.stride(0)), ctx.handle)
 
 
 def truncate(x: LowRankApprox, k: int) -> LowRankApprox:

@@ -11,6 +11,9 @@
 // on-device sums, for tests on a single B200.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -2350,6 +2353,148 @@ void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_
     }
 }
 
+
+// ------------------------------------------------------------ SORD files ----
+// "SORD", u32 version = 1, u64 rows, u64 cols, rows*cols little-endian
+// float64, row-major. Streamed through two pinned staging buffers so that the disk
+// read (write) of one chunk overlaps the host<->device copy of the other and the
+// host never holds the whole matrix (a 137 GB FP64 file can land as 68.7 GB FP32).
+struct SordHeader {
+    int64_t rows = 0, cols = 0;
+};
+
+SordHeader sord_read_header(int fd, const char* path) {
+    unsigned char h[24];
+    if (pread(fd, h, 24, 0) != 24) throw Error{SORSVD_ERR_SHAPE, std::string("shape: SORD header truncated: ") + path};
+    if (memcmp(h, "SORD", 4) != 0) throw Error{SORSVD_ERR_PARAMETER, std::string("parameter: not a SORD file: ") + path};
+    uint32_t ver;
+    uint64_t r, cc;
+    memcpy(&ver, h + 4, 4);
+    memcpy(&r, h + 8, 8);
+    memcpy(&cc, h + 16, 8);
+    if (ver != 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: unsupported SORD version " + std::to_string(ver)};
+    if (r == 0 || cc == 0 || r > (1ull << 40) || cc > (1ull << 40))
+        throw Error{SORSVD_ERR_SHAPE, "shape: SORD dimensions out of range"};
+    struct stat st;
+    if (fstat(fd, &st) != 0 || (uint64_t)st.st_size != 24 + r * cc * 8)
+        throw Error{SORSVD_ERR_SHAPE, std::string("shape: SORD payload size does not match rows x cols: ") + path};
+    return SordHeader{(int64_t)r, (int64_t)cc};
+}
+
+struct Fd {
+    int fd = -1;
+    ~Fd() {
+        if (fd >= 0) close(fd);
+    }
+};
+
+int64_t sord_chunk_rows(int64_t cols) {
+    int64_t mb = 64;
+    if (const char* e = getenv("SORSVD_SORD_CHUNK_MB")) mb = std::max<int64_t>(1, atoll(e));  // tests
+    return std::max<int64_t>(1, (mb << 20) / (cols * 8));
+}
+
+struct PinnedPair {  // two pinned staging buffers + their reuse events
+    double* h[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    explicit PinnedPair(size_t bytes) {
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&h[i]), bytes, cudaHostAllocDefault));
+            CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        }
+    }
+    ~PinnedPair() {
+        for (int i = 0; i < 2; ++i) {
+            if (ev[i]) {
+                cudaEventSynchronize(ev[i]);
+                cudaEventDestroy(ev[i]);
+            }
+            if (h[i]) cudaFreeHost(h[i]);
+        }
+    }
+};
+
+void sord_load(sorsvd_ctx* c, const char* path, void* dA, int64_t lda, int dtype) {
+    Fd f;
+    f.fd = open(path, O_RDONLY);
+    if (f.fd < 0) throw Error{SORSVD_ERR_PARAMETER, std::string("parameter: cannot open ") + path};
+    const SordHeader hd = sord_read_header(f.fd, path);
+    if (lda < hd.cols) throw Error{SORSVD_ERR_SHAPE, "shape: lda < cols"};
+    if (dtype != SORSVD_F64 && dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
+    const int64_t cr = std::min(sord_chunk_rows(hd.cols), hd.rows);
+    const size_t cbytes = (size_t)cr * hd.cols * 8;
+    PinnedPair pp(cbytes);
+    double* stage[2] = {nullptr, nullptr};
+    if (dtype == SORSVD_F32) {
+        stage[0] = dbuf(c, "sord_stage0", (size_t)cr * hd.cols);
+        stage[1] = dbuf(c, "sord_stage1", (size_t)cr * hd.cols);
+    }
+    cudaStream_t s = c->stream;
+    int64_t r0 = 0;
+    for (int64_t ch = 0; r0 < hd.rows; ++ch, r0 += cr) {
+        const int b = (int)(ch & 1);
+        const int64_t nr = std::min(cr, hd.rows - r0);
+        const size_t nb = (size_t)nr * hd.cols * 8;
+        CK(cudaEventSynchronize(pp.ev[b]));  // the copy out of this buffer two chunks ago is done
+        size_t got = 0;
+        while (got < nb) {
+            const ssize_t k = pread(f.fd, reinterpret_cast<char*>(pp.h[b]) + got, nb - got,
+                                    (off_t)(24 + (size_t)r0 * hd.cols * 8 + got));
+            if (k <= 0) throw Error{SORSVD_ERR_SHAPE, std::string("shape: SORD read failed: ") + path};
+            got += (size_t)k;
+        }
+        if (dtype == SORSVD_F64) {
+            double* dst = static_cast<double*>(dA) + r0 * lda;
+            CK(cudaMemcpy2DAsync(dst, (size_t)lda * 8, pp.h[b], (size_t)hd.cols * 8, (size_t)hd.cols * 8, (size_t)nr,
+                                 cudaMemcpyHostToDevice, s));
+        } else {
+            CK(cudaMemcpyAsync(stage[b], pp.h[b], nb, cudaMemcpyHostToDevice, s));
+            cast_to_f32(c, stage[b], hd.cols, static_cast<float*>(dA) + r0 * lda, lda, nr, (int)hd.cols, s);
+        }
+        CK(cudaEventRecord(pp.ev[b], s));
+    }
+    CK(cudaStreamSynchronize(s));
+}
+
+void sord_save(sorsvd_ctx* c, const char* path, const double* dA, int64_t rows, int64_t cols, int64_t lda) {
+    if (rows < 1 || cols < 1 || lda < cols) throw Error{SORSVD_ERR_SHAPE, "shape: SORD save dimensions"};
+    Fd f;
+    f.fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (f.fd < 0) throw Error{SORSVD_ERR_PARAMETER, std::string("parameter: cannot create ") + path};
+    unsigned char h[24];
+    memcpy(h, "SORD", 4);
+    const uint32_t ver = 1;
+    const uint64_t r = (uint64_t)rows, cc = (uint64_t)cols;
+    memcpy(h + 4, &ver, 4);
+    memcpy(h + 8, &r, 8);
+    memcpy(h + 16, &cc, 8);
+    if (pwrite(f.fd, h, 24, 0) != 24) throw Error{SORSVD_ERR_INTERNAL, "SORD write failed"};
+    const int64_t cr = std::min(sord_chunk_rows(cols), rows);
+    PinnedPair pp((size_t)cr * cols * 8);
+    cudaStream_t s = c->stream;
+    auto issue = [&](int64_t ch) {  // device -> pinned buffer ch & 1
+        const int64_t a0 = ch * cr, nr = std::min(cr, rows - a0);
+        CK(cudaMemcpy2DAsync(pp.h[ch & 1], (size_t)cols * 8, dA + a0 * lda, (size_t)lda * 8, (size_t)cols * 8,
+                             (size_t)nr, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(pp.ev[ch & 1], s));
+    };
+    const int64_t nch = cdiv(rows, cr);
+    issue(0);
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) issue(ch + 1);  // next chunk's copy overlaps this chunk's disk write
+        CK(cudaEventSynchronize(pp.ev[ch & 1]));
+        const int64_t a0 = ch * cr, nr = std::min(cr, rows - a0);
+        const size_t nb = (size_t)nr * cols * 8;
+        size_t put = 0;
+        while (put < nb) {
+            const ssize_t k = pwrite(f.fd, reinterpret_cast<const char*>(pp.h[ch & 1]) + put, nb - put,
+                                     (off_t)(24 + (size_t)a0 * cols * 8 + put));
+            if (k <= 0) throw Error{SORSVD_ERR_INTERNAL, std::string("SORD write failed: ") + path};
+            put += (size_t)k;
+        }
+    }
+}
+
 // ----------------------------------------------------------------- RPCA ----
 double device_sumsq(sorsvd_ctx* c, const double* x, int64_t m, int64_t n, int64_t ld) {
     const int blocks = c->num_sms * 4;
@@ -3109,6 +3254,39 @@ int sorsvd_approx_error_fro_device(sorsvd_ctx* c, int64_t m, int64_t n, const vo
         CK(cudaMemcpyAsync(h, tot, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         *err = sqrt(h[0]);
+    });
+}
+
+int sorsvd_sord_header(const char* path, int64_t* rows, int64_t* cols) {
+    try {
+        if (!path || !rows || !cols) return SORSVD_ERR_PARAMETER;
+        Fd f;
+        f.fd = open(path, O_RDONLY);
+        if (f.fd < 0) return SORSVD_ERR_PARAMETER;
+        const SordHeader h = sord_read_header(f.fd, path);
+        *rows = h.rows;
+        *cols = h.cols;
+        return SORSVD_OK;
+    } catch (const Error& e) {
+        g_global_err = e.msg;
+        return e.status;
+    }
+}
+
+int sorsvd_load_sord_device(sorsvd_ctx* c, const char* path, void* dA, int64_t lda, int32_t dtype) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (!path || !dA) throw Error{SORSVD_ERR_PARAMETER, "parameter: null argument"};
+        sord_load(c, path, dA, lda, dtype);
+    });
+}
+
+int sorsvd_save_sord_device(sorsvd_ctx* c, const char* path, const double* dA, int64_t rows, int64_t cols,
+                            int64_t lda) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (!path || !dA) throw Error{SORSVD_ERR_PARAMETER, "parameter: null argument"};
+        sord_save(c, path, dA, rows, cols, lda);
     });
 }
 

@@ -100,3 +100,21 @@ def test_cpp_dropin_header_compiles_against_reference():
         import subprocess
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
     assert os.path.exists(path)
+
+
+def test_sord_header_cpu(tmp_path):
+    # SORD files: header parsing through the C ABI needs no GPU
+    import paper_1804_00462_b200 as P
+    a = O.gaussian_matrix(37, 11, 3)
+    p = str(tmp_path / "a.sord")
+    O.write_sord(p, a)
+    assert P.sord_header(p) == (37, 11)
+    np.testing.assert_array_equal(O.read_sord(p), a)
+    bad = tmp_path / "bad.sord"
+    bad.write_bytes(b"NOPE" + open(p, "rb").read()[4:])
+    with pytest.raises(P.ParameterError):
+        P.sord_header(str(bad))
+    short = tmp_path / "short.sord"
+    short.write_bytes(open(p, "rb").read()[:-8])
+    with pytest.raises(P.ShapeError):
+        P.sord_header(str(short))
