@@ -1850,7 +1850,9 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     // truncated_svd(M, k)   (sketch.hpp:103)
     run_jacobi(c, ell, b.Mk, Np, b.Uk, Np, b.Sk, b.Vk, Np, b.sweeps, s);
     record_stage(c, timing, 4);
-    // U = Q1 Ut_k, V = Q2 Vt_k   (sketch.hpp:105,107)
+    // U = Q1 Ut_k, V = Q2 Vt_k   (sketch.hpp:105,107), the two products side by side
+    CK(cudaEventRecord(c->ev_fork, s));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     {
         GemmCall g;
         g.A = b.Q1;
@@ -1873,8 +1875,11 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         h.N = Np;
         h.C = b.Vo;
         h.ldc = Np;
-        run_gemm(c, h, s);
+        h.ws_name = "gemm_ws_side";
+        run_gemm(c, h, c->side);
     }
+    CK(cudaEventRecord(c->ev_join, c->side));
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     record_stage(c, timing, 5);
 }
 
