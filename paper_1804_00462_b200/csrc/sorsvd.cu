@@ -2258,23 +2258,27 @@ void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_
         int* sweeps;
         QrPlan *p1, *p2;
     };
+    // Q1_t, Q2_t live from the QR phase to the basis products (one pair per trial);
+    // everything else is scratch of the trial's stream (trials t and t + S run one
+    // after the other on stream t % S), so memory grows by (m + n) Np per trial
     std::vector<Trial> tr(trials);
     for (int t = 0; t < trials; ++t) {
         const std::string tag = "b" + std::to_string(t) + "_";
+        const std::string sl = "bs" + std::to_string(t % S) + "_";
         Trial& x = tr[t];
-        x.T1 = dbuf(c, tag + "T1", (size_t)m * Np);
-        x.T2 = dbuf(c, tag + "T2", (size_t)n * Np);
         x.Q1 = dbuf(c, tag + "Q1", (size_t)m * Np);
         x.Q2 = dbuf(c, tag + "Q2", (size_t)n * Np);
-        x.Mk = dbuf(c, tag + "Mk", (size_t)Np * Np);
-        x.Uk = dbuf(c, tag + "Uk", (size_t)Np * Np);
-        x.Vk = dbuf(c, tag + "Vk", (size_t)Np * Np);
-        x.Sk = dbuf(c, tag + "Sk", (size_t)Np);
-        x.Uo = dbuf(c, tag + "Uo", (size_t)m * Np);
-        x.Vo = dbuf(c, tag + "Vo", (size_t)n * Np);
+        x.T1 = dbuf(c, sl + "T1", (size_t)m * Np);
+        x.T2 = dbuf(c, sl + "T2", (size_t)n * Np);
+        x.Mk = dbuf(c, sl + "Mk", (size_t)Np * Np);
+        x.Uk = dbuf(c, sl + "Uk", (size_t)Np * Np);
+        x.Vk = dbuf(c, sl + "Vk", (size_t)Np * Np);
+        x.Sk = dbuf(c, sl + "Sk", (size_t)Np);
+        x.Uo = dbuf(c, sl + "Uo", (size_t)m * Np);
+        x.Vo = dbuf(c, sl + "Vo", (size_t)n * Np);
         x.sweeps = reinterpret_cast<int*>(dbuf(c, tag + "sw", 1));
-        x.p1 = get_qr_plan(c, m, ell, 0, (tag + "T1").c_str());
-        x.p2 = get_qr_plan(c, n, ell, 0, (tag + "T2").c_str());
+        x.p1 = get_qr_plan(c, m, ell, 0, (sl + "T1").c_str());
+        x.p2 = get_qr_plan(c, n, ell, 0, (sl + "T2").c_str());
     }
     auto fork = [&]() {
         CK(cudaEventRecord(c->ev_fork, s));
