@@ -220,6 +220,8 @@ struct sorsvd_ctx {
     bool capturing = false;
     std::vector<double> host_omega;
     std::vector<double> host_psi2;  // tsr_svd's second test matrix (host draw)
+    double* om_pin = nullptr;       // host-buffer calls: page-locked Omega draw
+    size_t om_pin_n = 0;
     const int* pred = nullptr;  // predication of every launch (CholeskyQR2 vs Householder)
     int pred_skip = 0;
 };
@@ -3044,6 +3046,7 @@ void sorsvd_ctx_destroy(sorsvd_ctx* c) {
     for (auto& e : c->ev_h) cudaEventDestroy(e);
     for (auto& kv : c->sk_tables)
         for (int* d : kv.second.dev) cudaFree(d);
+    if (c->om_pin) cudaFreeHost(c->om_pin);
     for (cudaStream_t t : c->tstreams) cudaStreamDestroy(t);
     for (cudaEvent_t e : c->tevents) cudaEventDestroy(e);
     cudaStreamDestroy(c->side);
@@ -3091,11 +3094,32 @@ static void host_call(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const 
         double* dA = dbuf(c, "hostA", (abytes + 7) / 8);
         CK(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, c->stream));
         const double* dOm = nullptr;
+        sorsvd_desc dd = *d;
         if (omega && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
             double* p = dbuf(c, "hostOm", (size_t)d->n * d->ell);
             CK(cudaMemcpyAsync(p, omega, (size_t)d->n * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
             dOm = p;
+        } else if (method != SORSVD_TSR) {
+            // draw Omega = gaussian_matrix(n, ell, seed) (sketch.hpp:90) into a page-locked
+            // buffer while A's transfer runs, and upload it asynchronously right behind A (a
+            // pageable upload would stall the host behind A and then stage the copy); the call
+            // is synchronous, so the buffer is free again when it returns
+            const size_t cnt = (size_t)d->n * d->ell;
+            if (c->om_pin_n < cnt) {
+                if (c->om_pin) CK(cudaFreeHost(c->om_pin));
+                c->om_pin = nullptr;
+                CK(cudaHostAlloc(reinterpret_cast<void**>(&c->om_pin), cnt * sizeof(double), cudaHostAllocDefault));
+                c->om_pin_n = cnt;
+            }
+            c->host_omega.resize(cnt);
+            sorsvd_host::gaussian_fill(c->host_omega.data(), (uint64_t)cnt, d->seed, 0);
+            memcpy(c->om_pin, c->host_omega.data(), cnt * sizeof(double));
+            double* p = dbuf(c, "hostOm", cnt);
+            CK(cudaMemcpyAsync(p, c->om_pin, cnt * 8, cudaMemcpyHostToDevice, c->stream));
+            dOm = p;
+            dd.flags |= SORSVD_FLAG_OMEGA_GIVEN;
         }
+        d = &dd;
         const double* dPsi2 = nullptr;
         if (psi2 && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
             double* p = dbuf(c, "hostPsi2", (size_t)d->m * d->ell);
