@@ -3085,65 +3085,65 @@ int sorsvd_sor_svd_power_device(sorsvd_ctx* c, const sorsvd_desc* d, const void*
 // matrices) uploaded, U / sigma / V downloaded, all inside the timed call.
 static void host_call(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const double* omega, const double* psi2,
                       double* U, double* sigma, double* V, sorsvd_stats* st, int method) {
-        validate(d);
-        if (!A || !U || !sigma || !V) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
-        const size_t esz = d->dtype == SORSVD_F32 ? 4 : 8;
-        const size_t abytes = (size_t)d->m * d->lda * esz;
-        cudaEvent_t e0 = c->ev_h[0], e1 = c->ev_h[1], e2 = c->ev_h[2], e3 = c->ev_h[3];
-        CK(cudaEventRecord(e0, c->stream));
-        double* dA = dbuf(c, "hostA", (abytes + 7) / 8);
-        CK(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, c->stream));
-        const double* dOm = nullptr;
-        sorsvd_desc dd = *d;
-        if (omega && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
-            double* p = dbuf(c, "hostOm", (size_t)d->n * d->ell);
-            CK(cudaMemcpyAsync(p, omega, (size_t)d->n * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
-            dOm = p;
-        } else if (method != SORSVD_TSR) {
-            // draw Omega = gaussian_matrix(n, ell, seed) (sketch.hpp:90) into a page-locked
-            // buffer while A's transfer runs, and upload it asynchronously right behind A (a
-            // pageable upload would stall the host behind A and then stage the copy); the call
-            // is synchronous, so the buffer is free again when it returns
-            const size_t cnt = (size_t)d->n * d->ell;
-            if (c->om_pin_n < cnt) {
-                if (c->om_pin) CK(cudaFreeHost(c->om_pin));
-                c->om_pin = nullptr;
-                CK(cudaHostAlloc(reinterpret_cast<void**>(&c->om_pin), cnt * sizeof(double), cudaHostAllocDefault));
-                c->om_pin_n = cnt;
-            }
-            c->host_omega.resize(cnt);
-            sorsvd_host::gaussian_fill(c->host_omega.data(), (uint64_t)cnt, d->seed, 0);
-            memcpy(c->om_pin, c->host_omega.data(), cnt * sizeof(double));
-            double* p = dbuf(c, "hostOm", cnt);
-            CK(cudaMemcpyAsync(p, c->om_pin, cnt * 8, cudaMemcpyHostToDevice, c->stream));
-            dOm = p;
-            dd.flags |= SORSVD_FLAG_OMEGA_GIVEN;
+    validate(d);
+    if (!A || !U || !sigma || !V) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+    const size_t esz = d->dtype == SORSVD_F32 ? 4 : 8;
+    const size_t abytes = (size_t)d->m * d->lda * esz;
+    cudaEvent_t e0 = c->ev_h[0], e1 = c->ev_h[1], e2 = c->ev_h[2], e3 = c->ev_h[3];
+    CK(cudaEventRecord(e0, c->stream));
+    double* dA = dbuf(c, "hostA", (abytes + 7) / 8);
+    CK(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, c->stream));
+    const double* dOm = nullptr;
+    sorsvd_desc dd = *d;
+    if (omega && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+        double* p = dbuf(c, "hostOm", (size_t)d->n * d->ell);
+        CK(cudaMemcpyAsync(p, omega, (size_t)d->n * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
+        dOm = p;
+    } else if (method != SORSVD_TSR) {
+        // draw Omega = gaussian_matrix(n, ell, seed) (sketch.hpp:90) into a page-locked
+        // buffer while A's transfer runs, and upload it asynchronously right behind A (a
+        // pageable upload would stall the host behind A and then stage the copy); the call
+        // is synchronous, so the buffer is free again when it returns
+        const size_t cnt = (size_t)d->n * d->ell;
+        if (c->om_pin_n < cnt) {
+            if (c->om_pin) CK(cudaFreeHost(c->om_pin));
+            c->om_pin = nullptr;
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&c->om_pin), cnt * sizeof(double), cudaHostAllocDefault));
+            c->om_pin_n = cnt;
         }
-        d = &dd;
-        const double* dPsi2 = nullptr;
-        if (psi2 && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
-            double* p = dbuf(c, "hostPsi2", (size_t)d->m * d->ell);
-            CK(cudaMemcpyAsync(p, psi2, (size_t)d->m * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
-            dPsi2 = p;
-        }
-        CK(cudaEventRecord(e1, c->stream));
-        double* dU = dbuf(c, "hostU", (size_t)d->m * d->k);
-        double* dS = dbuf(c, "hostS", (size_t)d->k);
-        double* dV = dbuf(c, "hostV", (size_t)d->n * d->k);
-        sorsvd_stats local{};
-        sor_device(c, d, dA, dOm, dU, dS, dV, &local, method, dPsi2);
-        CK(cudaEventRecord(e2, c->stream));
-        CK(cudaMemcpyAsync(U, dU, (size_t)d->m * d->k * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(V, dV, (size_t)d->n * d->k * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(sigma, dS, (size_t)d->k * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaEventRecord(e3, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        float h2d = 0.f, d2h = 0.f;
-        CK(cudaEventElapsedTime(&h2d, e0, e1));
-        CK(cudaEventElapsedTime(&d2h, e2, e3));
-        local.ms_h2d = h2d;
-        local.ms_d2h = d2h;
-        if (st) *st = local;
+        c->host_omega.resize(cnt);
+        sorsvd_host::gaussian_fill(c->host_omega.data(), (uint64_t)cnt, d->seed, 0);
+        memcpy(c->om_pin, c->host_omega.data(), cnt * sizeof(double));
+        double* p = dbuf(c, "hostOm", cnt);
+        CK(cudaMemcpyAsync(p, c->om_pin, cnt * 8, cudaMemcpyHostToDevice, c->stream));
+        dOm = p;
+        dd.flags |= SORSVD_FLAG_OMEGA_GIVEN;
+    }
+    d = &dd;
+    const double* dPsi2 = nullptr;
+    if (psi2 && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
+        double* p = dbuf(c, "hostPsi2", (size_t)d->m * d->ell);
+        CK(cudaMemcpyAsync(p, psi2, (size_t)d->m * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
+        dPsi2 = p;
+    }
+    CK(cudaEventRecord(e1, c->stream));
+    double* dU = dbuf(c, "hostU", (size_t)d->m * d->k);
+    double* dS = dbuf(c, "hostS", (size_t)d->k);
+    double* dV = dbuf(c, "hostV", (size_t)d->n * d->k);
+    sorsvd_stats local{};
+    sor_device(c, d, dA, dOm, dU, dS, dV, &local, method, dPsi2);
+    CK(cudaEventRecord(e2, c->stream));
+    CK(cudaMemcpyAsync(U, dU, (size_t)d->m * d->k * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(V, dV, (size_t)d->n * d->k * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(sigma, dS, (size_t)d->k * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaEventRecord(e3, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float h2d = 0.f, d2h = 0.f;
+    CK(cudaEventElapsedTime(&h2d, e0, e1));
+    CK(cudaEventElapsedTime(&d2h, e2, e3));
+    local.ms_h2d = h2d;
+    local.ms_d2h = d2h;
+    if (st) *st = local;
 }
 
 int sorsvd_sor_svd_power(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const double* omega, double* U,

@@ -243,6 +243,19 @@ def test_config1_device_api_and_determinism(P, torch_mod, golden):
                            20, 0, 7), g["c1_s"], g["c1_u"], g["c1_v"])
 
 
+def test_host_api_equals_device_api(P, torch_mod):
+    # the host-buffer call draws Omega into a page-locked buffer and uploads it behind A; the
+    # device call draws it inside sor_device: the same bits either way (sketch.hpp:90)
+    A = O.gen_lowrank_decay(900, 700, 30, lambda j: 2.0 ** (-j / 3), 1e-6, 17)
+    h = P.sor_svd_power(A, 20, P.SketchConfig(24, 1, 31))
+    d = P.sor_svd_power(torch_mod.from_numpy(A).cuda(), 20, P.SketchConfig(24, 1, 31))
+    np.testing.assert_array_equal(h.sigma, d.sigma.cpu().numpy())
+    np.testing.assert_array_equal(h.u, d.u.cpu().numpy())
+    r = P.r_svd(A, 16, 1, 8)
+    rd = P.r_svd(torch_mod.from_numpy(A).cuda(), 16, 1, 8)
+    np.testing.assert_array_equal(r.sigma, rd.sigma.cpu().numpy())
+
+
 def test_explicit_omega_equals_seeded(P):
     A = O.gaussian_matrix(120, 90, 4)
     om = O.gaussian_matrix(90, 10, 55)
