@@ -9,7 +9,7 @@ for spec in "c2 0" "c2 1" "c3 0" "c3tf32 0"; do
   set -- $spec
   python tools/run_pass.py --config $1 --ta $2 --reps 2 > /dev/null 2>&1 || { echo "pass $1 failed"; continue; }
   rep=/tmp/pass_$1_ta$2
-  ncu --set full --clock-control none --import-source on -k regex:"gemm_f64_kernel|tc_gemm_tf32" -c 1 \
+  ncu -f --set full --clock-control none --import-source on -k regex:"gemm_f64_kernel|tc_gemm_tf32" -c 1 \
       -o $rep python tools/run_pass.py --config $1 --ta $2 --reps 1 > gpurun_out/ncu_pass_$1_ta$2.log 2>&1
   echo "ncu $1 ta=$2 rc=$?"
   ncu -i $rep.ncu-rep --page raw --csv > gpurun_out/ncu_pass_$1_ta$2_raw.csv 2>/dev/null
