@@ -210,3 +210,32 @@ def test_concurrent_contexts_thin_qr_deterministic(env):
             assert torch.equal(o, out[0])
     for c in ctxs:
         c.close()
+
+
+def test_sharded_approx_error_matches_single(env):
+    # approx_error over row-sharded A (each rank its row block of A and U): the sum of
+    # squares is reduced over ranks and equals the single-rank value
+    P, torch = env
+    A = O.gen_lowrank_decay(3000, 500, 30, lambda j: 2.0 ** (-j / 4), 1e-3, 77)
+    out, u = _run_sharded(P, torch, A, 16, P.SketchConfig(20, 1, 5), 3)
+    s, v = out[0].sigma.cpu().numpy(), out[0].v.cpu().numpy()
+    x = O.LowRankApprox(u, s, v, 0, 0, 16, 1, 5)
+    ref = O.approx_error(A, x)
+    g = P.EmuGroup(3)
+    ctxs = [P.Context(0, rank=r, emu_group=g) for r in range(3)]
+    blocks = np.array_split(np.arange(3000), 3)
+    res = [None] * 3
+
+    def work(r):
+        a, b = blocks[r][0], blocks[r][-1] + 1
+        xr = O.LowRankApprox(u[a:b], s, v, 0, 0, 16, 1, 5)
+        res[r] = P.approx_error(torch.from_numpy(np.ascontiguousarray(A[a:b])).cuda(), xr, ctx=ctxs[r])
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(3)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    for c in ctxs:
+        c.close()
+    g.close()
+    assert res[0] == res[1] == res[2]
+    assert abs(res[0] - ref) <= 1e-10 * ref
