@@ -522,14 +522,32 @@ __global__ void jacobi_p2p_kernel(JacobiArgs a) {
     __shared__ __align__(8) unsigned long long mbar[2][32];
     __shared__ int flag[3];
     __shared__ int s_sweeps;
+    // de Rijk-style start: the columns enter the ring sorted by decreasing norm (ties by
+    // index), which saves a sweep on graded cores (C2: 8 -> 7). perm[p] = the column of M
+    // at ring position p; V's rows are mapped back through it at the end.
+    __shared__ double cnorm[KPAD];
+    __shared__ int perm[KPAD];
+    for (int cidx = threadIdx.x; cidx < k; cidx += blockDim.x) {
+        double ss = 0.0;
+        for (int i = 0; i < k; ++i) ss = fma(a.M[(size_t)i * a.ldm + cidx], a.M[(size_t)i * a.ldm + cidx], ss);
+        cnorm[cidx] = ss;
+    }
+    __syncthreads();
+    for (int cidx = threadIdx.x; cidx < k; cidx += blockDim.x) {
+        int rk = 0;
+        for (int f = 0; f < k; ++f) rk += (cnorm[f] > cnorm[cidx]) || (cnorm[f] == cnorm[cidx] && f < cidx);
+        perm[rk] = cidx;
+    }
+    __syncthreads();
 
     if (active) {
         for (int h = 0; h < 2; ++h) {
             const int col = 2 * slot + h;
+            const int src = col < k ? perm[col] : 0;
             double* G = buf0 + (size_t)warp * SLOT + (size_t)h * 2 * KPAD;
             double* Vv = G + KPAD;
             for (int i = lane; i < KPAD; i += 32) {
-                G[i] = (col < k && i < k) ? a.M[(size_t)i * a.ldm + col] : 0.0;
+                G[i] = (col < k && i < k) ? a.M[(size_t)i * a.ldm + src] : 0.0;
                 Vv[i] = (col < k && i == col) ? 1.0 : 0.0;
             }
         }
@@ -714,7 +732,7 @@ __global__ void jacobi_p2p_kernel(JacobiArgs a) {
             const double sg = G[bi] < 0.0 ? -1.0 : 1.0;
             for (int i = lane; i < k; i += 32) {
                 a.U[(size_t)i * a.ldu + rk] = sv > 0.0 ? sg * G[i] / sv : 0.0;
-                a.V[(size_t)i * a.ldv + rk] = sg * Vv[i];
+                a.V[(size_t)perm[i] * a.ldv + rk] = sg * Vv[i];  // row i of V is ring position i
             }
             if (lane == 0) a.S[rk] = sv;
         }
