@@ -9,7 +9,8 @@
 //     y'  = y + mu (d - l - s')
 //     w'  = d - s' + y'/mu'   (next iteration's SOR-SVD input)
 //     res += (d - l - s')^2   (stopping test)
-// Traffic: read D, Y; write S, Y, W (40 B/entry). The residual is reduced
+// Traffic: read D, Y; write S, Y, W (40 B/entry). D and Y are loaded before the
+// rank-ell product so their latency hides behind it. The residual is reduced
 // deterministically (per-block partials, fixed-order final sum).
 #pragma once
 #include "common.cuh"
@@ -41,7 +42,7 @@ struct RpcaArgs {
     int pred_skip;
 };
 
-__global__ void __launch_bounds__(kRpcaThreads) rpca_update_kernel(RpcaArgs a) {
+__global__ void __launch_bounds__(kRpcaThreads, 2) rpca_update_kernel(RpcaArgs a) {
     if (a.pred && *a.pred == a.pred_skip) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
     const int64_t i0 = (int64_t)blockIdx.y * 64 + (warp >> 1) * 16;
@@ -52,6 +53,32 @@ __global__ void __launch_bounds__(kRpcaThreads) rpca_update_kernel(RpcaArgs a) {
     for (int x = 0; x < 2; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    // each lane's two columns are adjacent: 16-byte loads / stores of D, Y, S, W when the
+    // rows are 16-byte aligned (same arithmetic as the element path)
+    const bool vec = a.mode == 0 && ((a.ldd | a.ldx) & 1) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(a.D) | reinterpret_cast<uintptr_t>(a.S) |
+                       reinterpret_cast<uintptr_t>(a.Y) | reinterpret_cast<uintptr_t>(a.W)) & 15) == 0;
+    // D (into registers) and Y (cp.async into this thread's shared-memory slots) are
+    // issued before the factor loop, so their DRAM latency overlaps the L2-resident U/V
+    // fragment loads and the DMMA chain instead of following it. Registers for both
+    // would cost occupancy (142 regs -> 1 block per SM); this split keeps 2.
+    double2 dpre[2][4];
+    __shared__ double2 ysm[8][kRpcaThreads];
+    if (vec) {
+#pragma unroll
+        for (int fm = 0; fm < 2; ++fm) {
+            const int64_t i = i0 + fm * 8 + g;
+#pragma unroll
+            for (int fn = 0; fn < 4; ++fn) {
+                const int64_t j = j0 + fn * 8 + 2 * t4;
+                const bool ok = i < a.m && j + 1 < a.n;
+                dpre[fm][fn] = ok ? __ldcs(reinterpret_cast<const double2*>(a.D + i * a.ldd + j))
+                                  : make_double2(0.0, 0.0);
+                cp_async16(&ysm[fm * 4 + fn][threadIdx.x], ok ? a.Y + i * a.ldx + j : a.Y, ok ? 16 : 0);
+            }
+        }
+        cp_async_commit();
+    }
     for (int kk0 = 0; kk0 < a.k; kk0 += 4) {
         const int kk = kk0 + t4;
         const double z = kk < a.k ? fmax(a.sig[kk] - inv, 0.0) : 0.0;
@@ -72,12 +99,8 @@ __global__ void __launch_bounds__(kRpcaThreads) rpca_update_kernel(RpcaArgs a) {
             for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
     }
     double res = 0.0;
-    // each lane's two columns are adjacent: 16-byte loads / stores of D, Y, S, W when the
-    // rows are 16-byte aligned (same arithmetic as the element path)
-    const bool vec = a.mode == 0 && ((a.ldd | a.ldx) & 1) == 0 &&
-                     ((reinterpret_cast<uintptr_t>(a.D) | reinterpret_cast<uintptr_t>(a.S) |
-                       reinterpret_cast<uintptr_t>(a.Y) | reinterpret_cast<uintptr_t>(a.W)) & 15) == 0;
     if (vec) {
+        cp_async_wait<0>();  // own slots only: no block barrier needed
 #pragma unroll
         for (int fm = 0; fm < 2; ++fm) {
             const int64_t i = i0 + fm * 8 + g;
@@ -102,8 +125,8 @@ __global__ void __launch_bounds__(kRpcaThreads) rpca_update_kernel(RpcaArgs a) {
                     }
                     continue;
                 }
-                const double2 d2 = __ldcs(reinterpret_cast<const double2*>(a.D + i * a.ldd + j));
-                const double2 y2 = __ldcs(reinterpret_cast<const double2*>(a.Y + i * a.ldx + j));
+                const double2 d2 = dpre[fm][fn];
+                const double2 y2 = ysm[fm * 4 + fn][threadIdx.x];
                 double sv[2], yn[2], wv[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
