@@ -497,6 +497,29 @@ def test_rpca_c4_scaled_vs_oracle(P):
     assert np.linalg.norm(r.s - ro.s) <= 1e-9 * np.linalg.norm(ro.s)
 
 
+@pytest.mark.parametrize("m,n", [(1003, 131), (777, 64), (130, 66), (515, 300)])
+def test_rpca_ragged_vs_oracle(P, m, n):
+    # tiles cut at both edges (m, n not multiples of 64; odd n leaves a last single column
+    # in the 16-byte path of rpca_update_kernel)
+    D, _, _ = O.gen_c4(7, m=m, n=n)
+    mu0 = 1.25 / O.norm_spectral(D)
+    ocfg = O.RpcaConfig(lam=1 / np.sqrt(max(m, n)), mu0=mu0, ell=10, q=1, seed=5, max_iter=100)
+    ro = O.rpca_alm(D, ocfg)
+    r = P.rpca_alm(D, P.RpcaConfig(lam=ocfg.lam, mu0=mu0, ell=10, q=1, seed=5, max_iter=100))
+    assert r.iterations == ro.iterations and r.converged == ro.converged
+    assert r.rank_l == ro.rank_l and r.nnz_s == ro.nnz_s
+    assert np.linalg.norm(r.l - ro.l) <= 1e-9 * np.linalg.norm(ro.l)
+    assert np.linalg.norm(r.s - ro.s) <= 1e-9 * np.linalg.norm(ro.s)
+    if n % 2:  # device D with an even (padded) row stride: the 16-byte path with a ragged last column
+        import torch
+        buf = torch.zeros((m, n + 1), dtype=torch.float64, device="cuda")
+        buf[:, :n] = torch.from_numpy(D).cuda()
+        rd = P.rpca_alm(buf[:, :n], P.RpcaConfig(lam=ocfg.lam, mu0=mu0, ell=10, q=1, seed=5, max_iter=100))
+        assert rd.iterations == ro.iterations and rd.nnz_s == ro.nnz_s
+        assert np.linalg.norm(rd.l.cpu().numpy() - ro.l) <= 1e-9 * np.linalg.norm(ro.l)
+        assert np.linalg.norm(rd.s.cpu().numpy() - ro.s) <= 1e-9 * np.linalg.norm(ro.s)
+
+
 def test_rpca_zero_input(P):
     r = P.rpca_alm(np.zeros((30, 20)), P.RpcaConfig(ell=3, q=1, seed=1))
     assert r.iterations == 1 and r.converged and np.all(r.l == 0) and np.all(r.s == 0)
