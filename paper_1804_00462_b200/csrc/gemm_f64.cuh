@@ -350,4 +350,41 @@ __global__ void reduce_splits_kernel(const double* __restrict__ ws, int64_t coun
     }
 }
 
+// Few outputs, many splits (Gram matrices of the CholeskyQR gates, the n x ell TN
+// passes of C4): one warp per double2 output, lane l adds splits l, l+32, ... in
+// order (independent loads across lanes, S/32 dependent L2 trips instead of S/16),
+// then a fixed butterfly across the lanes. Deterministic for a given S.
+__global__ void reduce_splits_warp_kernel(const double* __restrict__ ws, int64_t count2, int S, int64_t stride,
+                                          double* __restrict__ out, const int* pred, int pred_skip) {
+    if (pred && *pred == pred_skip) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (i >= count2) return;
+    const double2* __restrict__ w2 = reinterpret_cast<const double2*>(ws);
+    const int64_t st2 = stride / 2;
+    double2 acc = make_double2(0.0, 0.0);
+    int s = lane;
+    for (; s + 96 < S; s += 128) {
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = w2[(int64_t)(s + 32 * u) * st2 + i];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            acc.x += v[u].x;
+            acc.y += v[u].y;
+        }
+    }
+    for (; s < S; s += 32) {
+        const double2 v = w2[(int64_t)s * st2 + i];
+        acc.x += v.x;
+        acc.y += v.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) reinterpret_cast<double2*>(out)[i] = acc;
+}
+
 }  // namespace sorsvd_dev

@@ -516,8 +516,14 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
     if (S > 1) {
         if (g.ldc % 2) throw Error{SORSVD_ERR_INTERNAL, "gemm: odd ldc with splits"};
         const int64_t count2 = g.M * g.ldc / 2;
-        const int blocks = (int)std::min<int64_t>(cdiv(count2, 256), (int64_t)c->num_sms * 8);
-        reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, g.M * g.ldc, g.C, c->pred, c->pred_skip);
+        if (S >= 32 && count2 <= 8192 && !getenv("SORSVD_REDUCE_SERIAL")) {
+            const int blocks = (int)cdiv(count2 * 32, 256);
+            reduce_splits_warp_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, g.M * g.ldc, g.C, c->pred,
+                                                             c->pred_skip);
+        } else {
+            const int blocks = (int)std::min<int64_t>(cdiv(count2, 256), (int64_t)c->num_sms * 8);
+            reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, g.M * g.ldc, g.C, c->pred, c->pred_skip);
+        }
         check_launch(c);
     }
 }
