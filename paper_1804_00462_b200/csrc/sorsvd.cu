@@ -366,9 +366,13 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         // tiny outputs (Gram matrices of the CholeskyQR gates, C1 / C4 shapes): the split
         // reduction is a chain of dependent L2 round trips (16 partials per trip in
         // reduce_splits_kernel), ~48 K-rows each, not a bandwidth term
-        const double trip = (g.M * g.N <= 4096) ? 3.0 : 0.0;  // 16 partials per trip
+        // (reduce_splits_warp_kernel from 32 splits: 128 partials per trip; 1.0 measured
+        // best of 3.0 / 1.0 / 0.375: C4 solve 9.21 / 8.89 / 8.87 ms, C1 call 0.323 / 0.312 / 0.319 ms)
+        static const double trip_w = getenv("SORSVD_TRIP_W") ? atof(getenv("SORSVD_TRIP_W")) : 1.0;
+        const bool tiny = g.M * g.N <= 4096;
         for (int64_t cand = 1; cand <= maxS; ++cand) {
             const double waves = (double)cdiv(base * cand, c->num_sms);
+            const double trip = tiny ? (cand >= 32 ? trip_w : 3.0) : 0.0;
             const double cost = waves * ((double)g.K / cand + 96.0) +
                                 (cand > 1 ? 0.02 * cand * g.M * g.N / (double)c->num_sms + trip * cand : 0.0);
             if (cost < best * 0.999) {
