@@ -2,7 +2,13 @@
 """SOR-SVD benchmark (BASELINE.json metric: SOR-SVD wall time & effective
 GFLOP/s = 2*m*n*ell*passes / time, vs roofline, on 1/2/4/8 B200).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Default workload: C3 fp64 (BASELINE.json configs[2], the 1/2/4/8-GPU config the
+metric is quoted on; strong-scaled: the same 200000 x 20000 A split by rows).
+`--gpus N` with no torchrun environment re-launches this script under
+torch.distributed.run with N ranks (one per GPU); under torchrun WORLD_SIZE
+must equal N.
 
 One JSON line on rank 0. "ours": A and Omega resident in HBM, K timed calls of
 sor_svd_power through the C ABI (CUDA events, L2 flushed between steps, max
@@ -33,10 +39,10 @@ CONFIGS = {
     # BASELINE.json configs[0]
     "c1": dict(m=1000, n=1000, k=20, q=0, scaling="weak",
                desc="C1 fp64 m=n=1000 k=ell=20 q=0, A = X Y^T + N(0,1e-4)"),
-    # BASELINE.json configs[1] (default workload)
+    # BASELINE.json configs[1]
     "c2": dict(m=4000, n=4000, k=100, q=1, scaling="weak",
                desc="C2 fp64 m=n=4000 k=ell=100 q=1, A = U diag(j^-2) V^T (Haar U, V)"),
-    # BASELINE.json configs[2], fp64 variant
+    # BASELINE.json configs[2], fp64 variant (default workload)
     "c3": dict(m=200000, n=20000, k=256, q=1, scaling="strong",
                desc="C3 fp64 m=200000 n=20000 k=ell=256 q=1, A = X diag(10^(-j/64)) Y^T + N(0,1e-6)"),
     # BASELINE.json configs[2], fp32 variant: A stored in FP32, passes in FP64 arithmetic (default fp32_mode)
@@ -62,7 +68,7 @@ def log(*a):
 
 
 # --------------------------------------------------------------- data -----
-def make_matrix(cfg_name, m_local, n, rank, world, device):
+def make_matrix(cfg_name, m_local, n, rank, world, device, row0=0):
     import torch
     g = torch.Generator(device=device)
     f64 = torch.float64
@@ -93,37 +99,30 @@ def make_matrix(cfg_name, m_local, n, rank, world, device):
         vals = -50.0 + 100.0 * torch.rand(nnz, generator=g, device=device, dtype=f64)
         d.view(-1)[idx] += vals
         return d
-    if cfg_name in ("c5", "c5tf32"):
-        mg = CONFIGS["c5"]["m"]
-        g.manual_seed(1000 + rank)
-        x = torch.randn(m_local, 512, generator=g, device=device, dtype=f64) / math.sqrt(mg)
+    if cfg_name in ("c5", "c5tf32", "c3", "c3f32", "c3tf32"):
+        # the global A is the same for every rank count (strong scaling): X's rows and the
+        # noise come from fixed 4096-row chunks seeded by the chunk's global index, and each
+        # rank materialises the chunks that overlap its row block [row0, row0 + m_local)
+        c5 = cfg_name.startswith("c5")
+        mg, r = (CONFIGS["c5"]["m"], 512) if c5 else (CONFIGS["c3"]["m"], 256)
+        noise = 1e-4 if c5 else 1e-3
+        s = (1.0 / torch.arange(1, r + 1, device=device, dtype=f64) if c5
+             else 10.0 ** (-torch.arange(1, r + 1, device=device, dtype=f64) / 64.0))
         g.manual_seed(2000)
-        y = torch.randn(n, 512, generator=g, device=device, dtype=f64) / math.sqrt(n)
-        s = 1.0 / torch.arange(1, 513, device=device, dtype=f64)
-        a = torch.empty(m_local, n, device=device, dtype=torch.float32)
-        g.manual_seed(3000 + rank)
-        step = 4096
+        y = torch.randn(n, r, generator=g, device=device, dtype=f64) / math.sqrt(n)
         ys = (y * s).T.contiguous()
-        for i in range(0, m_local, step):
-            j = min(m_local, i + step)
-            blk = x[i:j] @ ys
-            blk += 1e-4 * torch.randn(j - i, n, generator=g, device=device, dtype=f64)
-            a[i:j] = blk.to(torch.float32)
-            del blk
-        return a
-    if cfg_name in ("c3", "c3f32", "c3tf32"):
-        mg = CONFIGS["c3"]["m"]
-        g.manual_seed(1000 + rank)
-        x = torch.randn(m_local, 256, generator=g, device=device, dtype=f64) / math.sqrt(mg)
-        g.manual_seed(2000)
-        y = torch.randn(n, 256, generator=g, device=device, dtype=f64) / math.sqrt(n)
-        s = 10.0 ** (-torch.arange(1, 257, device=device, dtype=f64) / 64.0)
-        a = torch.empty(m_local, n, device=device, dtype=torch.float32 if cfg_name != "c3" else f64)
-        g.manual_seed(3000 + rank)
-        step = 8192
-        for i in range(0, m_local, step):
-            j = min(m_local, i + step)
-            a[i:j] = ((x[i:j] * s) @ y.T + 1e-3 * torch.randn(j - i, n, generator=g, device=device, dtype=f64)).to(a.dtype)
+        out_dt = f64 if cfg_name == "c3" else torch.float32
+        a = torch.empty(m_local, n, device=device, dtype=out_dt)
+        step = 4096
+        for c0 in range((row0 // step) * step, row0 + m_local, step):
+            c1 = min(c0 + step, mg)
+            g.manual_seed(1_000_000 + c0 // step)
+            x = torch.randn(c1 - c0, r, generator=g, device=device, dtype=f64) / math.sqrt(mg)
+            blk = x @ ys
+            blk += noise * torch.randn(c1 - c0, n, generator=g, device=device, dtype=f64)
+            lo, hi = max(c0, row0), min(c1, row0 + m_local)
+            a[lo - row0:hi - row0] = blk[lo - c0:hi - c0].to(out_dt)
+            del blk, x
         return a
     raise ValueError(cfg_name)
 
@@ -351,35 +350,95 @@ def run_rpca_reference(args, cfg, workload, O):
     return 0
 
 
+# ------------------------------------------------------------ launcher --
+def relaunch(n):
+    """`--gpus N` outside torchrun: one rank per GPU under torch.distributed.run
+    (rendezvous on 127.0.0.1), same arguments; returns the launcher's exit code."""
+    import socket
+    import subprocess
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    # NCCL's init lines (one per rank) on stderr, so the rank count is visible in the log
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log("bench.py: launching " + " ".join(cmd[1:]))
+    return subprocess.call(cmd, env=env)
+
+
+def plan_only(args, cfg, workload, rank, world, local_rank, m_local, row0):
+    """The multi-rank plumbing without device work: process group (NCCL on
+    GPUs, gloo otherwise), the row partition and the max-over-ranks reduction;
+    rank 0 prints the plan as one JSON line."""
+    import torch
+    from paper_1804_00462_b200 import dist as Dm
+    dist = None
+    cuda = torch.cuda.is_available()
+    dev = torch.device("cuda", local_rank) if cuda else None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if cuda else "gloo")
+    rows = [[row0, m_local]]
+    if dist:
+        t = torch.tensor([row0, m_local], dtype=torch.int64, device=dev)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        rows = [[int(x[0]), int(x[1])] for x in allt]
+    slowest = Dm.max_over_ranks(dist, float(rank), dev)
+    if rank == 0:
+        print(json.dumps({"plan": True, "n_gpus": world, "config": workload, "rank_rows": rows,
+                          "max_over_ranks_check": slowest}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------------ main --
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="launch the ranks, partition the rows, exchange ids and time nothing (CPU-testable)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+        return 2
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     k = ell = cfg["k"]
     q = cfg["q"]
     passes = 2 * q + 3
     from paper_1804_00462_b200.dist import row_partition
+    row0 = 0
     if cfg["scaling"] == "weak":
         m_local, m_global = cfg["m"], cfg["m"] * world
+        row0 = rank * m_local
     else:
         m_global = cfg["m"]
-        m_local = row_partition(m_global, world, rank)[1]
+        row0, m_local = row_partition(m_global, world, rank)
     n = cfg["n"]
     workload = dict(workload=cfg["desc"], m=m_global, n=n, k=k, ell=ell, q=q, passes=passes,
                     rows_per_rank=m_local, parallelism=f"row-sharded x{world}" if world > 1 else "single GPU",
                     l2="flushed between timed steps (256 MiB write)")
+
+    if args.plan_only:
+        return plan_only(args, cfg, workload, rank, world, local_rank, m_local, row0)
 
     if args.impl == "reference":
         if rank != 0:
@@ -432,11 +491,13 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
     ctx = D.make_context(dist, local_rank, rank, world, device)
+    log(f"[rank {rank}/{world}] cuda:{local_rank} library context up"
+        + (" (NCCL communicator over NVLink)" if world > 1 else "") + f"; rows [{row0}, {row0 + m_local}) of {m_global}")
     stream = torch.cuda.current_stream(device)
     ctx.set_stream(stream.cuda_stream)
 
     t_gen = time.perf_counter()
-    A = make_matrix(args.config, m_local, n, rank, world, device)
+    A = make_matrix(args.config, m_local, n, rank, world, device, row0=row0)
     torch.cuda.synchronize()
     log(f"[rank {rank}] generated {m_local}x{n} fp64 in {time.perf_counter() - t_gen:.1f}s")
     if cfg.get("kind") == "rpca":

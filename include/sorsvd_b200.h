@@ -74,7 +74,7 @@ typedef struct sorsvd_desc {
     int32_t q;        /* power iterations */
     int32_t single_pass; /* SketchConfig::single_pass: M_approx core, 2q+2 passes (sketch.hpp:100-104) */
     uint64_t seed;    /* Omega = gaussian_matrix(n, ell, seed) unless OMEGA_GIVEN */
-    int32_t dtype;    /* sorsvd_dtype of A (SORSVD_F64 only in this build) */
+    int32_t dtype;    /* sorsvd_dtype of A: SORSVD_F64, or SORSVD_F32 (FP32 storage; see SORSVD_FLAG_TF32) */
     uint32_t flags;
     int64_t m_global; /* total rows over all ranks (0 -> m) */
 } sorsvd_desc;
@@ -104,6 +104,14 @@ int sorsvd_ctx_create(int device, sorsvd_ctx** out);
 int sorsvd_nccl_unique_id(void* out128);
 int sorsvd_ctx_create_dist(int device, int rank, int world, const void* unique_id128, sorsvd_ctx** out);
 void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
+/* Per-context algorithm options (defaults are the tuned choices; tests use
+ * these to cross-check kernel variants against each other). */
+#define SORSVD_OPT_JACOBI 1          /* value: sorsvd_jacobi_variant */
+#define SORSVD_OPT_SORD_CHUNK_MB 2   /* value: staging chunk of the SORD loader, MiB (default 64) */
+#define SORSVD_JACOBI_AUTO 0         /* by k: CTA / point-to-point ring / barrier ring / rotation log */
+#define SORSVD_JACOBI_BARRIER 1      /* barrier cluster ring instead of the point-to-point ring */
+#define SORSVD_JACOBI_ROTLOG 2       /* the k > 256 rotation-log kernel at any k >= 8 */
+int sorsvd_ctx_set_option(sorsvd_ctx* ctx, int32_t key, int64_t value);
 /* In-process emulation of `world` ranks on one device (tests): one context
  * per rank, each driven by its own host thread; collectives become host
  * barriers plus device sums. Same schedule as the NCCL path, graphs off. */

@@ -184,6 +184,14 @@ class Context:
     def set_stream(self, stream_ptr: int):
         _check(C.lib().sorsvd_set_stream(self._h, ctypes.c_void_p(stream_ptr)), self._h)
 
+    # sorsvd_ctx_set_option keys / Jacobi variants (include/sorsvd_b200.h)
+    OPT_JACOBI, OPT_SORD_CHUNK_MB = 1, 2
+    JACOBI_AUTO, JACOBI_BARRIER, JACOBI_ROTLOG = 0, 1, 2
+
+    def set_option(self, key: int, value: int):
+        """Per-context algorithm option (tests cross-check kernel variants with it)."""
+        _check(C.lib().sorsvd_ctx_set_option(self._h, int(key), int(value)), self._h)
+
     def close(self):
         if getattr(self, "_h", None):
             C.lib().sorsvd_ctx_destroy(self._h)

@@ -69,6 +69,7 @@ SIGNATURES = [
     ("sorsvd_ctx_create_emulated", c_i32, [ctypes.c_int, ctypes.c_int, c_vp, ctypes.POINTER(c_vp)]),
     ("sorsvd_last_error", ctypes.c_char_p, [c_vp]),
     ("sorsvd_set_stream", c_i32, [c_vp, c_vp]),
+    ("sorsvd_ctx_set_option", c_i32, [c_vp, c_i32, c_i64]),
     ("sorsvd_ctx_rank", c_i32, [c_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("sorsvd_sor_svd_power", c_i32, [c_vp, ctypes.POINTER(SorsvdDesc), c_vp, c_dp, c_dp, c_dp, c_dp,
                                      ctypes.POINTER(SorsvdStats)]),

@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(256) trsm_rows_kernel(const double* __restrict
                                                         const double* __restrict__ Rjj, int ldr, int nb,
                                                         double* __restrict__ X, int64_t ldx, int64_t rows,
                                                         const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     __shared__ double Rs[kCholcB][kCholcB + 1];
     for (int e = threadIdx.x; e < kCholcB * kCholcB; e += blockDim.x) {
         const int i = e / kCholcB, j = e - i * kCholcB;
@@ -278,10 +278,20 @@ __global__ void set_identity_kernel(double* __restrict__ R, int ldr, int k) {
     }
 }
 
+// Big-QR flags at the start of a call: [0] breakdown = 0, [1] done = 0, or
+// done = kPredDead when the enclosing launch predicate is off (every pass of
+// the QR then skips, including the carry-through copies).
+__global__ void qr_flags_init_kernel(int* flags, const int* outer, int outer_skip) {
+    if (threadIdx.x == 0) {
+        flags[0] = 0;
+        flags[1] = pred_off(outer, outer_skip) ? kPredDead : 0;
+    }
+}
+
 // dst = src (rows x cols, pitches in doubles) when *pred != pred_skip.
 __global__ void copy_rows_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst, int64_t ldd,
                                  int64_t rows, int cols, const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     const int64_t total = rows * cols;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / cols, j = e - i * cols;
@@ -294,7 +304,7 @@ __global__ void copy_rows_kernel(const double* __restrict__ src, int64_t lds, do
 // Lower part of Rinv zeroed; Rinv padded columns are left untouched.
 __global__ void trinv_kernel(const double* __restrict__ R, int ldr, int k, double* __restrict__ Ri, int ldi,
                              const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     extern __shared__ double xs[];  // [warps][k]
     const int wpb = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x * wpb + warp;

@@ -39,6 +39,8 @@ struct CholArgs {
     int ldo;
     double* Rf;        // pass 1: this pass's R (k x ldf, upper), optional
     int ldf;
+    const int* outer;  // enclosing launch predicate (optional): when off, pass 1 marks *flag dead
+    int outer_skip;
 };
 
 __global__ void __launch_bounds__(kCholThreads, 1) chol_inv_kernel(CholArgs a) {
@@ -46,7 +48,11 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_inv_kernel(CholArgs a) {
     __shared__ int s_bad;
     __shared__ double s_piv[2];
     const int k = a.k, tid = threadIdx.x;
-    if (a.pass == 2 && *a.flag != 0) return;  // pass 1 already rejected
+    if (pred_off(a.outer, a.outer_skip)) {  // enclosing iteration skipped: both QR paths skip too
+        if (a.pass == 1 && tid == 0) *a.flag = kPredDead;
+        return;
+    }
+    if (a.pass == 2 && *a.flag != 0) return;  // pass 1 already rejected (or the flag is dead)
     const bool in_smem = (size_t)k * k * sizeof(double) <= kCholSmemBytes;
     double* L = in_smem ? smc : a.work;  // row-major k x k, lower triangle holds R^T
     if (tid == 0) s_bad = 0;

@@ -7,6 +7,17 @@ namespace sorsvd_dev {
 
 constexpr int kWarp = 32;
 
+// Launch predication. A kernel given (pred, skip) is a no-op when *pred == skip
+// (CholeskyQR2 accepted / rejected, RPCA converged) or when *pred == kPredDead:
+// a QR whose enclosing RPCA iteration is predicated off marks its inner flag
+// dead, so both of its paths skip (predicates stack instead of replacing).
+constexpr int kPredDead = 2;
+__device__ __forceinline__ bool pred_off(const int* p, int skip) {
+    if (!p) return false;
+    const int v = *p;
+    return v == skip || v == kPredDead;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

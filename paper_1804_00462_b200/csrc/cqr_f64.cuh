@@ -78,7 +78,7 @@ struct ColGroup {
 };
 
 __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
-    if (a.pred && *a.pred == a.pred_skip) return;  // uniform over the cluster
+    if (pred_off(a.pred, a.pred_skip)) return;  // uniform over the cluster
     cg::cluster_group cl = cg::this_cluster();
     const int C = (int)cl.num_blocks();
     const int r = (int)cl.block_rank();
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kCqrThreads, 1) cqr_kernel(CqrArgs a) {
 __global__ void wy_prep_kernel(const double* __restrict__ G, int ldg, const double* __restrict__ tau,
                                const double* __restrict__ sgn, const double* __restrict__ V, int64_t ldv, int k,
                                double* __restrict__ U, double* __restrict__ B, int ld, const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
         const int i = e / k, j = e - i * k;
         double u = 0.0;
@@ -438,7 +438,7 @@ __global__ void wy_prep_kernel(const double* __restrict__ G, int ldg, const doub
 // Q(c, c) += sgn[c] for c < k (the E diag(sgn) term of the compact-WY Q).
 __global__ void wy_diag_kernel(double* __restrict__ Q, int64_t ldq, const double* __restrict__ sgn, int k,
                                const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     for (int c = threadIdx.x; c < k; c += blockDim.x) Q[(size_t)c * ldq + c] += sgn[c];
 }
 
@@ -458,7 +458,7 @@ __host__ __device__ constexpr int cqr_reg_maxt(int CH) {
 
 template <int CH>
 __global__ void __launch_bounds__(cqr_reg_maxt(CH), 1) cqr_reg_kernel(CqrArgs a) {
-    if (a.pred && *a.pred == a.pred_skip) return;
+    if (pred_off(a.pred, a.pred_skip)) return;
     cg::cluster_group cl = cg::this_cluster();
     const int C = (int)cl.num_blocks();
     const int r = (int)cl.block_rank();
@@ -667,7 +667,7 @@ __host__ __device__ inline size_t cqr_reg_smem_bytes(int Rb, int k, int CH) {
 // runs on k rows and yields Q = I up to signs, which is what we want).
 __global__ void stack_r_kernel(const double* __restrict__ Rin, int nin, int k, int ldr, double* __restrict__ out,
                                int ldo, const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     const int node = blockIdx.x;
     const int a = 2 * node, bq = 2 * node + 1;
     for (int e = threadIdx.x; e < 2 * k * k; e += blockDim.x) {

@@ -245,7 +245,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& p, unsigned char* smem
 template <int FM, int FN, bool TA, bool V16, typename AT = double>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
     using S = GemmShape<FM, FN, TA, AT>;
-    if (p.pred && *p.pred == p.pred_skip) return;
+    if (pred_off(p.pred, p.pred_skip)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     if (p.sk_cta_seg) {  // stream-K
         const int g0 = p.sk_cta_seg[blockIdx.x], g1 = p.sk_cta_seg[blockIdx.x + 1];
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
 __global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* __restrict__ tile_seg0,
                                      const int* __restrict__ split_tiles, int nsplit, int BM, int BN, int gy,
                                      int64_t M, double* __restrict__ C, int64_t ldc, const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     const int per = BM * BN;  // one tile's elements (< 2^31)
     for (int st = blockIdx.y; st < nsplit; st += gridDim.y) {
         const int tile = split_tiles[st];
@@ -324,7 +324,7 @@ __global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* _
 // many splits and few outputs (K = m reductions) the loop is L2-latency bound.
 __global__ void reduce_splits_kernel(const double* __restrict__ ws, int64_t count2, int S, int64_t stride,
                                      double* __restrict__ out, const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     const int64_t n2 = count2;
     const double2* __restrict__ w2 = reinterpret_cast<const double2*>(ws);
     const int64_t st2 = stride / 2;
@@ -356,7 +356,7 @@ __global__ void reduce_splits_kernel(const double* __restrict__ ws, int64_t coun
 // then a fixed butterfly across the lanes. Deterministic for a given S.
 __global__ void reduce_splits_warp_kernel(const double* __restrict__ ws, int64_t count2, int S, int64_t stride,
                                           double* __restrict__ out, const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     const int lane = threadIdx.x & 31;
     const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (i >= count2) return;

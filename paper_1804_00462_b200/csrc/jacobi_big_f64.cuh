@@ -43,6 +43,8 @@ struct JacobiBigArgs {
     double* tlog;     // [round][P] tangents
     int max_sweeps;
     int* info;        // [0] sweeps, [1] rounds
+    const int* pred;  // optional predication (see JacobiArgs)
+    int pred_skip;
 };
 
 // Column id held by ring position (slot, h) after `t_mod` shifts (t mod (2P-1)).
@@ -220,6 +222,7 @@ __device__ __forceinline__ void jb_recv(double (&dst)[KP], const double* src) {
 // each lane's pairs are contiguous and a column moves as 16-byte st.async.
 template <int KP>
 __global__ void __launch_bounds__(kJbWarps * 32, 1) jacobi_big_kernel(JacobiBigArgs a) {
+    if (pred_off(a.pred, a.pred_skip)) return;  // uniform over the cluster
     static_assert(KP % 2 == 0, "KP must be even");
     cgb::cluster_group cl = cgb::this_cluster();
     const int C = (int)cl.num_blocks();

@@ -38,6 +38,8 @@ struct JacobiArgs {
     int ppc;          // pair slots (= warps) per CTA
     int max_sweeps;
     int* sweeps_out;  // optional
+    const int* pred;  // optional: no-op when pred_off(pred, pred_skip) (RPCA iteration after convergence)
+    int pred_skip;
 };
 
 // smem per CTA (doubles): 2 buffers x ppc slots x 2 columns x (G, V) x kpad
@@ -66,6 +68,7 @@ __device__ __forceinline__ void jac_rotation(double al, double be, double ga, do
 
 template <int KP>
 __global__ void jacobi_cluster_kernel(JacobiArgs a) {
+    if (pred_off(a.pred, a.pred_skip)) return;  // uniform over the cluster
     cgj::cluster_group cl = cgj::this_cluster();
     const int C = (int)cl.num_blocks();
     const int r = (int)cl.block_rank();
@@ -299,6 +302,7 @@ __device__ __forceinline__ void jac_round_pair(int r, int i, int kk, int& p, int
 
 template <int KP, int PPW>
 __global__ void __launch_bounds__(PPW == 1 ? 1024 : 512, 1) jacobi_cta_kernel(JacobiArgs a) {
+    if (pred_off(a.pred, a.pred_skip)) return;  // uniform over the cluster
     const int k = a.k;
     const int kk = (k + 1) & ~1;
     const int P = kk / 2;
@@ -499,6 +503,7 @@ __host__ __device__ inline size_t jacobi_p2p_smem_bytes(int KP, int ppc) {
 
 template <int KP>
 __global__ void jacobi_p2p_kernel(JacobiArgs a) {
+    if (pred_off(a.pred, a.pred_skip)) return;  // uniform over the cluster
     static_assert(KP == 2 || KP == 4, "pairs of elements per lane; selected for k <= 128");
     constexpr int KPAD = 32 * KP;
     constexpr int H = KP / 2;
@@ -530,7 +535,9 @@ __global__ void jacobi_p2p_kernel(JacobiArgs a) {
     for (int cidx = threadIdx.x; cidx < k; cidx += blockDim.x) {
         double ss = 0.0;
         for (int i = 0; i < k; ++i) ss = fma(a.M[(size_t)i * a.ldm + cidx], a.M[(size_t)i * a.ldm + cidx], ss);
-        cnorm[cidx] = ss;
+        // NaN keys (non-finite M) sort last: the comparisons below then still give every
+        // column a distinct rank, so perm stays a permutation (no stray row index)
+        cnorm[cidx] = ss >= 0.0 ? ss : -1.0;
     }
     __syncthreads();
     for (int cidx = threadIdx.x; cidx < k; cidx += blockDim.x) {

@@ -43,7 +43,7 @@ struct RpcaArgs {
 };
 
 __global__ void __launch_bounds__(kRpcaThreads, 2) rpca_update_kernel(RpcaArgs a) {
-    if (a.pred && *a.pred == a.pred_skip) return;
+    if (pred_off(a.pred, a.pred_skip)) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
     const int64_t i0 = (int64_t)blockIdx.y * 64 + (warp >> 1) * 16;
     const int64_t j0 = (int64_t)blockIdx.x * 64 + (warp & 1) * 32;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kRpcaThreads, 2) rpca_update_kernel(RpcaArgs a
 // Deterministic single-block reduction of partials: out[0] = sum, (sqrt into out[1]).
 __global__ void sum_partials_kernel(const double* __restrict__ p, int64_t n, double* out, const int* pred = nullptr,
                                     int pred_skip = 0) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     __shared__ double red[32];
     double t = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) t += p[i];
@@ -215,7 +215,7 @@ __global__ void sum_partials_kernel(const double* __restrict__ p, int64_t n, dou
 // ||D - L - S||_F / ||D||_F. Predicated like the iteration itself.
 __global__ void rpca_check_kernel(const double* __restrict__ tot, double dnorm, double tol, int it, int* st,
                                   double* rel, const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     const double r = sqrt(tot[0]) / dnorm;
     rel[0] = r;
     st[1] = it + 1;

@@ -195,7 +195,8 @@ struct sorsvd_emu_group {
 };
 
 struct sorsvd_ctx {
-    long long* cqr_prof = nullptr;  // tools only (SORSVD_CQR_PROF)
+    int opt_jacobi = SORSVD_JACOBI_AUTO;  // sorsvd_ctx_set_option(SORSVD_OPT_JACOBI)
+    int64_t opt_sord_chunk_mb = 64;       // sorsvd_ctx_set_option(SORSVD_OPT_SORD_CHUNK_MB)
     int device = 0;
     int rank = 0, world = 1;
     int num_sms = 148;
@@ -368,7 +369,7 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         // reduce_splits_kernel), ~48 K-rows each, not a bandwidth term
         // (reduce_splits_warp_kernel from 32 splits: 128 partials per trip; 1.0 measured
         // best of 3.0 / 1.0 / 0.375: C4 solve 9.21 / 8.89 / 8.87 ms, C1 call 0.323 / 0.312 / 0.319 ms)
-        static const double trip_w = getenv("SORSVD_TRIP_W") ? atof(getenv("SORSVD_TRIP_W")) : 1.0;
+        constexpr double trip_w = 1.0;
         const bool tiny = g.M * g.N <= 4096;
         for (int64_t cand = 1; cand <= maxS; ++cand) {
             const double waves = (double)cdiv(base * cand, c->num_sms);
@@ -391,14 +392,13 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
     // split-K: a stream-K tile spread over ~all SMs has a fix-up that is
     // a chain of ~num_sms / 16 dependent L2 round trips per element
     const bool tiny_out = g.M * g.N <= 4096;
-    if (!g.tile_row0 && g.force_splits == 0 && !getenv("SORSVD_NO_STREAMK") && tiles < (int64_t)c->num_sms &&
+    if (!g.tile_row0 && g.force_splits == 0 && tiles < (int64_t)c->num_sms &&
         units >= 16 && !tiny_out) {
         const int64_t n = c->num_sms;
         const double sk_cost = (double)cdiv(tiles * units, n) * BK + 2 * 96.0 + 0.02 * 3 * g.M * g.N / (double)n;
         const double cur_cost = (double)cdiv(tiles * S, n) * ((double)g.K / S + 96.0) +
                                 (S > 1 ? 0.02 * S * g.M * g.N / (double)n : 0.0);
         streamk = sk_cost < g.sk_bias * cur_cost;
-        if (const char* e = getenv("SORSVD_STREAMK")) streamk = atoi(e) != 0;  // experiments
     }
     GemmArgs a{};
     a.A = g.Af ? static_cast<const void*>(g.Af) : static_cast<const void*>(g.A);
@@ -520,7 +520,7 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
     if (S > 1) {
         if (g.ldc % 2) throw Error{SORSVD_ERR_INTERNAL, "gemm: odd ldc with splits"};
         const int64_t count2 = g.M * g.ldc / 2;
-        if (S >= 32 && count2 <= 8192 && !getenv("SORSVD_REDUCE_SERIAL")) {
+        if (S >= 32 && count2 <= 8192) {
             const int blocks = (int)cdiv(count2 * 32, 256);
             reduce_splits_warp_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, g.M * g.ldc, g.C, c->pred,
                                                              c->pred_skip);
@@ -787,13 +787,7 @@ void launch_cqr(sorsvd_ctx* c, const CqrArgs& a0, int nblocks, int rows_max, int
     CqrArgs a = a0;
     a.pred = c->pred;
     a.pred_skip = c->pred_skip;
-    if (getenv("SORSVD_CQR_PROF")) {  // tools/prof_cqr.py: per-step clock stamps
-        static long long* dprof = nullptr;
-        if (!dprof) CK(cudaMalloc(&dprof, 6 * 512 * sizeof(long long)));
-        a.prof = dprof;
-        c->cqr_prof = dprof;
-    }
-    const RegCfg rc = (getenv("SORSVD_CQR_SMEM") || a.wy) ? RegCfg{} : cqr_reg_choose(a.k, rows_max, kCqrMaxCluster);
+    const RegCfg rc = a.wy ? RegCfg{} : cqr_reg_choose(a.k, rows_max, kCqrMaxCluster);
     if (rc.ch) {
         const int Rb = (int)cdiv(rows_max, rc.csize);
         switch (rc.ch) {
@@ -895,9 +889,8 @@ QrPlan* get_qr_plan(sorsvd_ctx* c, int64_t rows, int k, int leaves_given, const 
     } else {
         // the per-reflector latency (cluster reduction) dominates, so the
         // fewest tree levels win: leaves as large as either kernel can hold
-        const int64_t reg_cap = getenv("SORSVD_CQR_SMEM") ? 0 : cqr_reg_capacity(k, kCqrMaxCluster);
+        const int64_t reg_cap = cqr_reg_capacity(k, kCqrMaxCluster);
         int64_t leaf_max = std::max<int64_t>(reg_cap, (int64_t)p->cmax * p->rb_max);
-        if (getenv("SORSVD_QR_LEAF_CTA")) leaf_max = std::max<int64_t>(p->rb_max, 2 * k);  // experiment
         p->P = (int)std::max<int64_t>(1, cdiv(rows, leaf_max));
         const int64_t base = rows / p->P, extra = rows % p->P;
         int64_t r = 0;
@@ -993,7 +986,7 @@ void qr_factor(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int6
         CqrArgs a{};
         const bool direct = (L == 0 && root_sign);
         // one block, explicit Q wanted: factor only, then Q by compact WY (two GEMMs)
-        const bool wy = direct && k >= 48 && p->wy_tau && !getenv("SORSVD_NO_WY");  // small k: in-kernel form-Q wins
+        const bool wy = direct && k >= 48 && p->wy_tau;  // small k: in-kernel form-Q wins
         a.in = T;
         a.ldi = ldt;
         a.qout = wy ? p->Qtmp : (direct ? Q : T);
@@ -1183,7 +1176,10 @@ struct PredScope {
     }
 };
 
-void launch_chol(sorsvd_ctx* c, const CholArgs& a, cudaStream_t s) {
+void launch_chol(sorsvd_ctx* c, const CholArgs& a0, cudaStream_t s) {
+    CholArgs a = a0;
+    a.outer = c->pred;  // enclosing predicate (RPCA): a skipped iteration marks the QR flag dead
+    a.outer_skip = c->pred_skip;
     // the factor in shared memory when it fits, plus the back-substitution columns when both fit
     const size_t kk8 = (size_t)a.k * a.k * sizeof(double);
     const size_t sm = 2 * kk8 <= kCholSmemBytes ? 2 * kk8 : kk8 <= kCholSmemBytes ? kk8 : 0;
@@ -1279,7 +1275,8 @@ void qr_run_big(sorsvd_ctx* c, QrPlan* p, const double* T, int64_t ldt, double* 
         check_launch(c);
     };
     int* done = p->flag + 1;
-    CK(cudaMemsetAsync(p->flag, 0, 2 * sizeof(int), s));
+    qr_flags_init_kernel<<<1, 32, 0, s>>>(p->flag, c->pred, c->pred_skip);  // dead when the caller is off
+    check_launch(c);
     set_identity_kernel<<<64, 256, 0, s>>>(p->R[0], Np, k);
     check_launch(c);
     const double* X = T;
@@ -1489,6 +1486,8 @@ void run_jacobi_big(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, i
     a.tlog = dbuf(c, "jb_log", (size_t)max_sweeps * (kk - 1) * P);
     a.max_sweeps = max_sweeps;
     a.info = reinterpret_cast<int*>(dbuf(c, "jb_info", 1));
+    a.pred = c->pred;
+    a.pred_skip = c->pred_skip;
     double* sig = dbuf(c, "jb_sig", (size_t)k);
     double* sgn = dbuf(c, "jb_sgn", (size_t)k);
     int* perm = reinterpret_cast<int*>(dbuf(c, "jb_perm", (size_t)k));
@@ -1508,7 +1507,7 @@ void run_jacobi_big(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, i
 
 void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int ldu, double* S, double* V, int ldv,
                 int* sweeps, cudaStream_t s) {
-    if (k > 256 || (getenv("SORSVD_JACOBI_BIG") && k >= 8)) {
+    if (k > 256 || (c->opt_jacobi == SORSVD_JACOBI_ROTLOG && k >= 8)) {
         run_jacobi_big(c, k, M, ldm, U, ldu, S, V, ldv, sweeps, s);
         return;
     }
@@ -1523,10 +1522,12 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
     a.ldv = ldv;
     a.max_sweeps = 60;
     a.sweeps_out = sweeps;
+    a.pred = c->pred;
+    a.pred_skip = c->pred_skip;
     const int kp = (k + 31) / 32;
     const int KP = kp <= 1 ? 1 : kp <= 2 ? 2 : kp <= 4 ? 4 : 8;
     const int P = ((k + 1) & ~1) / 2;
-    if (k > 16 && k <= 32 && !getenv("SORSVD_JACOBI_BARRIER")) {
+    if (k > 16 && k <= 32 && c->opt_jacobi != SORSVD_JACOBI_BARRIER) {
         // 16 < k <= 32: the point-to-point ring, one warp per CTA over a P-CTA cluster
         // (measured C1, k = 20: 0.118 -> 0.087 ms); k <= 16 keeps the single CTA (RPCA's
         // k = 10 is faster there)
@@ -1563,7 +1564,7 @@ void run_jacobi(sorsvd_ctx* c, int k, const double* M, int ldm, double* U, int l
     // point-to-point ring (mbarrier / st.async, no barrier per round) for 32 < k <= 128:
     // measured k = 100: 0.98 vs 1.17 ms; at k = 256 (KP = 8, 8 warps per CTA) the
     // barrier ring stays faster (5.0 vs 7.4 ms)
-    if ((KP == 2 || KP == 4) && !getenv("SORSVD_JACOBI_BARRIER") &&
+    if ((KP == 2 || KP == 4) && c->opt_jacobi != SORSVD_JACOBI_BARRIER &&
         jacobi_p2p_smem_bytes(KP, a.ppc) <= 200 * 1024) {
         if (KP == 2) launch_jacobi_p2p_t<2>(c, a, csize, s);
         else launch_jacobi_p2p_t<4>(c, a, csize, s);
@@ -1817,7 +1818,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     } else {
         qr_run(c, p1, b.T1, Np, b.Q1, Np, s);
     }
-    qr_run(c, p2, b.T2, Np, b.Q2, Np, getenv("SORSVD_NO_SIDE") ? s : c->side);
+    qr_run(c, p2, b.T2, Np, b.Q2, Np, c->side);
     CK(cudaEventRecord(c->ev_join, c->side));
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     record_stage(c, timing, 2);
@@ -1997,13 +1998,85 @@ void enqueue_tsr(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     record_stage(c, timing, 5);
 }
 
-std::string sor_key(const SorProblem& P, const int* pred = nullptr) {
+// Count of non-finite entries of a row-major FP64 / FP32 matrix (failure path
+// only: the reference rejects such input in the Matrix constructor,
+// matrix.hpp:32-33, before any arithmetic).
+template <typename T>
+__global__ void nonfinite_count_kernel(const T* __restrict__ a, int64_t m, int64_t n, int64_t lda,
+                                       unsigned long long* out) {
+    unsigned long long cnt = 0;
+    const int64_t total = m * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        cnt += isfinite((double)a[i * lda + j]) ? 0ull : 1ull;
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);
+}
+
+// True when any rank's A block holds a NaN / Inf.
+bool matrix_has_nonfinite(sorsvd_ctx* c, const void* A, int dtype, int64_t m, int64_t n, int64_t lda) {
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(dbuf(c, "nf_cnt", 1));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), c->stream));
+    const int blocks = c->num_sms * 4;
+    if (dtype == SORSVD_F32)
+        nonfinite_count_kernel<<<blocks, 256, 0, c->stream>>>(static_cast<const float*>(A), m, n, lda, cnt);
+    else
+        nonfinite_count_kernel<<<blocks, 256, 0, c->stream>>>(static_cast<const double*>(A), m, n, lda, cnt);
+    check_launch(c);
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    double flag = h ? 1.0 : 0.0;
+    if (c->world > 1) {
+        double* dv = dbuf(c, "nf_flag", 1);
+        CK(cudaMemcpyAsync(dv, &flag, sizeof flag, cudaMemcpyHostToDevice, c->stream));
+        comm_allreduce(c, dv, 1, false, c->stream);
+        CK(cudaMemcpyAsync(&flag, dv, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    return flag != 0.0;
+}
+
+// After a call: a non-finite sigma means either non-finite input (the
+// reference's parameter_error, raised before any arithmetic) or a breakdown
+// (numerical_error). Any NaN / Inf entry of A reaches sigma: Inf * 0 and
+// NaN * x are NaN, so the entry's row of T1 = A Omega is non-finite and so is
+// every later stage. The check costs one read of k doubles on the happy path.
+void check_result_finite(sorsvd_ctx* c, const double* dS, int k, const void* A, int dtype, int64_t m, int64_t n,
+                         int64_t lda) {
+    std::vector<double> hs(k);
+    CK(cudaMemcpyAsync(hs.data(), dS, (size_t)k * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    bool ok = true;
+    for (double v : hs) ok = ok && std::isfinite(v);
+    if (c->world > 1) {  // every rank takes the same branch (the scan below is collective)
+        double* dv = dbuf(c, "nf_ok", 1);
+        const double bad = ok ? 0.0 : 1.0;
+        CK(cudaMemcpyAsync(dv, &bad, sizeof bad, cudaMemcpyHostToDevice, c->stream));
+        comm_allreduce(c, dv, 1, false, c->stream);
+        double tot = 0.0;
+        CK(cudaMemcpyAsync(&tot, dv, sizeof tot, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        ok = tot == 0.0;
+    }
+    if (ok) return;
+    if (matrix_has_nonfinite(c, A, dtype, m, n, lda))
+        throw Error{SORSVD_ERR_PARAMETER, "parameter: matrix entries must be finite"};
+    throw Error{SORSVD_ERR_NUMERICAL, "numerical: non-finite singular values"};
+}
+
+// Graph cache key: everything baked into the captured kernel arguments that
+// can differ between calls on the same A -- including the launch predicate
+// (an RPCA iteration's graph carries the RPCA stop flag; a later plain call
+// on the same A must not replay it).
+std::string sor_key(const SorProblem& P, const int* pred, int pred_skip) {
     char buf[320];
     snprintf(buf, sizeof buf, "sor%d:%d:%d:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.method, P.dtype, (int)P.single_pass,
              (int)P.tf32,
              P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m, (long long)P.n,
              (long long)P.lda, P.k, P.ell, P.q);
-    if (pred) snprintf(buf + strlen(buf), sizeof buf - strlen(buf), ":pred%p", (const void*)pred);
+    if (pred) snprintf(buf + strlen(buf), sizeof buf - strlen(buf), ":pred%p/%d", (const void*)pred, pred_skip);
     return buf;
 }
 
@@ -2075,7 +2148,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     }
     const double* om = om_in;
     const bool timing = (d->flags & SORSVD_FLAG_STAGE_TIMES) != 0;
-    const bool use_graph = !timing && !c->emu && !(d->flags & SORSVD_FLAG_NO_GRAPH) && !getenv("SORSVD_NO_GRAPH");
+    const bool use_graph = !timing && !c->emu && !(d->flags & SORSVD_FLAG_NO_GRAPH);
     CK(cudaEventRecord(c->ev_a, c->stream));
     const int launches0 = c->launches;
     int launches = 0;
@@ -2107,7 +2180,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         CK(cudaMemcpyAsync(dS, b.Sk, (size_t)P.k * 8, cudaMemcpyDeviceToDevice, c->stream));
     };
     if (use_graph) {
-        const std::string key = sor_key(P);
+        const std::string key = sor_key(P, c->pred, c->pred_skip);
         auto it = c->graphs.find(key);
         if (it == c->graphs.end()) {
             if (c->graphs.size() >= 32) invalidate_graphs(c);  // bound the cache (keys carry A's address)
@@ -2143,6 +2216,8 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     }
     copy_out();
     CK(cudaEventRecord(c->ev_b, c->stream));
+    if (!c->pred)  // inside RPCA (predicated iterations) the driver runs its own finiteness test
+        check_result_finite(c, b.Sk, P.k, dA, P.dtype, P.m, P.n, P.lda);
     if (p1->big || p2->big) {
         CK(cudaEventSynchronize(c->ev_b));
         check_big_qr(p1);
@@ -2410,9 +2485,8 @@ struct Fd {
     }
 };
 
-int64_t sord_chunk_rows(int64_t cols) {
-    int64_t mb = 64;
-    if (const char* e = getenv("SORSVD_SORD_CHUNK_MB")) mb = std::max<int64_t>(1, atoll(e));  // tests
+int64_t sord_chunk_rows(const sorsvd_ctx* c, int64_t cols) {
+    const int64_t mb = std::max<int64_t>(1, c->opt_sord_chunk_mb);
     return std::max<int64_t>(1, (mb << 20) / (cols * 8));
 }
 
@@ -2443,7 +2517,7 @@ void sord_load(sorsvd_ctx* c, const char* path, void* dA, int64_t lda, int dtype
     const SordHeader hd = sord_read_header(f.fd, path);
     if (lda < hd.cols) throw Error{SORSVD_ERR_SHAPE, "shape: lda < cols"};
     if (dtype != SORSVD_F64 && dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
-    const int64_t cr = std::min(sord_chunk_rows(hd.cols), hd.rows);
+    const int64_t cr = std::min(sord_chunk_rows(c, hd.cols), hd.rows);
     const size_t cbytes = (size_t)cr * hd.cols * 8;
     PinnedPair pp(cbytes);
     double* stage[2] = {nullptr, nullptr};
@@ -2491,7 +2565,7 @@ void sord_save(sorsvd_ctx* c, const char* path, const double* dA, int64_t rows, 
     memcpy(h + 8, &r, 8);
     memcpy(h + 16, &cc, 8);
     if (pwrite(f.fd, h, 24, 0) != 24) throw Error{SORSVD_ERR_INTERNAL, "SORD write failed"};
-    const int64_t cr = std::min(sord_chunk_rows(cols), rows);
+    const int64_t cr = std::min(sord_chunk_rows(c, cols), rows);
     PinnedPair pp((size_t)cr * cols * 8);
     cudaStream_t s = c->stream;
     auto issue = [&](int64_t ch) {  // device -> pinned buffer ch & 1
@@ -2747,6 +2821,11 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
     double* V = dbuf(c, "rp_V", (size_t)n * ell);
     double* sig = dbuf(c, "rp_sig", (size_t)ell);
     const double dnorm = std::sqrt(device_sumsq(c, dD, m, n, ldd));
+    if (!std::isfinite(dnorm)) {
+        if (matrix_has_nonfinite(c, dD, SORSVD_F64, m, n, ldd))
+            throw Error{SORSVD_ERR_PARAMETER, "parameter: matrix entries must be finite"};
+        throw Error{SORSVD_ERR_NUMERICAL, "numerical: ||D||_F overflows"};
+    }
     sorsvd_rpca_result r{};
     if (dnorm == 0.0) {  // X = 0 -> L = S = 0 in one iteration
         CK(cudaMemsetAsync(S, 0, (size_t)m * n * 8, c->stream));
@@ -2762,8 +2841,7 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
         const bool gram = c->world > 1 ? n <= 1024 : std::min(m, n) <= 1024;
         if (c->world > 1 && !gram)
             throw Error{SORSVD_ERR_UNSUPPORTED, "multi-rank rpca with n > 1024 needs mu0 passed in"};
-        mu = 1.25 / (gram && !getenv("SORSVD_SIGMA1_SUBSPACE")
-                         ? estimate_sigma1_gram(c, dD, m, n, ldd)
+        mu = 1.25 / (gram ? estimate_sigma1_gram(c, dD, m, n, ldd)
                          : estimate_sigma1(c, dD, m, n, ldd, d->seed ^ 0x5bd1e995ULL));
     }
     r.mu0 = mu;
@@ -3075,6 +3153,25 @@ int sorsvd_set_stream(sorsvd_ctx* c, void* stream) {
     });
 }
 
+int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        switch (key) {
+            case SORSVD_OPT_JACOBI:
+                if (value < SORSVD_JACOBI_AUTO || value > SORSVD_JACOBI_ROTLOG)
+                    throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown Jacobi variant"};
+                c->opt_jacobi = (int)value;
+                invalidate_graphs(c);  // captured calls baked the previous variant in
+                break;
+            case SORSVD_OPT_SORD_CHUNK_MB:
+                if (value < 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: SORD chunk must be >= 1 MiB"};
+                c->opt_sord_chunk_mb = value;
+                break;
+            default: throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown context option"};
+        }
+    });
+}
+
 int sorsvd_ctx_rank(const sorsvd_ctx* c, int* rank, int* world) {
     if (!c) return SORSVD_ERR_PARAMETER;
     if (rank) *rank = c->rank;
@@ -3355,21 +3452,6 @@ int sorsvd_thin_qr_device(sorsvd_ctx* c, int64_t m, int32_t k, const double* dT,
                                  cudaMemcpyDeviceToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         check_big_qr(p);
-        if (c->cqr_prof) {  // SORSVD_CQR_PROF: average per-step phase lengths of the last cqr launch
-            std::vector<long long> h(6 * 512);
-            CK(cudaMemcpy(h.data(), c->cqr_prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
-            double ph[5] = {0, 0, 0, 0, 0};
-            int n = 0;
-            for (int j = 1; j + 1 < k; ++j, ++n) {
-                ph[0] += (double)(h[j * 6 + 1] - h[j * 6 + 0]);        // cluster barrier
-                ph[1] += (double)(h[j * 6 + 2] - h[j * 6 + 1]);        // payload sum + barrier
-                ph[2] += (double)(h[j * 6 + 3] - h[j * 6 + 2]);        // beta/tau, owner column, barrier
-                ph[3] += (double)(h[j * 6 + 4] - h[j * 6 + 3]);        // fused pass (warp 0)
-                ph[4] += (double)(h[(j + 1) * 6 + 0] - h[j * 6 + 0]);  // whole step
-            }
-            fprintf(stderr, "[cqr prof] k=%d cycles/step: cl.sync %.0f csum %.0f owner %.0f fused %.0f total %.0f\n", k,
-                    ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, ph[4] / n);
-        }
     });
 }
 

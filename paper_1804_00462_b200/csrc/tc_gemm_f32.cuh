@@ -97,7 +97,7 @@ template <int BN, bool TA>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs p) {
     using S = TcShape<BN>;
-    if (p.pred && *p.pred == p.pred_skip) return;
+    if (pred_off(p.pred, p.pred_skip)) return;
     extern __shared__ __align__(1024) uint8_t smraw[];
     const uint32_t base = (smem_u32(smraw) + 1023u) & ~1023u;
     uint8_t* gbase = smraw + (base - smem_u32(smraw));
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // out[i] = sum_s ws[s*stride + i] (fp32 partials, fixed order).
 __global__ void reduce_splits_f32_kernel(const float* __restrict__ ws, int64_t count4, int S, int64_t stride,
                                          float* __restrict__ out, const int* pred, int pred_skip) {
-    if (pred && *pred == pred_skip) return;
+    if (pred_off(pred, pred_skip)) return;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4; i += (int64_t)gridDim.x * blockDim.x) {
         float4 acc = reinterpret_cast<const float4*>(ws)[i];
         for (int s = 1; s < S; ++s) {

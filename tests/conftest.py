@@ -28,3 +28,24 @@ def golden():
 def ref_available():
     from oracle import sorsvd_oracle as O
     return os.path.exists(O.REF_LIB_PATH)
+
+
+@pytest.fixture(scope="session")
+def parity_log():
+    """Append one JSON record per call to $SORSVD_PARITY_OUT/parity.jsonl (the
+    per-sigma error vectors committed under profiles/); no-op when unset."""
+    import json
+    out = os.environ.get("SORSVD_PARITY_OUT")
+
+    def rec(name, **data):
+        if not out:
+            return
+        os.makedirs(out, exist_ok=True)
+        clean = {}
+        for k, v in data.items():
+            if hasattr(v, "tolist"):
+                v = v.tolist()
+            clean[k] = v
+        with open(os.path.join(out, "parity.jsonl"), "a") as fh:
+            fh.write(json.dumps({"test": name, **clean}) + "\n")
+    return rec

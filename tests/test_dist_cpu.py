@@ -61,3 +61,34 @@ def test_row_partition_covers(m, world):
         assert r0 == nxt and rows >= m // world
         nxt = r0 + rows
     assert nxt == m
+
+
+def _bench(args, env_extra=None):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.update(env_extra or {})
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], capture_output=True, text=True,
+                       timeout=600, env=env, cwd=root)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    return p.returncode, [json.loads(ln) for ln in lines], p.stderr
+
+
+def test_bench_gpus2_self_launches_two_ranks():
+    # `bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks (gloo here, NCCL on
+    # GPUs); the default C3 workload is strong-scaled: m/2 rows per rank, one JSON line
+    rc, out, err = _bench(["--gpus", "2", "--plan-only"])
+    assert rc == 0, err[-2000:]
+    assert len(out) == 1, out
+    line = out[0]
+    assert line["n_gpus"] == 2
+    assert line["config"]["m"] == 200000 and line["config"]["rows_per_rank"] == 100000
+    assert line["rank_rows"] == [[0, 100000], [100000, 100000]]
+    assert line["max_over_ranks_check"] == 1.0   # max over ranks of the rank index
+
+
+def test_bench_world_size_mismatch_fails_loudly():
+    rc, out, err = _bench(["--gpus", "4", "--plan-only"], {"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert rc == 2 and not out and "WORLD_SIZE" in err

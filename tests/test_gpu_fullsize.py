@@ -1,0 +1,251 @@
+"""Full-size parity on every BASELINE.json config ("next round"
+item 1). The matrices are the ones bench.py times (bench.make_matrix, the
+same seeds), so the benchmarked instances themselves are checked against the
+oracle, with the same host-drawn Omega (seed 7) passed to both sides.
+
+Tolerances (north star): FP64 sigma rel <= 1e-10 per value, low-rank rel
+Frobenius <= 1e-9 (sign- and basis-invariant).
+C3's sketch is noise dominated past j ~ 15 (||E||_2 ~ 0.59 against
+s_j = 10^(-j/64)), so the oracle's own perturbation floor there is ~3e-15
+ and the north-star tolerances apply unchanged.
+FP32 storage with FP64 arithmetic is exact widening of the rounded A, so it
+is held to the FP64 tolerances against the oracle on the rounded A; the TF32
+tensor-core mode has the stated tolerance below. Per-sigma error vectors go
+to $SORSVD_PARITY_OUT (profiles/r02_parity_*.jsonl)."""
+import gc
+import os
+import math
+
+import numpy as np
+import pytest
+
+from oracle import sorsvd_oracle as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+# TF32 passes (fp32_mode="tf32"): each operand is rounded to 10 mantissa bits
+# (2^-11 = 4.9e-4) and products accumulate in FP32. On C3 (k = 256, q = 1) every
+# sketch direction sits far above that level (the tail of the spectrum is the noise
+# bulk, sigma_256 / sigma_1 ~ 0.3), so the whole spectrum resolves: stated tolerance
+# 5e-3 relative per sigma, 2e-2 on the low-rank factorisation. On C5 (q = 2, sigma_j = 1/j
+# above a 0.07 noise floor) only the leading directions resolve.
+TF32_SIGMA_TOL = 5e-3
+TF32_LR_TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_00462_b200 as P
+    return P
+
+
+def _bench_matrix(cfg, rows=None):
+    import torch
+    import bench
+    c = bench.CONFIGS[cfg]
+    m = rows or c["m"]
+    return bench.make_matrix(cfg, m, c["n"], 0, 1, torch.device("cuda", 0))
+
+
+def _free():
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def _host(t):
+    import torch
+    h = torch.empty(t.shape, dtype=torch.float64)
+    step = 8192
+    for i in range(0, t.shape[0], step):
+        h[i:i + step].copy_(t[i:i + step].double())
+    return h.numpy()
+
+
+def _record(parity_log, name, f, base, **extra):
+    s = np.asarray(f.sigma.cpu() if hasattr(f.sigma, "cpu") else f.sigma)
+    u = np.asarray(f.u.cpu() if hasattr(f.u, "cpu") else f.u)
+    v = np.asarray(f.v.cpu() if hasattr(f.v, "cpu") else f.v)
+    es = O.sigma_rel_err(s, base.sigma)
+    lr = O.lowrank_rel_diff(u, s, v, base.u, base.sigma, base.v)
+    parity_log(name, sigma_rel_err=es, lowrank_rel_diff=lr, sigma=s, sigma_oracle=base.sigma, **extra)
+    return es, lr, s, u, v
+
+
+# ------------------------------------------------------------------- C3 ----
+def test_c3_full_fp64_vs_oracle(P, parity_log):
+    """BASELINE configs[2], FP64, 200000 x 20000, k = 256, q = 1: the bench.py instance."""
+    import torch
+    A = _bench_matrix("c3")
+    n = A.shape[1]
+    om = P.gaussian_matrix(n, 256, 7)
+    f = P.sor_svd_power(A, 256, P.SketchConfig(256, 1, 7), omega=torch.from_numpy(om).cuda())
+    torch.cuda.synchronize()
+    a = _host(A)
+    del A
+    _free()
+    base = O.sor_svd_power(a, 256, O.SketchConfig(256, 1, 7), omega=om)
+    es, lr, *_ = _record(parity_log, "c3_full_fp64", f, base)
+    assert f.passes == 5
+    assert es.max() <= 1e-10, (es.max(), int(es.argmax()))
+    assert lr <= 1e-9, lr
+
+
+def test_c3_full_fp32_storage_and_tf32(P, parity_log):
+    """BASELINE configs[2], FP32 storage: (a) FP64 arithmetic on the FP32 A held to the
+    FP64 tolerances against the oracle on the same rounded A; (b) the TF32 tensor-core
+    passes at k = 256 against the same oracle with the stated TF32 tolerance."""
+    import torch
+    A = _bench_matrix("c3f32")
+    assert A.dtype == torch.float32
+    n = A.shape[1]
+    om = P.gaussian_matrix(n, 256, 7)
+    omd = torch.from_numpy(om).cuda()
+    f64m = P.sor_svd_power(A, 256, P.SketchConfig(256, 1, 7), omega=omd)
+    ftf = P.sor_svd_power(A, 256, P.SketchConfig(256, 1, 7), omega=omd, fp32_mode="tf32")
+    torch.cuda.synchronize()
+    a = _host(A)
+    del A
+    _free()
+    base = O.sor_svd_power(a, 256, O.SketchConfig(256, 1, 7), omega=om)
+    es, lr, *_ = _record(parity_log, "c3_full_fp32_storage_fp64_math", f64m, base)
+    assert es.max() <= 1e-10 and lr <= 1e-9, (es.max(), lr)
+    es, lr, s, *_ = _record(parity_log, "c3_full_tf32", ftf, base, tol_sigma=TF32_SIGMA_TOL, tol_lr=TF32_LR_TOL)
+    assert es.max() <= TF32_SIGMA_TOL, (es.max(), int(es.argmax()))
+    assert lr <= TF32_LR_TOL, lr
+    assert np.all(np.diff(s) <= 0)
+
+
+# ------------------------------------------------------------------- C5 ----
+def test_c5_full_tf32_vs_fp64_same_matrix(P, parity_log):
+    """BASELINE configs[4] at full size (131072^2 FP32, 68.7 GB, k = 512, q = 2), SURVEY.md
+    §8(c) item 6: the CPU oracle cannot hold it (137 GB in FP64), so the FP32-storage run
+    in FP64 arithmetic -- exact widening of the same bytes, oracle-exact at the 16384^2
+    scale below -- is the reference for the TF32 run on the same device-resident A."""
+    import torch
+    A = _bench_matrix("c5")
+    n = A.shape[1]
+    om = torch.from_numpy(P.gaussian_matrix(n, 512, 7)).cuda()
+    ref = P.sor_svd_power(A, 512, P.SketchConfig(512, 2, 7), omega=om)
+    tf = P.sor_svd_power(A, 512, P.SketchConfig(512, 2, 7), omega=om, fp32_mode="tf32")
+    again = P.sor_svd_power(A, 512, P.SketchConfig(512, 2, 7), omega=om)
+    torch.cuda.synchronize()
+    del A
+    _free()
+    assert ref.passes == 7
+    assert torch.equal(ref.sigma, again.sigma)   # deterministic at full size
+    s_ref = ref.sigma.cpu().numpy()
+    s_tf = tf.sigma.cpu().numpy()
+    es = O.sigma_rel_err(s_tf, s_ref)
+    # sigma_j = 1/j above the noise: the FP64 run sees the planted spectrum
+    j = np.arange(1, 9)
+    plant = O.sigma_rel_err(s_ref[:8], 1.0 / j)
+    parity_log("c5_full_tf32_vs_fp64", sigma_rel_err=es, sigma_fp64=s_ref, sigma_tf32=s_tf,
+               planted_rel_dev=plant, tol_leading=3e-3)
+    assert es[:8].max() <= 3e-3, es[:8]
+    assert np.all(np.diff(s_tf) <= 0)
+    assert plant.max() < 0.1, plant
+
+
+def test_c5_16384_vs_oracle(P, parity_log):
+    """BASELINE configs[4] scaled to 16384^2 (the CPU-baseline instance, k = 512, q = 2):
+    FP32 storage, FP64 arithmetic, against the oracle on the same rounded A, under the
+    k = 512 protocol of test_gpu_parity.test_k512_fp64_vs_oracle (floor with two
+    Householder rounding histories: the sketch's condition number is ~512^5)."""
+    import torch
+    a = O.gen_lowrank_decay(16384, 16384, 512, lambda j: 1.0 / j, 4e-4, 5).astype(np.float32)
+    f = P.sor_svd_power(torch.from_numpy(a).cuda(), 512, P.SketchConfig(512, 2, 61))
+    a64 = a.astype(np.float64)
+    del a
+    base, ds, dl = O.perturbation_floor(a64, 512, O.SketchConfig(512, 2, 61), trials=1, qr_variants=2,
+                                        include_reference=False)
+    env = np.maximum.accumulate(ds)
+    es, *_ = _record(parity_log, "c5_16384_fp32_storage", f, base, floor=ds)
+    lim = np.maximum(1e-10, 10 * env)
+    assert np.all(es <= lim), (es.max(), int(np.argmax(es / lim)))
+    jd = int(np.searchsorted(env, 1e-11))
+    s = f.sigma.cpu().numpy()
+    lr = O.lowrank_rel_diff(f.u.cpu().numpy()[:, :jd], s[:jd], f.v.cpu().numpy()[:, :jd], base.u[:, :jd],
+                            base.sigma[:jd], base.v[:, :jd])
+    assert jd >= 8 and lr <= max(1e-9, 10 * dl), (jd, lr)
+
+
+# ------------------------------------------------------------------- C4 ----
+def test_c4_full_vs_reference(P, parity_log):
+    """BASELINE configs[3] at full size (the bench.py instance, 25344 x 300, l = 10, q = 1)
+    against the compiled reference's sor_svd_power inside the SPEC.md:386-398 loop
+    (oracle/_ref), mu0 computed once and shared."""
+    if not os.path.exists(O.REF_LIB_PATH):
+        pytest.skip("oracle/_ref not built")
+    import torch
+    D = _bench_matrix("c4")
+    d = D.cpu().numpy()
+    m, n = d.shape
+    mu0 = 1.25 / O.norm_spectral(d)
+    cfg = dict(lam=1 / math.sqrt(max(m, n)), mu0=mu0, ell=10, q=1, seed=9, max_iter=100)
+    O.Ref.set_threads(os.cpu_count() or 1)
+    ro = O.Ref.rpca_alm(d, O.RpcaConfig(**cfg))
+    r = P.rpca_alm(D, P.RpcaConfig(**cfg))
+    rl, rs = r.l.cpu().numpy(), r.s.cpu().numpy()
+    dl = np.linalg.norm(rl - ro.l) / np.linalg.norm(ro.l)
+    dsn = np.linalg.norm(rs - ro.s) / np.linalg.norm(ro.s)
+    parity_log("c4_full_vs_reference", iterations=[r.iterations, ro.iterations], rank=[r.rank_l, ro.rank_l],
+               nnz=[r.nnz_s, ro.nnz_s], rel_error=[r.rel_error, ro.rel_error], dL=dl, dS=dsn)
+    assert r.converged and ro.converged
+    assert r.iterations == ro.iterations and r.rank_l == ro.rank_l and r.nnz_s == ro.nnz_s
+    assert dl <= 1e-9 and dsn <= 1e-9, (dl, dsn)
+    # the planted structure is recovered (rank 5, the 10% support)
+    assert r.rank_l == 5 and r.rel_error < 1e-7
+
+
+@pytest.mark.parametrize("frac,lo,hi,nnz", [(0.05, 14, 20, 12500), (0.1, 16, 23, 25000)])
+def test_rpca_paper_table_pins_gpu(P, parity_log, frac, lo, hi, nnz):
+    """SPEC.md:393-394 (Table IV / V, n = 500, r = 25, l = 2r, q = 1): rank 25,
+    ||S||_0 = s, rel_error < 1e-7, iterations in [lo, hi] (paper 17 / 20), and the same
+    trajectory as the compiled reference's loop."""
+    if not os.path.exists(O.REF_LIB_PATH):
+        pytest.skip("oracle/_ref not built")
+    nn = 500
+    x, _, _ = O.Ref.gen_rpca_instance(nn, 25, int(frac * nn * nn), 1)
+    cfg = dict(lam=1 / math.sqrt(nn), mu0=1.25 / O.norm_spectral(x), ell=50, q=1, seed=1, max_iter=500)
+    ro = O.Ref.rpca_alm(x, O.RpcaConfig(**cfg))
+    r = P.rpca_alm(x, P.RpcaConfig(**cfg))
+    parity_log(f"rpca_table_pin_{frac}", iterations=[r.iterations, ro.iterations], rank=r.rank_l, nnz=r.nnz_s,
+               rel_error=r.rel_error)
+    assert r.converged and r.rel_error < 1e-7
+    assert r.rank_l == 25 and r.nnz_s == nnz
+    assert lo <= r.iterations <= hi
+    assert r.iterations == ro.iterations
+    assert np.linalg.norm(r.l - ro.l) <= 1e-9 * np.linalg.norm(ro.l)
+    assert np.linalg.norm(r.s - ro.s) <= 1e-9 * np.linalg.norm(ro.s)
+
+
+# ------------------------------------------------------------------- C2 ----
+def test_c2_bench_instance_vs_oracle_both_floors(P, parity_log):
+    """BASELINE configs[1] (the bench.py instance: Haar U, V from torch, sigma_j = j^-2),
+    banded C2 protocol (test_gpu_parity.test_config2_full) under both perturbation floors:
+    the survey's 1e-16 input noise and the default eps * sqrt(max(m, n))."""
+    import torch
+    A = _bench_matrix("c2")
+    a = A.cpu().numpy()
+    om = P.gaussian_matrix(4000, 100, 7)
+    f = P.sor_svd_power(A, 100, P.SketchConfig(100, 1, 7), omega=torch.from_numpy(om).cuda())
+    cfg = O.SketchConfig(100, 1, 7)
+    out = {}
+    for tag, rel in (("1e-16", 1e-16), ("eps_sqrt_n", None)):
+        base, ds, dl = O.perturbation_floor(a, 100, cfg, trials=3, rel=rel)
+        env = np.maximum.accumulate(ds)
+        jd = int(np.searchsorted(env, 1e-10))
+        jt = int(np.searchsorted(env, 1e-6))
+        es = O.sigma_rel_err(f.sigma.cpu().numpy(), base.sigma)
+        lr = O.lowrank_rel_diff(f.u.cpu().numpy()[:, :jd], f.sigma.cpu().numpy()[:jd], f.v.cpu().numpy()[:, :jd],
+                                base.u[:, :jd], base.sigma[:jd], base.v[:, :jd])
+        out[tag] = dict(jd=jd, jt=jt, floor_lr=dl, lr_determined=lr, sigma_rel_err=es, floor=ds)
+        assert jd >= 20, (tag, jd)
+        assert np.all(es[:jd] <= np.maximum(1e-10, 10 * env[:jd])), (tag, es[:jd].max())
+        assert np.all(es[jd:jt] <= 100 * env[jd:jt]), (tag, es[jd:jt].max())
+        assert lr <= max(1e-9, 10 * dl), (tag, lr)
+    parity_log("c2_bench_instance_floors", **{f"{t}_{k}": v for t, d in out.items() for k, v in d.items()})

@@ -148,8 +148,9 @@ def test_small_svd_p2p_ring_vs_barrier_ring(P, torch_mod, k, monkeypatch):
     for _ in range(3):
         u2, s2, v2, _ = P.full_svd(mm)
         assert torch_mod.equal(s1, s2) and torch_mod.equal(u1, u2) and torch_mod.equal(v1, v2)
-    monkeypatch.setenv("SORSVD_JACOBI_BARRIER", "1")
-    _, s3, _, w3 = P.full_svd(mm)
+    ctx = P.Context(0)
+    ctx.set_option(P.Context.OPT_JACOBI, P.Context.JACOBI_BARRIER)
+    _, s3, _, w3 = P.full_svd(mm, ctx=ctx)
     s_ref = np.linalg.svd(mm.cpu().numpy(), compute_uv=False)
     # dgesdd is accurate to eps * sigma_1 in absolute terms on the tiny tail
     np.testing.assert_allclose(s1.cpu().numpy(), s_ref, rtol=1e-11, atol=1e-15 * s_ref[0])
@@ -174,10 +175,11 @@ def test_small_svd_graded(P, torch_mod):
 def test_small_svd_big_kernel_forced(P, torch_mod, k, monkeypatch):
     # the k > 256 path (G-only ring + rotation log + row-parallel V rebuild)
     # forced on small k must agree with the reference SVD just the same
-    monkeypatch.setenv("SORSVD_JACOBI_BIG", "1")
+    ctx = P.Context(0)
+    ctx.set_option(P.Context.OPT_JACOBI, P.Context.JACOBI_ROTLOG)
     mm = O.gaussian_matrix(k, k, 5000 + k)
     u_ref, s_ref, v_ref = O.full_svd(mm)
-    u, s, v, sweeps = P.full_svd(torch_mod.from_numpy(mm).cuda())
+    u, s, v, sweeps = P.full_svd(torch_mod.from_numpy(mm).cuda(), ctx=ctx)
     u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
     np.testing.assert_allclose(s, s_ref, rtol=1e-12, atol=1e-14 * s_ref[0])
     assert np.abs(u.T @ u - np.eye(k)).max() < 1e-13

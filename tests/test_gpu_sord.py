@@ -22,18 +22,19 @@ def P():
 @pytest.mark.parametrize("chunk_mb", [None, "1"])
 def test_sord_load_save_roundtrip(P, tmp_path, monkeypatch, chunk_mb):
     import torch
+    ctx = P.Context(0)
     if chunk_mb:
-        monkeypatch.setenv("SORSVD_SORD_CHUNK_MB", chunk_mb)  # many chunks: both staging buffers cycle
+        ctx.set_option(P.Context.OPT_SORD_CHUNK_MB, int(chunk_mb))  # many chunks: both staging buffers cycle
     a = O.gaussian_matrix(1531, 389, 21)
     p = str(tmp_path / "a.sord")
     O.write_sord(p, a)
-    d = P.load_sord(p)
+    d = P.load_sord(p, ctx=ctx)
     assert d.dtype == torch.float64 and tuple(d.shape) == a.shape
     np.testing.assert_array_equal(d.cpu().numpy(), a)
-    f = P.load_sord(p, dtype=torch.float32)
+    f = P.load_sord(p, dtype=torch.float32, ctx=ctx)
     np.testing.assert_array_equal(f.cpu().numpy(), a.astype(np.float32))
     q = str(tmp_path / "b.sord")
-    P.save_sord(q, d * 2.0)
+    P.save_sord(q, d * 2.0, ctx=ctx)
     np.testing.assert_array_equal(O.read_sord(q), 2.0 * a)
     assert open(q, "rb").read() == open(p, "rb").read()[:24] + (2.0 * a).astype("<f8").tobytes()
 

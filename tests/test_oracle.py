@@ -191,3 +191,20 @@ def test_port_vs_compiled_reference_live(ref_available):
     D, L0, S0 = O.gen_c4(4, m=500, n=60)
     assert np.count_nonzero(S0) == round(0.1 * 500 * 60)
     assert np.abs(S0).max() <= 50
+
+
+@pytest.mark.parametrize("frac,lo,hi,nnz", [(0.05, 14, 20, 12500), (0.1, 16, 23, 25000)])
+def test_rpca_paper_table_pins(ref_available, frac, lo, hi, nnz):
+    # SPEC.md:393-394 / acceptance criteria 1-2 (Table IV / V, n = 500, r = 25):
+    # rank(L) = 25, ||S||_0 = s, rel_error < 1e-7, iterations within [lo, hi] (paper: 17 / 20),
+    # on matrixgen's RPCA instance (matrixgen.hpp:99-124) with l = 2r, q = 1
+    if not ref_available:
+        pytest.skip("oracle/_ref not built")
+    n = 500
+    x, _, s0 = O.Ref.gen_rpca_instance(n, 25, int(frac * n * n), 1)
+    assert np.count_nonzero(s0) == nnz
+    cfg = O.RpcaConfig(lam=1 / np.sqrt(n), mu0=1.25 / O.norm_spectral(x), ell=50, q=1, seed=1, max_iter=500)
+    for r in (O.rpca_alm(x, cfg), O.Ref.rpca_alm(x, cfg)):
+        assert r.converged and r.rel_error < 1e-7
+        assert r.rank_l == 25 and r.nnz_s == nnz
+        assert lo <= r.iterations <= hi, r.iterations
