@@ -22,18 +22,24 @@ SOURCES = ["sorsvd.cu", "host_rng.cpp"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h")))
 
 
+def _deps():
+    return [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "sorsvd_b200.h")]
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "sorsvd_b200.h")]
-    return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
+    return any(os.path.getmtime(p) > t for p in _deps() if os.path.exists(p))
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
+    # the library is stamped with the newest source time seen when the build started, so
+    # an edit made while nvcc runs still marks it stale
+    t_src = max(os.path.getmtime(p) for p in _deps() if os.path.exists(p))
     objs = []
     for src in SOURCES:
         obj = os.path.join(OUT_DIR, src + ".o")
@@ -47,6 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl", "-lpthread"], check=True)
     os.replace(tmp, LIB)
+    os.utime(LIB, (t_src, t_src))
     return LIB
 
 

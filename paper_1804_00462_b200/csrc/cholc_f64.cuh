@@ -51,6 +51,14 @@ struct CholcArgs {
     int* done;          // sticky: set to 1 when G is already I to within done_tol (X orthonormal)
     double done_tol;
     int* shifted;       // out: 1 when this pass used the shift (diagnostics)
+    // mode 0: the adaptive pass above. Modes 1 / 2: a CholeskyQR2 factorisation for
+    // k where chol_inv_kernel's factor no longer fits one CTA's shared memory (k > 160),
+    // same gates as chol_inv_kernel (cholqr_f64.cuh): `flag` is the CholeskyQR2 flag
+    // (0 accept, 1 fall back to Householder); pass 1 rejects on a pivot ratio below
+    // 1e-14, pass 2 (skipped once pass 1 rejected) on max |G - I| > 1e-2.
+    int mode;
+    const int* outer;   // enclosing launch predicate (modes 1/2): pass 1 marks flag dead when off
+    int outer_skip;
 };
 
 __host__ __device__ inline size_t cholc_smem_bytes(int k) {
@@ -64,8 +72,16 @@ __host__ __device__ inline size_t cholc_smem_bytes(int k) {
 //   otherwise                       -> R = chol(G + s I)   (shifted pass)
 __global__ void __launch_bounds__(kCholcThreads, 1) cholc_kernel(CholcArgs a) {
     cgc::cluster_group cl = cgc::this_cluster();
-    if (*a.done) return;  // uniform over the cluster
     const int C = (int)cl.num_blocks(), r = (int)cl.block_rank();
+    if (a.mode == 0) {
+        if (*a.done) return;  // uniform over the cluster
+    } else {
+        if (pred_off(a.outer, a.outer_skip)) {  // enclosing iteration skipped: both QR paths skip
+            if (a.mode == 1 && r == 0 && threadIdx.x == 0) *a.flag = kPredDead;
+            return;
+        }
+        if (a.mode == 2 && *a.flag != 0) return;  // pass 1 rejected (or dead)
+    }
     const int k = a.k, kp = C * kCholcB, tid = threadIdx.x;
     constexpr int B = kCholcB;
     extern __shared__ __align__(16) double sh[];
@@ -77,7 +93,7 @@ __global__ void __launch_bounds__(kCholcThreads, 1) cholc_kernel(CholcArgs a) {
     __shared__ double s_piv, s_shift, s_dev, s_pmin, s_pmax;
     const int row0 = r * B;
     // gate: max |G - I| over this CTA's rows, reduced over the cluster
-    {
+    if (a.mode != 1) {
         double dev = 0.0;
         for (int e = tid; e < B * k; e += blockDim.x) {
             const int i = e / k, j = e - i * k, gi = row0 + i;
@@ -97,13 +113,18 @@ __global__ void __launch_bounds__(kCholcThreads, 1) cholc_kernel(CholcArgs a) {
         double dmax = 0.0;
         for (int q = 0; q < C; ++q) dmax = fmax(dmax, *cl.map_shared_rank(&s_dev, q));
         cl.sync();
-        if (dmax < a.done_tol) {
+        if (a.mode == 0 && dmax < a.done_tol) {
             if (r == 0 && tid == 0) *a.done = 1;
+            return;
+        }
+        if (a.mode == 2 && !(dmax <= 1e-2)) {  // Q' too far from orthonormal: Householder instead
+            if (r == 0 && tid == 0) *a.flag = 1;
             return;
         }
     }
     int any_bad = 1;
-    for (int attempt = 0; attempt < 2 && any_bad; ++attempt) {
+    const int attempts = a.mode == 0 ? 2 : 1;  // CholeskyQR2 passes are never shifted
+    for (int attempt = 0; attempt < attempts && any_bad; ++attempt) {
         if (tid == 0) {
             s_bad = 0;
             s_pmin = 1e300;
@@ -214,7 +235,8 @@ __global__ void __launch_bounds__(kCholcThreads, 1) cholc_kernel(CholcArgs a) {
             pmax = fmax(pmax, *cl.map_shared_rank(&s_pmax, q));
         }
         // the plain pass is only trusted when cond(X) < ~1e6 (pivot ratio ~ 1/cond^2)
-        if (attempt == 0 && !(pmin > 1e-12 * pmax)) any_bad = 1;
+        const double piv_gate = a.mode == 0 ? 1e-12 : a.mode == 1 ? 1e-14 : 0.0;
+        if (attempt == 0 && !(pmin > piv_gate * pmax)) any_bad = 1;
         cl.sync();  // peers done reading the flags before the next attempt resets them
         if (!any_bad && r == 0 && tid == 0 && a.shifted) *a.shifted = attempt;
     }
@@ -226,6 +248,7 @@ __global__ void __launch_bounds__(kCholcThreads, 1) cholc_kernel(CholcArgs a) {
             const int jl = e / k, i = e - jl * k, j = row0 + jl;
             if (j < k) a.R[(size_t)i * a.ldr + j] = (i <= j) ? Ls[(size_t)jl * kp + i] : 0.0;
         }
+        if (a.mode == 1 && r == 0 && tid == 0) *a.flag = 0;
     }
 }
 
@@ -296,6 +319,19 @@ __global__ void copy_rows_kernel(const double* __restrict__ src, int64_t lds, do
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / cols, j = e - i * cols;
         dst[i * ldd + j] = src[i * lds + j];
+    }
+}
+
+// Rout = R2 R1 for upper-triangular k x k factors (CholeskyQR2's R), one thread
+// per upper element: Rout_ij = sum_{l=i..j} R2_il R1_lj.
+__global__ void triu_mul_kernel(const double* __restrict__ R2, int ld2, const double* __restrict__ R1, int ld1,
+                                double* __restrict__ Ro, int ldo, int k, const int* pred, int pred_skip) {
+    if (pred_off(pred, pred_skip)) return;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+        const int i = e / k, j = e - i * k;
+        double acc = 0.0;
+        for (int l = i; l <= j; ++l) acc = fma(R2[(size_t)i * ld2 + l], R1[(size_t)l * ld1 + j], acc);
+        Ro[(size_t)i * ldo + j] = j >= i ? acc : 0.0;
     }
 }
 

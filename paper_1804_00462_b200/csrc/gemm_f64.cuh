@@ -45,15 +45,17 @@ struct GemmArgs {
     double alpha;
     const int* pred;  // optional device flag: the launch is a no-op when *pred == pred_skip
     int pred_skip;
-    // stream-K (grid underfilled by whole tiles): CTA c runs segments
-    // [sk_cta_seg[c], sk_cta_seg[c+1]) of the (tile, k-range) list; a segment
-    // covering a whole tile writes C directly, partial ones go to slot g of
-    // `sk_ws` (BM x BN each) and streamk_fixup_kernel sums them in slot order
+    // stream-K (grid underfilled by whole tiles, or a partial last wave): CTA c runs
+    // segments [sk_cta_seg[c], sk_cta_seg[c+1]) of the (tile, k-range) list; a segment
+    // covering a whole tile writes C directly, partial ones go to workspace slot
+    // sk_seg_slot[g] of `sk_ws` (BM x BN each) and streamk_fixup_kernel sums them in
+    // slot order
     const int* sk_cta_seg;
     const int* sk_seg_tile;
     const int* sk_seg_k0;  // in BK units
     const int* sk_seg_k1;
-    int sk_units;          // BK units per tile
+    const int* sk_seg_slot;  // workspace slot of a partial segment (-1: whole tile, written to C)
+    int sk_units;            // BK units per tile
     int sk_gy;             // column chunks per row tile
     double* sk_ws;
     int gy_fused;          // > 0: blockIdx.x = row_tile * gy_fused + column chunk (chunks of a row tile
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
                                                p.C + nt * S::BN, row0, p.ldc);
             else
                 gemm_tile<FM, FN, TA, V16, AT>(p, smem_raw, row0, rows, 0, nt * S::BN, kBegin, kEnd,
-                                               p.sk_ws + (size_t)gs * S::BM * S::BN, 0, S::BN);
+                                               p.sk_ws + (size_t)p.sk_seg_slot[gs] * S::BM * S::BN, 0, S::BN);
         }
         return;
     }
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_f64_kernel(GemmArgs p) {
 // slot loads are issued 16 ahead of the ordered adds, since a tile split over
 // ~100 segments (a K = m reduction onto one tile) is otherwise a chain of
 // dependent L2 round trips.
-__global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* __restrict__ tile_seg0,
+__global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* __restrict__ split_slot0,
                                      const int* __restrict__ split_tiles, int nsplit, int BM, int BN, int gy,
                                      int64_t M, double* __restrict__ C, int64_t ldc, const int* pred, int pred_skip) {
     if (pred_off(pred, pred_skip)) return;
@@ -298,7 +300,7 @@ __global__ void streamk_fixup_kernel(const double* __restrict__ ws, const int* _
     for (int st = blockIdx.y; st < nsplit; st += gridDim.y) {
         const int tile = split_tiles[st];
         const int mt = tile / gy, nt = tile - mt * gy;
-        const int g0 = tile_seg0[tile], g1 = tile_seg0[tile + 1];
+        const int g0 = split_slot0[st], g1 = split_slot0[st + 1];  // the tile's partial slots, in order
         for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < per; w += gridDim.x * blockDim.x) {
             const int r = w / BN, col = w - r * BN;
             const int64_t row = (int64_t)mt * BM + r;

@@ -44,7 +44,13 @@ struct JacobiArgs {
 
 // smem per CTA (doubles): 2 buffers x ppc slots x 2 columns x (G, V) x kpad
 //   + ids (2 x ppc x 2 ints, as doubles) + sigma/rank scratch
-__host__ __device__ inline int jac_kpad(int k) { return ((k + 31) / 32) * 32; }
+// Column length held per ring slot: 32 * KP, KP = the kernel's per-lane element count
+// (1, 2, 4, 8 by k, as run_jacobi selects it). Every lane reads KP elements per column,
+// so the slot must span all 32 * KP of them (zero padded past k).
+__host__ __device__ inline int jac_kpad(int k) {
+    const int kp = (k + 31) / 32;
+    return 32 * (kp <= 1 ? 1 : kp <= 2 ? 2 : kp <= 4 ? 4 : 8);
+}
 __host__ __device__ inline size_t jacobi_smem_bytes(int k, int ppc) {
     const size_t slot = 4 * (size_t)jac_kpad(k);
     return (2 * (size_t)ppc * slot + 2 * 2 * (size_t)ppc + 4 * (size_t)ppc + 64) * sizeof(double);
@@ -75,7 +81,7 @@ __global__ void jacobi_cluster_kernel(JacobiArgs a) {
     const int k = a.k, ppc = a.ppc;
     const int kk = (k + 1) & ~1;
     const int P = kk / 2;
-    const int KPAD = jac_kpad(k);
+    constexpr int KPAD = 32 * KP;  // == jac_kpad(k) for the KP run_jacobi picks
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = r * ppc + warp;  // global pair slot of this warp
     const bool active = warp < ppc && slot < P;

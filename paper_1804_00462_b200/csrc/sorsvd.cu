@@ -201,6 +201,9 @@ struct sorsvd_ctx {
     int rank = 0, world = 1;
     int num_sms = 148;
     cudaStream_t own_stream = nullptr, stream = nullptr, side = nullptr;
+    cudaStream_t comm_stream = nullptr;  // multi-rank: all-reduces of finished T2 blocks, under the next blocks' GEMMs
+    static constexpr int kTnBlocks = 4;
+    cudaEvent_t ev_blk[kTnBlocks] = {}, ev_comm = nullptr;
     std::vector<cudaStream_t> tstreams;  // batched trials (created on first use)
     std::vector<cudaEvent_t> tevents;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_a = nullptr, ev_b = nullptr;
@@ -211,8 +214,8 @@ struct sorsvd_ctx {
     std::map<std::string, std::unique_ptr<QrPlan>> plans;
     std::map<std::string, GraphEntry> graphs;
     struct SkTable {
-        std::vector<int*> dev;  // cta_seg, seg_tile, seg_k0, seg_k1, tile_seg0, split_tiles
-        int nsplit = 0, nseg = 0;
+        std::vector<int*> dev;  // cta_seg, seg_tile, seg_k0, seg_k1, split_slot0, split_tiles, seg_slot
+        int nsplit = 0, nseg = 0, nslot = 0;
     };
     std::map<std::string, SkTable> sk_tables;  // stream-K segment tables, by shape
     ncclComm_t comm = nullptr;
@@ -310,8 +313,8 @@ struct GemmCall {
     const char* ws_name = "gemm_ws";
     const float* Af = nullptr;  // FP32-storage A (FP64 arithmetic); overrides A
     // stream-K is taken when its modelled cost is below sk_bias x split-K's; the
-    // A-streaming passes with one column chunk use 1.0 (measured: C2 pass
-    // 145 -> 137 us), everything else keeps the margin its numerics were pinned with
+    // A-streaming passes use 1.0 (measured: C2 pass 145 -> 137 us; C3's partial last
+    // wave), everything else keeps the margin its numerics were pinned with
     double sk_bias = 0.95;
 };
 
@@ -391,11 +394,16 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
     // stream-K from 16 BK-units per tile (C1: 0.333 -> 0.321 ms per call); tiny outputs keep
     // split-K: a stream-K tile spread over ~all SMs has a fix-up that is
     // a chain of ~num_sms / 16 dependent L2 round trips per element
+    // Also past one wave of tiles (the A-streaming passes: C3's NN pass is 3126 tiles =
+    // 21.12 waves, so a whole-tile schedule idles 88% of the SMs for the last wave): every
+    // CTA then runs ~tiles/n whole tiles plus a partial one at each end of its unit
+    // range, and only those <= 2n boundary tiles go through the fix-up.
     const bool tiny_out = g.M * g.N <= 4096;
-    if (!g.tile_row0 && g.force_splits == 0 && tiles < (int64_t)c->num_sms &&
-        units >= 16 && !tiny_out) {
+    if (!g.tile_row0 && g.force_splits == 0 && units >= 16 && !tiny_out) {
         const int64_t n = c->num_sms;
-        const double sk_cost = (double)cdiv(tiles * units, n) * BK + 2 * 96.0 + 0.02 * 3 * g.M * g.N / (double)n;
+        const int BNk = g.N <= 128 ? g.N : 128;
+        const double fix_elems = tiles < n ? (double)g.M * g.N : (double)std::min<int64_t>(tiles, 2 * n) * BM * BNk;
+        const double sk_cost = (double)cdiv(tiles * units, n) * BK + 2 * 96.0 + 0.02 * 3 * fix_elems / (double)n;
         const double cur_cost = (double)cdiv(tiles * S, n) * ((double)g.K / S + 96.0) +
                                 (S > 1 ? 0.02 * S * g.M * g.N / (double)n : 0.0);
         streamk = sk_cost < g.sk_bias * cur_cost;
@@ -428,7 +436,7 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         a.c_split_stride = 0;
     }
     std::vector<int> sk_split_tiles_h;
-    const int* sk_tile_seg0 = nullptr;
+    const int* sk_split_slot0 = nullptr;
     const int* sk_split_tiles = nullptr;
     if (streamk) {
         const int n = c->num_sms;
@@ -438,7 +446,8 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         auto it = c->sk_tables.find(key);
         if (it == c->sk_tables.end()) {
             if (c->capturing) throw Error{SORSVD_ERR_INTERNAL, "stream-K table creation during capture"};
-            std::vector<int> cta_seg{0}, seg_tile, seg_k0, seg_k1, tile_seg0(tiles + 1, 0), split;
+            std::vector<int> cta_seg{0}, seg_tile, seg_k0, seg_k1, tile_seg0(tiles + 1, 0), split, seg_slot,
+                split_slot0;
             for (int cc = 0; cc < n; ++cc) {
                 int64_t u0 = cc * T / n, u1 = (cc + 1) * T / n;
                 while (u0 < u1) {
@@ -455,6 +464,21 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
                 if (tile_seg0[t + 1] > 1) split.push_back((int)t);
                 tile_seg0[t + 1] += tile_seg0[t];
             }
+            // partial segments get compact workspace slots, in segment order: the slots of
+            // one split tile are then a contiguous range, and the ranges follow `split`
+            int slot = 0;
+            for (size_t q = 0; q < seg_tile.size(); ++q) {
+                const bool whole = seg_k0[q] == 0 && seg_k1[q] == units;
+                seg_slot.push_back(whole ? -1 : slot);
+                if (!whole) {
+                    if (split_slot0.empty() || seg_tile[q] != seg_tile[q - 1] || seg_slot[q - 1] < 0)
+                        split_slot0.push_back(slot);
+                    ++slot;
+                }
+            }
+            split_slot0.push_back(slot);
+            if (split_slot0.size() != split.size() + 1)
+                throw Error{SORSVD_ERR_INTERNAL, "stream-K: slot table mismatch"};
             auto up = [&](const std::vector<int>& v) {
                 int* d = nullptr;
                 CK(cudaMalloc(&d, std::max<size_t>(v.size(), 1) * sizeof(int)));
@@ -462,9 +486,10 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
                 return d;
             };
             sorsvd_ctx::SkTable t;
-            t.dev = {up(cta_seg), up(seg_tile), up(seg_k0), up(seg_k1), up(tile_seg0), up(split)};
+            t.dev = {up(cta_seg), up(seg_tile), up(seg_k0), up(seg_k1), up(split_slot0), up(split), up(seg_slot)};
             t.nsplit = (int)split.size();
             t.nseg = (int)seg_tile.size();
+            t.nslot = slot;
             it = c->sk_tables.emplace(key, t).first;
         }
         const std::vector<int*>& tab = it->second.dev;
@@ -472,12 +497,13 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
         a.sk_seg_tile = tab[1];
         a.sk_seg_k0 = tab[2];
         a.sk_seg_k1 = tab[3];
-        sk_tile_seg0 = tab[4];
+        sk_split_slot0 = tab[4];
         sk_split_tiles = tab[5];
+        a.sk_seg_slot = tab[6];
         a.sk_units = (int)units;
         a.sk_gy = (int)gy;
         const int BN = g.N <= 128 ? g.N : 128;
-        a.sk_ws = dbuf(c, std::string(g.ws_name) + "_sk", (size_t)it->second.nseg * BM * BN);
+        a.sk_ws = dbuf(c, std::string(g.ws_name) + "_sk", (size_t)std::max(it->second.nslot, 1) * BM * BN);
         sk_split_tiles_h.resize((size_t)it->second.nsplit);
     }
     const bool f32a = g.Af != nullptr;
@@ -511,7 +537,7 @@ void run_gemm(sorsvd_ctx* c, const GemmCall& g, cudaStream_t s) {
             const int BN = g.N <= 128 ? g.N : 128;
             const dim3 fgrid((unsigned)cdiv((int64_t)BM * BN, 256), (unsigned)std::min(nsplit, 65535));
             streamk_fixup_kernel<<<fgrid, 256, 0, s>>>(
-                a.sk_ws, sk_tile_seg0, sk_split_tiles, nsplit, BM, BN, (int)gy, g.M, g.C, g.ldc, c->pred,
+                a.sk_ws, sk_split_slot0, sk_split_tiles, nsplit, BM, BN, (int)gy, g.M, g.C, g.ldc, c->pred,
                 c->pred_skip);
             check_launch(c);
         }
@@ -1198,6 +1224,26 @@ void launch_chol(sorsvd_ctx* c, const CholArgs& a0, cudaStream_t s) {
 // rows of Q.
 void allreduce_sum(sorsvd_ctx* c, double* buf, size_t count, cudaStream_t s);
 
+// cholc_kernel over a ceil(k/32)-CTA cluster (CTA r holds rows [32r, 32r+32) of L).
+void launch_cholc(sorsvd_ctx* c, const CholcArgs& a, cudaStream_t s) {
+    const int C = (a.k + kCholcB - 1) / kCholcB;
+    allow_smem(cholc_kernel, true);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)C);
+    cfg.blockDim = dim3(kCholcThreads);
+    cfg.dynamicSmemBytes = cholc_smem_bytes(a.k);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, cholc_kernel, a));
+    check_launch(c);
+}
+
 void qr_run_big(sorsvd_ctx* c, QrPlan* p, const double* T, int64_t ldt, double* Q, int64_t ldq, cudaStream_t s,
                 int64_t rows_global = 0, bool distributed = false) {
     const int k = p->k, Np = p->Np;
@@ -1256,23 +1302,7 @@ void qr_run_big(sorsvd_ctx* c, QrPlan* p, const double* T, int64_t ldt, double* 
         a.flag = p->flag;
         a.done = p->flag + 1;
         a.done_tol = 1e-13;
-        const int C = (k + kCholcB - 1) / kCholcB;
-        const size_t sm = cholc_smem_bytes(k);
-        allow_smem(cholc_kernel, true);
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)C);
-        cfg.blockDim = dim3(kCholcThreads);
-        cfg.dynamicSmemBytes = sm;
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = C;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&cfg, cholc_kernel, a));
-        check_launch(c);
+        launch_cholc(c, a, s);
     };
     int* done = p->flag + 1;
     qr_flags_init_kernel<<<1, 32, 0, s>>>(p->flag, c->pred, c->pred_skip);  // dead when the caller is off
@@ -1364,7 +1394,51 @@ void qr_run(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int64_t
         run_gemm(c, g, s);
     };
     if (ldt != Np) throw Error{SORSVD_ERR_INTERNAL, "qr_run: T must be padded to Np"};
+    // k > 160: the factor no longer fits one CTA's shared memory and chol_inv_kernel would run
+    // its k sequential steps out of global memory (k = 256: 3.7 ms per factorisation); the
+    // factor is then spread over a cluster (cholc_kernel in CholeskyQR2 mode, same gates) and
+    // R^{-1} comes from a column-parallel back substitution
+    const bool cluster_chol = (size_t)k * k * sizeof(double) > kCholSmemBytes;
+    auto cluster_pass = [&](int pass, const double* G, double* R, double* Ri) {
+        CholcArgs a{};
+        a.G = G;
+        a.ldg = Np;
+        a.k = k;
+        a.R = R;
+        a.ldr = k;
+        a.flag = p->flag;
+        a.mode = pass;
+        a.outer = c->pred;
+        a.outer_skip = c->pred_skip;
+        launch_cholc(c, a, s);
+        const int wpb = 8;
+        trinv_kernel<<<(k + wpb - 1) / wpb, 32 * wpb, (size_t)wpb * k * sizeof(double), s>>>(R, k, k, Ri, Np,
+                                                                                             p->flag, 1);
+        check_launch(c);
+    };
     gram(T, ldt, p->G1);
+    if (cluster_chol) {
+        cluster_pass(1, p->G1, p->R1, p->Ri1);
+        {
+            PredScope ps(c, p->flag, 1);  // skipped when pass 1 rejected
+            rmul(T, ldt, p->Ri1, p->Qtmp, Np);
+            gram(p->Qtmp, Np, p->G2);
+        }
+        cluster_pass(2, p->G2, p->cwork, p->Ri2);
+        triu_mul_kernel<<<std::min<int>((k * k + 255) / 256, c->num_sms * 4), 256, 0, s>>>(p->cwork, k, p->R1, k,
+                                                                                           p->R[L], k, k, p->flag, 1);
+        check_launch(c);
+        {
+            PredScope ps(c, p->flag, 1);
+            rmul(p->Qtmp, Np, p->Ri2, Q, ldq);
+        }
+        {
+            PredScope ps(c, p->flag, 0);  // Householder only when CholeskyQR2 was rejected
+            qr_factor(c, p, T, ldt, Q, ldq, true, s);
+            qr_formq(c, p, T, ldt, Q, ldq, nullptr, s);
+        }
+        return;
+    }
     CholArgs a1{};
     a1.G = p->G1;
     a1.ldg = Np;
@@ -1748,6 +1822,51 @@ void enqueue_m_approx(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, c
     check_launch(c);
 }
 
+// T2 = A^T T1 summed over the ranks' row blocks (sketch.hpp:96). Single rank: one
+// launch. Multi-rank: the pass runs as kTnBlocks launches over column blocks of A
+// (row blocks of T2), and each finished block's all-reduce is issued on the comm
+// stream while the next block's GEMM runs, so only the last block's reduction
+// is exposed; the compute stream joins the comm stream before T2 is used.
+void tn_pass_reduced(sorsvd_ctx* c, const SorProblem& P, const double* T1, double* T2, cudaStream_t s) {
+    const int Np = P.Np;
+    auto tn = [&](int64_t n0, int64_t n1) {
+        GemmCall g2;
+        g2.ta = true;
+        g2.A = P.A ? P.A + n0 : nullptr;
+        g2.Af = P.Af ? P.Af + n0 : nullptr;
+        g2.lda = P.lda;
+        g2.M = n1 - n0;
+        g2.K = P.m;
+        g2.B = T1;
+        g2.ldb = Np;
+        g2.N = Np;
+        g2.C = T2 + n0 * Np;
+        g2.ldc = Np;
+        g2.sk_bias = 1.0;
+        run_gemm(c, g2, s);
+    };
+    constexpr int NB = sorsvd_ctx::kTnBlocks;
+    const int BM = gemm_bm_for(Np);
+    if (c->world <= 1 || P.n < (int64_t)NB * BM) {
+        tn(0, P.n);
+        allreduce_sum(c, T2, (size_t)P.n * Np, s);
+        return;
+    }
+    // block edges on tile boundaries (multiples of BM keep A's column offset 16-byte aligned)
+    const int64_t tiles = cdiv(P.n, BM);
+    for (int bi = 0; bi < NB; ++bi) {
+        const int64_t n0 = std::min<int64_t>(P.n, tiles * bi / NB * BM);
+        const int64_t n1 = bi == NB - 1 ? P.n : std::min<int64_t>(P.n, tiles * (bi + 1) / NB * BM);
+        if (n1 <= n0) continue;
+        tn(n0, n1);
+        CK(cudaEventRecord(c->ev_blk[bi], s));
+        CK(cudaStreamWaitEvent(c->comm_stream, c->ev_blk[bi], 0));
+        comm_allreduce(c, T2 + n0 * Np, (size_t)(n1 - n0) * Np, false, c->comm_stream);
+    }
+    CK(cudaEventRecord(c->ev_comm, c->comm_stream));
+    CK(cudaStreamWaitEvent(s, c->ev_comm, 0));
+}
+
 // Enqueue one sor_svd_power on c->stream (T2 must already hold Omega, padded).
 void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, QrPlan* pg,
                  bool timing) {
@@ -1778,23 +1897,9 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g1.N = Np;
         g1.C = b.T1;
         g1.ldc = Np;
-        g1.sk_bias = Np <= 128 ? 1.0 : 0.95;
+        g1.sk_bias = 1.0;
         run_gemm(c, g1, s);
-        GemmCall g2;  // T2 = A^T * T1   (sketch.hpp:96)
-        g2.ta = true;
-        g2.A = P.A;
-        g2.Af = P.Af;
-        g2.lda = P.lda;
-        g2.M = P.n;
-        g2.K = P.m;
-        g2.B = b.T1;
-        g2.ldb = Np;
-        g2.N = Np;
-        g2.C = b.T2;
-        g2.ldc = Np;
-        g2.sk_bias = Np <= 128 ? 1.0 : 0.95;
-        run_gemm(c, g2, s);
-        allreduce_sum(c, b.T2, (size_t)P.n * Np, s);
+        tn_pass_reduced(c, P, b.T1, b.T2, s);  // T2 = A^T * T1   (sketch.hpp:96), summed over ranks
     }
     if (P.tf32) {  // the QR / SVD stages run in FP64
         cast_to_f64(c, b.T1f, P.Np32, b.T1, Np, P.m, ell, s);
@@ -1843,7 +1948,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g.C = b.Y;
         g.ldc = Np;
         g.Af = P.Af;
-        g.sk_bias = Np <= 128 ? 1.0 : 0.95;
+        g.sk_bias = 1.0;
         if (!P.tf32) run_gemm(c, g, s);
         GemmCall h;
         h.ta = true;
@@ -1919,7 +2024,7 @@ void pass_gemm(sorsvd_ctx* c, const SorProblem& P, bool ta, const double* B, dou
     g.N = P.Np;
     g.C = C;
     g.ldc = P.Np;
-    g.sk_bias = P.Np <= 128 ? 1.0 : 0.95;
+    g.sk_bias = 1.0;
     run_gemm(c, g, s);
 }
 
@@ -3027,6 +3132,9 @@ void ctx_init(sorsvd_ctx* c, int device) {
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev_blk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
     c->stream = c->own_stream;
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -3137,6 +3245,9 @@ void sorsvd_ctx_destroy(sorsvd_ctx* c) {
     if (c->om_pin) cudaFreeHost(c->om_pin);
     for (cudaStream_t t : c->tstreams) cudaStreamDestroy(t);
     for (cudaEvent_t e : c->tevents) cudaEventDestroy(e);
+    for (auto& e : c->ev_blk) cudaEventDestroy(e);
+    cudaEventDestroy(c->ev_comm);
+    cudaStreamDestroy(c->comm_stream);
     cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->own_stream);
     delete c;
@@ -3596,7 +3707,7 @@ static int pass_device_impl(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int
         g.N = Np;
         g.C = dT;
         g.ldc = Np;
-        g.sk_bias = Np <= 128 ? 1.0 : 0.95;  // as the sketch passes of enqueue_sor
+        g.sk_bias = 1.0;  // as the sketch passes of enqueue_sor
         run_gemm(c, g, c->stream);  // warm-up (sizes the split workspace)
         const int l0 = c->launches;
         CK(cudaEventRecord(c->ev_a, c->stream));

@@ -159,6 +159,31 @@ def test_small_svd_p2p_ring_vs_barrier_ring(P, torch_mod, k, monkeypatch):
     assert 1 <= w1 <= 40 and 1 <= w3 <= 40
 
 
+@pytest.mark.parametrize("k", [129, 150, 160, 200, 224, 255, 256])
+def test_small_svd_barrier_ring_all_widths(P, torch_mod, k):
+    # 128 < k <= 256 runs the barrier cluster ring with 8 elements per lane: every lane
+    # reads 256 entries per column, so the ring slots must be 256 long whatever k is
+    # (a slot of round_up(k, 32) let lanes read the neighbouring column for k % 256 != 0)
+    mm = O.gaussian_matrix(k, k, 900 + k)
+    mm[:, 3] = 1.0
+    u, s, v, sweeps = P.full_svd(torch_mod.from_numpy(mm).cuda())
+    s_ref = np.linalg.svd(mm, compute_uv=False)
+    u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+    np.testing.assert_allclose(s, s_ref, rtol=1e-11, atol=1e-14 * s_ref[0])
+    assert np.abs(u.T @ u - np.eye(k)).max() < 1e-12
+    assert np.abs((u * s) @ v.T - mm).max() < 1e-12 * s_ref[0]
+    assert 1 <= sweeps <= 30
+
+
+@pytest.mark.parametrize("ell", [136, 200, 248])
+def test_sor_svd_ell_between_128_and_256(P, ell):
+    A = O.gen_lowrank_decay(3000, 1200, 300, lambda j: 10.0 ** (-j / 64.0), 1e-3, ell)
+    cfg = O.SketchConfig(ell, 1, 5)
+    base, ds, dl = O.perturbation_floor(A, ell, cfg, trials=1)
+    f = P.sor_svd_power(A, ell, P.SketchConfig(ell, 1, 5))
+    _check_parity(f, base.sigma, base.u, base.v, ds, dl)
+
+
 def test_small_svd_graded(P, torch_mod):
     # strongly graded spectrum: one-sided Jacobi keeps relative accuracy
     k = 60

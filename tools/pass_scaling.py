@@ -1,5 +1,5 @@
 """FP64 pass throughput vs problem size (ell fixed): separates fixed per-launch
-overhead from the DMMA main-loop rate. Env SORSVD_NO_STREAMK=1 compares split-K."""
+overhead from the DMMA main-loop rate.."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
