@@ -61,6 +61,10 @@ typedef enum sorsvd_flop_variant {
 #define SORSVD_FLAG_TF32 0x10u        /* dtype F32: passes on the TF32 tensor cores (fast; ~1e-3 relative,
                                          resolves only sketch directions above the TF32 rounding level).
                                          Default for F32: FP64 arithmetic on the FP32-stored A. */
+#define SORSVD_FLAG_OZAKI 0x20u       /* FP64 arithmetic (F64, or F32 storage) with the A-streaming passes
+                                         computed as exact int8 slice products on the tcgen05 tensor cores
+                                         (Ozaki scheme, 7 x 7-bit slices, levels t+u <= 9): error below the
+                                         reference dgemm's own sum rounding; several times the DMMA rate */
 
 typedef struct sorsvd_ctx sorsvd_ctx;
 
@@ -120,8 +124,10 @@ int sorsvd_emu_group_create(int world, sorsvd_emu_group** out);
 void sorsvd_emu_group_destroy(sorsvd_emu_group* group);
 int sorsvd_ctx_create_emulated(int device, int rank, sorsvd_emu_group* group, sorsvd_ctx** out);
 const char* sorsvd_last_error(const sorsvd_ctx* ctx);
-/* Bind the context to a caller stream (cudaStream_t, may be 0 for the
- * context's own stream). */
+/* Bind the context to a caller stream (cudaStream_t). NULL (the default for a
+ * new context) means the legacy default stream: the context computes on its own
+ * stream and every call is ordered after the work already queued on the
+ * default stream, and before anything queued there after the call. */
 int sorsvd_set_stream(sorsvd_ctx* ctx, void* stream);
 int sorsvd_ctx_rank(const sorsvd_ctx* ctx, int* rank, int* world);
 
@@ -249,6 +255,14 @@ int sorsvd_measure_peaks(sorsvd_ctx* ctx, double* fp64_tflops, double* hbm_read_
 /* One A-streaming pass (sketch.hpp:95 when ta = 0, :96 when ta = 1) repeated
  * `reps` times between CUDA events; dX / dT padded to ld = ell rounded up to 8
  * (or to 128 when ell > 128). Reports the average pass time. */
+/* The Ozaki scale exponents of A (tests): row_e[m], col_e[n] (device), max|.| < 2^e. */
+int sorsvd_ozaki_scales_device(sorsvd_ctx* ctx, int64_t m, int64_t n, int64_t lda, int32_t dtype, const void* dA,
+                               int32_t* row_e, int32_t* col_e);
+/* One Ozaki pass (SORSVD_FLAG_OZAKI's kernels) C = op(A) X for tests / timing; dtype of A F64 or F32,
+ * X and C FP64 padded like sorsvd_pass_device. ms_scales: the per-call max|A| read. */
+int sorsvd_pass_ozaki_device(sorsvd_ctx* ctx, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell,
+                             int32_t dtype, const void* dA, const double* dX, double* dT, int32_t reps,
+                             double* ms_avg, double* ms_scales);
 int sorsvd_pass_device(sorsvd_ctx* ctx, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell, const double* dA,
                        const double* dX, double* dT, int32_t reps, double* ms_avg, int32_t* launches_per_pass);
 

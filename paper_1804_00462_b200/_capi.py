@@ -27,6 +27,7 @@ FLAG_NO_GRAPH = 0x2
 FLAG_STAGE_TIMES = 0x4
 FLAG_BASIC = 0x8
 FLAG_TF32 = 0x10
+FLAG_OZAKI = 0x20
 
 
 class SorsvdDesc(ctypes.Structure):
@@ -100,6 +101,9 @@ SIGNATURES = [
     ("sorsvd_matmul_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]),
     ("sorsvd_matmul_f32_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]),
     ("sorsvd_measure_peaks", c_i32, [c_vp, c_dp, c_dp]),
+    ("sorsvd_ozaki_scales_device", c_i32, [c_vp, c_i64, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    ("sorsvd_pass_ozaki_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32,
+                                         c_dp, c_dp]),
     ("sorsvd_pass_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_dp,
                                    ctypes.POINTER(c_i32)]),
     ("sorsvd_pass_f32_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_dp,

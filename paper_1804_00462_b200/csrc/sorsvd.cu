@@ -42,6 +42,7 @@
 #include "mapprox_f64.cuh"
 #include "jacobi_big_f64.cuh"
 #include "cholc_f64.cuh"
+#include "ozaki_i8.cuh"
 #include <cfloat>
 
 using namespace sorsvd_dev;
@@ -202,6 +203,12 @@ struct sorsvd_ctx {
     int num_sms = 148;
     cudaStream_t own_stream = nullptr, stream = nullptr, side = nullptr;
     cudaStream_t comm_stream = nullptr;  // multi-rank: all-reduces of finished T2 blocks, under the next blocks' GEMMs
+    // Ordered with the legacy default stream (the caller passed no stream, e.g. torch's default
+    // stream): every entry point waits for the work already queued there and makes it wait for
+    // the call's own work (events), while the context computes on its own non-blocking stream
+    // (CUDA graphs cannot be captured on the legacy stream).
+    bool legacy_order = true;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     static constexpr int kTnBlocks = 4;
     cudaEvent_t ev_blk[kTnBlocks] = {}, ev_comm = nullptr;
     std::vector<cudaStream_t> tstreams;  // batched trials (created on first use)
@@ -1673,6 +1680,7 @@ struct SorProblem {
     int64_t m_global;
     bool single_pass;
     bool tf32;         // dtype F32 with SORSVD_FLAG_TF32: passes on the tcgen05 tensor cores
+    bool ozaki;        // SORSVD_FLAG_OZAKI: FP64 passes as int8 slice products on the tcgen05 tensor cores
     int method = SORSVD_SOR_POWER;  // SORSVD_RSVD / SORSVD_TSR: the baselines of sketch.hpp:124-149
 };
 
@@ -1822,6 +1830,109 @@ void enqueue_m_approx(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, c
     check_launch(c);
 }
 
+// ------------------------------------------------------ Ozaki (int8) passes --
+// Left-operand exponents of A for both orientations (rows for NN, columns for
+// TN) from one read of A (ozaki_i8.cuh). Once per call: A is fixed across the
+// call's 2q+3 passes.
+struct OzScales {
+    const int* row_e = nullptr;  // m
+    const int* col_e = nullptr;  // n
+};
+
+OzScales oz_prepare_a(sorsvd_ctx* c, const SorProblem& P, cudaStream_t s) {
+    auto* rmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_rowmax", (size_t)P.m));
+    auto* cmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_colmax", (size_t)P.n));
+    int* re = reinterpret_cast<int*>(dbuf(c, "oz_rowe", (size_t)(P.m + 1) / 2));
+    int* ce = reinterpret_cast<int*>(dbuf(c, "oz_cole", (size_t)(P.n + 1) / 2));
+    CK(cudaMemsetAsync(rmax, 0, (size_t)P.m * 8, s));
+    CK(cudaMemsetAsync(cmax, 0, (size_t)P.n * 8, s));
+    const dim3 grid((unsigned)cdiv(P.n, 512), (unsigned)cdiv(P.m, 64));
+    if (P.dtype == SORSVD_F32)
+        ozaki_absmax_kernel<float><<<grid, 256, 0, s>>>(P.Af, P.lda, P.m, P.n, rmax, cmax);
+    else
+        ozaki_absmax_kernel<double><<<grid, 256, 0, s>>>(P.A, P.lda, P.m, P.n, rmax, cmax);
+    check_launch(c);
+    ozaki_exp_kernel<<<(unsigned)std::min<int64_t>(cdiv(P.m, 256), c->num_sms * 8), 256, 0, s>>>(rmax, P.m, re);
+    check_launch(c);
+    ozaki_exp_kernel<<<(unsigned)std::min<int64_t>(cdiv(P.n, 256), c->num_sms * 8), 256, 0, s>>>(cmax, P.n, ce);
+    check_launch(c);
+    return OzScales{re, ce};
+}
+
+template <bool TA, typename AT>
+void launch_ozaki_t(const OzArgs& a0, unsigned grid, cudaStream_t s) {
+    OzArgs a = a0;
+    // A tiles by TMA when its rows are 16-byte aligned (the tensor map's stride rule), else
+    // the converters load them from global memory themselves
+    const bool tma = ((uintptr_t)a.A % 16) == 0 && ((a.lda * (int64_t)sizeof(AT)) % 16) == 0;
+    CUtensorMap map{};
+    if (tma) {
+        const int64_t rows = TA ? a.K : a.M, cols = TA ? a.M : a.K;  // A is rows x cols row-major either way
+        cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+        cuuint64_t strides[1] = {(cuuint64_t)(a.lda * (int64_t)sizeof(AT))};
+        const int e16 = 128 / (int)sizeof(AT);  // elements per 128-byte swizzle row
+        cuuint32_t box[2] = {(cuuint32_t)e16, (cuuint32_t)(TA ? kOzBK : kOzBM)};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = encode_tiled()(&map, sizeof(AT) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                    2, const_cast<void*>(a.A), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error{SORSVD_ERR_CUDA, "cuda: cuTensorMapEncodeTiled failed " + std::to_string((int)r)};
+        allow_smem(ozaki_gemm_kernel<TA, AT, true>);
+        ozaki_gemm_kernel<TA, AT, true><<<grid, kOzThreads, kOzSmem, s>>>(map, a);
+    } else {
+        allow_smem(ozaki_gemm_kernel<TA, AT, false>);
+        ozaki_gemm_kernel<TA, AT, false><<<grid, kOzThreads, kOzSmem, s>>>(map, a);
+    }
+}
+
+// C (M x Np) = op(A) X with X (K x Np row-major): NN (M = m, K = n, lexp = rows)
+// or TN (M = n, K = m, lexp = columns). X is cut into digit planes first.
+void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const int* lexp, const double* X, double* C,
+               cudaStream_t s, int dbg = 0) {
+    const int Np = P.Np;
+    const int NC = (int)cdiv(Np, kOzBN);
+    const int64_t M = ta ? P.n : P.m, K = ta ? P.m : P.n;
+    const int64_t KT = cdiv(K, kOzBK);
+    auto* xmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_xmax", (size_t)Np));
+    int* xexp = reinterpret_cast<int*>(dbuf(c, "oz_xexp", (size_t)(Np + 1) / 2));
+    int8_t* Xd = reinterpret_cast<int8_t*>(dbuf(c, ta ? "oz_xd_tn" : "oz_xd_nn", (size_t)(KT * NC * kOzXStep + 7) / 8));
+    CK(cudaMemsetAsync(xmax, 0, (size_t)Np * 8, s));
+    ozaki_colmax_kernel<<<dim3((unsigned)cdiv(Np, 256), (unsigned)cdiv(K, 256)), 256, 0, s>>>(X, Np, K, Np, xmax);
+    check_launch(c);
+    ozaki_exp_kernel<<<1, 256, 0, s>>>(xmax, Np, xexp);
+    check_launch(c);
+    const int64_t items = KT * 2 * (int64_t)NC * kOzBN;
+    ozaki_xdigits_kernel<<<(unsigned)std::min<int64_t>(cdiv(items, 256), (int64_t)c->num_sms * 16), 256, 0, s>>>(
+        X, Np, K, Np, NC, xexp, Xd);
+    check_launch(c);
+    OzArgs a{};
+    a.A = P.dtype == SORSVD_F32 ? static_cast<const void*>(P.Af) : static_cast<const void*>(P.A);
+    a.lda = P.lda;
+    a.M = M;
+    a.K = K;
+    a.lexp = lexp;
+    a.Xd = Xd;
+    a.xexp = xexp;
+    a.NC = NC;
+    a.N = Np;
+    a.C = C;
+    a.ldc = Np;
+    a.dbg = dbg;
+    a.vec = ((uintptr_t)a.A % 16) == 0 && (P.dtype == SORSVD_F32 ? P.lda % 4 : P.lda % 2) == 0;
+    a.pred = c->pred;
+    a.pred_skip = c->pred_skip;
+    const unsigned grid = (unsigned)(cdiv(M, kOzBM) * NC);
+    if (P.dtype == SORSVD_F32) {
+        if (ta) launch_ozaki_t<true, float>(a, grid, s);
+        else launch_ozaki_t<false, float>(a, grid, s);
+    } else {
+        if (ta) launch_ozaki_t<true, double>(a, grid, s);
+        else launch_ozaki_t<false, double>(a, grid, s);
+    }
+    check_launch(c);
+}
+
 // T2 = A^T T1 summed over the ranks' row blocks (sketch.hpp:96). Single rank: one
 // launch. Multi-rank: the pass runs as kTnBlocks launches over column blocks of A
 // (row blocks of T2), and each finished block's all-reduce is issued on the comm
@@ -1873,6 +1984,8 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     cudaStream_t s = c->stream;
     const int Np = P.Np, ell = P.ell;
     record_stage(c, timing, 0);
+    OzScales oz;
+    if (P.ozaki) oz = oz_prepare_a(c, P, s);
     for (int i = 0; i <= P.q; ++i) {
         if (P.single_pass && i == P.q) {  // t2_pre: the row sketch entering the last iteration (sketch.hpp:94)
             if (P.tf32)
@@ -1884,6 +1997,12 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
             run_tc_gemm(c, false, P.Af, P.lda, P.m, P.n, b.T2f, P.Np32, P.Np32, b.T1f, P.Np32, s);
             run_tc_gemm(c, true, P.Af, P.lda, P.n, P.m, b.T1f, P.Np32, P.Np32, b.T2f, P.Np32, s);
             comm_allreduce(c, b.T2f, (size_t)P.n * P.Np32, true, s);
+            continue;
+        }
+        if (P.ozaki) {  // FP64 passes as int8 slice products (ozaki_i8.cuh)
+            run_ozaki(c, P, false, oz.row_e, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
+            run_ozaki(c, P, true, oz.col_e, b.T1, b.T2, s);   // T2 = A^T T1 (sketch.hpp:96)
+            allreduce_sum(c, b.T2, (size_t)P.n * Np, s);
             continue;
         }
         GemmCall g1;  // T1 = A * T2     (sketch.hpp:95); FP32 A widened to FP64 in the kernel
@@ -1949,7 +2068,8 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g.ldc = Np;
         g.Af = P.Af;
         g.sk_bias = 1.0;
-        if (!P.tf32) run_gemm(c, g, s);
+        if (P.ozaki) run_ozaki(c, P, false, oz.row_e, b.Q2, b.Y, s);
+        else if (!P.tf32) run_gemm(c, g, s);
         GemmCall h;
         h.ta = true;
         h.A = b.Q1;
@@ -2177,8 +2297,8 @@ void check_result_finite(sorsvd_ctx* c, const double* dS, int k, const void* A, 
 // on the same A must not replay it).
 std::string sor_key(const SorProblem& P, const int* pred, int pred_skip) {
     char buf[320];
-    snprintf(buf, sizeof buf, "sor%d:%d:%d:%d:%p:%lld:%lld:%lld:%d:%d:%d", P.method, P.dtype, (int)P.single_pass,
-             (int)P.tf32,
+    snprintf(buf, sizeof buf, "sor%d:%d:%d:%d%d:%p:%lld:%lld:%lld:%d:%d:%d", P.method, P.dtype, (int)P.single_pass,
+             (int)P.tf32, (int)P.ozaki,
              P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m, (long long)P.n,
              (long long)P.lda, P.k, P.ell, P.q);
     if (pred) snprintf(buf + strlen(buf), sizeof buf - strlen(buf), ":pred%p/%d", (const void*)pred, pred_skip);
@@ -2226,6 +2346,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     P.m_global = d->m_global > 0 ? d->m_global : d->m;
     P.single_pass = d->single_pass != 0 && !baseline;
     P.tf32 = d->dtype == SORSVD_F32 && (d->flags & SORSVD_FLAG_TF32);
+    P.ozaki = !P.tf32 && (d->flags & SORSVD_FLAG_OZAKI) && !baseline;
     QrPlan *p1, *p2, *pg;
     SorBuffers b = prepare_sor(c, P, &p1, &p2, &pg);
     double* psi2_in = nullptr;
@@ -3114,7 +3235,16 @@ template <typename F>
 int guarded(sorsvd_ctx* c, F&& f) {
     try {
         if (c) CK(cudaSetDevice(c->device));
+        const bool order = c && c->legacy_order && c->ev_in && !c->capturing;
+        if (order) {
+            CK(cudaEventRecord(c->ev_in, cudaStreamLegacy));
+            CK(cudaStreamWaitEvent(c->stream, c->ev_in, 0));
+        }
         f();
+        if (order) {
+            CK(cudaEventRecord(c->ev_out, c->stream));
+            CK(cudaStreamWaitEvent(cudaStreamLegacy, c->ev_out, 0));
+        }
         return SORSVD_OK;
     } catch (const Error& e) {
         if (c && c->emu) c->emu->poison();  // release peers blocked in a collective
@@ -3135,6 +3265,8 @@ void ctx_init(sorsvd_ctx* c, int device) {
     CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
     for (auto& e : c->ev_blk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
     c->stream = c->own_stream;
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -3247,6 +3379,8 @@ void sorsvd_ctx_destroy(sorsvd_ctx* c) {
     for (cudaEvent_t e : c->tevents) cudaEventDestroy(e);
     for (auto& e : c->ev_blk) cudaEventDestroy(e);
     cudaEventDestroy(c->ev_comm);
+    cudaEventDestroy(c->ev_in);
+    cudaEventDestroy(c->ev_out);
     cudaStreamDestroy(c->comm_stream);
     cudaStreamDestroy(c->side);
     cudaStreamDestroy(c->own_stream);
@@ -3258,9 +3392,12 @@ const char* sorsvd_last_error(const sorsvd_ctx* c) { return c ? c->err.c_str() :
 int sorsvd_set_stream(sorsvd_ctx* c, void* stream) {
     if (!c) return SORSVD_ERR_PARAMETER;
     return guarded(c, [&] {
+        // NULL: the caller's work is on the legacy default stream (torch's default stream):
+        // compute on the own stream, ordered with it by events (see legacy_order)
         cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
         if (s != c->stream) invalidate_graphs(c);
         c->stream = s;
+        c->legacy_order = stream == nullptr;
     });
 }
 
@@ -3718,6 +3855,65 @@ static int pass_device_impl(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int
         CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
         if (ms_avg) *ms_avg = ms / std::max(reps, 1);
         if (launches_per_pass) *launches_per_pass = (c->launches - l0) / std::max(reps, 1);
+    });
+}
+
+// The Ozaki scale exponents of A (tests): row_e[m] and col_e[n], e with max|.| < 2^e.
+int sorsvd_ozaki_scales_device(sorsvd_ctx* c, int64_t m, int64_t n, int64_t lda, int32_t dtype, const void* dA,
+                               int32_t* row_e, int32_t* col_e) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        SorProblem P{};
+        P.dtype = dtype;
+        P.A = dtype == SORSVD_F64 ? static_cast<const double*>(dA) : nullptr;
+        P.Af = dtype == SORSVD_F32 ? static_cast<const float*>(dA) : nullptr;
+        P.m = m;
+        P.n = n;
+        P.lda = lda;
+        OzScales oz = oz_prepare_a(c, P, c->stream);
+        CK(cudaMemcpyAsync(row_e, oz.row_e, (size_t)m * 4, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(col_e, oz.col_e, (size_t)n * 4, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// One Ozaki (int8 tensor-core) pass C = op(A) X (kernel tests and the bench's
+// roofline line): ms_avg = the pass (X digits + GEMM), ms_scales = the per-call
+// scale read of A that the 2q+3 passes of a call share.
+int sorsvd_pass_ozaki_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int64_t lda, int32_t ell, int32_t dtype,
+                             const void* dA, const double* dX, double* dT, int32_t reps, double* ms_avg,
+                             double* ms_scales) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        const int dbg = (dtype >> 8) & 7;  // kernel timing experiments (tools/oz_pass.py): bits 8-10 of dtype
+        dtype &= 0xff;
+        (void)dbg;
+        if (dtype != SORSVD_F64 && dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
+        SorProblem P{};
+        P.dtype = dtype;
+        P.A = dtype == SORSVD_F64 ? static_cast<const double*>(dA) : nullptr;
+        P.Af = dtype == SORSVD_F32 ? static_cast<const float*>(dA) : nullptr;
+        P.m = m;
+        P.n = n;
+        P.lda = lda;
+        P.ell = ell;
+        P.k = ell;
+        P.Np = npad(ell);
+        P.ozaki = true;
+        CK(cudaEventRecord(c->ev_h[0], c->stream));
+        OzScales oz = oz_prepare_a(c, P, c->stream);
+        CK(cudaEventRecord(c->ev_h[1], c->stream));
+        run_ozaki(c, P, ta != 0, ta ? oz.col_e : oz.row_e, dX, dT, c->stream);  // warm-up
+        CK(cudaEventRecord(c->ev_a, c->stream));
+        for (int r = 0; r < reps; ++r)
+            run_ozaki(c, P, ta != 0, ta ? oz.col_e : oz.row_e, dX, dT, c->stream, dbg);
+        CK(cudaEventRecord(c->ev_b, c->stream));
+        CK(cudaEventSynchronize(c->ev_b));
+        float ms = 0.f, msc = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
+        CK(cudaEventElapsedTime(&msc, c->ev_h[0], c->ev_h[1]));
+        if (ms_avg) *ms_avg = ms / std::max(reps, 1);
+        if (ms_scales) *ms_scales = msc;
     });
 }
 
