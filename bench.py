@@ -548,6 +548,8 @@ def main():
     stages = {key: round(fs.stats[key], 4) for key in ("ms_total", "ms_passes", "ms_qr", "ms_project", "ms_svd",
                                                         "ms_basis")}
     stages["jacobi_sweeps"] = fs.stats["jacobi_sweeps"]
+    pass_kind = int(fs.stats.get("pass_kind", 0))  # 0 FP64 DMMA, 1 Ozaki int8 (FP64), 2 TF32
+    stages["pass_engine"] = ["fp64 DMMA", "fp64 via Ozaki int8 tensor cores", "tf32 tensor cores"][pass_kind]
     stages["note"] = "un-graphed call with per-stage CUDA events; passes = the 2q+2 sketch passes"
 
     # ---- roofline of the dominant kernel (the A-streaming pass) ----
@@ -616,10 +618,40 @@ def main():
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get(args.config, {}).get("pass_nn_dram_bytes")
+            traffic = json.load(open(tr_path)).get(args.config, {}).get(
+                "pass_nn_dram_bytes_ozaki" if pass_kind == 1 else "pass_nn_dram_bytes")
         except Exception:
             traffic = None
-    if ai >= ridge:
+    if pass_kind == 1:
+        # the library's pass engine here: ozaki_gemm_kernel (tcgen05 kind::i8). Its roofline is the
+        # INT8 tensor rate: 34 int8 digit products per FP64 multiply-add (ozaki_i8.cuh), against
+        # 2 x the measured BF16 burst (the INT8 dense rate is twice BF16 on B200; MEASURED_PEAKS.json
+        # has no INT8 entry). The FP64-equivalent rate is reported beside it.
+        oz = P._capi.lib().sorsvd_pass_ozaki_device
+        ms_o, ms_sc = ctypes.c_double(), ctypes.c_double()
+        dt_code = 1 if f32 else 0
+        P._check(oz(ctx.handle, 0, m_local, n, n, ell, dt_code, A.data_ptr(), X.data_ptr(), T.data_ptr(),
+                    max(args.steps, 5), ctypes.byref(ms_o), ctypes.byref(ms_sc)), ctx.handle)
+        ms_ot = ctypes.c_double()
+        P._check(oz(ctx.handle, 1, m_local, n, n, ell, dt_code, A.data_ptr(), T.data_ptr(), T2.data_ptr(),
+                    max(args.steps, 5), ctypes.byref(ms_ot), ctypes.byref(ms_sc)), ctx.handle)
+        int8_ops = 34.0 * pass_flops
+        i8_peak = 2.0 * mp.get("bf16_tflops", 1590.0)
+        achieved = int8_ops / (ms_o.value * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOPS (int8)",
+                "frac": achieved / i8_peak, "traffic": traffic,
+                "kernel": "ozaki_gemm_kernel (tcgen05.mma kind::i8, TMA-staged A, 34 digit products / FP64 FMA), "
+                          "NN pass T1 = A*X",
+                "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (burst): INT8 dense = 2x BF16 on B200",
+                "ms_per_launch": ms_o.value, "int8_ops_per_launch": int8_ops, "flops_per_launch": pass_flops,
+                "fp64_equiv_tflops": pass_flops / (ms_o.value * 1e-3) / 1e12,
+                "fp64_equiv_over_dmma_peak": pass_flops / (ms_o.value * 1e-3) / 1e12 / fp64_peak,
+                "dmma_peak_tflops": fp64_peak, "ms_scales_per_call": ms_sc.value,
+                "tn_pass": {"ms": ms_ot.value, "achieved": int8_ops / (ms_ot.value * 1e-3) / 1e12},
+                "dmma_pass_for_comparison": {"ms_nn": ms_pass.value, "ms_tn": ms_pass_t.value,
+                                             "tflops_nn": pass_flops / (ms_pass.value * 1e-3) / 1e12},
+                "hbm_gbs_measured": hbm_peak, "hbm_frac": pass_bytes / (ms_o.value * 1e-3) / 1e9 / hbm_peak}
+    elif ai >= ridge:
         achieved = pass_flops / (ms_pass.value * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TFLOP/s",
                 "frac": achieved / tensor_peak, "traffic": traffic, "kernel": kname + ", NN pass T1 = A*X",
@@ -684,7 +716,9 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": ("f32/tf32" if tf32 else "f32 storage, f64 arithmetic") if f32 else "f64",
+                "scaling": cfg["scaling"], "vs_baseline": None,
+                "dtype": (("f32/tf32" if tf32 else "f32 storage, f64 arithmetic") if f32 else "f64")
+                + (" (passes: exact int8 digit products on the tensor cores, Ozaki)" if pass_kind == 1 else ""),
                 "data": "synthetic", "config": workload, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "stages_ms": stages,
                 "wall_s_timed_region": t_wall, "ms_steps": [round(x, 4) for x in ms_steps]}

@@ -63,8 +63,11 @@ typedef enum sorsvd_flop_variant {
                                          Default for F32: FP64 arithmetic on the FP32-stored A. */
 #define SORSVD_FLAG_OZAKI 0x20u       /* FP64 arithmetic (F64, or F32 storage) with the A-streaming passes
                                          computed as exact int8 slice products on the tcgen05 tensor cores
-                                         (Ozaki scheme, 7 x 7-bit slices, levels t+u <= 9): error below the
-                                         reference dgemm's own sum rounding; several times the DMMA rate */
+                                         (Ozaki scheme: 7 signed byte digits of a 55-bit fixed point, the 34
+                                         products with digit levels >= 5): error at or below the reference
+                                         dgemm's own sum rounding. Default for large passes (m n ell >= 2^36,
+                                         ell >= 32); this flag forces it */
+#define SORSVD_FLAG_DMMA 0x40u        /* force the FP64 DMMA passes (the default below that size) */
 
 typedef struct sorsvd_ctx sorsvd_ctx;
 
@@ -98,6 +101,8 @@ typedef struct sorsvd_stats {
     int32_t method;      /* sorsvd_method */
     int32_t launches;    /* kernel launches issued for the call */
     int32_t jacobi_sweeps;
+    int32_t pass_kind;   /* how the passes over A ran: 0 FP64 DMMA, 1 Ozaki int8 (FP64), 2 TF32 */
+    int32_t reserved;
 } sorsvd_stats;
 
 /* ---- context -------------------------------------------------------------- */

@@ -358,7 +358,7 @@ def _decompose(kind: str, a, k: int, cfg: SketchConfig, flags: int, omega, psi2,
 
 def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Context] = None,
                   stage_times: bool = False, use_graph: bool = True, m_global: int = 0,
-                  _basic: bool = False, fp32_mode: str = "fp64", fp64_mode: str = "dmma") -> LowRankApprox:
+                  _basic: bool = False, fp32_mode: str = "fp64", fp64_mode: str = "auto") -> LowRankApprox:
     """Subspace-orbit randomized SVD with q power iterations (sketch.hpp:87).
 
     a: numpy (m, n) on the host or a CUDA torch tensor; float64 runs the FP64
@@ -367,17 +367,17 @@ def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Contex
     on the TF32 tensor cores (fast; ~1e-3 relative and only the sketch
     directions above the TF32 rounding level are resolved). QR and
     the core SVD are FP64 and results are FP64 either way.
-    fp64_mode: how the FP64 passes are computed: "dmma" (the FP64 tensor pipe) or
-    "ozaki" (exact int8 slice products on the tcgen05 tensor cores, ozaki_i8.cuh).
+    fp64_mode: how the FP64 passes are computed: "dmma" (the FP64 tensor pipe),
+    "ozaki" (exact int8 slice products on the tcgen05 tensor cores, ozaki_i8.cuh),
+    or "auto" (default: ozaki for large passes, m*n*ell >= 2^36 and ell >= 32).
     omega: optional (n, ell) test matrix; default gaussian_matrix(n, ell, seed)
     exactly as the reference draws it (sketch.hpp:90)."""
     if fp32_mode not in ("fp64", "tf32"):
         raise ParameterError("parameter: fp32_mode must be 'fp64' or 'tf32'")
-    if fp64_mode not in ("dmma", "ozaki"):
-        raise ParameterError("parameter: fp64_mode must be 'dmma' or 'ozaki'")
+    if fp64_mode not in ("auto", "dmma", "ozaki"):
+        raise ParameterError("parameter: fp64_mode must be 'auto', 'dmma' or 'ozaki'")
     flags = C.FLAG_TF32 if fp32_mode == "tf32" else 0
-    if fp64_mode == "ozaki":
-        flags |= C.FLAG_OZAKI
+    flags |= {"auto": 0, "dmma": C.FLAG_DMMA, "ozaki": C.FLAG_OZAKI}[fp64_mode]
     if stage_times:
         flags |= C.FLAG_STAGE_TIMES
     if not use_graph:

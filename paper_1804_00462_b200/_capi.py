@@ -28,6 +28,7 @@ FLAG_STAGE_TIMES = 0x4
 FLAG_BASIC = 0x8
 FLAG_TF32 = 0x10
 FLAG_OZAKI = 0x20
+FLAG_DMMA = 0x40
 
 
 class SorsvdDesc(ctypes.Structure):
@@ -40,7 +41,7 @@ class SorsvdStats(ctypes.Structure):
                 ("ms_passes", ctypes.c_double), ("ms_qr", ctypes.c_double), ("ms_project", ctypes.c_double),
                 ("ms_svd", ctypes.c_double), ("ms_basis", ctypes.c_double), ("flops_passes", ctypes.c_double),
                 ("bytes_passes", ctypes.c_double), ("passes", c_i32), ("method", c_i32), ("launches", c_i32),
-                ("jacobi_sweeps", c_i32)]
+                ("jacobi_sweeps", c_i32), ("pass_kind", c_i32), ("reserved", c_i32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

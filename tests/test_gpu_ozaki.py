@@ -1,0 +1,185 @@
+"""The Ozaki-scheme FP64 passes (ozaki_i8.cuh: exact int8 slice products on
+the tcgen05 tensor cores) against FP64 references: the pass kernel itself
+against an FP64 GEMM of the same operands, and whole sor_svd_power calls in
+fp64_mode="ozaki" against the CPU oracle under the same parity protocol as
+the DMMA path (tests/test_gpu_parity.py)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import sorsvd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+# error bound of one pass, per output entry, in units of sqrt(K) max|a_row| max|x_col|:
+# the 2^-55 fixed-point grid and the dropped digit levels give ~1e-15 (measured <= 3e-15);
+# FP64 dgemm's own sum rounding is of the same order
+PASS_TOL = 2e-14
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1804_00462_b200 as P
+    return P
+
+
+def _npad(ell):
+    return (ell + 7) // 8 * 8 if ell <= 128 else (ell + 127) // 128 * 128
+
+
+def _pass(P, A, X, ta, m, n, ell, lda=None, dtype=0, reps=1):
+    import torch
+    ctx = P.Context(0)
+    ctx.set_stream(torch.cuda.current_stream(0).cuda_stream)
+    Np = _npad(ell)
+    T = torch.full(((n if ta else m), Np), float("nan"), device="cuda", dtype=torch.float64)
+    ms, msc = ctypes.c_double(), ctypes.c_double()
+    P._check(P._capi.lib().sorsvd_pass_ozaki_device(ctx.handle, ta, m, n, lda or n, ell, dtype, A.data_ptr(),
+                                                     X.data_ptr(), T.data_ptr(), reps, ctypes.byref(ms),
+                                                     ctypes.byref(msc)), ctx.handle)
+    torch.cuda.synchronize()
+    return T
+
+
+def _operands(m, n, ell, ta, seed, lda=None, f32=False):
+    import torch
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    lda = lda or n
+    buf = torch.randn(m, lda, generator=g, device="cuda", dtype=torch.float64)
+    buf *= torch.exp(2.0 * torch.randn(m, 1, generator=g, device="cuda", dtype=torch.float64))  # graded rows
+    if f32:
+        buf = buf.float()
+    A = buf[:, :n]
+    Np = _npad(ell)
+    K = m if ta else n
+    X = torch.zeros(K, Np, device="cuda", dtype=torch.float64)
+    X[:, :ell] = torch.randn(K, ell, generator=g, device="cuda", dtype=torch.float64)
+    return buf, A, X
+
+
+@pytest.mark.parametrize("m,n,ell,ta,lda,f32", [
+    (1000, 700, 20, 0, None, False), (1000, 700, 20, 1, None, False),
+    (4001, 999, 100, 0, None, False), (3999, 1001, 100, 1, None, False),   # odd lda: no TMA
+    (513, 2049, 256, 0, None, False), (513, 2049, 256, 1, None, False),
+    (300, 20000, 10, 1, None, False), (20000, 300, 10, 0, None, False),
+    (130, 33, 8, 0, None, False), (33, 130, 8, 1, None, False),
+    (20000, 2000, 256, 0, None, False), (20000, 2000, 256, 1, None, False),
+    (700, 500, 64, 0, 513, False), (700, 500, 64, 1, 513, False),         # padded lda
+    (4000, 3000, 64, 0, None, True), (4000, 3000, 64, 1, None, True),     # FP32 storage
+    (4000, 3001, 64, 0, None, True), (3001, 4000, 200, 1, None, True),
+    (40000, 1000, 512, 1, None, False), (1000, 40000, 136, 0, None, False),  # several TMEM drains
+])
+def test_ozaki_pass_vs_fp64(P, m, n, ell, ta, lda, f32):
+    import torch
+    buf, A, X = _operands(m, n, ell, ta, m + 7 * n + ell, lda, f32)
+    T = _pass(P, buf, X, ta, m, n, ell, lda=lda or n, dtype=1 if f32 else 0)
+    A64 = A.double()
+    ref = (A64.T if ta else A64) @ X
+    K = m if ta else n
+    amax = A64.abs().amax(dim=0 if ta else 1)
+    xmax = X.abs().amax(dim=0).clamp_min(1e-300)
+    err = (T - ref).abs()[:, :ell] / (amax[:, None] * xmax[None, :ell] * np.sqrt(K)).clamp_min(1e-300)
+    assert not torch.isnan(T[:, :ell]).any()
+    assert err.max().item() <= PASS_TOL, err.max().item()
+    if T.shape[1] > ell:
+        assert torch.all(T[:, ell:] == 0)
+
+
+def test_ozaki_pass_deterministic(P):
+    import torch
+    buf, A, X = _operands(20000, 2000, 256, 1, 5)
+    outs = [_pass(P, buf, X, 1, 20000, 2000, 256) for _ in range(3)]
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+
+
+def test_ozaki_pass_nonfinite_and_zero_rows(P):
+    import torch
+    buf, A, X = _operands(600, 400, 32, 0, 9)
+    A[5, 17] = float("nan")
+    A[9, :] = 0.0
+    X[3, 7] = float("inf")
+    T = _pass(P, buf, X, 0, 600, 400, 32)
+    assert torch.isnan(T[5, :32]).all()        # the row with a NaN
+    assert torch.isnan(T[:, 7]).all()          # the column of X with an Inf
+    ok = [j for j in range(32) if j != 7]
+    assert torch.all(T[9, ok] == 0)            # an all-zero row
+    ref = A @ X
+    rows = [i for i in range(600) if i != 5]
+    d = (T[rows][:, ok] - ref[rows][:, ok]).abs().max().item()
+    assert d <= 1e-12 * ref[rows][:, ok].abs().max().item()
+
+
+# ---------------------------------------------------------- whole decompositions --
+def _check_parity(got, base, ds=None, dl=0.0, tol_s=1e-10, tol_lr=1e-9):
+    s = np.asarray(got.sigma.cpu() if hasattr(got.sigma, "cpu") else got.sigma)
+    u = np.asarray(got.u.cpu() if hasattr(got.u, "cpu") else got.u)
+    v = np.asarray(got.v.cpu() if hasattr(got.v, "cpu") else got.v)
+    es = O.sigma_rel_err(s, base.sigma)
+    lim = np.maximum(tol_s, 10 * np.maximum.accumulate(ds)) if ds is not None else tol_s
+    assert np.all(es <= lim), (es.max(), es)
+    lr = O.lowrank_rel_diff(u, s, v, base.u, base.sigma, base.v)
+    assert lr <= max(tol_lr, 10 * dl), lr
+
+
+def test_ozaki_golden_cases(P, golden):
+    g, meta = golden
+    for name in meta["cases"]:
+        md = meta["meta"][name]
+        A = g[name + "_A"]
+        f = P.sor_svd_power(A, md["k"], P.SketchConfig(md["ell"], md["q"], md["seed"]), fp64_mode="ozaki")
+        assert f.stats["pass_kind"] == 1
+        _, ds, dl = O.perturbation_floor(A, md["k"], O.SketchConfig(md["ell"], md["q"], md["seed"]))
+        base = type("B", (), {"sigma": g[name + "_s"], "u": g[name + "_u"], "v": g[name + "_v"]})
+        _check_parity(f, base, ds, dl)
+
+
+@pytest.mark.parametrize("m,n,k,ell,q,sp", [(400, 300, 10, 10, 0, False), (300, 400, 10, 14, 2, False),
+                                            (2001, 1500, 50, 60, 1, False), (2001, 1500, 50, 60, 1, True),
+                                            (64, 1000, 8, 8, 1, False)])
+def test_ozaki_shapes_vs_oracle(P, m, n, k, ell, q, sp):
+    A = O.gen_lowrank_decay(m, n, min(m, n) - 1 if min(m, n) < 40 else 40, lambda j: 2.0 ** (-j / 4), 1e-3, m + n)
+    cfg = O.SketchConfig(ell, q, 17, single_pass=sp)
+    base, ds, dl = O.perturbation_floor(A, k, cfg)
+    f = P.sor_svd_power(A, k, P.SketchConfig(ell, q, 17, single_pass=sp), fp64_mode="ozaki")
+    _check_parity(f, base, ds, dl)
+
+
+def test_ozaki_config3_scaled_k256_and_f32(P):
+    import torch
+    A = O.gen_lowrank_decay(20000, 2000, 256, lambda j: 10.0 ** (-j / 64.0), 1e-3, 3)
+    cfg = O.SketchConfig(256, 1, 31)
+    base, ds, dl = O.perturbation_floor(A, 256, cfg, trials=1)
+    f = P.sor_svd_power(A, 256, P.SketchConfig(256, 1, 31), fp64_mode="ozaki")
+    _check_parity(f, base, ds, dl)
+    a32 = A.astype(np.float32)
+    base32 = O.sor_svd_power(a32.astype(np.float64), 256, cfg)
+    f32 = P.sor_svd_power(torch.from_numpy(a32).cuda(), 256, P.SketchConfig(256, 1, 31), fp64_mode="ozaki")
+    _check_parity(f32, base32, ds, dl)
+
+
+def test_ozaki_k512(P):
+    A = O.gen_lowrank_decay(4096, 3000, 512, lambda j: 1.0 / j, 1e-6, 5)
+    cfg = O.SketchConfig(512, 1, 41)
+    base, ds, dl = O.perturbation_floor(A, 512, cfg, trials=1, qr_variants=2)
+    f = P.sor_svd_power(A, 512, P.SketchConfig(512, 1, 41), fp64_mode="ozaki")
+    env = np.maximum.accumulate(ds)
+    es = O.sigma_rel_err(f.sigma, base.sigma)
+    assert np.all(es <= np.maximum(1e-10, 10 * env)), es.max()
+
+
+def test_auto_mode_selection(P):
+    import torch
+    small = O.gen_lowrank_decay(400, 300, 20, lambda j: 1.0 / j, 1e-6, 2)
+    assert P.sor_svd_power(small, 10, P.SketchConfig(10, 1, 1)).stats["pass_kind"] == 0    # auto -> DMMA
+    assert P.sor_svd_power(small, 10, P.SketchConfig(10, 1, 1), fp64_mode="ozaki").stats["pass_kind"] == 1
+    big = torch.randn(20000, 20000, dtype=torch.float64, device="cuda")                  # m n ell = 2^36.2
+    f = P.sor_svd_power(big, 200, P.SketchConfig(200, 0, 1))
+    assert f.stats["pass_kind"] == 1
+    assert P.sor_svd_power(big, 200, P.SketchConfig(200, 0, 1), fp64_mode="dmma").stats["pass_kind"] == 0
+    g = P.sor_svd_power(big, 200, P.SketchConfig(200, 0, 1), fp64_mode="dmma")
+    np.testing.assert_allclose(f.sigma.cpu().numpy(), g.sigma.cpu().numpy(), rtol=1e-12)
