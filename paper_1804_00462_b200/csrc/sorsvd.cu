@@ -43,6 +43,7 @@
 #include "jacobi_big_f64.cuh"
 #include "cholc_f64.cuh"
 #include "ozaki_i8.cuh"
+#include "smallk_f64.cuh"
 #include <cfloat>
 
 using namespace sorsvd_dev;
@@ -1373,6 +1374,19 @@ void qr_run(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int64_t
     const int k = p->k, Np = p->Np;
     const int L = (int)p->nodes.size() - 1;
     auto gram = [&](const double* X, int64_t ldx, double* G) {
+        if (k <= 32) {  // one launch: per-warp register partials, last-CTA ordered sum (smallk_f64.cuh)
+            const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->num_sms, cdiv(p->rows, 128)));
+            double* ws = dbuf(c, p->ws_name + ":gram", (size_t)c->num_sms * 32 * 32);
+            unsigned int* ticket = reinterpret_cast<unsigned int*>(dbuf(c, p->ws_name + ":ticket", 1));
+            if (k <= 16)
+                gram_tall_kernel<16><<<grid, kGramThreads, 0, s>>>(X, ldx, p->rows, k, ws, ticket, G, Np, c->pred,
+                                                                   c->pred_skip);
+            else
+                gram_tall_kernel<32><<<grid, kGramThreads, 0, s>>>(X, ldx, p->rows, k, ws, ticket, G, Np, c->pred,
+                                                                   c->pred_skip);
+            check_launch(c);
+            return;
+        }
         GemmCall g;
         g.ta = true;
         g.A = X;

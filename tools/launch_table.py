@@ -21,7 +21,8 @@ def load(path):
 
 
 if __name__ == "__main__":
-    seq = [(n, v) for n, v in load(sys.argv[1]) if "sorsvd_dev" in n or "gemm" in n and "cutlass" not in n]
+    seq = [(n, v) for n, v in load(sys.argv[1]) if "at::" not in n and "cutlass" not in n and "cublas" not in n.lower()
+           and "elementwise" not in n and "distribution" not in n]
     tot, cnt = collections.OrderedDict(), collections.Counter()
     for n, v in seq:
         key = n.split("(")[0].replace("void ", "").replace("sorsvd_dev::", "")
