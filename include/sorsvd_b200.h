@@ -260,6 +260,9 @@ int sorsvd_measure_peaks(sorsvd_ctx* ctx, double* fp64_tflops, double* hbm_read_
 /* One A-streaming pass (sketch.hpp:95 when ta = 0, :96 when ta = 1) repeated
  * `reps` times between CUDA events; dX / dT padded to ld = ell rounded up to 8
  * (or to 128 when ell > 128). Reports the average pass time. */
+/* Test hook: copy count doubles of the context workspace buffer `name` ("T1", "T2", "Q1", "Q2",
+ * "Mk", ...) to the device pointer dst. */
+int sorsvd_debug_buffer(sorsvd_ctx* ctx, const char* name, double* dst, int64_t count);
 /* The Ozaki scale exponents of A (tests): row_e[m], col_e[n] (device), max|.| < 2^e. */
 int sorsvd_ozaki_scales_device(sorsvd_ctx* ctx, int64_t m, int64_t n, int64_t lda, int32_t dtype, const void* dA,
                                int32_t* row_e, int32_t* col_e);

@@ -102,6 +102,7 @@ SIGNATURES = [
     ("sorsvd_matmul_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]),
     ("sorsvd_matmul_f32_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]),
     ("sorsvd_measure_peaks", c_i32, [c_vp, c_dp, c_dp]),
+    ("sorsvd_debug_buffer", c_i32, [c_vp, ctypes.c_char_p, c_vp, c_i64]),
     ("sorsvd_ozaki_scales_device", c_i32, [c_vp, c_i64, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp]),
     ("sorsvd_pass_ozaki_device", c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32,
                                          c_dp, c_dp]),

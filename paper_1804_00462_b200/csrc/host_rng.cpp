@@ -67,7 +67,10 @@ void gaussian_fill(double* out, uint64_t count, uint64_t seed, int nthreads) {
     std::vector<std::thread> th;
     const uint64_t per = ((count / nt) + 1) & ~1ULL;  // even chunk starts keep pairs together
     for (uint64_t t = 0; t < nt; ++t) {
-        const uint64_t a = t * per, b = (t + 1) * per < count ? (t + 1) * per : count;
+        // the last chunk runs to the end: nt * per can fall short of count (per is rounded
+        // down to even), which left the last element pair of Omega unwritten
+        const uint64_t a = t * per;
+        const uint64_t b = (t + 1 == nt || (t + 1) * per > count) ? count : (t + 1) * per;
         if (a >= b) break;
         th.emplace_back(fill_range, out, a, b, seed);
     }

@@ -1953,9 +1953,18 @@ void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const int* lexp, con
 // (row blocks of T2), and each finished block's all-reduce is issued on the comm
 // stream while the next block's GEMM runs, so only the last block's reduction
 // is exposed; the compute stream joins the comm stream before T2 is used.
-void tn_pass_reduced(sorsvd_ctx* c, const SorProblem& P, const double* T1, double* T2, cudaStream_t s) {
+void tn_pass_reduced(sorsvd_ctx* c, const SorProblem& P, const double* T1, double* T2, cudaStream_t s,
+                     const int* oz_col_e = nullptr) {
     const int Np = P.Np;
     auto tn = [&](int64_t n0, int64_t n1) {
+        if (P.ozaki) {  // the column block [n0, n1) of A as its own TN problem (its columns' exponents)
+            SorProblem Q = P;
+            Q.A = P.A ? P.A + n0 : nullptr;
+            Q.Af = P.Af ? P.Af + n0 : nullptr;
+            Q.n = n1 - n0;
+            run_ozaki(c, Q, true, oz_col_e + n0, T1, T2 + n0 * Np, s);
+            return;
+        }
         GemmCall g2;
         g2.ta = true;
         g2.A = P.A ? P.A + n0 : nullptr;
@@ -1972,7 +1981,7 @@ void tn_pass_reduced(sorsvd_ctx* c, const SorProblem& P, const double* T1, doubl
         run_gemm(c, g2, s);
     };
     constexpr int NB = sorsvd_ctx::kTnBlocks;
-    const int BM = gemm_bm_for(Np);
+    const int BM = P.ozaki ? kOzBM : gemm_bm_for(Np);
     if (c->world <= 1 || P.n < (int64_t)NB * BM) {
         tn(0, P.n);
         allreduce_sum(c, T2, (size_t)P.n * Np, s);
@@ -2016,8 +2025,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         }
         if (P.ozaki) {  // FP64 passes as int8 slice products (ozaki_i8.cuh)
             run_ozaki(c, P, false, oz.row_e, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
-            run_ozaki(c, P, true, oz.col_e, b.T1, b.T2, s);   // T2 = A^T T1 (sketch.hpp:96)
-            allreduce_sum(c, b.T2, (size_t)P.n * Np, s);
+            tn_pass_reduced(c, P, b.T1, b.T2, s, oz.col_e);   // T2 = A^T T1 (sketch.hpp:96), summed over ranks
             continue;
         }
         GemmCall g1;  // T1 = A * T2     (sketch.hpp:95); FP32 A widened to FP64 in the kernel
@@ -3882,6 +3890,19 @@ static int pass_device_impl(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, int
         CK(cudaEventElapsedTime(&ms, c->ev_a, c->ev_b));
         if (ms_avg) *ms_avg = ms / std::max(reps, 1);
         if (launches_per_pass) *launches_per_pass = (c->launches - l0) / std::max(reps, 1);
+    });
+}
+
+// Test hook: copy `count` doubles of the context workspace buffer `name` (e.g. "T1",
+// "T2", "Q1", "Q2", "Mk") to dst, after the stream's work so far.
+int sorsvd_debug_buffer(sorsvd_ctx* c, const char* name, double* dst, int64_t count) {
+    if (!c || !name || !dst) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        auto it = c->bufs.find(name);
+        if (it == c->bufs.end() || it->second.bytes < (size_t)count * 8)
+            throw Error{SORSVD_ERR_PARAMETER, std::string("parameter: no workspace buffer ") + name};
+        CK(cudaMemcpyAsync(dst, it->second.p, (size_t)count * 8, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
     });
 }
 

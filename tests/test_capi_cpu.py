@@ -57,6 +57,10 @@ def test_gaussian_matrix_matches_reference_stream(lib):
             assert np.array_equal(P.gaussian_matrix(r, c, s, nthreads=nt), O.gaussian_matrix(r, c, s))
     big = P.gaussian_matrix(1000, 333, 5)  # multi-threaded path, odd split points
     assert np.array_equal(big, O.gaussian_matrix(1000, 333, 5))
+    # thread counts whose even-rounded chunk undershoots the total: the last chunk must run
+    # to the end (1100 x 64 on 3 threads left the final pair unwritten)
+    for (r, c, nt) in [(1100, 64, 3), (1100, 64, 0), (1025, 64, 7), (800, 100, 5), (70001, 1, 3), (4000, 100, 16)]:
+        assert np.array_equal(P.gaussian_matrix(r, c, 9, nthreads=nt), O.gaussian_matrix(r, c, 9)), (r, c, nt)
 
 
 def test_sub_seed_and_flops(lib):

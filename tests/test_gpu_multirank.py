@@ -13,7 +13,7 @@ from oracle import sorsvd_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _run_sharded(P, torch, A, k, cfg, world, dtype=None):
+def _run_sharded(P, torch, A, k, cfg, world, dtype=None, fp64_mode="auto"):
     m = A.shape[0]
     g = P.EmuGroup(world)
     base, extra = divmod(m, world)
@@ -33,7 +33,7 @@ def _run_sharded(P, torch, A, k, cfg, world, dtype=None):
             blk = torch.from_numpy(np.ascontiguousarray(A[a:b])).cuda()
             if dtype is not None:
                 blk = blk.to(dtype)
-            out[r] = P.sor_svd_power(blk, k, cfg, ctx=ctxs[r], m_global=m)
+            out[r] = P.sor_svd_power(blk, k, cfg, ctx=ctxs[r], m_global=m, fp64_mode=fp64_mode)
             torch.cuda.synchronize()
         except Exception as e:  # surface in the main thread
             err[r] = e
@@ -78,6 +78,25 @@ def test_sharded_matches_oracle(env, world, m, n, k, q):
     es = O.sigma_rel_err(s0, base.sigma)
     assert np.all(es <= np.maximum(1e-10, 10 * np.maximum.accumulate(ds))), es
     lr = O.lowrank_rel_diff(u, s0, v0, base.u, base.sigma, base.v)
+    assert lr <= max(1e-9, 10 * dl), lr
+
+
+@pytest.mark.parametrize("world,m,n,k,q", [(2, 3000, 800, 20, 1), (4, 6000, 1100, 64, 1), (3, 2999, 700, 16, 2)])
+def test_sharded_ozaki_matches_oracle(env, world, m, n, k, q):
+    # the int8 tensor-core passes over row blocks: per-rank scales, the T2 partials summed in
+    # FP64 across ranks in column blocks on the comm stream (tn_pass_reduced)
+    P, torch = env
+    A = O.gen_lowrank_decay(m, n, 40, lambda j: 2.0 ** (-j / 4), 1e-3, m + world + 1)
+    cfg = O.SketchConfig(k, q, 13)
+    base, ds, dl = O.perturbation_floor(A, k, cfg)
+    out, u = _run_sharded(P, torch, A, k, P.SketchConfig(k, q, 13), world, fp64_mode="ozaki")
+    assert all(o.stats["pass_kind"] == 1 for o in out)
+    s0 = out[0].sigma.cpu().numpy()
+    for o in out[1:]:
+        np.testing.assert_array_equal(o.sigma.cpu().numpy(), s0)
+    es = O.sigma_rel_err(s0, base.sigma)
+    assert np.all(es <= np.maximum(1e-10, 10 * np.maximum.accumulate(ds))), es
+    lr = O.lowrank_rel_diff(u, s0, out[0].v.cpu().numpy(), base.u, base.sigma, base.v)
     assert lr <= max(1e-9, 10 * dl), lr
 
 
