@@ -9,9 +9,9 @@ cap() {  # regex tag cmd...
   echo "$tag rc=$?"
   ncu -i /tmp/k_$tag.ncu-rep --page raw --csv > gpurun_out/ncuk_${tag}_raw.csv 2>/dev/null
 }
-cap cqr_kernel cqr python tools/time_qr_c2.py 4000 100
-cap jacobi_p2p jac100 python tools/one_svd.py 100
-cap rpca_update rpca python tools/one_c4.py
+cap cqr_kernel cqr python tools/time_qr.py 4000 100
+cap jacobi_p2p jac100 python tools/time_jacobi.py 100
+cap rpca_update rpca python tools/run_config.py c4
 cap approx_err aerr python -c "
 import sys; sys.path.insert(0, '.')
 import torch, bench, paper_1804_00462_b200 as P

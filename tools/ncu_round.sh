@@ -3,8 +3,8 @@
 # (summarised to CSV on the box; only the C2 NN report itself is kept).
 set -u
 mkdir -p gpurun_out
-python tools/one_c2.py > /dev/null 2>&1 || exit 1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python tools/one_c2.py > /dev/null 2>&1
+python tools/run_config.py c2 > /dev/null 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python tools/run_config.py c2 > /dev/null 2>&1
 for spec in "c2 0" "c2 1" "c3 0" "c3tf32 0"; do
   set -- $spec
   python tools/run_pass.py --config $1 --ta $2 --reps 2 > /dev/null 2>&1 || { echo "pass $1 failed"; continue; }
