@@ -102,7 +102,8 @@ typedef struct sorsvd_stats {
     int32_t launches;    /* kernel launches issued for the call */
     int32_t jacobi_sweeps;
     int32_t pass_kind;   /* how the passes over A ran: 0 FP64 DMMA, 1 Ozaki int8 (FP64), 2 TF32 */
-    int32_t reserved;
+    int32_t oz_planes;   /* pass_kind 1: 1 = the passes streamed digit planes of A cut once per call
+                            (SORSVD_OPT_OZAKI_PLANES), 0 = A converted inside every pass */
 } sorsvd_stats;
 
 /* ---- context -------------------------------------------------------------- */
@@ -117,6 +118,9 @@ void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
  * these to cross-check kernel variants against each other). */
 #define SORSVD_OPT_JACOBI 1          /* value: sorsvd_jacobi_variant */
 #define SORSVD_OPT_SORD_CHUNK_MB 2   /* value: staging chunk of the SORD loader, MiB (default 64) */
+#define SORSVD_OPT_OZAKI_PLANES 3    /* value: 1 (default) = the Ozaki engine cuts A into int8 digit planes once per
+                                        call (7/8 of an FP64 A of extra HBM, taken when it fits) and its passes
+                                        stream them; 0 = always convert A inside every pass */
 #define SORSVD_JACOBI_AUTO 0         /* by k: CTA / point-to-point ring / barrier ring / rotation log */
 #define SORSVD_JACOBI_BARRIER 1      /* barrier cluster ring instead of the point-to-point ring */
 #define SORSVD_JACOBI_ROTLOG 2       /* the k > 256 rotation-log kernel at any k >= 8 */

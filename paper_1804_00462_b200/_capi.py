@@ -41,7 +41,7 @@ class SorsvdStats(ctypes.Structure):
                 ("ms_passes", ctypes.c_double), ("ms_qr", ctypes.c_double), ("ms_project", ctypes.c_double),
                 ("ms_svd", ctypes.c_double), ("ms_basis", ctypes.c_double), ("flops_passes", ctypes.c_double),
                 ("bytes_passes", ctypes.c_double), ("passes", c_i32), ("method", c_i32), ("launches", c_i32),
-                ("jacobi_sweeps", c_i32), ("pass_kind", c_i32), ("reserved", c_i32)]
+                ("jacobi_sweeps", c_i32), ("pass_kind", c_i32), ("oz_planes", c_i32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

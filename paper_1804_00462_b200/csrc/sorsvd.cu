@@ -43,6 +43,7 @@
 #include "jacobi_big_f64.cuh"
 #include "cholc_f64.cuh"
 #include "ozaki_i8.cuh"
+#include "ozaki_planes_i8.cuh"
 #include "smallk_f64.cuh"
 #include <cfloat>
 
@@ -198,6 +199,7 @@ struct sorsvd_emu_group {
 
 struct sorsvd_ctx {
     int opt_jacobi = SORSVD_JACOBI_AUTO;  // sorsvd_ctx_set_option(SORSVD_OPT_JACOBI)
+    int opt_oz_planes = 1;                // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_PLANES): 0 = convert inside every pass
     int64_t opt_sord_chunk_mb = 64;       // sorsvd_ctx_set_option(SORSVD_OPT_SORD_CHUNK_MB)
     int device = 0;
     int rank = 0, world = 1;
@@ -1696,6 +1698,7 @@ struct SorProblem {
     bool single_pass;
     bool tf32;         // dtype F32 with SORSVD_FLAG_TF32: passes on the tcgen05 tensor cores
     bool ozaki;        // SORSVD_FLAG_OZAKI: FP64 passes as int8 slice products on the tcgen05 tensor cores
+    bool oz_planes = false;  // ... from digit planes of A cut once per call (ozaki_planes_i8.cuh), memory permitting
     int method = SORSVD_SOR_POWER;  // SORSVD_RSVD / SORSVD_TSR: the baselines of sketch.hpp:124-149
 };
 
@@ -1852,12 +1855,62 @@ void enqueue_m_approx(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, c
 struct OzScales {
     const int* row_e = nullptr;  // m
     const int* col_e = nullptr;  // n
+    // the call's digit planes of A (ozaki_planes_i8.cuh), or null: converted inside every pass
+    int8_t* planes = nullptr;
+    int64_t pitch = 0, plane_stride = 0;
+    int64_t pm = 0, pn = 0;      // the planes' matrix (tensor-map extents)
 };
 
+int64_t oz_planes_pitch(int64_t n) { return (n + 15) / 16 * 16; }
+
+// Can this call keep 7 digit planes of A (7/8 of an FP64 A) beside A? Decided
+// before anything is enqueued (the answer is baked into the captured graph).
+bool oz_planes_fit(sorsvd_ctx* c, const SorProblem& P) {
+    if (c->opt_oz_planes == 0 || P.m >= INT_MAX || P.n >= INT_MAX) return false;
+    const size_t bytes = (size_t)kOzSlices * (size_t)P.m * (size_t)oz_planes_pitch(P.n);
+    auto it = c->bufs.find("oz_planes");
+    const size_t have = it == c->bufs.end() ? 0 : it->second.bytes;
+    if (have >= bytes) return true;
+    if (c->capturing) return false;
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    // growing frees the old buffer first; keep room for the call's other workspaces
+    const size_t reserve = (size_t)4 << 30;
+    return fr + have >= bytes + reserve + (size_t)(P.m + P.n) * P.Np * 8 * 4;
+}
+
+template <typename AT>
+void launch_rowplanes(sorsvd_ctx* c, const AT* A, const SorProblem& P, int* re, const OzScales& oz, cudaStream_t s) {
+    const int vec = ((uintptr_t)A % 16) == 0 && (P.lda * (int64_t)sizeof(AT)) % 16 == 0;
+    if (P.n >= 4096) {  // a block per row
+        const unsigned blocks = (unsigned)std::min<int64_t>(P.m, (int64_t)c->num_sms * 2);
+        ozaki_rowplanes_kernel<AT, 512><<<blocks, 512, 0, s>>>(A, P.lda, P.m, P.n, re, oz.planes, oz.pitch,
+                                                               oz.plane_stride, vec, c->pred, c->pred_skip);
+    } else {  // a warp per row
+        const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(P.m, 16), (int64_t)c->num_sms * 2);
+        ozaki_rowplanes_kernel<AT, 32><<<blocks, 512, 0, s>>>(A, P.lda, P.m, P.n, re, oz.planes, oz.pitch,
+                                                              oz.plane_stride, vec, c->pred, c->pred_skip);
+    }
+}
+
 OzScales oz_prepare_a(sorsvd_ctx* c, const SorProblem& P, cudaStream_t s) {
+    int* re = reinterpret_cast<int*>(dbuf(c, "oz_rowe", (size_t)(P.m + 1) / 2));
+    if (P.oz_planes) {
+        // cut A into its row-scaled digit planes once (row maxima and digits in one read of A);
+        // every pass of the call streams the planes, TN passes fold the row scales into T1
+        OzScales oz{re, nullptr};
+        oz.pitch = oz_planes_pitch(P.n);
+        oz.plane_stride = oz.pitch * P.m;
+        oz.pm = P.m;
+        oz.pn = P.n;
+        oz.planes = reinterpret_cast<int8_t*>(dbuf(c, "oz_planes", (size_t)(kOzSlices * oz.plane_stride + 7) / 8));
+        if (P.dtype == SORSVD_F32) launch_rowplanes<float>(c, P.Af, P, re, oz, s);
+        else launch_rowplanes<double>(c, P.A, P, re, oz, s);
+        check_launch(c);
+        return oz;
+    }
     auto* rmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_rowmax", (size_t)P.m));
     auto* cmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_colmax", (size_t)P.n));
-    int* re = reinterpret_cast<int*>(dbuf(c, "oz_rowe", (size_t)(P.m + 1) / 2));
     int* ce = reinterpret_cast<int*>(dbuf(c, "oz_cole", (size_t)(P.n + 1) / 2));
     CK(cudaMemsetAsync(rmax, 0, (size_t)P.m * 8, s));
     CK(cudaMemsetAsync(cmax, 0, (size_t)P.n * 8, s));
@@ -1901,32 +1954,114 @@ void launch_ozaki_t(const OzArgs& a0, unsigned grid, cudaStream_t s) {
     }
 }
 
-// C (M x Np) = op(A) X with X (K x Np row-major): NN (M = m, K = n, lexp = rows)
-// or TN (M = n, K = m, lexp = columns). X is cut into digit planes first.
-void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const int* lexp, const double* X, double* C,
-               cudaStream_t s, int dbg = 0) {
+// Split-K for the planes engine: the number of K splits that minimises the modelled pass
+// time on `sms` SMs (waves x (steps per split + fixed cost per CTA) + the partial sum).
+int oz_pick_splits(int64_t tiles, int KT, int64_t out_bytes, int sms) {
+    const double t_step = 0.62, t_fixed = 8.0;  // us: one 32-deep K step (34 digit MMAs); CTA prologue + drain
+    int best = 1;
+    double best_cost = 1e300;
+    for (int S = 1; S <= 16; ++S) {
+        const int per = (int)cdiv(KT, S);
+        if (S > 1 && per < 96) break;
+        const int Se = (int)cdiv(KT, per);
+        const double waves = (double)cdiv(tiles * Se, sms);
+        double cost = waves * (per * t_step + t_fixed);
+        if (Se > 1) cost += 5.0 + (double)(Se + 1) * (double)out_bytes / 5.0e6;  // reduce: 5 TB/s
+        if (cost < best_cost * 0.98) {
+            best_cost = cost;
+            best = Se;
+        }
+    }
+    return best;
+}
+
+// C (M x Np) = op(A) X with X (K x Np row-major): NN (M = m, K = n, left rows = rows
+// of A) or TN (M = n, K = m, left rows = columns [n0, n0 + P.n) of the call's A; P
+// describes that column block). X is cut into digit planes first. With the call's
+// digit planes of A (oz.planes) the pass streams them (ozaki_planes_i8.cuh), else A
+// is converted inside the pass kernel (ozaki_i8.cuh).
+void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const double* X, double* C,
+               cudaStream_t s, int dbg = 0, int64_t n0 = 0) {
     const int Np = P.Np;
     const int NC = (int)cdiv(Np, kOzBN);
     const int64_t M = ta ? P.n : P.m, K = ta ? P.m : P.n;
     const int64_t KT = cdiv(K, kOzBK);
+    const bool planes = oz.planes != nullptr;
     auto* xmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_xmax", (size_t)Np));
     int* xexp = reinterpret_cast<int*>(dbuf(c, "oz_xexp", (size_t)(Np + 1) / 2));
     int8_t* Xd = reinterpret_cast<int8_t*>(dbuf(c, ta ? "oz_xd_tn" : "oz_xd_nn", (size_t)(KT * NC * kOzXStep + 7) / 8));
     CK(cudaMemsetAsync(xmax, 0, (size_t)Np * 8, s));
-    ozaki_colmax_kernel<<<dim3((unsigned)cdiv(Np, 256), (unsigned)cdiv(K, 256)), 256, 0, s>>>(X, Np, K, Np, xmax);
-    check_launch(c);
-    ozaki_exp_kernel<<<1, 256, 0, s>>>(xmax, Np, xexp);
-    check_launch(c);
+    const dim3 cgrid((unsigned)cdiv(Np, 256), (unsigned)cdiv(K, 256));
     const int64_t items = KT * 2 * (int64_t)NC * kOzBN;
-    ozaki_xdigits_kernel<<<(unsigned)std::min<int64_t>(cdiv(items, 256), (int64_t)c->num_sms * 16), 256, 0, s>>>(
-        X, Np, K, Np, NC, xexp, Xd);
-    check_launch(c);
+    const unsigned xblocks = (unsigned)std::min<int64_t>(cdiv(items, 256), (int64_t)c->num_sms * 16);
+    if (planes && ta) {  // the planes are row-scaled: A's row scales ride on the right operand
+        ozaki_colmax_scaled_kernel<<<cgrid, 256, 0, s>>>(X, Np, K, Np, oz.row_e, xmax);
+        check_launch(c);
+        ozaki_exp_kernel<<<1, 256, 0, s>>>(xmax, Np, xexp);
+        check_launch(c);
+        ozaki_xdigits_scaled_kernel<<<xblocks, 256, 0, s>>>(X, Np, K, Np, NC, oz.row_e, xexp, Xd);
+        check_launch(c);
+    } else {
+        ozaki_colmax_kernel<<<cgrid, 256, 0, s>>>(X, Np, K, Np, xmax);
+        check_launch(c);
+        ozaki_exp_kernel<<<1, 256, 0, s>>>(xmax, Np, xexp);
+        check_launch(c);
+        ozaki_xdigits_kernel<<<xblocks, 256, 0, s>>>(X, Np, K, Np, NC, xexp, Xd);
+        check_launch(c);
+    }
+    if (planes) {
+        OzpArgs a{};
+        a.M = M;
+        a.K = K;
+        a.mn0 = (int)n0;
+        a.lexp = ta ? nullptr : oz.row_e;
+        a.Xd = Xd;
+        a.xexp = xexp;
+        a.NC = NC;
+        a.N = Np;
+        a.ldc = Np;
+        a.dbg = dbg;
+        a.pred = c->pred;
+        a.pred_skip = c->pred_skip;
+        const int64_t tiles = cdiv(M, kOzBM) * NC;
+        const int S = oz_pick_splits(tiles, (int)KT, M * Np * 8, c->num_sms);
+        a.kt_split = (int)cdiv(KT, S);
+        a.c_split_stride = M * Np;
+        double* ws = S > 1 ? dbuf(c, "oz_split", (size_t)S * M * Np) : nullptr;
+        a.C = S > 1 ? ws : C;
+        CUtensorMap map{};
+        cuuint64_t dims[3] = {(cuuint64_t)oz.pn, (cuuint64_t)oz.pm, (cuuint64_t)kOzSlices};
+        cuuint64_t strides[2] = {(cuuint64_t)oz.pitch, (cuuint64_t)oz.plane_stride};
+        cuuint32_t box[3] = {(cuuint32_t)(ta ? kOzBM : kOzBK), (cuuint32_t)(ta ? kOzBK : kOzBM), (cuuint32_t)kOzSlices};
+        cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, oz.planes, dims, strides, box, es,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    ta ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error{SORSVD_ERR_CUDA, "cuda: cuTensorMapEncodeTiled (planes) failed " + std::to_string((int)r)};
+        const dim3 grid((unsigned)tiles, (unsigned)S);
+        if (ta) {
+            allow_smem(ozaki_planes_gemm_kernel<true>);
+            ozaki_planes_gemm_kernel<true><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
+        } else {
+            allow_smem(ozaki_planes_gemm_kernel<false>);
+            ozaki_planes_gemm_kernel<false><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
+        }
+        check_launch(c);
+        if (S > 1) {
+            const int64_t count2 = M * Np / 2;
+            const int blocks = (int)std::min<int64_t>(cdiv(count2, 256), (int64_t)c->num_sms * 8);
+            reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, M * Np, C, c->pred, c->pred_skip);
+            check_launch(c);
+        }
+        return;
+    }
     OzArgs a{};
     a.A = P.dtype == SORSVD_F32 ? static_cast<const void*>(P.Af) : static_cast<const void*>(P.A);
     a.lda = P.lda;
     a.M = M;
     a.K = K;
-    a.lexp = lexp;
+    a.lexp = ta ? oz.col_e + n0 : oz.row_e;
     a.Xd = Xd;
     a.xexp = xexp;
     a.NC = NC;
@@ -1954,7 +2089,7 @@ void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const int* lexp, con
 // stream while the next block's GEMM runs, so only the last block's reduction
 // is exposed; the compute stream joins the comm stream before T2 is used.
 void tn_pass_reduced(sorsvd_ctx* c, const SorProblem& P, const double* T1, double* T2, cudaStream_t s,
-                     const int* oz_col_e = nullptr) {
+                     const OzScales* oz = nullptr) {
     const int Np = P.Np;
     auto tn = [&](int64_t n0, int64_t n1) {
         if (P.ozaki) {  // the column block [n0, n1) of A as its own TN problem (its columns' exponents)
@@ -1962,7 +2097,7 @@ void tn_pass_reduced(sorsvd_ctx* c, const SorProblem& P, const double* T1, doubl
             Q.A = P.A ? P.A + n0 : nullptr;
             Q.Af = P.Af ? P.Af + n0 : nullptr;
             Q.n = n1 - n0;
-            run_ozaki(c, Q, true, oz_col_e + n0, T1, T2 + n0 * Np, s);
+            run_ozaki(c, Q, true, *oz, T1, T2 + n0 * Np, s, 0, n0);
             return;
         }
         GemmCall g2;
@@ -2024,8 +2159,8 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
             continue;
         }
         if (P.ozaki) {  // FP64 passes as int8 slice products (ozaki_i8.cuh)
-            run_ozaki(c, P, false, oz.row_e, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
-            tn_pass_reduced(c, P, b.T1, b.T2, s, oz.col_e);   // T2 = A^T T1 (sketch.hpp:96), summed over ranks
+            run_ozaki(c, P, false, oz, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
+            tn_pass_reduced(c, P, b.T1, b.T2, s, &oz);  // T2 = A^T T1 (sketch.hpp:96), summed over ranks
             continue;
         }
         GemmCall g1;  // T1 = A * T2     (sketch.hpp:95); FP32 A widened to FP64 in the kernel
@@ -2091,7 +2226,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g.ldc = Np;
         g.Af = P.Af;
         g.sk_bias = Np <= 128 ? 1.0 : 0.95;
-        if (P.ozaki) run_ozaki(c, P, false, oz.row_e, b.Q2, b.Y, s);
+        if (P.ozaki) run_ozaki(c, P, false, oz, b.Q2, b.Y, s);
         else if (!P.tf32) run_gemm(c, g, s);
         GemmCall h;
         h.ta = true;
@@ -2320,8 +2455,8 @@ void check_result_finite(sorsvd_ctx* c, const double* dS, int k, const void* A, 
 // on the same A must not replay it).
 std::string sor_key(const SorProblem& P, const int* pred, int pred_skip) {
     char buf[320];
-    snprintf(buf, sizeof buf, "sor%d:%d:%d:%d%d:%p:%lld:%lld:%lld:%d:%d:%d", P.method, P.dtype, (int)P.single_pass,
-             (int)P.tf32, (int)P.ozaki,
+    snprintf(buf, sizeof buf, "sor%d:%d:%d:%d%d%d:%p:%lld:%lld:%lld:%d:%d:%d", P.method, P.dtype, (int)P.single_pass,
+             (int)P.tf32, (int)P.ozaki, (int)P.oz_planes,
              P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m, (long long)P.n,
              (long long)P.lda, P.k, P.ell, P.q);
     if (pred) snprintf(buf + strlen(buf), sizeof buf - strlen(buf), ":pred%p/%d", (const void*)pred, pred_skip);
@@ -2383,6 +2518,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     P.ozaki = !P.tf32 && !baseline && ozaki_wanted(d->flags, P.m, P.n, P.ell);
     QrPlan *p1, *p2, *pg;
     SorBuffers b = prepare_sor(c, P, &p1, &p2, &pg);
+    P.oz_planes = P.ozaki && oz_planes_fit(c, P);
     double* psi2_in = nullptr;
     if (method == SORSVD_TSR) {  // Psi2 = gaussian_matrix(m, ell, seed ^ 1)   (sketch.hpp:142)
         psi2_in = dbuf(c, "psi2_in", (size_t)P.m * P.ell);
@@ -2498,6 +2634,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         st->bytes_passes = (double)d->m * d->n * (d->dtype == SORSVD_F32 ? 4.0 : 8.0) * launched;
         st->launches = launches;
         st->pass_kind = P.tf32 ? 2 : P.ozaki ? 1 : 0;
+        st->oz_planes = P.oz_planes ? 1 : 0;
         int sw = 0;
         CK(cudaMemcpy(&sw, b.sweeps, sizeof(int), cudaMemcpyDeviceToHost));
         st->jacobi_sweeps = sw;
@@ -3446,6 +3583,10 @@ int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
                 c->opt_jacobi = (int)value;
                 invalidate_graphs(c);  // captured calls baked the previous variant in
                 break;
+            case SORSVD_OPT_OZAKI_PLANES:
+                c->opt_oz_planes = value != 0;
+                invalidate_graphs(c);
+                break;
             case SORSVD_OPT_SORD_CHUNK_MB:
                 if (value < 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: SORD chunk must be >= 1 MiB"};
                 c->opt_sord_chunk_mb = value;
@@ -3948,13 +4089,14 @@ int sorsvd_pass_ozaki_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, in
         P.k = ell;
         P.Np = npad(ell);
         P.ozaki = true;
+        P.oz_planes = oz_planes_fit(c, P);
         CK(cudaEventRecord(c->ev_h[0], c->stream));
         OzScales oz = oz_prepare_a(c, P, c->stream);
         CK(cudaEventRecord(c->ev_h[1], c->stream));
-        run_ozaki(c, P, ta != 0, ta ? oz.col_e : oz.row_e, dX, dT, c->stream);  // warm-up
+        run_ozaki(c, P, ta != 0, oz, dX, dT, c->stream);  // warm-up
         CK(cudaEventRecord(c->ev_a, c->stream));
         for (int r = 0; r < reps; ++r)
-            run_ozaki(c, P, ta != 0, ta ? oz.col_e : oz.row_e, dX, dT, c->stream, dbg);
+            run_ozaki(c, P, ta != 0, oz, dX, dT, c->stream, dbg);
         CK(cudaEventRecord(c->ev_b, c->stream));
         CK(cudaEventSynchronize(c->ev_b));
         float ms = 0.f, msc = 0.f;

@@ -1,5 +1,6 @@
-"""The Ozaki-scheme FP64 passes (ozaki_i8.cuh: exact int8 slice products on
-the tcgen05 tensor cores) against FP64 references: the pass kernel itself
+"""The Ozaki-scheme FP64 passes (exact int8 slice products on the tcgen05
+tensor cores; ozaki_planes_i8.cuh: A cut into digit planes once per call,
+ozaki_i8.cuh: A converted inside every pass) against FP64 references: the pass kernel itself
 against an FP64 GEMM of the same operands, and whole sor_svd_power calls in
 fp64_mode="ozaki" against the CPU oracle under the same parity protocol as
 the DMMA path (tests/test_gpu_parity.py)."""
@@ -31,9 +32,10 @@ def _npad(ell):
     return (ell + 7) // 8 * 8 if ell <= 128 else (ell + 127) // 128 * 128
 
 
-def _pass(P, A, X, ta, m, n, ell, lda=None, dtype=0, reps=1):
+def _pass(P, A, X, ta, m, n, ell, lda=None, dtype=0, reps=1, planes=True):
     import torch
     ctx = P.Context(0)
+    ctx.set_option(P.Context.OPT_OZAKI_PLANES, int(planes))
     ctx.set_stream(torch.cuda.current_stream(0).cuda_stream)
     Np = _npad(ell)
     T = torch.full(((n if ta else m), Np), float("nan"), device="cuda", dtype=torch.float64)
@@ -73,15 +75,21 @@ def _operands(m, n, ell, ta, seed, lda=None, f32=False):
     (4000, 3000, 64, 0, None, True), (4000, 3000, 64, 1, None, True),     # FP32 storage
     (4000, 3001, 64, 0, None, True), (3001, 4000, 200, 1, None, True),
     (40000, 1000, 512, 1, None, False), (1000, 40000, 136, 0, None, False),  # several TMEM drains
+    (70000, 600, 64, 1, None, False),                                        # planes engine: split-K
 ])
-def test_ozaki_pass_vs_fp64(P, m, n, ell, ta, lda, f32):
+@pytest.mark.parametrize("planes", [True, False])
+def test_ozaki_pass_vs_fp64(P, m, n, ell, ta, lda, f32, planes):
     import torch
     buf, A, X = _operands(m, n, ell, ta, m + 7 * n + ell, lda, f32)
-    T = _pass(P, buf, X, ta, m, n, ell, lda=lda or n, dtype=1 if f32 else 0)
+    T = _pass(P, buf, X, ta, m, n, ell, lda=lda or n, dtype=1 if f32 else 0, planes=planes)
     A64 = A.double()
     ref = (A64.T if ta else A64) @ X
     K = m if ta else n
+    # the per-call planes are scaled by rows for both orientations: the TN error is relative to
+    # the largest row maximum met in the column, not to the column's own maximum
     amax = A64.abs().amax(dim=0 if ta else 1)
+    if ta and planes:
+        amax = torch.maximum(amax, (A64.abs().amax(dim=1)[:, None] * (A64 != 0)).amax(dim=0))
     xmax = X.abs().amax(dim=0).clamp_min(1e-300)
     err = (T - ref).abs()[:, :ell] / (amax[:, None] * xmax[None, :ell] * np.sqrt(K)).clamp_min(1e-300)
     assert not torch.isnan(T[:, :ell]).any()
@@ -90,20 +98,32 @@ def test_ozaki_pass_vs_fp64(P, m, n, ell, ta, lda, f32):
         assert torch.all(T[:, ell:] == 0)
 
 
-def test_ozaki_pass_deterministic(P):
+@pytest.mark.parametrize("planes", [True, False])
+def test_ozaki_pass_deterministic(P, planes):
     import torch
     buf, A, X = _operands(20000, 2000, 256, 1, 5)
-    outs = [_pass(P, buf, X, 1, 20000, 2000, 256) for _ in range(3)]
+    outs = [_pass(P, buf, X, 1, 20000, 2000, 256, planes=planes) for _ in range(3)]
     assert all(torch.equal(outs[0], o) for o in outs[1:])
 
 
-def test_ozaki_pass_nonfinite_and_zero_rows(P):
+def test_ozaki_planes_tn_nonfinite(P):
+    """TN from row-scaled planes: a non-finite entry of A reaches every output (as NaN), like the
+    reference's A^T T1 with T1's row already non-finite."""
+    import torch
+    buf, A, X = _operands(600, 400, 32, 1, 9)
+    A[5, 17] = float("inf")
+    T = _pass(P, buf, X, 1, 600, 400, 32, planes=True)
+    assert torch.isnan(T[:, :32]).all()
+
+
+@pytest.mark.parametrize("planes", [True, False])
+def test_ozaki_pass_nonfinite_and_zero_rows(P, planes):
     import torch
     buf, A, X = _operands(600, 400, 32, 0, 9)
     A[5, 17] = float("nan")
     A[9, :] = 0.0
     X[3, 7] = float("inf")
-    T = _pass(P, buf, X, 0, 600, 400, 32)
+    T = _pass(P, buf, X, 0, 600, 400, 32, planes=planes)
     assert torch.isnan(T[5, :32]).all()        # the row with a NaN
     assert torch.isnan(T[:, 7]).all()          # the column of X with an Inf
     ok = [j for j in range(32) if j != 7]
@@ -126,13 +146,16 @@ def _check_parity(got, base, ds=None, dl=0.0, tol_s=1e-10, tol_lr=1e-9):
     assert lr <= max(tol_lr, 10 * dl), lr
 
 
-def test_ozaki_golden_cases(P, golden):
+@pytest.mark.parametrize("planes", [True, False])
+def test_ozaki_golden_cases(P, golden, planes):
     g, meta = golden
+    ctx = P.Context(0)
+    ctx.set_option(P.Context.OPT_OZAKI_PLANES, int(planes))
     for name in meta["cases"]:
         md = meta["meta"][name]
         A = g[name + "_A"]
-        f = P.sor_svd_power(A, md["k"], P.SketchConfig(md["ell"], md["q"], md["seed"]), fp64_mode="ozaki")
-        assert f.stats["pass_kind"] == 1
+        f = P.sor_svd_power(A, md["k"], P.SketchConfig(md["ell"], md["q"], md["seed"]), fp64_mode="ozaki", ctx=ctx)
+        assert f.stats["pass_kind"] == 1 and f.stats["oz_planes"] == int(planes)
         _, ds, dl = O.perturbation_floor(A, md["k"], O.SketchConfig(md["ell"], md["q"], md["seed"]))
         base = type("B", (), {"sigma": g[name + "_s"], "u": g[name + "_u"], "v": g[name + "_v"]})
         _check_parity(f, base, ds, dl)
