@@ -549,6 +549,7 @@ def main():
                                                         "ms_basis")}
     stages["jacobi_sweeps"] = fs.stats["jacobi_sweeps"]
     pass_kind = int(fs.stats.get("pass_kind", 0))  # 0 FP64 DMMA, 1 Ozaki int8 (FP64), 2 TF32
+    oz_planes = bool(fs.stats.get("oz_planes", 0))   # Ozaki: A cut into int8 digit planes once per call
     stages["pass_engine"] = ["fp64 DMMA", "fp64 via Ozaki int8 tensor cores", "tf32 tensor cores"][pass_kind]
     stages["note"] = "un-graphed call with per-stage CUDA events; passes = the 2q+2 sketch passes"
 
@@ -619,11 +620,14 @@ def main():
     if os.path.exists(tr_path):
         try:
             traffic = json.load(open(tr_path)).get(args.config, {}).get(
-                "pass_nn_dram_bytes_ozaki" if pass_kind == 1 else "pass_nn_dram_bytes")
+                ("pass_nn_dram_bytes_ozaki_planes" if oz_planes else "pass_nn_dram_bytes_ozaki") if pass_kind == 1
+                else "pass_nn_dram_bytes")
         except Exception:
             traffic = None
     if pass_kind == 1:
-        # the library's pass engine here: ozaki_gemm_kernel (tcgen05 kind::i8). Its roofline is the
+        # the library's pass engine here: ozaki_planes_gemm_kernel (A's digit planes cut once per
+        # call, ozaki_planes_i8.cuh) or ozaki_gemm_kernel (A converted inside the pass), both
+        # tcgen05 kind::i8. Its roofline is the
         # INT8 tensor rate: 34 int8 digit products per FP64 multiply-add (ozaki_i8.cuh), against
         # 2 x the measured BF16 burst (the INT8 dense rate is twice BF16 on B200; MEASURED_PEAKS.json
         # has no INT8 entry). The FP64-equivalent rate is reported beside it.
@@ -640,13 +644,17 @@ def main():
         achieved = int8_ops / (ms_o.value * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOPS (int8)",
                 "frac": achieved / i8_peak, "traffic": traffic,
-                "kernel": "ozaki_gemm_kernel (tcgen05.mma kind::i8, TMA-staged A, 34 digit products / FP64 FMA), "
-                          "NN pass T1 = A*X",
+                "kernel": ("ozaki_planes_gemm_kernel (tcgen05.mma kind::i8 on A's int8 digit planes, cut once per call "
+                           "and streamed by 3-D TMA; 34 digit products / FP64 FMA), NN pass T1 = A*X" if oz_planes else
+                           "ozaki_gemm_kernel (tcgen05.mma kind::i8, TMA-staged A converted in the pass, 34 digit "
+                           "products / FP64 FMA), NN pass T1 = A*X"),
                 "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (burst): INT8 dense = 2x BF16 on B200",
                 "ms_per_launch": ms_o.value, "int8_ops_per_launch": int8_ops, "flops_per_launch": pass_flops,
                 "fp64_equiv_tflops": pass_flops / (ms_o.value * 1e-3) / 1e12,
                 "fp64_equiv_over_dmma_peak": pass_flops / (ms_o.value * 1e-3) / 1e12 / fp64_peak,
                 "dmma_peak_tflops": fp64_peak, "ms_scales_per_call": ms_sc.value,
+                "scales_per_call": ("row exponents + the 7 digit planes of A in one read (ozaki_rowplanes_kernel)"
+                                    if oz_planes else "row / column exponents of A (ozaki_absmax_kernel)"),
                 "tn_pass": {"ms": ms_ot.value, "achieved": int8_ops / (ms_ot.value * 1e-3) / 1e12},
                 "dmma_pass_for_comparison": {"ms_nn": ms_pass.value, "ms_tn": ms_pass_t.value,
                                              "tflops_nn": pass_flops / (ms_pass.value * 1e-3) / 1e12},

@@ -3,6 +3,7 @@ launch lists and kernel captures in tools/ncu_*.sh).
 
   python tools/run_config.py c2      # sor_svd_power on the C2 matrix (graph off: one launch per kernel)
   python tools/run_config.py c4      # one RPCA solve on the C4 matrix
+  python tools/run_config.py c3      # sor_svd_power on bench.py's C3 matrix
 """
 import os
 import sys
@@ -30,6 +31,15 @@ def main(cfg: str) -> None:
             r = P.rpca_alm(Dd, rc)
         torch.cuda.synchronize()
         print(r.iterations)
+    elif cfg == "c3":  # bench.py's own C3 instance (device-generated)
+        import bench
+        c = bench.CONFIGS["c3"]
+        A = bench.make_matrix("c3", c["m"], c["n"], 0, 1, torch.device("cuda", 0))
+        om = torch.from_numpy(P.gaussian_matrix(c["n"], c["k"], 7)).cuda()
+        for _ in range(2):
+            f = P.sor_svd_power(A, c["k"], P.SketchConfig(c["k"], c["q"], 7), omega=om, use_graph=False)
+        torch.cuda.synchronize()
+        print(f.sigma[:3], f.stats)
     else:
         raise SystemExit(f"unknown config {cfg!r}")
 
