@@ -225,10 +225,25 @@ int sorsvd_rpca_alm_device(sorsvd_ctx* ctx, const sorsvd_rpca_desc* desc, const 
  * buffers: ||A - U diag(sigma) V^T||_F in one fused pass over A (A m x lda,
  * FP64 or FP32 by dtype; U m x ldu, V n x ldv, first k columns). Multi-rank:
  * A and U are this rank's row block and the sum of squares is reduced over
- * ranks. The spectral norm (dgesdd of the m x n difference) is not provided. */
+ * ranks. */
 int sorsvd_approx_error_fro_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const void* dA, int64_t lda, int32_t dtype,
                                    int32_t k, const double* dU, int64_t ldu, const double* dSigma, const double* dV,
                                    int64_t ldv, double* err);
+
+/* approx_error(a, x, NormKind::spectral) (sketch.hpp:168-172; the reference: dgesdd 'N' of the
+ * dense difference, dense.hpp:173-176): E = A - U diag(sigma) V^T is formed on the device and
+ * sigma_1(E) comes from norm(spectral) below. Single rank. The bound harness (bounds.hpp:289-290)
+ * asks for both norms per trial. */
+int sorsvd_approx_error_spectral_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const void* dA, int64_t lda,
+                                        int32_t dtype, int32_t k, const double* dU, int64_t ldu,
+                                        const double* dSigma, const double* dV, int64_t ldv, double* err);
+
+/* norm(a, NormKind::spectral) (dense.hpp:173-176) of a device FP64 matrix: min(m, n) <= 1024 ->
+ * Gram matrix, 12 rescaled squarings and a 16-column Rayleigh-Ritz step (<= 1e-12 relative
+ * against dgesdd, clustered leading values included); larger -> block subspace iteration with
+ * Rayleigh-Ritz to a stationary value (seed draws its start block). Also RPCA's mu0. */
+int sorsvd_norm_spectral_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, uint64_t seed,
+                                double* out);
 
 /* ---- SORD matrix files ----------------------------------------
  * "SORD", u32 version = 1, u64 rows, u64 cols, then rows*cols little-endian

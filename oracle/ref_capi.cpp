@@ -12,6 +12,7 @@
 // here around the reference's own sor_svd_power (sketch.hpp:87), with the
 // ambiguity ledger frozen as in SURVEY.md Appendix B (S0=Y0=0, mu capped with
 // min, k=ell, seed+it per iteration, mu0 passed in).
+#include <sorsvd/bounds.hpp>
 #include <sorsvd/dense.hpp>
 #include <sorsvd/matrix.hpp>
 #include <sorsvd/matrixgen.hpp>
@@ -43,6 +44,9 @@ int guarded(F&& f) {
     } catch (const sorsvd::numerical_error& e) {
         g_err = e.what();
         return 3;
+    } catch (const sorsvd::bound_inapplicable_error& e) {
+        g_err = e.what();
+        return 5;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 4;
@@ -195,6 +199,73 @@ int ref_gen_rpca_instance(std::int64_t n, std::int64_t r, long long s, std::uint
         put(inst.l_true, l);
         put(inst.s_true, sp);
     });
+}
+
+// bounds.hpp:94-222: the formula evaluators on a given spectrum and split norms
+// (det_*: Phi from the two norms; avg_*: NaN when p < 2).
+int ref_bound_formulas(int nsig, const double* sigma, int k, int ell, int p, int q, double norm_omega2,
+                       double norm_omega1_pinv, int full_row_rank, double* det_sv, double* det_fro2,
+                       double* avg_sv, double* avg_fro2, double* best_p_fro2) {
+    return guarded([&] {
+        std::vector<double> sg(sigma, sigma + nsig);
+        sorsvd::BoundParams bp{k, ell, p, q};
+        sorsvd::OmegaSplit sp{sorsvd::Matrix(1, 1), sorsvd::Matrix(1, 1), norm_omega2, norm_omega1_pinv,
+                              full_row_rank != 0};
+        std::vector<double> d = sorsvd::det_sv_lower_bound(sg, bp, sp);
+        std::memcpy(det_sv, d.data(), d.size() * sizeof(double));
+        det_fro2[0] = sorsvd::det_lowrank_bound(sg, bp, sp, sorsvd::NormKind::frobenius);
+        det_fro2[1] = sorsvd::det_lowrank_bound(sg, bp, sp, sorsvd::NormKind::spectral);
+        if (p >= 2) {
+            std::vector<double> a = sorsvd::avg_sv_lower_bound(sg, bp);
+            std::memcpy(avg_sv, a.data(), a.size() * sizeof(double));
+            avg_fro2[0] = sorsvd::avg_lowrank_bound(sg, bp, sorsvd::NormKind::frobenius);
+            avg_fro2[1] = sorsvd::avg_lowrank_bound(sg, bp, sorsvd::NormKind::spectral);
+        } else {
+            for (int j = 0; j < k; ++j) avg_sv[j] = NAN;
+            avg_fro2[0] = avg_fro2[1] = NAN;
+        }
+        if (k + 2 <= ell) {
+            best_p_fro2[0] = sorsvd::avg_lowrank_bound_best_p(sg, k, ell, q, sorsvd::NormKind::frobenius);
+            best_p_fro2[1] = sorsvd::avg_lowrank_bound_best_p(sg, k, ell, q, sorsvd::NormKind::spectral);
+        } else {
+            best_p_fro2[0] = best_p_fro2[1] = NAN;
+        }
+    });
+}
+
+// RESTATEMENT of bounds.hpp:50-71 from the reference's own matmul / singular_values / norm:
+// out = {||Omega_2||_2, ||Omega_1^+||_2, full_row_rank}. The reference function itself cannot
+// be called: its return statement (bounds.hpp:65-70) moves omega2 into the result and THEN
+// evaluates norm(omega2, spectral) on the moved-from matrix (rows/cols kept, buffer empty), so
+// dgesdd is handed a null buffer (a segfault with this OpenBLAS). The intended order -- the
+// norm of Omega_2 before it is moved -- is what is restated here; for the same reason
+// bound_tightness_experiment (bounds.hpp:265-379, which calls omega_split at :300) is restated
+// in oracle/sorsvd_oracle.py around the reference's sor_svd_power, approx_error, gaussian_matrix
+// and the evaluators above.
+int ref_omega_split(std::int64_t n, const double* v, const double* omega, int k, int ell, int p, int q,
+                    double* out3) {
+    return guarded([&] {
+        sorsvd::BoundParams bp{k, ell, p, q};
+        bp.validate();
+        const sorsvd::Matrix vm = wrap(n, n, v), om = wrap(n, ell, omega);
+        const std::size_t lead = (std::size_t)(ell - p);
+        if (lead > (std::size_t)n) throw sorsvd::parameter_error("omega_split: ell - p exceeds n");
+        const sorsvd::Matrix o1 = sorsvd::matmul(vm.block(0, 0, (std::size_t)n, lead), om, sorsvd::Trans::transpose,
+                                                 sorsvd::Trans::none);
+        const sorsvd::Matrix o2 = sorsvd::matmul(vm.block(0, lead, (std::size_t)n, (std::size_t)n - lead), om,
+                                                 sorsvd::Trans::transpose, sorsvd::Trans::none);
+        const std::vector<double> s1 = sorsvd::singular_values(o1);
+        const double smax = s1.empty() ? 0.0 : s1.front(), smin = s1.empty() ? 0.0 : s1.back();
+        const bool frr = smin > (double)n * DBL_EPSILON * smax;
+        out3[0] = sorsvd::norm(o2, sorsvd::NormKind::spectral);
+        out3[1] = frr ? 1.0 / smin : INFINITY;
+        out3[2] = frr ? 1.0 : 0.0;
+    });
+}
+
+// matrixgen.hpp:84-91
+int ref_gen_polydecay(std::int64_t n, std::uint64_t seed, double* out) {
+    return guarded([&] { put(sorsvd::gen_polydecay((std::size_t)n, seed), out); });
 }
 
 // RESTATEMENT (the reference has no RPCA code): SPEC.md:386-398,

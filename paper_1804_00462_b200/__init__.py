@@ -479,12 +479,13 @@ def tsr_svd(a, ell: int, seed: int, psi1=None, psi2=None, ctx: Optional[Context]
 
 
 def approx_error(a, x: LowRankApprox, kind: str = "frobenius", ctx: Optional[Context] = None) -> float:
-    """sketch.hpp:168-172: ||a - reconstruct(x)|| for kind "frobenius", in one fused
-    pass over a on the device (the m x n reconstruction is never formed). The
-    spectral norm needs a dense SVD of the difference and is not provided."""
+    """sketch.hpp:168-172: ||a - reconstruct(x)||. kind "frobenius": one fused pass
+    over a on the device (the m x n reconstruction is never formed). kind
+    "spectral": the difference is formed on the device and its sigma_1 comes from
+    `norm(., "spectral")` (the reference: dgesdd of the dense difference)."""
     import torch
-    if kind != "frobenius":
-        raise UnsupportedError("approx_error: only the Frobenius norm runs on the device")
+    if kind not in ("frobenius", "spectral"):
+        raise ParameterError("parameter: approx_error supports frobenius and spectral norms")
     dev = a.device if _is_torch_cuda(a) else torch.device("cuda", 0)
     A = a if _is_torch_cuda(a) else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     if A.dtype not in (torch.float64, torch.float32) or A.dim() != 2 or A.stride(1) != 1:
@@ -498,10 +499,38 @@ def approx_error(a, x: LowRankApprox, kind: str = "frobenius", ctx: Optional[Con
     ctx = ctx or default_context(dev.index or 0)
     _torch_stream(ctx, A)
     out = ctypes.c_double()
-    _check(C.lib().sorsvd_approx_error_fro_device(ctx.handle, m, n, A.data_ptr(), A.stride(0),
-                                                  C.F32 if A.dtype == torch.float32 else C.F64, s.shape[0],
-                                                  u.data_ptr(), u.shape[1], s.data_ptr(), v.data_ptr(), v.shape[1],
-                                                  ctypes.byref(out)), ctx.handle)
+    fn = C.lib().sorsvd_approx_error_fro_device if kind == "frobenius" else C.lib().sorsvd_approx_error_spectral_device
+    _check(fn(ctx.handle, m, n, A.data_ptr(), A.stride(0), C.F32 if A.dtype == torch.float32 else C.F64, s.shape[0],
+              u.data_ptr(), u.shape[1], s.data_ptr(), v.data_ptr(), v.shape[1], ctypes.byref(out)), ctx.handle)
+    return out.value
+
+
+def norm(a, kind: str = "frobenius", ctx: Optional[Context] = None, seed: int = 0) -> float:
+    """dense.hpp:163-176 on a CUDA (or host) float64 matrix: "frobenius" or "spectral"
+    (sigma_1 by Gram squaring + Rayleigh-Ritz for min(m, n) <= 1024, else block
+    subspace iteration; the reference runs dgesdd on the whole matrix)."""
+    import torch
+    if kind not in ("frobenius", "spectral"):
+        raise ParameterError("parameter: norm supports frobenius and spectral")
+    dev = a.device if _is_torch_cuda(a) else torch.device("cuda", 0)
+    A = (a if _is_torch_cuda(a) else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev))
+    if A.dtype != torch.float64 or A.dim() != 2 or A.stride(1) != 1:
+        raise ShapeError("shape: norm expects a row-major float64 matrix")
+    ctx = ctx or default_context(dev.index or 0)
+    _torch_stream(ctx, A)
+    m, n = A.shape
+    if kind == "frobenius":
+        z = torch.zeros((1, 1), dtype=torch.float64, device=dev)
+        out = ctypes.c_double()
+        _check(C.lib().sorsvd_approx_error_fro_device(ctx.handle, m, n, A.data_ptr(), A.stride(0), C.F64, 1,
+                                                      torch.zeros((m, 1), dtype=torch.float64, device=dev).data_ptr(),
+                                                      1, z.data_ptr(),
+                                                      torch.zeros((n, 1), dtype=torch.float64, device=dev).data_ptr(),
+                                                      1, ctypes.byref(out)), ctx.handle)
+        return out.value
+    out = ctypes.c_double()
+    _check(C.lib().sorsvd_norm_spectral_device(ctx.handle, m, n, A.data_ptr(), A.stride(0), seed & (2**64 - 1),
+                                               ctypes.byref(out)), ctx.handle)
     return out.value
 
 

