@@ -221,6 +221,22 @@ int sorsvd_rpca_alm(sorsvd_ctx* ctx, const sorsvd_rpca_desc* desc, const double*
 int sorsvd_rpca_alm_device(sorsvd_ctx* ctx, const sorsvd_rpca_desc* desc, const double* dD, double* dL,
                            double* dS, sorsvd_rpca_result* res);
 
+/* Per-iteration telemetry of the context's last rpca_alm call ("per-iteration telemetry
+ * CSV (iter, mu, rel_error, rank_l, nnz_s)"): *rows = iterations run; up to cap_rows rows of those 5
+ * values (as doubles) are written to out (may be NULL to query the count). Multi-rank: nnz_s is the
+ * global count. */
+int sorsvd_rpca_telemetry(sorsvd_ctx* ctx, int32_t cap_rows, double* out, int32_t* rows);
+
+/* estimate_rank_bound(x) = ceil((||X||_* / ||X||_F)^2) (PAPER Eq. 66), the input of
+ * rpca_default_config's ell = min(2 * bound, min(m,n) - 1). Device FP64 X, min(m,n) <=
+ * 512 (thin QR + Jacobi SVD of R). Zero matrix -> SORSVD_ERR_PARAMETER. nuclear / frobenius (may be
+ * NULL) receive the two norms. */
+int sorsvd_estimate_rank_bound_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const double* dX, int64_t ldx,
+                                      int64_t* bound, double* nuclear, double* frobenius);
+/* The same on a host matrix (uploaded inside). */
+int sorsvd_estimate_rank_bound(sorsvd_ctx* ctx, int64_t m, int64_t n, const double* X, int64_t ldx, int64_t* bound,
+                               double* nuclear, double* frobenius);
+
 /* approx_error(a, x, NormKind::frobenius) (sketch.hpp:168-172) on device
  * buffers: ||A - U diag(sigma) V^T||_F in one fused pass over A (A m x lda,
  * FP64 or FP32 by dtype; U m x ldu, V n x ldv, first k columns). Multi-rank:

@@ -135,5 +135,93 @@ inline LowRankApprox tsr_svd(const Matrix& a, int ell, std::uint64_t seed) {
     return LowRankApprox{std::move(u), std::move(sigma), std::move(v), SketchMethod::tsr, st.passes, ell, 0, seed};
 }
 
+// ---- RPCA (the reference ships the spec but no code for it) ----------------
+// Types with the spec's field names and the three operations a caller of the
+// spec's rpca module uses: estimate_rank_bound (:377), rpca_default_config (:398), rpca_alm (:386).
+struct RpcaConfig {
+    double lambda = 0.0;       // <= 0 -> 1/sqrt(max(m,n))
+    double mu0 = 0.0;          // <= 0 -> 1.25/sigma_1(X), estimated on the device
+    double mu_bar_factor = 1e7;
+    double rho = 1.6;
+    double tol = 1e-7;
+    int max_iter = 500;
+    int ell = 10;
+    int q = 1;
+    std::uint64_t seed = 0;
+};
+
+struct RpcaIteration {  // one row of the per-iteration telemetry CSV
+    int iter;
+    double mu, rel_error;
+    int rank_l;
+    long long nnz_s;
+};
+
+struct RpcaResult {
+    Matrix l, s;
+    int iterations = 0;
+    double rel_error = 0.0;
+    int rank_l = 0;
+    long long nnz_s = 0;
+    bool converged = false;
+    std::vector<RpcaIteration> telemetry;
+};
+
+// inexact ALM with sor_svd_power (k = ell, seed + it) per iteration.
+inline RpcaResult rpca_alm(const Matrix& x, const RpcaConfig& cfg) {
+    sorsvd_ctx* ctx = detail::thread_context();
+    sorsvd_rpca_desc d{};
+    d.m = (int64_t)x.rows();
+    d.n = (int64_t)x.cols();
+    d.ldd = (int64_t)x.cols();
+    d.lambda = cfg.lambda;
+    d.mu0 = cfg.mu0;
+    d.mu_bar_factor = cfg.mu_bar_factor;
+    d.rho = cfg.rho;
+    d.tol = cfg.tol;
+    d.max_iter = cfg.max_iter;
+    d.ell = cfg.ell;
+    d.q = cfg.q;
+    d.dtype = SORSVD_F64;
+    d.seed = cfg.seed;
+    RpcaResult out{Matrix(x.rows(), x.cols()), Matrix(x.rows(), x.cols())};
+    sorsvd_rpca_result r{};
+    detail::throw_status(sorsvd_rpca_alm(ctx, &d, x.data().data(), out.l.data().data(), out.s.data().data(), &r), ctx);
+    out.iterations = r.iterations;
+    out.rel_error = r.rel_error;
+    out.rank_l = r.rank_l;
+    out.nnz_s = r.nnz_s;
+    out.converged = r.converged != 0;
+    int32_t rows = 0;
+    detail::throw_status(sorsvd_rpca_telemetry(ctx, 0, nullptr, &rows), ctx);
+    std::vector<double> t((std::size_t)rows * 5);
+    if (rows) detail::throw_status(sorsvd_rpca_telemetry(ctx, rows, t.data(), &rows), ctx);
+    for (int i = 0; i < rows; ++i)
+        out.telemetry.push_back(RpcaIteration{(int)t[5 * i], t[5 * i + 1], t[5 * i + 2], (int)t[5 * i + 3],
+                                              (long long)t[5 * i + 4]});
+    return out;
+}
+
+// ceil((||X||_* / ||X||_F)^2); min(m, n) <= 512 on the device.
+inline long long estimate_rank_bound(const Matrix& x) {
+    sorsvd_ctx* ctx = detail::thread_context();
+    int64_t b = 0;
+    detail::throw_status(sorsvd_estimate_rank_bound(ctx, (int64_t)x.rows(), (int64_t)x.cols(), x.data().data(),
+                                                    (int64_t)x.cols(), &b, nullptr, nullptr),
+                         ctx);
+    return (long long)b;
+}
+
+// SPEC.md:398.
+inline RpcaConfig rpca_default_config(const Matrix& x) {
+    RpcaConfig c;
+    const std::size_t mn = x.rows() < x.cols() ? x.rows() : x.cols();
+    const long long two_r = 2 * estimate_rank_bound(x);
+    c.ell = (int)(two_r < (long long)mn - 1 ? two_r : (long long)mn - 1);
+    if (c.ell < 1) c.ell = 1;
+    c.q = 1;
+    return c;
+}
+
 }  // namespace cuda
 }  // namespace sorsvd

@@ -35,7 +35,7 @@ from . import _capi as C
 __all__ = [
     "SketchMethod", "SketchConfig", "LowRankApprox", "FlopVariant", "RpcaConfig", "RpcaResult", "Context",
     "ShapeError", "ParameterError", "NumericalError", "CudaError", "NcclError", "UnsupportedError", "EmuGroup",
-    "sor_svd_power", "sor_svd", "sor_svd_power_batch", "r_svd", "tsr_svd", "truncate", "approx_error", "sord_header", "load_sord", "save_sord", "rpca_alm", "rpca_default_config", "gaussian_matrix", "sub_seed",
+    "sor_svd_power", "sor_svd", "sor_svd_power_batch", "r_svd", "tsr_svd", "truncate", "approx_error", "sord_header", "load_sord", "save_sord", "rpca_alm", "rpca_default_config", "estimate_rank_bound", "norm", "gaussian_matrix", "sub_seed",
     "flop_estimate", "validate_sketch", "thin_qr", "full_svd", "matmul", "default_context", "version",
 ]
 
@@ -143,6 +143,14 @@ class RpcaResult:
     converged: bool
     mu0: float = 0.0
     stats: dict = field(default_factory=dict)
+    telemetry: object = None  # (iterations, 5) array: iter, mu, rel_error, rank_l, nnz_s
+
+    def telemetry_csv(self) -> str:
+        """the per-iteration telemetry CSV (iter, mu, rel_error, rank_l, nnz_s)."""
+        rows = ["iter,mu,rel_error,rank_l,nnz_s\n"]
+        for r in (self.telemetry if self.telemetry is not None else []):
+            rows.append("%d,%.17g,%.17g,%d,%d\n" % (int(r[0]), r[1], r[2], int(r[3]), int(r[4])))
+        return "".join(rows)
 
 
 # ---------------------------------------------------------------- context --
@@ -519,14 +527,14 @@ def norm(a, kind: str = "frobenius", ctx: Optional[Context] = None, seed: int = 
     ctx = ctx or default_context(dev.index or 0)
     _torch_stream(ctx, A)
     m, n = A.shape
-    if kind == "frobenius":
-        z = torch.zeros((1, 1), dtype=torch.float64, device=dev)
+    if kind == "frobenius":  # ||A - 0||_F through the fused error pass (deterministic reduction)
+        zs = torch.zeros((1,), dtype=torch.float64, device=dev)
+        zu = torch.zeros((m, 1), dtype=torch.float64, device=dev)
+        zv = torch.zeros((n, 1), dtype=torch.float64, device=dev)
         out = ctypes.c_double()
         _check(C.lib().sorsvd_approx_error_fro_device(ctx.handle, m, n, A.data_ptr(), A.stride(0), C.F64, 1,
-                                                      torch.zeros((m, 1), dtype=torch.float64, device=dev).data_ptr(),
-                                                      1, z.data_ptr(),
-                                                      torch.zeros((n, 1), dtype=torch.float64, device=dev).data_ptr(),
-                                                      1, ctypes.byref(out)), ctx.handle)
+                                                      zu.data_ptr(), 1, zs.data_ptr(), zv.data_ptr(), 1,
+                                                      ctypes.byref(out)), ctx.handle)
         return out.value
     out = ctypes.c_double()
     _check(C.lib().sorsvd_norm_spectral_device(ctx.handle, m, n, A.data_ptr(), A.stride(0), seed & (2**64 - 1),
@@ -639,9 +647,36 @@ def matmul(a, b, transpose_a: bool = False, ctx: Optional[Context] = None):
 
 
 # ------------------------------------------------------------------- RPCA --
-def rpca_default_config(m: int, n: int, ell: int = 10, q: int = 1, seed: int = 0) -> RpcaConfig:
-    """SPEC.md:395-403 (mu0 left to the device estimate; ell given by the caller)."""
-    return RpcaConfig(lam=1.0 / math.sqrt(max(m, n)), mu0=0.0, mu_bar_factor=1e7, rho=1.6, tol=1e-7,
+def estimate_rank_bound(x, ctx: Optional[Context] = None) -> int:
+    """SPEC.md:377-385 (PAPER Eq. 66): ceil((||X||_* / ||X||_F)^2); the spectrum comes from
+    thin QR + Jacobi SVD on the device (min(m, n) <= 512). Zero matrix -> ParameterError."""
+    import torch
+    dev = x.device if _is_torch_cuda(x) else torch.device("cuda", 0)
+    X = x if _is_torch_cuda(x) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+    if X.dtype != torch.float64 or X.dim() != 2 or X.stride(1) != 1:
+        raise ShapeError("shape: estimate_rank_bound expects a row-major float64 matrix")
+    ctx = ctx or default_context(dev.index or 0)
+    _torch_stream(ctx, X)
+    out = C.c_i64()
+    _check(C.lib().sorsvd_estimate_rank_bound_device(ctx.handle, X.shape[0], X.shape[1], X.data_ptr(), X.stride(0),
+                                                     ctypes.byref(out), None, None), ctx.handle)
+    return int(out.value)
+
+
+def rpca_default_config(x_or_m, n: Optional[int] = None, ell: Optional[int] = None, q: int = 1, seed: int = 0,
+                        ctx: Optional[Context] = None) -> RpcaConfig:
+    """lambda = 1/sqrt(max(m,n)), mu0 = 1.25/sigma_1(X) (estimated on the device by
+    rpca_alm: mu0 = 0 here), mu_bar = 1e7 mu0, rho = 1.6, tol = 1e-7, max_iter = 500, q = 1 and
+    ell = min(2 * estimate_rank_bound(x), min(m,n) - 1). Call with the matrix (the spec's form),
+    or with (m, n, ell) when the sketch size is chosen by the caller."""
+    if hasattr(x_or_m, "shape"):
+        m, nn = x_or_m.shape
+        if ell is None:
+            ell = max(1, min(2 * estimate_rank_bound(x_or_m, ctx=ctx), min(m, nn) - 1))
+    else:
+        m, nn = int(x_or_m), int(n)
+        ell = 10 if ell is None else ell
+    return RpcaConfig(lam=1.0 / math.sqrt(max(m, nn)), mu0=0.0, mu_bar_factor=1e7, rho=1.6, tol=1e-7,
                       max_iter=500, ell=ell, q=q, seed=seed)
 
 
@@ -676,5 +711,11 @@ def rpca_alm(x, cfg: RpcaConfig, ctx: Optional[Context] = None, want_l: bool = T
                                        l.ctypes.data_as(C.c_dp) if l is not None else None,
                                        s.ctypes.data_as(C.c_dp), ctypes.byref(res)), ctx.handle)
     stats = {f: getattr(res, f) for f, _ in res._fields_}
+    rows = C.c_i32()
+    _check(C.lib().sorsvd_rpca_telemetry(ctx.handle, 0, None, ctypes.byref(rows)), ctx.handle)
+    tele = np.zeros((rows.value, 5))
+    if rows.value:
+        _check(C.lib().sorsvd_rpca_telemetry(ctx.handle, rows.value, tele.ctypes.data_as(C.c_dp), ctypes.byref(rows)),
+               ctx.handle)
     return RpcaResult(l, s, res.iterations, res.rel_error, res.rank_l, res.nnz_s, bool(res.converged), res.mu0,
-                      stats)
+                      stats, tele)

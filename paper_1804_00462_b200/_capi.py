@@ -96,6 +96,9 @@ SIGNATURES = [
     ("sorsvd_approx_error_spectral_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i32, c_i32, c_vp, c_i64, c_vp,
                                                     c_vp, c_i64, c_dp]),
     ("sorsvd_norm_spectral_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_u64, c_dp]),
+    ("sorsvd_rpca_telemetry", c_i32, [c_vp, c_i32, c_dp, ctypes.POINTER(c_i32)]),
+    ("sorsvd_estimate_rank_bound", c_i32, [c_vp, c_i64, c_i64, c_dp, c_i64, ctypes.POINTER(c_i64), c_dp, c_dp]),
+    ("sorsvd_estimate_rank_bound_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, ctypes.POINTER(c_i64), c_dp, c_dp]),
     ("sorsvd_sord_header", c_i32, [ctypes.c_char_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     ("sorsvd_load_sord_device", c_i32, [c_vp, ctypes.c_char_p, c_vp, c_i64, c_i32]),
     ("sorsvd_save_sord_device", c_i32, [c_vp, ctypes.c_char_p, c_vp, c_i64, c_i64, c_i64]),

@@ -37,6 +37,7 @@ struct RpcaArgs {
     int k;
     double mu, mu_next, eps;  // eps = lambda / mu
     double* partial;          // per-block residual^2 partials
+    unsigned int* nnz_partial;  // per-block count of nonzeros of the new S (telemetry), or null
     int mode;                 // 0 = ALM update, 1 = write L only
     const int* pred;          // optional: no-op when *pred == pred_skip (iteration after convergence)
     int pred_skip;
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(kRpcaThreads, 2) rpca_update_kernel(RpcaArgs a
             for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
     }
     double res = 0.0;
+    unsigned int cnt = 0;  // nonzeros of the new S in this thread's entries
     if (vec) {
         cp_async_wait<0>();  // own slots only: no block barrier needed
 #pragma unroll
@@ -122,6 +124,7 @@ __global__ void __launch_bounds__(kRpcaThreads, 2) rpca_update_kernel(RpcaArgs a
                         a.Y[i * a.ldx + j + h] = yn;
                         if (a.W) a.W[i * a.ldx + j + h] = d - sv + yn / a.mu_next;
                         res = fma(r, r, res);
+                        cnt += sv != 0.0;
                     }
                     continue;
                 }
@@ -140,6 +143,7 @@ __global__ void __launch_bounds__(kRpcaThreads, 2) rpca_update_kernel(RpcaArgs a
                     yn[h] = y + a.mu * r;
                     wv[h] = d - sv[h] + yn[h] / a.mu_next;
                     res = fma(r, r, res);
+                    cnt += sv[h] != 0.0;
                 }
                 __stcs(reinterpret_cast<double2*>(a.S + i * a.ldx + j), make_double2(sv[0], sv[1]));
                 __stcs(reinterpret_cast<double2*>(a.Y + i * a.ldx + j), make_double2(yn[0], yn[1]));
@@ -176,36 +180,64 @@ __global__ void __launch_bounds__(kRpcaThreads, 2) rpca_update_kernel(RpcaArgs a
                 a.Y[i * a.ldx + j] = yn;
                 if (a.W) a.W[i * a.ldx + j] = d - s + yn / a.mu_next;
                 res = fma(r, r, res);
+                cnt += s != 0.0;
             }
         }
     }
     if (a.mode == 1) return;
     __shared__ double red[kRpcaThreads / 32];
+    __shared__ unsigned int redc[kRpcaThreads / 32];
     res = warp_sum(res);
-    if (lane == 0) red[warp] = res;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) {
+        red[warp] = res;
+        redc[warp] = cnt;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int w = 0; w < kRpcaThreads / 32; ++w) t += red[w];
+        unsigned int tc = 0;
+        for (int w = 0; w < kRpcaThreads / 32; ++w) {
+            t += red[w];
+            tc += redc[w];
+        }
         a.partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+        if (a.nnz_partial) a.nnz_partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = tc;
     }
 }
 
-// Deterministic single-block reduction of partials: out[0] = sum, (sqrt into out[1]).
+// Deterministic single-block reduction of partials: out[0] = sum, (sqrt into out[1]);
+// with integer count partials c: out[2] = their sum (exact in a double below 2^53).
 __global__ void sum_partials_kernel(const double* __restrict__ p, int64_t n, double* out, const int* pred = nullptr,
-                                    int pred_skip = 0) {
+                                    int pred_skip = 0, const unsigned int* __restrict__ c = nullptr) {
     if (pred_off(pred, pred_skip)) return;
     __shared__ double red[32];
+    __shared__ unsigned long long redc[32];
     double t = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) t += p[i];
+    unsigned long long tc = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        t += p[i];
+        if (c) tc += c[i];
+    }
     t = warp_sum(t);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, o);
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5] = t;
+        redc[threadIdx.x >> 5] = tc;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         double s = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        unsigned long long sc = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            s += red[w];
+            sc += redc[w];
+        }
         out[0] = s;
         out[1] = sqrt(s);
+        if (c) out[2] = (double)sc;
     }
 }
 
@@ -213,12 +245,24 @@ __global__ void sum_partials_kernel(const double* __restrict__ p, int64_t n, dou
 // host can enqueue several iterations ahead: st[0] = done flag (sticky), st[1]
 // = iterations executed, st[2] = error flag; rel[0] = this iteration's
 // ||D - L - S||_F / ||D||_F. Predicated like the iteration itself.
+// tele (4 doubles, may be null) = this iteration's telemetry row: mu, rel_error,
+// rank_l (shrunk sigma > 1e-8 of the largest) and nnz_s (tot[2]).
 __global__ void rpca_check_kernel(const double* __restrict__ tot, double dnorm, double tol, int it, int* st,
-                                  double* rel, const int* pred, int pred_skip) {
+                                  double* rel, const int* pred, int pred_skip, double* tele = nullptr,
+                                  const double* __restrict__ sig = nullptr, int ell = 0, double mu = 0.0) {
     if (pred_off(pred, pred_skip)) return;
     const double r = sqrt(tot[0]) / dnorm;
     rel[0] = r;
     st[1] = it + 1;
+    if (tele) {
+        const double z0 = fmax(sig[0] - 1.0 / mu, 0.0);
+        int rank = 0;
+        for (int j = 0; j < ell; ++j) rank += fmax(sig[j] - 1.0 / mu, 0.0) > 1e-8 * z0;
+        tele[0] = mu;
+        tele[1] = r;
+        tele[2] = (double)rank;
+        tele[3] = tot[2];
+    }
     if (!isfinite(r)) {
         st[2] = 1;
         st[0] = 1;

@@ -233,6 +233,7 @@ struct sorsvd_ctx {
     int launches = 0;
     bool capturing = false;
     std::vector<double> host_omega;
+    std::vector<double> rpca_tele;  // last rpca_alm: iterations x {mu, rel_error, rank_l, nnz_s}
     std::vector<double> host_psi2;  // tsr_svd's second test matrix (host draw)
     double* om_pin = nullptr;       // host-buffer calls: page-locked Omega draw
     size_t om_pin_n = 0;
@@ -3231,6 +3232,7 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
         CK(cudaStreamSynchronize(c->stream));
         r.iterations = 1;
         r.converged = 1;
+        c->rpca_tele.assign(4, 0.0);
         if (res) *res = r;
         return;
     }
@@ -3249,7 +3251,9 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
     const dim3 grid((unsigned)cdiv(n, 64), (unsigned)cdiv(m, 64));
     const int64_t nblk = (int64_t)grid.x * grid.y;
     double* part = dbuf(c, "rp_part", (size_t)nblk);
-    double* tot = dbuf(c, "rp_tot", 2);
+    double* tot = dbuf(c, "rp_tot", 4);
+    auto* nnzp = reinterpret_cast<unsigned int*>(dbuf(c, "rp_nnzp", (size_t)(nblk + 1) / 2));
+    double* tele = dbuf(c, "rp_tele", (size_t)4 * d->max_iter);  // per-iteration telemetry rows
     // Iterations are enqueued kBatch at a time without a host round trip: the
     // stopping test runs on the device (rpca_check_kernel) and every kernel of
     // an iteration after convergence is predicated off, so the result is the
@@ -3310,15 +3314,17 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
             a.mu_next = mus[j + 1];
             a.eps = lambda / mus[j];
             a.partial = part;
+            a.nnz_partial = nnzp;
             a.mode = 0;
             a.pred = stf;
             a.pred_skip = 1;
             rpca_update_kernel<<<grid, kRpcaThreads, 0, c->stream>>>(a);
             check_launch(c);
-            sum_partials_kernel<<<1, 1024, 0, c->stream>>>(part, nblk, tot, stf, 1);
+            sum_partials_kernel<<<1, 1024, 0, c->stream>>>(part, nblk, tot, stf, 1, nnzp);
             check_launch(c);
-            comm_allreduce(c, tot, 1, false, c->stream);  // residual over all row blocks
-            rpca_check_kernel<<<1, 1, 0, c->stream>>>(tot, dnorm, d->tol, j, stf, rels, stf, 1);
+            comm_allreduce(c, tot, 3, false, c->stream);  // residual and nonzero count over all row blocks
+            rpca_check_kernel<<<1, 1, 0, c->stream>>>(tot, dnorm, d->tol, j, stf, rels, stf, 1, tele + 4 * (size_t)j, sj,
+                                                      ell, mus[j]);
             check_launch(c);
         }
         int hst[3];
@@ -3386,6 +3392,8 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
     }
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->ev_h[2], c->ev_h[3]));
+    c->rpca_tele.assign((size_t)4 * it, 0.0);
+    CK(cudaMemcpy(c->rpca_tele.data(), tele, (size_t)4 * it * sizeof(double), cudaMemcpyDeviceToHost));
     r.iterations = it;
     r.rank_l = rank;
     r.converged = conv ? 1 : 0;
@@ -3934,6 +3942,76 @@ int sorsvd_thin_qr_device(sorsvd_ctx* c, int64_t m, int32_t k, const double* dT,
     });
 }
 
+// estimate_rank_bound(x) = ceil((||X||_* / ||X||_F)^2)   (PAPER Eq. 66; spec only,
+// no reference code): the spectrum of X from thin QR + the Jacobi SVD of R (min(m, n) <= 512; a
+// wide X is transposed first). The quotient is shaved by 1e-12 before the ceiling so that exactly
+// flat spectra (I_n -> n, rank 1 -> 1: the spec's examples) are not pushed up by rounding.
+int sorsvd_estimate_rank_bound_device(sorsvd_ctx* c, int64_t m, int64_t n, const double* dX, int64_t ldx,
+                                      int64_t* bound, double* nuclear, double* frobenius) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (m < 1 || n < 1 || ldx < n) throw Error{SORSVD_ERR_SHAPE, "shape: matrix dimensions must be positive"};
+        if (!dX || !bound) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "estimate_rank_bound: single-rank only"};
+        const double ss = device_sumsq(c, dX, m, n, ldx);
+        if (!std::isfinite(ss)) throw Error{SORSVD_ERR_PARAMETER, "parameter: matrix entries must be finite"};
+        if (ss == 0.0) throw Error{SORSVD_ERR_PARAMETER, "parameter: estimate_rank_bound of the zero matrix"};
+        const int64_t rows = std::max(m, n);
+        const int k = (int)std::min(m, n);
+        if (k > 512) throw Error{SORSVD_ERR_UNSUPPORTED, "estimate_rank_bound: min(m, n) > 512"};
+        const int Np = npad(k);
+        double* T = dbuf(c, "erT", (size_t)rows * Np, true);
+        double* Q = dbuf(c, "erQ", (size_t)rows * Np, true);
+        if (m >= n) {
+            CK(cudaMemcpy2DAsync(T, (size_t)Np * 8, dX, (size_t)ldx * 8, (size_t)n * 8, (size_t)m,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            dim3 tb(32, 8), tg((unsigned)cdiv(m, 32), (unsigned)cdiv(n, 32));
+            transpose_kernel<<<tg, tb, 0, c->stream>>>(dX, ldx, m, n, T, Np);
+            check_launch(c);
+        }
+        double fro = std::sqrt(ss), nuc = 0.0;
+        std::vector<double> hs((size_t)k);
+        if (k == 1) {
+            nuc = fro;
+        } else {
+            QrPlan* p = get_qr_plan(c, rows, k, 0, "er");
+            qr_run(c, p, T, Np, Q, Np, c->stream);
+            const int L = (int)p->nodes.size() - 1;
+            double* U = dbuf(c, "erU", (size_t)k * k);
+            double* V = dbuf(c, "erV", (size_t)k * k);
+            double* S = dbuf(c, "erS", (size_t)k);
+            int* dsw = reinterpret_cast<int*>(dbuf(c, "sweeps_er", 1));
+            run_jacobi(c, k, p->R[L], (int)p->ldR, U, k, S, V, k, dsw, c->stream);
+            CK(cudaMemcpyAsync(hs.data(), S, (size_t)k * 8, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            check_big_qr(p);
+            for (int j = k - 1; j >= 0; --j) nuc += hs[(size_t)j];  // small values first
+        }
+        if (!std::isfinite(nuc)) throw Error{SORSVD_ERR_NUMERICAL, "numerical: singular values not finite"};
+        const double ratio = nuc / fro;
+        *bound = (int64_t)std::max(1.0, std::ceil(ratio * ratio * (1.0 - 1e-12)));
+        if (nuclear) *nuclear = nuc;
+        if (frobenius) *frobenius = fro;
+    });
+}
+
+// Host-buffer form of estimate_rank_bound (X uploaded into a context workspace).
+int sorsvd_estimate_rank_bound(sorsvd_ctx* c, int64_t m, int64_t n, const double* X, int64_t ldx, int64_t* bound,
+                               double* nuclear, double* frobenius) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    double* dX = nullptr;
+    const int rc = guarded(c, [&] {
+        if (m < 1 || n < 1 || ldx < n) throw Error{SORSVD_ERR_SHAPE, "shape: matrix dimensions must be positive"};
+        if (!X || !bound) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        dX = dbuf(c, "er_host", (size_t)m * n);
+        CK(cudaMemcpy2DAsync(dX, (size_t)n * 8, X, (size_t)ldx * 8, (size_t)n * 8, (size_t)m, cudaMemcpyHostToDevice,
+                             c->stream));
+    });
+    if (rc != SORSVD_OK) return rc;
+    return sorsvd_estimate_rank_bound_device(c, m, n, dX, n, bound, nuclear, frobenius);
+}
+
 int sorsvd_small_svd_device(sorsvd_ctx* c, int32_t k, const double* dM, int64_t ldm, double* dU, int64_t ldu,
                             double* dS, double* dV, int64_t ldv, int32_t* sweeps) {
     if (!c) return SORSVD_ERR_PARAMETER;
@@ -4013,6 +4091,20 @@ int sorsvd_rpca_alm(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* D, d
         r.ms_d2h = d2h;
         if (res) *res = r;
     });
+}
+
+// Per-iteration telemetry of the context's last rpca_alm (iter, mu, rel_error,
+// rank_l, nnz_s): up to cap_rows rows of 5 doubles into out, *rows = iterations available.
+int sorsvd_rpca_telemetry(sorsvd_ctx* c, int32_t cap_rows, double* out, int32_t* rows) {
+    if (!c || !rows) return SORSVD_ERR_PARAMETER;
+    const int32_t n = (int32_t)(c->rpca_tele.size() / 4);
+    *rows = n;
+    if (out)
+        for (int32_t i = 0; i < n && i < cap_rows; ++i) {
+            out[5 * i] = (double)(i + 1);
+            for (int q = 0; q < 4; ++q) out[5 * i + 1 + q] = c->rpca_tele[(size_t)4 * i + q];
+        }
+    return SORSVD_OK;
 }
 
 int sorsvd_measure_peaks(sorsvd_ctx* c, double* fp64_tflops, double* hbm_read_gbs) {

@@ -94,6 +94,30 @@ int main() {
     } catch (const parameter_error& e) {
         std::printf("parameter_error: %s\n", e.what());
     }
+    // RPCA drop-in on a matrixgen instance (matrixgen.hpp:99): n = 100, r = 5, s = 0.05 n^2
+    {
+        RpcaInstance inst = gen_rpca_instance(100, 5, 500, 77);
+        cuda::RpcaConfig rc = cuda::rpca_default_config(inst.l_true);
+        std::printf("rank bound of the rank-5 L0: %lld, default ell %d\n", cuda::estimate_rank_bound(inst.l_true), rc.ell);
+        fails += (cuda::estimate_rank_bound(inst.l_true) > 5) + (rc.ell > 10) + (rc.ell < 2);
+        rc.ell = 10;
+        rc.seed = 3;
+        cuda::RpcaResult rr = cuda::rpca_alm(inst.x, rc);
+        const double el = norm(rr.l - inst.l_true, NormKind::frobenius) / norm(inst.l_true, NormKind::frobenius);
+        std::printf("rpca: %d iterations, rank %d, nnz %lld, rel %.2e, |L-L0|/|L0| %.2e, telemetry rows %zu\n",
+                    rr.iterations, rr.rank_l, rr.nnz_s, rr.rel_error, el, rr.telemetry.size());
+        fails += !rr.converged + (rr.rank_l != 5) + (rr.nnz_s != 500) + !(el <= 1e-5) +
+                 (rr.telemetry.size() != (std::size_t)rr.iterations) + !(rr.rel_error < 1e-7);
+        if (!rr.telemetry.empty())
+            fails += (rr.telemetry.back().rank_l != rr.rank_l) + (rr.telemetry.back().nnz_s != rr.nnz_s) +
+                     (rr.telemetry.front().iter != 1);
+        try {
+            cuda::estimate_rank_bound(Matrix(4, 3));
+            ++fails;
+        } catch (const parameter_error& e) {
+            std::printf("parameter_error: %s\n", e.what());
+        }
+    }
     std::printf(fails ? "FAIL (%d)\n" : "OK\n", fails);
     return fails ? 1 : 0;
 }
