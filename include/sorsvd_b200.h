@@ -261,6 +261,24 @@ int sorsvd_approx_error_spectral_device(sorsvd_ctx* ctx, int64_t m, int64_t n, c
 int sorsvd_norm_spectral_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, uint64_t seed,
                                 double* out);
 
+/* ---- test-matrix generators on the device (matrixgen.hpp) ---------------
+ * gaussian_matrix(rows, cols, seed) (random.hpp:60-65) filled on the device: the reference's
+ * splitmix64 words and uniforms, with the device's log / sincos (a few ulp from the host draw of
+ * sorsvd_gaussian_matrix, which is bit-identical to the reference). */
+int sorsvd_gaussian_matrix_device(sorsvd_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* dOut, int64_t ld);
+/* Rows [row0, row0 + m) of the m_global x n matrix (x_scale X) diag(sigma) (y_scale Y)^T + noise_std E
+ * (BASELINE.json configs 1, 3, 5): X = gaussian_matrix(m_global, r, sub_seed(seed, 1)) and
+ * Y = gaussian_matrix(n, r, sub_seed(seed, 2)) drawn on the host (reference-exact) and uploaded; row i of E =
+ * NormalStream(sub_seed(sub_seed(seed, 3), i)) drawn in the kernel. sigma: r host values. dtype selects
+ * FP64 or FP32 storage of A (lda in elements). m_global <= 0 -> row0 + m. */
+int sorsvd_gen_lowrank_device(sorsvd_ctx* ctx, int64_t m, int64_t n, int32_t r, const double* sigma, double x_scale,
+                              double y_scale, double noise_std, uint64_t seed, int64_t row0, int64_t m_global,
+                              int32_t dtype, void* dA, int64_t lda);
+/* gen_rpca_instance(n, r, s, seed) (matrixgen.hpp:99-124): X = L + S (n x n, dense) on the device; dL / dS
+ * (may be NULL) receive the two components. The support and signs of S are identical to the reference's. */
+int sorsvd_gen_rpca_instance_device(sorsvd_ctx* ctx, int64_t n, int32_t r, long long s, uint64_t seed, double* dX,
+                                    double* dL, double* dS);
+
 /* ---- SORD matrix files ----------------------------------------
  * "SORD", u32 version = 1, u64 rows, u64 cols, then rows*cols little-endian
  * float64, row-major. The loader streams the file into device memory through two
@@ -323,7 +341,10 @@ int sorsvd_pass_f32a_device(sorsvd_ctx* ctx, int32_t ta, int64_t m, int64_t n, i
 
 /* ---- host helpers mirroring random.hpp / sketch.hpp ----------------------- */
 uint64_t sorsvd_sub_seed(uint64_t seed, uint64_t stream);                    /* random.hpp:24 */
-int sorsvd_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out, int nthreads); /* random.hpp:60 */
+int sorsvd_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out, int nthreads);
+/* Rows [row0, row0 + rows) of gaussian_matrix(., cols, seed) (the splitmix64 stream is counter based: a row
+ * block of a larger draw, e.g. one rank's rows of a sharded factor, is drawn without its prefix). */
+int sorsvd_gaussian_rows(int64_t cols, int64_t row0, int64_t rows, uint64_t seed, double* out, int nthreads); /* random.hpp:60 */
 long long sorsvd_flop_estimate(long long m, long long n, long long ell, long long k, long long q,
                                int variant);                                  /* sketch.hpp:178 */
 int sorsvd_validate_sketch(int64_t m, int64_t n, int32_t k, int32_t ell, int32_t q); /* sketch.hpp:62 */

@@ -35,7 +35,7 @@ from . import _capi as C
 __all__ = [
     "SketchMethod", "SketchConfig", "LowRankApprox", "FlopVariant", "RpcaConfig", "RpcaResult", "Context",
     "ShapeError", "ParameterError", "NumericalError", "CudaError", "NcclError", "UnsupportedError", "EmuGroup",
-    "sor_svd_power", "sor_svd", "sor_svd_power_batch", "r_svd", "tsr_svd", "truncate", "approx_error", "sord_header", "load_sord", "save_sord", "rpca_alm", "rpca_default_config", "estimate_rank_bound", "norm", "gaussian_matrix", "sub_seed",
+    "sor_svd_power", "sor_svd", "sor_svd_power_batch", "r_svd", "tsr_svd", "truncate", "approx_error", "sord_header", "load_sord", "save_sord", "rpca_alm", "rpca_default_config", "estimate_rank_bound", "norm", "gaussian_matrix_device", "gen_lowrank_device", "gen_rpca_instance_device", "gaussian_matrix", "sub_seed",
     "flop_estimate", "validate_sketch", "thin_qr", "full_svd", "matmul", "default_context", "version",
 ]
 
@@ -540,6 +540,49 @@ def norm(a, kind: str = "frobenius", ctx: Optional[Context] = None, seed: int = 
     _check(C.lib().sorsvd_norm_spectral_device(ctx.handle, m, n, A.data_ptr(), A.stride(0), seed & (2**64 - 1),
                                                ctypes.byref(out)), ctx.handle)
     return out.value
+
+
+# ------------------------------------------------- generators on the device --
+def gaussian_matrix_device(rows: int, cols: int, seed: int, device: int = 0, ctx: Optional[Context] = None):
+    """random.hpp:60-65 filled on the device (reference words / uniforms, device log / sincos:
+    a few ulp from `gaussian_matrix`, which is bit-identical to the reference)."""
+    import torch
+    out = torch.empty((rows, cols), dtype=torch.float64, device=torch.device("cuda", device))
+    ctx = ctx or default_context(device)
+    _torch_stream(ctx, out)
+    _check(C.lib().sorsvd_gaussian_matrix_device(ctx.handle, rows, cols, seed & (2**64 - 1), out.data_ptr(), cols),
+           ctx.handle)
+    return out
+
+
+def gen_lowrank_device(m: int, n: int, sigma, noise_std: float, seed: int, x_scale: float = 1.0, y_scale: float = 1.0,
+                       dtype=None, row0: int = 0, m_global: int = 0, device: int = 0, ctx: Optional[Context] = None):
+    """Rows [row0, row0 + m) of (x_scale X) diag(sigma) (y_scale Y)^T + noise_std E, the low-rank-plus-noise
+    family of BASELINE.json configs 1 / 3 / 5, generated in HBM (see sorsvd_gen_lowrank_device)."""
+    import torch
+    dtype = dtype or torch.float64
+    if dtype not in (torch.float64, torch.float32):
+        raise ParameterError("parameter: dtype must be float64 or float32")
+    sg = np.ascontiguousarray(sigma, dtype=np.float64)
+    out = torch.empty((m, n), dtype=dtype, device=torch.device("cuda", device))
+    ctx = ctx or default_context(device)
+    _torch_stream(ctx, out)
+    _check(C.lib().sorsvd_gen_lowrank_device(ctx.handle, m, n, sg.size, sg.ctypes.data_as(C.c_dp), x_scale, y_scale,
+                                             noise_std, seed & (2**64 - 1), row0, m_global,
+                                             C.F32 if dtype == torch.float32 else C.F64, out.data_ptr(), n), ctx.handle)
+    return out
+
+
+def gen_rpca_instance_device(n: int, r: int, s: int, seed: int, device: int = 0, ctx: Optional[Context] = None):
+    """matrixgen.hpp:99-124 on the device: (x, l_true, s_true) as CUDA float64 n x n tensors."""
+    import torch
+    dev = torch.device("cuda", device)
+    x, l, sp = (torch.empty((n, n), dtype=torch.float64, device=dev) for _ in range(3))
+    ctx = ctx or default_context(device)
+    _torch_stream(ctx, x)
+    _check(C.lib().sorsvd_gen_rpca_instance_device(ctx.handle, n, r, s, seed & (2**64 - 1), x.data_ptr(), l.data_ptr(),
+                                                   sp.data_ptr()), ctx.handle)
+    return x, l, sp
 
 
 def sord_header(path: str):

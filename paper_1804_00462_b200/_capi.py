@@ -96,6 +96,10 @@ SIGNATURES = [
     ("sorsvd_approx_error_spectral_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_i32, c_i32, c_vp, c_i64, c_vp,
                                                     c_vp, c_i64, c_dp]),
     ("sorsvd_norm_spectral_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, c_u64, c_dp]),
+    ("sorsvd_gaussian_matrix_device", c_i32, [c_vp, c_i64, c_i64, c_u64, c_vp, c_i64]),
+    ("sorsvd_gen_lowrank_device", c_i32, [c_vp, c_i64, c_i64, c_i32, c_dp, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_double, c_u64, c_i64, c_i64, c_i32, c_vp, c_i64]),
+    ("sorsvd_gen_rpca_instance_device", c_i32, [c_vp, c_i64, c_i32, ctypes.c_longlong, c_u64, c_vp, c_vp, c_vp]),
     ("sorsvd_rpca_telemetry", c_i32, [c_vp, c_i32, c_dp, ctypes.POINTER(c_i32)]),
     ("sorsvd_estimate_rank_bound", c_i32, [c_vp, c_i64, c_i64, c_dp, c_i64, ctypes.POINTER(c_i64), c_dp, c_dp]),
     ("sorsvd_estimate_rank_bound_device", c_i32, [c_vp, c_i64, c_i64, c_vp, c_i64, ctypes.POINTER(c_i64), c_dp, c_dp]),
@@ -120,6 +124,7 @@ SIGNATURES = [
                                         ctypes.POINTER(c_i32)]),
     ("sorsvd_sub_seed", c_u64, [c_u64, c_u64]),
     ("sorsvd_gaussian_matrix", c_i32, [c_i64, c_i64, c_u64, c_dp, ctypes.c_int]),
+    ("sorsvd_gaussian_rows", c_i32, [c_i64, c_i64, c_i64, c_u64, c_dp, ctypes.c_int]),
     ("sorsvd_flop_estimate", ctypes.c_longlong, [ctypes.c_longlong] * 5 + [ctypes.c_int]),
     ("sorsvd_validate_sketch", c_i32, [c_i64, c_i64, c_i32, c_i32, c_i32]),
     ("sorsvd_version", ctypes.c_char_p, []),

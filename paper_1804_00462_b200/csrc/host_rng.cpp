@@ -7,10 +7,12 @@
 // seed + t*gamma), so the row-major fill parallelises exactly: element e uses
 // words 2*floor(e/2)+1 and 2*floor(e/2)+2; even e takes r*cos(t), odd r*sin(t)
 // (NormalStream::next, random.hpp:35-48).
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <string>
 #include <thread>
+#include <unordered_set>
 #include <vector>
 
 #include "host_api.hpp"
@@ -75,6 +77,62 @@ void gaussian_fill(double* out, uint64_t count, uint64_t seed, int nthreads) {
         th.emplace_back(fill_range, out, a, b, seed);
     }
     for (auto& x : th) x.join();
+}
+
+// Elements [e0, e1) of the stream of `seed` into out[0 .. e1 - e0): a row block of a larger
+// gaussian_matrix (the generators' row-sharded factors).
+void gaussian_fill_range(double* out, uint64_t e0, uint64_t e1, uint64_t seed, int nthreads) {
+    if (e1 <= e0) return;
+    if (nthreads <= 0) {
+        nthreads = (int)std::thread::hardware_concurrency();
+        if (nthreads <= 0) nthreads = 1;
+    }
+    const uint64_t count = e1 - e0, min_chunk = 1 << 15;
+    uint64_t nt = (uint64_t)nthreads;
+    if (count / min_chunk + 1 < nt) nt = count / min_chunk + 1;
+    double* base = out - e0;  // fill_range indexes by the absolute element number
+    if (nt <= 1) {
+        fill_range(base, e0, e1, seed);
+        return;
+    }
+    std::vector<std::thread> th;
+    const uint64_t per = ((count / nt) + 2) & ~1ULL;
+    for (uint64_t t = 0; t < nt; ++t) {
+        // chunk edges on even absolute element numbers keep the Box-Muller pairs together
+        uint64_t a = e0 + t * per, b = e0 + (t + 1) * per;
+        if (t > 0) a &= ~1ULL;
+        b &= ~1ULL;
+        if (t + 1 == nt || b > e1) b = e1;
+        if (a >= b) break;
+        th.emplace_back(fill_range, base, a, b, seed);
+        if (b == e1) break;
+    }
+    for (auto& x : th) x.join();
+}
+
+// The sparse component of gen_rpca_instance (matrixgen.hpp:106-121): s distinct cells of
+// {0, ..., cells - 1} by Floyd's sampling from the stream of sub_seed(seed, 3), sorted, with values
+// +-50 from the words of sub_seed(seed, 4). Integer arithmetic only: identical to the reference.
+void rpca_support(long long cells, long long s, uint64_t seed, std::vector<long long>& pos, std::vector<double>& val) {
+    pos.clear();
+    val.clear();
+    if (s <= 0) return;
+    uint64_t st = sub_seed(seed, 3);
+    std::unordered_set<long long> chosen;
+    chosen.reserve((size_t)s * 2);
+    for (long long j = cells - s; j < cells; ++j) {
+        st += kGamma;
+        const long long t = (long long)(mix(st) % (uint64_t)(j + 1));
+        if (!chosen.insert(t).second) chosen.insert(j);
+    }
+    pos.assign(chosen.begin(), chosen.end());
+    std::sort(pos.begin(), pos.end());
+    uint64_t sg = sub_seed(seed, 4);
+    val.resize(pos.size());
+    for (size_t i = 0; i < pos.size(); ++i) {
+        sg += kGamma;
+        val[i] = (mix(sg) & 1ULL) ? 50.0 : -50.0;
+    }
 }
 
 long long flop_estimate(long long m, long long n, long long ell, long long k, long long q, int variant) {

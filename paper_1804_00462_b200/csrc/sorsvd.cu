@@ -44,6 +44,7 @@
 #include "cholc_f64.cuh"
 #include "ozaki_i8.cuh"
 #include "ozaki_planes_i8.cuh"
+#include "gen_f64.cuh"
 #include "smallk_f64.cuh"
 #include <cfloat>
 
@@ -4093,6 +4094,108 @@ int sorsvd_rpca_alm(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* D, d
     });
 }
 
+// ---- f4: test-matrix generators on the device (gen_f64.cuh) ---------------------------------
+// gaussian_matrix(rows, cols, seed) (random.hpp:60-65) written straight into device memory; the
+// words and uniforms are the reference's, log / sincos are the device's (a few ulp from glibc's).
+int sorsvd_gaussian_matrix_device(sorsvd_ctx* c, int64_t rows, int64_t cols, uint64_t seed, double* dOut, int64_t ld) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (rows < 1 || cols < 1 || ld < cols) throw Error{SORSVD_ERR_SHAPE, "shape: matrix dimensions must be positive"};
+        if (!dOut) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        const int64_t pairs = (rows * cols + 1) / 2;
+        gaussian_fill_kernel<<<(unsigned)std::min<int64_t>(cdiv(pairs, 256), (int64_t)c->num_sms * 16), 256, 0, c->stream>>>(
+            dOut, rows, cols, ld, seed, 1.0);
+        check_launch(c);
+    });
+}
+
+// The low-rank-plus-noise family of BASELINE.json's configs 1, 3 and 5, rows [row0, row0 + m) of the
+// m_global x n matrix A = (x_scale X) diag(sigma) (y_scale Y)^T + noise_std E:
+//   X = gaussian_matrix(m_global, r, sub_seed(seed, 1)), Y = gaussian_matrix(n, r, sub_seed(seed, 2))
+//   (drawn on the host, bit-identical to the reference stream, and uploaded: (m + n) r values),
+//   E's global row i = the first n normals of NormalStream(sub_seed(sub_seed(seed, 3), i)), drawn in
+//   the kernel (m n values). Each rank of a row-sharded run generates its own block.
+int sorsvd_gen_lowrank_device(sorsvd_ctx* c, int64_t m, int64_t n, int32_t r, const double* sigma, double x_scale,
+                              double y_scale, double noise_std, uint64_t seed, int64_t row0, int64_t m_global,
+                              int32_t dtype, void* dA, int64_t lda) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (m < 1 || n < 1 || r < 1 || lda < n || row0 < 0) throw Error{SORSVD_ERR_SHAPE, "shape: bad generator shape"};
+        if (m_global <= 0) m_global = row0 + m;
+        if (row0 + m > m_global) throw Error{SORSVD_ERR_SHAPE, "shape: row block outside the matrix"};
+        if (!sigma || !dA) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        if (dtype != SORSVD_F64 && dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
+        std::vector<double> hx((size_t)m * r), hy((size_t)n * r);
+        sorsvd_host::gaussian_fill_range(hx.data(), (uint64_t)row0 * r, (uint64_t)(row0 + m) * r,
+                                         sorsvd_host::sub_seed(seed, 1), 0);
+        sorsvd_host::gaussian_fill(hy.data(), (uint64_t)n * r, sorsvd_host::sub_seed(seed, 2), 0);
+        for (double& v : hx) v *= x_scale;
+        for (double& v : hy) v *= y_scale;
+        double* X = dbuf(c, "gen_X", (size_t)m * r);
+        double* Y = dbuf(c, "gen_Y", (size_t)n * r);
+        double* S = dbuf(c, "gen_S", (size_t)r);
+        CK(cudaMemcpyAsync(X, hx.data(), hx.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(Y, hy.data(), hy.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(S, sigma, (size_t)r * 8, cudaMemcpyHostToDevice, c->stream));
+        const dim3 grid((unsigned)cdiv(n, 64), (unsigned)cdiv(m, 64));
+        const uint64_t ns = sorsvd_host::sub_seed(seed, 3);
+        if (dtype == SORSVD_F64)
+            gen_lowrank_kernel<double><<<grid, kRpcaThreads, 0, c->stream>>>(static_cast<double*>(dA), lda, m, n, X, r, S,
+                                                                            Y, r, r, noise_std, ns, row0);
+        else
+            gen_lowrank_kernel<float><<<grid, kRpcaThreads, 0, c->stream>>>(static_cast<float*>(dA), lda, m, n, X, r, S, Y,
+                                                                           r, r, noise_std, ns, row0);
+        check_launch(c);
+        CK(cudaStreamSynchronize(c->stream));  // the host staging vectors go out of scope
+    });
+}
+
+// gen_rpca_instance(n, r, s, seed) (matrixgen.hpp:99-124) assembled on the device: L = U V^T from the
+// host-drawn n x r factors (streams 1, 2) on DMMA tiles, the sparse support by Floyd's sampling and the
+// +-50 signs on the host (integer arithmetic, identical to the reference), scattered into S and X.
+int sorsvd_gen_rpca_instance_device(sorsvd_ctx* c, int64_t n, int32_t r, long long s, uint64_t seed, double* dX,
+                                    double* dL, double* dS) {
+    if (!c) return SORSVD_ERR_PARAMETER;
+    return guarded(c, [&] {
+        if (r < 1 || r >= n) throw Error{SORSVD_ERR_PARAMETER, "parameter: gen_rpca_instance needs 1 <= r < n"};
+        const long long cells = (long long)n * n;
+        if (s < 0 || s > cells) throw Error{SORSVD_ERR_PARAMETER, "parameter: sparse cardinality s out of [0, n^2]"};
+        if (!dX) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
+        std::vector<double> hu((size_t)n * r), hv((size_t)n * r), ones((size_t)r, 1.0), val;
+        std::vector<long long> pos;
+        sorsvd_host::gaussian_fill(hu.data(), hu.size(), sorsvd_host::sub_seed(seed, 1), 0);
+        sorsvd_host::gaussian_fill(hv.data(), hv.size(), sorsvd_host::sub_seed(seed, 2), 0);
+        sorsvd_host::rpca_support(cells, s, seed, pos, val);
+        double* U = dbuf(c, "gen_X", (size_t)n * r);
+        double* V = dbuf(c, "gen_Y", (size_t)n * r);
+        double* S1 = dbuf(c, "gen_S", (size_t)r);
+        auto* dpos = reinterpret_cast<long long*>(dbuf(c, "gen_pos", std::max<size_t>(pos.size(), 1)));
+        double* dval = dbuf(c, "gen_val", std::max<size_t>(val.size(), 1));
+        CK(cudaMemcpyAsync(U, hu.data(), hu.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(V, hv.data(), hv.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(S1, ones.data(), (size_t)r * 8, cudaMemcpyHostToDevice, c->stream));
+        if (!pos.empty()) {
+            CK(cudaMemcpyAsync(dpos, pos.data(), pos.size() * 8, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(dval, val.data(), val.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        }
+        const dim3 grid((unsigned)cdiv(n, 64), (unsigned)cdiv(n, 64));
+        gen_lowrank_kernel<double><<<grid, kRpcaThreads, 0, c->stream>>>(dX, n, n, n, U, r, S1, V, r, r, 0.0, 0, 0);
+        check_launch(c);
+        if (dL) CK(cudaMemcpyAsync(dL, dX, (size_t)cells * 8, cudaMemcpyDeviceToDevice, c->stream));
+        if (dS) CK(cudaMemsetAsync(dS, 0, (size_t)cells * 8, c->stream));
+        if (!pos.empty()) {
+            const unsigned blocks = (unsigned)std::min<int64_t>(cdiv((int64_t)pos.size(), 256), (int64_t)c->num_sms * 8);
+            scatter_add_kernel<<<blocks, 256, 0, c->stream>>>(dX, n, n, dpos, dval, (int64_t)pos.size());
+            check_launch(c);
+            if (dS) {
+                scatter_add_kernel<<<blocks, 256, 0, c->stream>>>(dS, n, n, dpos, dval, (int64_t)pos.size());
+                check_launch(c);
+            }
+        }
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
 // Per-iteration telemetry of the context's last rpca_alm (iter, mu, rel_error,
 // rank_l, nnz_s): up to cap_rows rows of 5 doubles into out, *rows = iterations available.
 int sorsvd_rpca_telemetry(sorsvd_ctx* c, int32_t cap_rows, double* out, int32_t* rows) {
@@ -4309,6 +4412,17 @@ int sorsvd_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, double* ou
         return SORSVD_ERR_SHAPE;
     }
     sorsvd_host::gaussian_fill(out, (uint64_t)rows * cols, seed, nthreads);
+    return SORSVD_OK;
+}
+
+// Rows [row0, row0 + rows) of gaussian_matrix(., cols, seed): the stream is counter based, so a
+// row block of a larger draw (a rank's rows of a sharded factor) needs no prefix.
+int sorsvd_gaussian_rows(int64_t cols, int64_t row0, int64_t rows, uint64_t seed, double* out, int nthreads) {
+    if (rows < 1 || cols < 1 || row0 < 0 || !out) {
+        g_global_err = "shape: matrix dimensions must be positive";
+        return SORSVD_ERR_SHAPE;
+    }
+    sorsvd_host::gaussian_fill_range(out, (uint64_t)row0 * cols, (uint64_t)(row0 + rows) * cols, seed, nthreads);
     return SORSVD_OK;
 }
 

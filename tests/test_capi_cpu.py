@@ -122,3 +122,20 @@ def test_sord_header_cpu(tmp_path):
     short.write_bytes(open(p, "rb").read()[:-8])
     with pytest.raises(P.ShapeError):
         P.sord_header(str(short))
+
+
+def test_gaussian_rows_is_a_slice_of_the_full_draw():
+    """sorsvd_gaussian_rows (counter-based stream, random.hpp:27-55): any row block equals the same rows of
+    gaussian_matrix, for odd / even offsets and every thread count (the Box-Muller pairs straddle rows)."""
+    import ctypes
+    import paper_1804_00462_b200 as P
+    from oracle import sorsvd_oracle as O
+    lib = P._capi.lib()
+    for cols, total, seed in [(7, 41, 5), (20, 30000, 6), (1, 9, 7), (33, 5001, 8)]:
+        full = O.gaussian_matrix(total, cols, seed)
+        for row0, rows in [(0, total), (1, total - 1), (3, 17), (total - 5, 5), (total // 2 + 1, total // 3)]:
+            rows = min(rows, total - row0)
+            for nt in (1, 3, 16):
+                out = np.full((rows, cols), np.nan)
+                assert lib.sorsvd_gaussian_rows(cols, row0, rows, seed, out.ctypes.data_as(P._capi.c_dp), nt) == 0
+                assert np.array_equal(out, full[row0:row0 + rows]), (cols, total, row0, rows, nt)
