@@ -398,7 +398,7 @@ def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Contex
 
 
 def sor_svd_power_batch(a, k: int, cfg: SketchConfig, trials: int, seeds=None, omegas=None,
-                        ctx: Optional[Context] = None) -> list:
+                        ctx: Optional[Context] = None, m_global: int = 0) -> list:
     """`trials` independent sor_svd_power calls on one A (the Monte-Carlo loop of
     bounds.hpp:262-379): trial t uses seeds[t], default cfg.seed + t
     (bounds.hpp:288), or omegas[t] (trials, n, ell). Every pass over A serves
@@ -419,7 +419,7 @@ def sor_svd_power_batch(a, k: int, cfg: SketchConfig, trials: int, seeds=None, o
         ctx = ctx or default_context(a.device.index or 0)
         _torch_stream(ctx, a)
         m, n = a.shape
-        d = _desc(m, n, a.stride(0), k, cfg, flags, 0, C.F32 if a.dtype == torch.float32 else C.F64)
+        d = _desc(m, n, a.stride(0), k, cfg, flags, m_global, C.F32 if a.dtype == torch.float32 else C.F64)
         u = torch.empty((trials, m, k), dtype=torch.float64, device=a.device)
         s = torch.empty((trials, k), dtype=torch.float64, device=a.device)
         v = torch.empty((trials, n, k), dtype=torch.float64, device=a.device)
@@ -436,7 +436,7 @@ def sor_svd_power_batch(a, k: int, cfg: SketchConfig, trials: int, seeds=None, o
         a = np.ascontiguousarray(a, dtype=np.float32 if a.dtype == np.float32 else np.float64)
         ctx = ctx or default_context(0)
         m, n = a.shape
-        d = _desc(m, n, n, k, cfg, flags, 0, C.F32 if a.dtype == np.float32 else C.F64)
+        d = _desc(m, n, n, k, cfg, flags, m_global, C.F32 if a.dtype == np.float32 else C.F64)
         u = _host_out((trials, m, k))
         s = _host_out((trials, k))
         v = _host_out((trials, n, k))
@@ -464,17 +464,17 @@ def sor_svd(a, k: int, cfg: SketchConfig, **kw) -> LowRankApprox:
 
 
 def r_svd(a, ell: int, q: int, seed: int, omega=None, ctx: Optional[Context] = None,
-          use_graph: bool = True) -> LowRankApprox:
+          use_graph: bool = True, m_global: int = 0) -> LowRankApprox:
     """One-sided randomized SVD baseline (sketch.hpp:124-136): all ell triplets,
     passes 2q+2. omega (n, ell) defaults to gaussian_matrix(n, ell, seed)."""
     cfg = SketchConfig(ell=ell, q=q, seed=seed)
     flags = 0 if use_graph else C.FLAG_NO_GRAPH
-    st, u, s, v = _decompose("rsvd", a, ell, cfg, flags, omega, None, ctx)
+    st, u, s, v = _decompose("rsvd", a, ell, cfg, flags, omega, None, ctx, m_global)
     return LowRankApprox(u, s, v, SketchMethod.rsvd, st.passes, ell, q, seed, st.as_dict())
 
 
 def tsr_svd(a, ell: int, seed: int, psi1=None, psi2=None, ctx: Optional[Context] = None,
-            use_graph: bool = True) -> LowRankApprox:
+            use_graph: bool = True, m_global: int = 0) -> LowRankApprox:
     """Two-sided randomized SVD baseline (sketch.hpp:139-149): Psi1 (n, ell) from
     seed, Psi2 (m, ell) from seed ^ 1 unless both are given; pseudo-inverse core;
     all ell triplets, passes 1."""
@@ -482,7 +482,7 @@ def tsr_svd(a, ell: int, seed: int, psi1=None, psi2=None, ctx: Optional[Context]
         raise ParameterError("parameter: give both psi1 and psi2 or neither")
     cfg = SketchConfig(ell=ell, q=0, seed=seed)
     flags = 0 if use_graph else C.FLAG_NO_GRAPH
-    st, u, s, v = _decompose("tsr", a, ell, cfg, flags, psi1, psi2, ctx)
+    st, u, s, v = _decompose("tsr", a, ell, cfg, flags, psi1, psi2, ctx, m_global)
     return LowRankApprox(u, s, v, SketchMethod.tsr, st.passes, ell, 0, seed, st.as_dict())
 
 

@@ -2085,6 +2085,28 @@ void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, 
     check_launch(c);
 }
 
+// Q = thin_qr(T).q of a row-sharded m x ell operand (the sketch T1 / Y; sketch.hpp:98, :129, :145):
+// single rank -> the plain QR; multi-rank -> the local TSQR runs to one R per rank, the k x k R's
+// cross ranks by all-gather, every rank solves the small cross-rank tree redundantly and applies
+// its own k x k factor to its local leaves (k > 256: the CholeskyQR Gram matrices are summed).
+void qr_rows(sorsvd_ctx* c, const SorProblem& P, QrPlan* p1, QrPlan* pg, double* T, double* Q, cudaStream_t s) {
+    const int Np = P.Np, ell = P.ell;
+    if (c->world > 1 && p1->big) {
+        qr_run_big(c, p1, T, Np, Q, Np, s, P.m_global, true);
+    } else if (c->world > 1) {
+        qr_factor(c, p1, T, Np, Q, Np, false, s);
+        const int L1 = (int)p1->nodes.size() - 1;
+        double* Rg = dbuf(c, "Rg", (size_t)c->world * ell * ell);
+        comm_allgather(c, p1->R[L1], Rg, (size_t)ell * ell, s);
+        qr_factor(c, pg, nullptr, 0, nullptr, 0, true, s, Rg);
+        qr_formq(c, pg, nullptr, 0, nullptr, 0, nullptr, s, true);
+        const double* Cg = qr_leaf_factors(pg, false) + (size_t)c->rank * ell * Np;
+        qr_formq(c, p1, T, Np, Q, Np, Cg, s);
+    } else {
+        qr_run(c, p1, T, Np, Q, Np, s);
+    }
+}
+
 // T2 = A^T T1 summed over the ranks' row blocks (sketch.hpp:96). Single rank: one
 // launch. Multi-rank: the pass runs as kTnBlocks launches over column blocks of A
 // (row blocks of T2), and each finished block's all-reduce is issued on the comm
@@ -2188,26 +2210,17 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     // Q1 = thin_qr(T1).q, Q2 = thin_qr(T2).q concurrently (sketch.hpp:98-99)
     CK(cudaEventRecord(c->ev_fork, s));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    if (c->world > 1 && p1->big) {
-        qr_run_big(c, p1, b.T1, Np, b.Q1, Np, s, P.m_global, true);  // Gram matrices summed over ranks
-    } else if (c->world > 1) {
-        qr_factor(c, p1, b.T1, Np, b.Q1, Np, false, s);
-        const int L1 = (int)p1->nodes.size() - 1;
-        double* Rg = dbuf(c, "Rg", (size_t)c->world * ell * ell);
-        comm_allgather(c, p1->R[L1], Rg, (size_t)ell * ell, s);
-        qr_factor(c, pg, nullptr, 0, nullptr, 0, true, s, Rg);
-        qr_formq(c, pg, nullptr, 0, nullptr, 0, nullptr, s, true);
-        const double* Cg = qr_leaf_factors(pg, false) + (size_t)c->rank * ell * Np;
-        qr_formq(c, p1, b.T1, Np, b.Q1, Np, Cg, s);
-    } else {
-        qr_run(c, p1, b.T1, Np, b.Q1, Np, s);
-    }
+    const bool keep_t1 = P.single_pass && c->world > 1;  // the sharded TSQR factors T1 in place
+    if (keep_t1) CK(cudaMemcpyAsync(b.Y, b.T1, (size_t)P.m * Np * 8, cudaMemcpyDeviceToDevice, s));
+    qr_rows(c, P, p1, pg, b.T1, b.Q1, s);
     qr_run(c, p2, b.T2, Np, b.Q2, Np, c->side);
     CK(cudaEventRecord(c->ev_join, c->side));
     CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     record_stage(c, timing, 2);
     if (P.single_pass) {
-        enqueue_m_approx(c, P, b, s);
+        SorBuffers bm = b;
+        if (keep_t1) bm.T1 = b.Y;
+        enqueue_m_approx(c, P, bm, s);
     } else {
     // M = Q1^T (A Q2)   (sketch.hpp:100-102)
     if (P.tf32) {
@@ -2331,18 +2344,21 @@ void enqueue_basis(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, cuda
 // (one more TN pass + a thin QR), then the ell x ell one-sided Jacobi on
 // Rb^T = U_B S (Vj)^T, so U_B comes out of the Jacobi kernel with the
 // reference sign canonicalisation (dense.hpp:80-95) and V = Qb Vj.
-void enqueue_rsvd(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, bool timing) {
+// Row-sharded A: Y and Qy are row blocks (local passes, the sharded TSQR), every A^T product is summed
+// over ranks, B^T's QR / the Jacobi SVD / V are replicated.
+void enqueue_rsvd(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, QrPlan* pg,
+                  bool timing) {
     cudaStream_t s = c->stream;
     record_stage(c, timing, 0);
     pass_gemm(c, P, false, b.T2, b.T1, s);  // Y = A Omega        (:127)
     for (int i = 0; i < P.q; ++i) {         // Y = A (A^T Y)      (:128)
-        pass_gemm(c, P, true, b.T1, b.T2, s);
+        tn_pass_reduced(c, P, b.T1, b.T2, s);
         pass_gemm(c, P, false, b.T2, b.T1, s);
     }
     record_stage(c, timing, 1);
-    qr_run(c, p1, b.T1, P.Np, b.Q1, P.Np, s);  // Qy = thin_qr(Y).q   (:129)
+    qr_rows(c, P, p1, pg, b.T1, b.Q1, s);      // Qy = thin_qr(Y).q   (:129)
     record_stage(c, timing, 2);
-    pass_gemm(c, P, true, b.Q1, b.T2, s);      // B^T = A^T Qy       (:130)
+    tn_pass_reduced(c, P, b.Q1, b.T2, s);      // B^T = A^T Qy       (:130)
     qr_run(c, p2, b.T2, P.Np, b.Q2, P.Np, s);  // B^T = Qb Rb
     const int L = (int)p2->nodes.size() - 1;
     transpose_pad_kernel<<<std::min(cdiv((int64_t)P.Np * P.Np, 256), (int64_t)c->num_sms), 256, 0, s>>>(
@@ -2360,12 +2376,32 @@ void enqueue_rsvd(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPla
 // full_svd(B), U = Q1 U_B, V = Q2 V_B. T2 holds Psi1, b.Psi2 holds Psi2.
 // The two sketches are two launches over A here (the reference counts the
 // pair as its one pass, sketch.hpp:148).
-void enqueue_tsr(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, bool timing) {
+// Row-sharded A: Psi2's rows are this rank's rows of gaussian_matrix(m_global, ell, seed ^ 1); Y2 is
+// summed over ranks; Q1 by the sharded TSQR; m_approx sums Q1^T Y1 over ranks.
+void enqueue_tsr(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, QrPlan* pg,
+                 bool timing) {
     cudaStream_t s = c->stream;
     record_stage(c, timing, 0);
-    pass_gemm(c, P, false, b.T2, b.T1, s);   // Y1 = A Psi1     (:143)
-    pass_gemm(c, P, true, b.Psi2, b.Y2, s);  // Y2 = A^T Psi2   (:144)
+    pass_gemm(c, P, false, b.T2, b.T1, s);       // Y1 = A Psi1     (:143)
+    tn_pass_reduced(c, P, b.Psi2, b.Y2, s);      // Y2 = A^T Psi2   (:144)
     record_stage(c, timing, 1);
+    if (c->world > 1) {  // collectives stay on one stream: the two QRs run one after the other
+        // the sharded TSQR factors its operand in place: keep Y1 for m_approx's Q1^T Y1
+        CK(cudaMemcpyAsync(b.Y, b.T1, (size_t)P.m * P.Np * 8, cudaMemcpyDeviceToDevice, s));
+        qr_rows(c, P, p1, pg, b.T1, b.Q1, s);
+        qr_run(c, p2, b.Y2, P.Np, b.Q2, P.Np, s);
+        record_stage(c, timing, 2);
+        SorBuffers bb = b;
+        bb.T2pre = b.T2;
+        bb.T1 = b.Y;
+        enqueue_m_approx(c, P, bb, s);
+        record_stage(c, timing, 3);
+        run_jacobi(c, P.ell, b.Mk, P.Np, b.Uk, P.Np, b.Sk, b.Vk, P.Np, b.sweeps, s);
+        record_stage(c, timing, 4);
+        enqueue_basis(c, P, b, s);
+        record_stage(c, timing, 5);
+        return;
+    }
     CK(cudaEventRecord(c->ev_fork, s));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     qr_run(c, p1, b.T1, P.Np, b.Q1, P.Np, s);        // (:145)
@@ -2491,6 +2527,22 @@ bool ozaki_wanted(uint32_t flags, int64_t m, int64_t n, int ell) {
     return (double)m * (double)n * (double)ell >= 68719476736.0 /* 2^36 */ && ell >= 32;
 }
 
+// First global row of this rank's block: the exclusive prefix sum of the ranks' row counts
+// (one small all-reduce of a world-long vector; 0 on a single rank).
+int64_t rank_row0(sorsvd_ctx* c, int64_t m) {
+    if (c->world <= 1) return 0;
+    double* dv = dbuf(c, "row_counts", (size_t)c->world);
+    std::vector<double> h((size_t)c->world, 0.0);
+    h[(size_t)c->rank] = (double)m;
+    CK(cudaMemcpyAsync(dv, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    comm_allreduce(c, dv, (size_t)c->world, false, c->stream);
+    CK(cudaMemcpyAsync(h.data(), dv, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    int64_t r0 = 0;
+    for (int r = 0; r < c->rank; ++r) r0 += (int64_t)h[(size_t)r];
+    return r0;
+}
+
 // Core device-side call. dOmega: n x ell dense (or null: drawn on the host).
 void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const double* dOmega, double* dU,
                 double* dS, double* dV, sorsvd_stats* st, int method = SORSVD_SOR_POWER,
@@ -2498,7 +2550,6 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     validate(d);
     const bool baseline = method == SORSVD_RSVD || method == SORSVD_TSR;
     if (baseline) {
-        if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "r_svd / tsr_svd: single-rank only in this build"};
         if (d->flags & SORSVD_FLAG_TF32) throw Error{SORSVD_ERR_UNSUPPORTED, "r_svd / tsr_svd: no TF32 mode"};
     }
     SorProblem P{};
@@ -2527,8 +2578,11 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         if (dPsi2 && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
             CK(cudaMemcpyAsync(psi2_in, dPsi2, (size_t)P.m * P.ell * 8, cudaMemcpyDeviceToDevice, c->stream));
         } else {
+            // this rank's rows [row0, row0 + m) of the m_global x ell draw
+            const int64_t row0 = rank_row0(c, P.m);
             c->host_psi2.resize((size_t)P.m * P.ell);
-            sorsvd_host::gaussian_fill(c->host_psi2.data(), (uint64_t)P.m * P.ell, d->seed ^ 1ULL, 0);
+            sorsvd_host::gaussian_fill_range(c->host_psi2.data(), (uint64_t)row0 * P.ell, (uint64_t)(row0 + P.m) * P.ell,
+                                             d->seed ^ 1ULL, 0);
             CK(cudaMemcpyAsync(psi2_in, c->host_psi2.data(), (size_t)P.m * P.ell * 8, cudaMemcpyHostToDevice,
                                c->stream));
         }
@@ -2563,9 +2617,9 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
             CK(cudaMemsetAsync(b.Psi2, 0, (size_t)P.m * P.Np * 8, c->stream));
             CK(cudaMemcpy2DAsync(b.Psi2, (size_t)P.Np * 8, psi2_in, (size_t)P.ell * 8, (size_t)P.ell * 8,
                                  (size_t)P.m, cudaMemcpyDeviceToDevice, c->stream));
-            enqueue_tsr(c, P, b, p1, p2, timing);
+            enqueue_tsr(c, P, b, p1, p2, pg, timing);
         } else if (method == SORSVD_RSVD) {
-            enqueue_rsvd(c, P, b, p1, p2, timing);
+            enqueue_rsvd(c, P, b, p1, p2, pg, timing);
         } else {
             enqueue_sor(c, P, b, p1, p2, pg, timing);
         }
@@ -2677,7 +2731,6 @@ void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_
                   const double* dOmegas, double* dU, double* dS, double* dV, sorsvd_stats* st) {
     validate(d);
     if (trials < 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: trials must be positive"};
-    if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "batched trials: single-rank only in this build"};
     if (d->flags & SORSVD_FLAG_TF32) throw Error{SORSVD_ERR_UNSUPPORTED, "batched trials: no TF32 mode"};
     if (d->single_pass) throw Error{SORSVD_ERR_UNSUPPORTED, "batched trials: single_pass not supported"};
     if (d->ell > kHouseMaxK) throw Error{SORSVD_ERR_UNSUPPORTED, "batched trials: ell <= 256"};
@@ -2692,7 +2745,8 @@ void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_
     P.ell = d->ell;
     P.q = d->q;
     P.Np = npad(d->ell);
-    P.m_global = P.m;
+    P.m_global = d->m_global > 0 ? d->m_global : P.m;
+    const bool multi = c->world > 1;  // row-sharded A: partial sums all-reduced, T1's QR by the sharded TSQR
     const int Np = P.Np, ell = P.ell, k = P.k;
     const int64_t m = P.m, n = P.n;
     const int Wt = trials * Np;                       // the trials' columns side by side
@@ -2737,10 +2791,18 @@ void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_
     for (int i = 0; i <= P.q; ++i) {  // sketch.hpp:93-97, all trials per launch
         pass(false, X, T1b);
         pass(true, T1b, X);
+        if (multi) comm_allreduce(c, X, (size_t)n * W, false, s);  // T2_all summed over the row blocks
     }
-    // per-trial QRs (sketch.hpp:98-99) side by side on the trial streams
-    const int S = std::min(trials, kTrialStreams);
+    // per-trial QRs (sketch.hpp:98-99) side by side on the trial streams (multi-rank: one after
+    // the other on the context stream, so that every rank issues its collectives in the same order)
+    const int S = multi ? 1 : std::min(trials, kTrialStreams);
     ensure_trial_streams(c, S);
+    QrPlan* pgm = multi ? get_qr_plan(c, (int64_t)c->world * ell, ell, c->world, "G") : nullptr;
+    if (multi) {
+        dbuf(c, "Rg", (size_t)c->world * ell * ell);
+        dbuf(c, "CinLocal", (size_t)ell * Np);
+    }
+    auto tstream = [&](int t) { return multi ? s : c->tstreams[t % S]; };
     struct Trial {
         double *T1, *T2, *Q1, *Q2, *Mk, *Uk, *Vk, *Sk, *Uo, *Vo;
         int* sweeps;
@@ -2769,10 +2831,12 @@ void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_
         x.p2 = get_qr_plan(c, n, ell, 0, (sl + "T2").c_str());
     }
     auto fork = [&]() {
+        if (multi) return;
         CK(cudaEventRecord(c->ev_fork, s));
         for (int j = 0; j < S; ++j) CK(cudaStreamWaitEvent(c->tstreams[j], c->ev_fork, 0));
     };
     auto join = [&]() {
+        if (multi) return;
         for (int j = 0; j < S; ++j) {
             CK(cudaEventRecord(c->tevents[j], c->tstreams[j]));
             CK(cudaStreamWaitEvent(s, c->tevents[j], 0));
@@ -2780,13 +2844,13 @@ void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_
     };
     fork();
     for (int t = 0; t < trials; ++t) {
-        cudaStream_t ts = c->tstreams[t % S];
+        cudaStream_t ts = tstream(t);
         Trial& x = tr[t];
         CK(cudaMemcpy2DAsync(x.T1, (size_t)Np * 8, T1b + (size_t)t * Np, (size_t)W * 8, (size_t)Np * 8, (size_t)m,
                              cudaMemcpyDeviceToDevice, ts));
         CK(cudaMemcpy2DAsync(x.T2, (size_t)Np * 8, X + (size_t)t * Np, (size_t)W * 8, (size_t)Np * 8, (size_t)n,
                              cudaMemcpyDeviceToDevice, ts));
-        qr_run(c, x.p1, x.T1, Np, x.Q1, Np, ts);
+        qr_rows(c, P, x.p1, pgm, x.T1, x.Q1, ts);
         qr_run(c, x.p2, x.T2, Np, x.Q2, Np, ts);
         CK(cudaMemcpy2DAsync(X + (size_t)t * Np, (size_t)W * 8, x.Q2, (size_t)Np * 8, (size_t)Np * 8, (size_t)n,
                              cudaMemcpyDeviceToDevice, ts));
@@ -2795,7 +2859,7 @@ void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_
     pass(false, X, Yb);  // Y_t = A Q2_t for all trials in one launch (sketch.hpp:100-102)
     fork();
     for (int t = 0; t < trials; ++t) {
-        cudaStream_t ts = c->tstreams[t % S];
+        cudaStream_t ts = tstream(t);
         Trial& x = tr[t];
         const std::string ws = "bws" + std::to_string(t % S);
         GemmCall h;  // M_t = Q1_t^T Y_t
@@ -2811,6 +2875,7 @@ void batch_device(sorsvd_ctx* c, const sorsvd_desc* d, int trials, const uint64_
         h.ldc = Np;
         h.ws_name = ws.c_str();
         run_gemm(c, h, ts);
+        if (multi) comm_allreduce(c, x.Mk, (size_t)ell * Np, false, ts);
         run_jacobi(c, ell, x.Mk, Np, x.Uk, Np, x.Sk, x.Vk, Np, x.sweeps, ts);  // sketch.hpp:103
         for (int hh = 0; hh < 2; ++hh) {  // U = Q1 Ut_k, V = Q2 Vt_k   (sketch.hpp:105,107)
             GemmCall g;

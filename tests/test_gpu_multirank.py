@@ -258,3 +258,103 @@ def test_sharded_approx_error_matches_single(env):
     g.close()
     assert res[0] == res[1] == res[2]
     assert abs(res[0] - ref) <= 1e-10 * ref
+
+
+def _sharded_call(P, torch, A, world, fn):
+    """fn(block, ctx, m_global) on every rank's contiguous row block of A, one host thread per rank."""
+    m = A.shape[0]
+    g = P.EmuGroup(world)
+    base, extra = divmod(m, world)
+    bounds, r0 = [], 0
+    for r in range(world):
+        cnt = base + (1 if r < extra else 0)
+        bounds.append((r0, r0 + cnt))
+        r0 += cnt
+    ctxs = [P.Context(0, rank=r, emu_group=g) for r in range(world)]
+    out, err = [None] * world, [None] * world
+
+    def work(r):
+        try:
+            a, b = bounds[r]
+            out[r] = fn(torch.from_numpy(np.ascontiguousarray(A[a:b])).cuda(), ctxs[r], m)
+            torch.cuda.synchronize()
+        except Exception as e:
+            err[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    for c in ctxs:
+        c.close()
+    g.close()
+    return out
+
+
+@pytest.mark.parametrize("world,m,n,ell,q", [(2, 3000, 500, 24, 1), (3, 2999, 700, 16, 0), (4, 4000, 300, 12, 2)])
+def test_sharded_r_svd_matches_single_rank(env, world, m, n, ell, q):
+    """r_svd (sketch.hpp:124-136) over row blocks: the sharded TSQR of Y, every A^T product summed over ranks."""
+    P, torch = env
+    A = O.gen_lowrank_decay(m, n, 40, lambda j: 2.0 ** (-j / 4), 1e-3, m + 3 * world)
+    ref = O.r_svd(A, ell, q, 19)
+    out = _sharded_call(P, torch, A, world, lambda blk, ctx, mg: P.r_svd(blk, ell, q, 19, ctx=ctx, m_global=mg))
+    s0, v0 = out[0].sigma.cpu().numpy(), out[0].v.cpu().numpy()
+    for o in out[1:]:
+        np.testing.assert_array_equal(o.sigma.cpu().numpy(), s0)
+        np.testing.assert_array_equal(o.v.cpu().numpy(), v0)
+    u = np.vstack([o.u.cpu().numpy() for o in out])
+    kk = min(ell, 10)
+    assert O.sigma_rel_err(s0[:kk], ref.sigma[:kk]).max() <= 1e-10
+    assert O.lowrank_rel_diff(u[:, :kk], s0[:kk], v0[:, :kk], ref.u[:, :kk], ref.sigma[:kk], ref.v[:, :kk]) <= 1e-8
+    assert out[0].passes == ref.passes
+
+
+@pytest.mark.parametrize("world,m,n,ell", [(2, 3000, 500, 24), (3, 2999, 700, 16)])
+def test_sharded_tsr_svd_matches_oracle(env, world, m, n, ell):
+    """tsr_svd (sketch.hpp:139-149) over row blocks: each rank draws ITS rows of Psi2 = gaussian_matrix(m, ell,
+    seed ^ 1) (counter-based stream), Y2 and Q1^T Y1 are summed over ranks."""
+    P, torch = env
+    A = O.gen_lowrank_decay(m, n, 12, lambda j: 2.0 ** (-j), 1e-9, m + 5 * world)
+    ref = O.tsr_svd(A, ell, 23)
+    out = _sharded_call(P, torch, A, world, lambda blk, ctx, mg: P.tsr_svd(blk, ell, 23, ctx=ctx, m_global=mg))
+    s0 = out[0].sigma.cpu().numpy()
+    for o in out[1:]:
+        np.testing.assert_array_equal(o.sigma.cpu().numpy(), s0)
+    assert O.sigma_rel_err(s0[:8], ref.sigma[:8]).max() <= 1e-8
+    single = P.tsr_svd(torch.from_numpy(A).cuda(), ell, 23)
+    assert O.sigma_rel_err(s0[:8], single.sigma.cpu().numpy()[:8]).max() <= 1e-9
+
+
+@pytest.mark.parametrize("world,m,n,k,q,trials", [(2, 3000, 400, 12, 1, 3), (4, 4001, 300, 8, 0, 5)])
+def test_sharded_batched_trials_match_oracle(env, world, m, n, k, q, trials):
+    """The bound harness's trial loop (bounds.hpp:288) over row blocks: each trial equals the oracle's call."""
+    P, torch = env
+    A = O.gen_lowrank_decay(m, n, 30, lambda j: 2.0 ** (-j / 3), 1e-4, m + 7 * world)
+    cfg = P.SketchConfig(k, q, 300)
+    out = _sharded_call(P, torch, A, world,
+                        lambda blk, ctx, mg: P.sor_svd_power_batch(blk, k, cfg, trials, ctx=ctx, m_global=mg))
+    for t in range(trials):
+        ref = O.sor_svd_power(A, k, O.SketchConfig(k, q, 300 + t))
+        s0 = out[0][t].sigma.cpu().numpy()
+        for o in out[1:]:
+            np.testing.assert_array_equal(o[t].sigma.cpu().numpy(), s0)
+        u = np.vstack([o[t].u.cpu().numpy() for o in out])
+        assert O.sigma_rel_err(s0, ref.sigma).max() <= 1e-10
+        assert O.lowrank_rel_diff(u, s0, out[0][t].v.cpu().numpy(), ref.u, ref.sigma, ref.v) <= 1e-9
+
+
+@pytest.mark.parametrize("world,m,n,k,ell,q", [(2, 3000, 600, 12, 16, 1), (3, 2999, 500, 8, 12, 0)])
+def test_sharded_single_pass_matches_oracle(env, world, m, n, k, ell, q):
+    """single_pass (sketch.hpp:54-58) over row blocks: Q1^T T1 needs the sketch T1 after its sharded QR."""
+    P, torch = env
+    A = O.gen_lowrank_decay(m, n, 30, lambda j: 2.0 ** (-j / 3), 1e-4, m + 11 * world)
+    ref = O.sor_svd_power(A, k, O.SketchConfig(ell, q, 41, single_pass=True))
+    out = _sharded_call(P, torch, A, world, lambda blk, ctx, mg: P.sor_svd_power(
+        blk, k, P.SketchConfig(ell, q, 41, single_pass=True), ctx=ctx, m_global=mg))
+    s0 = out[0].sigma.cpu().numpy()
+    assert O.sigma_rel_err(s0, ref.sigma).max() <= 1e-9
+    assert out[0].passes == 2 * q + 2
