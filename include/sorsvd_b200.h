@@ -118,6 +118,9 @@ void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
  * these to cross-check kernel variants against each other). */
 #define SORSVD_OPT_JACOBI 1          /* value: sorsvd_jacobi_variant */
 #define SORSVD_OPT_SORD_CHUNK_MB 2   /* value: staging chunk of the SORD loader, MiB (default 64) */
+#define SORSVD_OPT_FUSED_PAIR 4      /* value: 1 (default) = narrow sketches over narrow matrices (ell <= 16, n <= 512, FP64)
+                                        run each power step T1 = A X, T2 = A^T T1 and the projection as ONE sweep over A
+                                        (skinny_pair_f64.cuh); 0 = separate NN / TN GEMM passes */
 #define SORSVD_OPT_OZAKI_PLANES 3    /* value: 1 (default) = the Ozaki engine cuts A into int8 digit planes once per
                                         call (7/8 of an FP64 A of extra HBM, taken when it fits) and its passes
                                         stream them; 0 = always convert A inside every pass */

@@ -45,6 +45,7 @@
 #include "ozaki_i8.cuh"
 #include "ozaki_planes_i8.cuh"
 #include "gen_f64.cuh"
+#include "skinny_pair_f64.cuh"
 #include "smallk_f64.cuh"
 #include <cfloat>
 
@@ -200,6 +201,7 @@ struct sorsvd_emu_group {
 
 struct sorsvd_ctx {
     int opt_jacobi = SORSVD_JACOBI_AUTO;  // sorsvd_ctx_set_option(SORSVD_OPT_JACOBI)
+    int opt_fused_pair = 1;               // sorsvd_ctx_set_option(SORSVD_OPT_FUSED_PAIR): 0 = separate NN / TN GEMM passes
     int opt_oz_planes = 1;                // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_PLANES): 0 = convert inside every pass
     int64_t opt_sord_chunk_mb = 64;       // sorsvd_ctx_set_option(SORSVD_OPT_SORD_CHUNK_MB)
     int device = 0;
@@ -2161,6 +2163,49 @@ void tn_pass_reduced(sorsvd_ctx* c, const SorProblem& P, const double* T1, doubl
     CK(cudaStreamWaitEvent(s, c->ev_comm, 0));
 }
 
+// ---------------------------------------------- fused NN + TN sweeps (narrow) --
+// One power step T1 = A X, T2 = A^T T1 (or the projection M = Q1^T (A Q2)) in one sweep over A for
+// narrow sketches over narrow matrices (skinny_pair_f64.cuh): FP64 A, ell <= 16, n <= 512.
+bool pair_ok(const sorsvd_ctx* c, const SorProblem& P) {
+    return c->opt_fused_pair && P.dtype == SORSVD_F64 && !P.tf32 && !P.ozaki && P.Np <= kPairNP && P.n <= 512 && P.n >= 2;
+}
+
+// T1 (m x Np) = A X; out2 = A^T T1 (n x Np, proj = false) or L^T T1 (Np x Np, proj = true: L = Q1).
+void run_pair(sorsvd_ctx* c, const SorProblem& P, const double* X, double* T1, double* out2, bool proj,
+              const double* L, cudaStream_t s) {
+    PairArgs a{};
+    a.A = P.A;
+    a.lda = P.lda;
+    a.m = P.m;
+    a.n = (int)P.n;
+    a.X = X;
+    a.ldx = P.Np;
+    a.np = P.Np;
+    a.T1 = T1;
+    a.ldt = P.Np;
+    a.L = L;
+    a.ldl = P.Np;
+    a.vec = ((uintptr_t)P.A % 16) == 0 && P.lda % 2 == 0;
+    a.pred = c->pred;
+    a.pred_skip = c->pred_skip;
+    a.rb = pair_smem_bytes(a.n, 32, proj) <= (size_t)227 * 1024 ? 32 : 16;
+    const size_t smem = pair_smem_bytes(a.n, a.rb, proj);
+    const int rows2 = proj ? kPairNP : a.n;
+    const int grid = (int)std::min<int64_t>(c->num_sms, cdiv(P.m, a.rb));
+    a.part = dbuf(c, proj ? "pair_part_p" : "pair_part", (size_t)grid * rows2 * kPairNP);
+    if (proj) {
+        allow_smem(skinny_pair_kernel<true>);
+        skinny_pair_kernel<true><<<grid, kPairThreads, smem, s>>>(a);
+    } else {
+        allow_smem(skinny_pair_kernel<false>);
+        skinny_pair_kernel<false><<<grid, kPairThreads, smem, s>>>(a);
+    }
+    check_launch(c);
+    pair_reduce_kernel<<<(unsigned)cdiv((int64_t)rows2 * kPairNP, 32), 256, 0, s>>>(
+        a.part, grid, rows2, proj ? P.Np : rows2, P.Np, out2, P.Np, c->pred, c->pred_skip);
+    check_launch(c);
+}
+
 // Enqueue one sor_svd_power on c->stream (T2 must already hold Omega, padded).
 void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan* p1, QrPlan* p2, QrPlan* pg,
                  bool timing) {
@@ -2185,6 +2230,11 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         if (P.ozaki) {  // FP64 passes as int8 slice products (ozaki_i8.cuh)
             run_ozaki(c, P, false, oz, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
             tn_pass_reduced(c, P, b.T1, b.T2, s, &oz);  // T2 = A^T T1 (sketch.hpp:96), summed over ranks
+            continue;
+        }
+        if (pair_ok(c, P)) {  // T1 = A T2 and T2 = A^T T1 in one sweep over A (skinny_pair_f64.cuh)
+            run_pair(c, P, b.T2, b.T1, b.T2, false, nullptr, s);
+            allreduce_sum(c, b.T2, (size_t)P.n * Np, s);
             continue;
         }
         GemmCall g1;  // T1 = A * T2     (sketch.hpp:95); FP32 A widened to FP64 in the kernel
@@ -2241,6 +2291,10 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         g.ldc = Np;
         g.Af = P.Af;
         g.sk_bias = Np <= 128 ? 1.0 : 0.95;
+        if (pair_ok(c, P)) {  // Y = A Q2 and M = Q1^T Y in one sweep over A (skinny_pair_f64.cuh)
+            CK(cudaMemsetAsync(b.Mk, 0, (size_t)Np * Np * 8, s));
+            run_pair(c, P, b.Q2, b.Y, b.Mk, true, b.Q1, s);
+        } else {
         if (P.ozaki) run_ozaki(c, P, false, oz, b.Q2, b.Y, s);
         else if (!P.tf32) run_gemm(c, g, s);
         GemmCall h;
@@ -2255,6 +2309,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         h.C = b.Mk;
         h.ldc = Np;
         run_gemm(c, h, s);
+        }
         allreduce_sum(c, b.Mk, (size_t)ell * Np, s);
     }
     }
@@ -3656,6 +3711,10 @@ int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
                     throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown Jacobi variant"};
                 c->opt_jacobi = (int)value;
                 invalidate_graphs(c);  // captured calls baked the previous variant in
+                break;
+            case SORSVD_OPT_FUSED_PAIR:
+                c->opt_fused_pair = value != 0;
+                invalidate_graphs(c);
                 break;
             case SORSVD_OPT_OZAKI_PLANES:
                 c->opt_oz_planes = value != 0;

@@ -143,7 +143,10 @@ def test_approx_error_frobenius_vs_reference(P, golden):
     f = P.sor_svd_power(A, 20, P.SketchConfig(24, 1, 2))
     ref = O.approx_error(A.astype(np.float64), O.LowRankApprox(f.u, f.sigma, f.v, 0, 0, 20, 0, 0))
     assert abs(P.approx_error(A, f) - ref) <= 1e-10 * ref
-    with pytest.raises(P.UnsupportedError):
-        P.approx_error(A, f, "spectral")
+    # the spectral norm of the difference (device Gram / Rayleigh-Ritz estimate) vs dgesdd
+    ref2 = np.linalg.norm(A.astype(np.float64) - (f.u * f.sigma) @ f.v.T, 2)
+    assert abs(P.approx_error(A, f, "spectral") - ref2) <= 1e-9 * ref2
+    with pytest.raises(P.ParameterError):
+        P.approx_error(A, f, "nuclear")
     with pytest.raises(P.ShapeError):
         P.approx_error(A[:100], f)
