@@ -118,6 +118,9 @@ void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
  * these to cross-check kernel variants against each other). */
 #define SORSVD_OPT_JACOBI 1          /* value: sorsvd_jacobi_variant */
 #define SORSVD_OPT_SORD_CHUNK_MB 2   /* value: staging chunk of the SORD loader, MiB (default 64) */
+#define SORSVD_OPT_UPLOAD_CHUNK_MB 5 /* value: MiB per row chunk of A in host-buffer calls of the Ozaki planes engine (default
+                                        1536): A uploads in chunks on a copy stream and each chunk is converted and swept
+                                        by the first pass T1 = A Omega while the next one crosses PCIe */
 #define SORSVD_OPT_FUSED_PAIR 4      /* value: 1 (default) = narrow sketches over narrow matrices (ell <= 16, n <= 512, FP64)
                                         run each power step T1 = A X, T2 = A^T T1 and the projection as ONE sweep over A
                                         (skinny_pair_f64.cuh); 0 = separate NN / TN GEMM passes */

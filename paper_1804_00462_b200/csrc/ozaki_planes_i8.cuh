@@ -43,7 +43,8 @@ constexpr size_t kOzpSmem = 1024 + (size_t)kOzpStages * kOzStage + 256;
 struct OzpArgs {
     int64_t M;             // left rows of this launch: m (NN) or the column block's width (TN)
     int64_t K;             // n (NN) or m (TN)
-    int mn0;               // TN: first column of the block inside the planes (tensor-map coordinate)
+    int mn0;               // first left row of this launch inside the planes (tensor-map coordinate): TN the
+                           // column block's first column, NN the row block's first row
     const int* lexp;       // NN: exponent bounds of the left rows; TN: null (the row scales ride on X)
     const int8_t* Xd;      // digit planes of the right operand [K step][column chunk][slice][64 x 32 B]
     const int* xexp;       // per right column
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kOzpThreads, 1)
                 mbar_expect_tx(full(s), (uint32_t)kOzStage);
                 const uint32_t dst = base + s * kOzStage;
                 const int kt = kt_b + i;
-                if (!TA) tma_load_3d(dst, &tmA, full(s), kt * kOzBK, (int)m0, 0);
+                if (!TA) tma_load_3d(dst, &tmA, full(s), kt * kOzBK, p.mn0 + (int)m0, 0);
                 else tma_load_3d(dst, &tmA, full(s), p.mn0 + (int)m0, kt * kOzBK, 0);
                 oz_bulk_g2s(dst + kOzSlices * kOzAPlane, xsrc + (size_t)kt * p.NC * kOzXStep, (uint32_t)kOzXStep, full(s));
             }

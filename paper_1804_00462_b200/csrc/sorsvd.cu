@@ -201,6 +201,7 @@ struct sorsvd_emu_group {
 
 struct sorsvd_ctx {
     int opt_jacobi = SORSVD_JACOBI_AUTO;  // sorsvd_ctx_set_option(SORSVD_OPT_JACOBI)
+    int64_t opt_upload_chunk_mb = 1536;   // sorsvd_ctx_set_option(SORSVD_OPT_UPLOAD_CHUNK_MB): host-buffer calls of the planes engine
     int opt_fused_pair = 1;               // sorsvd_ctx_set_option(SORSVD_OPT_FUSED_PAIR): 0 = separate NN / TN GEMM passes
     int opt_oz_planes = 1;                // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_PLANES): 0 = convert inside every pass
     int64_t opt_sord_chunk_mb = 64;       // sorsvd_ctx_set_option(SORSVD_OPT_SORD_CHUNK_MB)
@@ -236,6 +237,7 @@ struct sorsvd_ctx {
     int launches = 0;
     bool capturing = false;
     std::vector<double> host_omega;
+    std::vector<cudaEvent_t> up_ev;  // pipelined host upload: one event per row chunk of A
     std::vector<double> rpca_tele;  // last rpca_alm: iterations x {mu, rel_error, rank_l, nnz_s}
     std::vector<double> host_psi2;  // tsr_svd's second test matrix (host draw)
     double* om_pin = nullptr;       // host-buffer calls: page-locked Omega draw
@@ -1703,6 +1705,8 @@ struct SorProblem {
     bool tf32;         // dtype F32 with SORSVD_FLAG_TF32: passes on the tcgen05 tensor cores
     bool ozaki;        // SORSVD_FLAG_OZAKI: FP64 passes as int8 slice products on the tcgen05 tensor cores
     bool oz_planes = false;  // ... from digit planes of A cut once per call (ozaki_planes_i8.cuh), memory permitting
+    bool pre_first = false;  // host-buffer call: planes and the first T1 = A Omega were produced chunk by chunk
+                             // while A was uploading (sor_device's pipelined upload)
     int method = SORSVD_SOR_POWER;  // SORSVD_RSVD / SORSVD_TSR: the baselines of sketch.hpp:124-149
 };
 
@@ -1897,20 +1901,36 @@ void launch_rowplanes(sorsvd_ctx* c, const AT* A, const SorProblem& P, int* re, 
     }
 }
 
+// The call's planes workspace (no kernels): exponents and the 7 digit planes of an m x n A.
+OzScales oz_planes_of(sorsvd_ctx* c, const SorProblem& P) {
+    OzScales oz{reinterpret_cast<int*>(dbuf(c, "oz_rowe", (size_t)(P.m + 1) / 2)), nullptr};
+    oz.pitch = oz_planes_pitch(P.n);
+    oz.plane_stride = oz.pitch * P.m;
+    oz.pm = P.m;
+    oz.pn = P.n;
+    oz.planes = reinterpret_cast<int8_t*>(dbuf(c, "oz_planes", (size_t)(kOzSlices * oz.plane_stride + 7) / 8));
+    return oz;
+}
+
+// Rows [r0, r0 + rows) of A -> their exponents and digit planes (a row chunk of the call's planes).
+void oz_convert_rows(sorsvd_ctx* c, const SorProblem& P, const OzScales& oz, int64_t r0, int64_t rows, cudaStream_t s) {
+    SorProblem Q = P;
+    Q.m = rows;
+    OzScales o = oz;
+    o.planes = oz.planes + r0 * oz.pitch;
+    int* re = const_cast<int*>(oz.row_e) + r0;
+    if (P.dtype == SORSVD_F32) launch_rowplanes<float>(c, P.Af + r0 * P.lda, Q, re, o, s);
+    else launch_rowplanes<double>(c, P.A + r0 * P.lda, Q, re, o, s);
+    check_launch(c);
+}
+
 OzScales oz_prepare_a(sorsvd_ctx* c, const SorProblem& P, cudaStream_t s) {
     int* re = reinterpret_cast<int*>(dbuf(c, "oz_rowe", (size_t)(P.m + 1) / 2));
     if (P.oz_planes) {
         // cut A into its row-scaled digit planes once (row maxima and digits in one read of A);
         // every pass of the call streams the planes, TN passes fold the row scales into T1
-        OzScales oz{re, nullptr};
-        oz.pitch = oz_planes_pitch(P.n);
-        oz.plane_stride = oz.pitch * P.m;
-        oz.pm = P.m;
-        oz.pn = P.n;
-        oz.planes = reinterpret_cast<int8_t*>(dbuf(c, "oz_planes", (size_t)(kOzSlices * oz.plane_stride + 7) / 8));
-        if (P.dtype == SORSVD_F32) launch_rowplanes<float>(c, P.Af, P, re, oz, s);
-        else launch_rowplanes<double>(c, P.A, P, re, oz, s);
-        check_launch(c);
+        OzScales oz = oz_planes_of(c, P);
+        oz_convert_rows(c, P, oz, 0, P.m, s);
         return oz;
     }
     auto* rmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_rowmax", (size_t)P.m));
@@ -1984,16 +2004,23 @@ int oz_pick_splits(int64_t tiles, int KT, int64_t out_bytes, int sms) {
 // describes that column block). X is cut into digit planes first. With the call's
 // digit planes of A (oz.planes) the pass streams them (ozaki_planes_i8.cuh), else A
 // is converted inside the pass kernel (ozaki_i8.cuh).
-void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const double* X, double* C,
-               cudaStream_t s, int dbg = 0, int64_t n0 = 0) {
+// The right operand X (K x Np) cut into its digit planes (per-column exponents): shared by every
+// launch over the same X.
+struct OzX {
+    int8_t* Xd = nullptr;
+    int* xexp = nullptr;
+};
+
+OzX oz_cut_x(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const double* X, cudaStream_t s) {
     const int Np = P.Np;
     const int NC = (int)cdiv(Np, kOzBN);
-    const int64_t M = ta ? P.n : P.m, K = ta ? P.m : P.n;
+    const int64_t K = ta ? P.m : P.n;
     const int64_t KT = cdiv(K, kOzBK);
     const bool planes = oz.planes != nullptr;
     auto* xmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_xmax", (size_t)Np));
-    int* xexp = reinterpret_cast<int*>(dbuf(c, "oz_xexp", (size_t)(Np + 1) / 2));
-    int8_t* Xd = reinterpret_cast<int8_t*>(dbuf(c, ta ? "oz_xd_tn" : "oz_xd_nn", (size_t)(KT * NC * kOzXStep + 7) / 8));
+    OzX x;
+    x.xexp = reinterpret_cast<int*>(dbuf(c, "oz_xexp", (size_t)(Np + 1) / 2));
+    x.Xd = reinterpret_cast<int8_t*>(dbuf(c, ta ? "oz_xd_tn" : "oz_xd_nn", (size_t)(KT * NC * kOzXStep + 7) / 8));
     CK(cudaMemsetAsync(xmax, 0, (size_t)Np * 8, s));
     const dim3 cgrid((unsigned)cdiv(Np, 256), (unsigned)cdiv(K, 256));
     const int64_t items = KT * 2 * (int64_t)NC * kOzBN;
@@ -2001,65 +2028,87 @@ void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, 
     if (planes && ta) {  // the planes are row-scaled: A's row scales ride on the right operand
         ozaki_colmax_scaled_kernel<<<cgrid, 256, 0, s>>>(X, Np, K, Np, oz.row_e, xmax);
         check_launch(c);
-        ozaki_exp_kernel<<<1, 256, 0, s>>>(xmax, Np, xexp);
+        ozaki_exp_kernel<<<1, 256, 0, s>>>(xmax, Np, x.xexp);
         check_launch(c);
-        ozaki_xdigits_scaled_kernel<<<xblocks, 256, 0, s>>>(X, Np, K, Np, NC, oz.row_e, xexp, Xd);
+        ozaki_xdigits_scaled_kernel<<<xblocks, 256, 0, s>>>(X, Np, K, Np, NC, oz.row_e, x.xexp, x.Xd);
         check_launch(c);
     } else {
         ozaki_colmax_kernel<<<cgrid, 256, 0, s>>>(X, Np, K, Np, xmax);
         check_launch(c);
-        ozaki_exp_kernel<<<1, 256, 0, s>>>(xmax, Np, xexp);
+        ozaki_exp_kernel<<<1, 256, 0, s>>>(xmax, Np, x.xexp);
         check_launch(c);
-        ozaki_xdigits_kernel<<<xblocks, 256, 0, s>>>(X, Np, K, Np, NC, xexp, Xd);
+        ozaki_xdigits_kernel<<<xblocks, 256, 0, s>>>(X, Np, K, Np, NC, x.xexp, x.Xd);
         check_launch(c);
     }
-    if (planes) {
-        OzpArgs a{};
-        a.M = M;
-        a.K = K;
-        a.mn0 = (int)n0;
-        a.lexp = ta ? nullptr : oz.row_e;
-        a.Xd = Xd;
-        a.xexp = xexp;
-        a.NC = NC;
-        a.N = Np;
-        a.ldc = Np;
-        a.dbg = dbg;
-        a.pred = c->pred;
-        a.pred_skip = c->pred_skip;
-        const int64_t tiles = cdiv(M, kOzBM) * NC;
-        const int S = oz_pick_splits(tiles, (int)KT, M * Np * 8, c->num_sms);
-        a.kt_split = (int)cdiv(KT, S);
-        a.c_split_stride = M * Np;
-        double* ws = S > 1 ? dbuf(c, "oz_split", (size_t)S * M * Np) : nullptr;
-        a.C = S > 1 ? ws : C;
-        CUtensorMap map{};
-        cuuint64_t dims[3] = {(cuuint64_t)oz.pn, (cuuint64_t)oz.pm, (cuuint64_t)kOzSlices};
-        cuuint64_t strides[2] = {(cuuint64_t)oz.pitch, (cuuint64_t)oz.plane_stride};
-        cuuint32_t box[3] = {(cuuint32_t)(ta ? kOzBM : kOzBK), (cuuint32_t)(ta ? kOzBK : kOzBM), (cuuint32_t)kOzSlices};
-        cuuint32_t es[3] = {1, 1, 1};
-        CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, oz.planes, dims, strides, box, es,
-                                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                    ta ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) throw Error{SORSVD_ERR_CUDA, "cuda: cuTensorMapEncodeTiled (planes) failed " + std::to_string((int)r)};
-        const dim3 grid((unsigned)tiles, (unsigned)S);
-        if (ta) {
-            allow_smem(ozaki_planes_gemm_kernel<true>);
-            ozaki_planes_gemm_kernel<true><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
-        } else {
-            allow_smem(ozaki_planes_gemm_kernel<false>);
-            ozaki_planes_gemm_kernel<false><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
-        }
+    return x;
+}
+
+// One launch of the planes engine over left rows [l0, l0 + M) of the planes (NN: rows of A; TN:
+// columns of A): C (M x Np, the caller's pointer to the block's first row) = op(A)[l0 ..] X.
+void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const OzX& x, double* C,
+                      int64_t l0, int64_t M, cudaStream_t s, int dbg = 0) {
+    const int Np = P.Np;
+    const int NC = (int)cdiv(Np, kOzBN);
+    const int64_t K = ta ? P.m : P.n;
+    const int64_t KT = cdiv(K, kOzBK);
+    OzpArgs a{};
+    a.M = M;
+    a.K = K;
+    a.mn0 = (int)l0;
+    a.lexp = ta ? nullptr : oz.row_e + l0;
+    a.Xd = x.Xd;
+    a.xexp = x.xexp;
+    a.NC = NC;
+    a.N = Np;
+    a.ldc = Np;
+    a.dbg = dbg;
+    a.pred = c->pred;
+    a.pred_skip = c->pred_skip;
+    const int64_t tiles = cdiv(M, kOzBM) * NC;
+    const int S = oz_pick_splits(tiles, (int)KT, M * Np * 8, c->num_sms);
+    a.kt_split = (int)cdiv(KT, S);
+    a.c_split_stride = M * Np;
+    double* ws = S > 1 ? dbuf(c, "oz_split", (size_t)S * M * Np) : nullptr;
+    a.C = S > 1 ? ws : C;
+    CUtensorMap map{};
+    cuuint64_t dims[3] = {(cuuint64_t)oz.pn, (cuuint64_t)oz.pm, (cuuint64_t)kOzSlices};
+    cuuint64_t strides[2] = {(cuuint64_t)oz.pitch, (cuuint64_t)oz.plane_stride};
+    cuuint32_t box[3] = {(cuuint32_t)(ta ? kOzBM : kOzBK), (cuuint32_t)(ta ? kOzBK : kOzBM), (cuuint32_t)kOzSlices};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, oz.planes, dims, strides, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, ta ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw Error{SORSVD_ERR_CUDA, "cuda: cuTensorMapEncodeTiled (planes) failed " + std::to_string((int)r)};
+    const dim3 grid((unsigned)tiles, (unsigned)S);
+    if (ta) {
+        allow_smem(ozaki_planes_gemm_kernel<true>);
+        ozaki_planes_gemm_kernel<true><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
+    } else {
+        allow_smem(ozaki_planes_gemm_kernel<false>);
+        ozaki_planes_gemm_kernel<false><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
+    }
+    check_launch(c);
+    if (S > 1) {
+        const int64_t count2 = M * Np / 2;
+        const int blocks = (int)std::min<int64_t>(cdiv(count2, 256), (int64_t)c->num_sms * 8);
+        reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, M * Np, C, c->pred, c->pred_skip);
         check_launch(c);
-        if (S > 1) {
-            const int64_t count2 = M * Np / 2;
-            const int blocks = (int)std::min<int64_t>(cdiv(count2, 256), (int64_t)c->num_sms * 8);
-            reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, M * Np, C, c->pred, c->pred_skip);
-            check_launch(c);
-        }
+    }
+}
+
+void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const double* X, double* C,
+               cudaStream_t s, int dbg = 0, int64_t n0 = 0) {
+    const int Np = P.Np;
+    const int NC = (int)cdiv(Np, kOzBN);
+    const int64_t M = ta ? P.n : P.m, K = ta ? P.m : P.n;
+    const OzX ox = oz_cut_x(c, P, ta, oz, X, s);
+    if (oz.planes) {
+        oz_launch_planes(c, P, ta, oz, ox, C, ta ? n0 : 0, M, s, dbg);
         return;
     }
+    int8_t* Xd = ox.Xd;
+    int* xexp = ox.xexp;
     OzArgs a{};
     a.A = P.dtype == SORSVD_F32 ? static_cast<const void*>(P.Af) : static_cast<const void*>(P.A);
     a.lda = P.lda;
@@ -2213,7 +2262,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     const int Np = P.Np, ell = P.ell;
     record_stage(c, timing, 0);
     OzScales oz;
-    if (P.ozaki) oz = oz_prepare_a(c, P, s);
+    if (P.ozaki) oz = P.pre_first ? oz_planes_of(c, P) : oz_prepare_a(c, P, s);
     for (int i = 0; i <= P.q; ++i) {
         if (P.single_pass && i == P.q) {  // t2_pre: the row sketch entering the last iteration (sketch.hpp:94)
             if (P.tf32)
@@ -2228,7 +2277,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
             continue;
         }
         if (P.ozaki) {  // FP64 passes as int8 slice products (ozaki_i8.cuh)
-            run_ozaki(c, P, false, oz, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
+            if (!(P.pre_first && i == 0)) run_ozaki(c, P, false, oz, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
             tn_pass_reduced(c, P, b.T1, b.T2, s, &oz);  // T2 = A^T T1 (sketch.hpp:96), summed over ranks
             continue;
         }
@@ -2582,6 +2631,59 @@ bool ozaki_wanted(uint32_t flags, int64_t m, int64_t n, int ell) {
     return (double)m * (double)n * (double)ell >= 68719476736.0 /* 2^36 */ && ell >= 32;
 }
 
+// Host-buffer calls: A's upload as row chunks on the copy stream (one event per chunk), so that the
+// Ozaki planes engine can convert chunk i and run the first pass T1 = A Omega over it while chunk
+// i + 1 is still crossing PCIe (sor_device). rows_per_chunk is a whole number of 128-row tiles
+// whose CTAs fill whole waves of the device.
+struct HostUpload {
+    bool chunked = false;
+    int64_t rows_per_chunk = 0;
+    int nchunks = 0;
+    int issued = 0;  // chunks whose copies are enqueued so far
+};
+
+// Enqueue the copies of chunks [up.issued, upto) on the copy stream. Chunk 0 goes first; the host
+// draws Omega while it crosses and enqueues Omega's (small) upload on the same stream before the
+// remaining chunks, so the compute stream has Omega when chunk 0 lands.
+void upload_issue(sorsvd_ctx* c, HostUpload& up, const void* A, void* dA, int64_t m, int64_t lda, size_t esz, int upto) {
+    const size_t row_bytes = (size_t)lda * esz;
+    for (int i = up.issued; i < upto && i < up.nchunks; ++i) {
+        const int64_t r0 = (int64_t)i * up.rows_per_chunk, rows = std::min(up.rows_per_chunk, m - r0);
+        CK(cudaMemcpyAsync(static_cast<char*>(dA) + (size_t)r0 * row_bytes, static_cast<const char*>(A) + (size_t)r0 * row_bytes,
+                           (size_t)rows * row_bytes, cudaMemcpyHostToDevice, c->comm_stream));
+        CK(cudaEventRecord(c->up_ev[(size_t)i], c->comm_stream));
+        up.issued = i + 1;
+    }
+}
+
+HostUpload upload_chunked(sorsvd_ctx* c, const void* A, void* dA, int64_t m, int64_t lda, size_t esz, int Np) {
+    HostUpload up;
+    const int NC = (int)cdiv(Np, kOzBN);
+    int g = c->num_sms, h = NC;  // gcd(num_sms, NC)
+    while (h) {
+        const int t = g % h;
+        g = h;
+        h = t;
+    }
+    const int64_t unit_rows = (int64_t)(c->num_sms / g) * kOzBM;  // tiles x NC CTAs = whole waves
+    const size_t row_bytes = (size_t)lda * esz;
+    int64_t units = std::max<int64_t>(
+        1, (int64_t)(((size_t)std::max<int64_t>(1, c->opt_upload_chunk_mb) << 20) / std::max<size_t>(1, unit_rows * row_bytes)));
+    up.rows_per_chunk = units * unit_rows;
+    up.nchunks = (int)cdiv(m, up.rows_per_chunk);
+    while ((int)c->up_ev.size() < up.nchunks) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->up_ev.push_back(e);
+    }
+    // the copy stream starts after whatever the compute stream has queued (the previous call's reads of dA)
+    CK(cudaEventRecord(c->ev_comm, c->stream));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_comm, 0));
+    up.chunked = true;
+    upload_issue(c, up, A, dA, m, lda, esz, 1);  // chunk 0 now; the rest after Omega's upload is enqueued
+    return up;
+}
+
 // First global row of this rank's block: the exclusive prefix sum of the ranks' row counts
 // (one small all-reduce of a world-long vector; 0 on a single rank).
 int64_t rank_row0(sorsvd_ctx* c, int64_t m) {
@@ -2601,7 +2703,7 @@ int64_t rank_row0(sorsvd_ctx* c, int64_t m) {
 // Core device-side call. dOmega: n x ell dense (or null: drawn on the host).
 void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const double* dOmega, double* dU,
                 double* dS, double* dV, sorsvd_stats* st, int method = SORSVD_SOR_POWER,
-                const double* dPsi2 = nullptr) {
+                const double* dPsi2 = nullptr, const HostUpload* up = nullptr) {
     validate(d);
     const bool baseline = method == SORSVD_RSVD || method == SORSVD_TSR;
     if (baseline) {
@@ -2655,11 +2757,16 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     }
     const double* om = om_in;
     const bool timing = (d->flags & SORSVD_FLAG_STAGE_TIMES) != 0;
-    const bool use_graph = !timing && !c->emu && !(d->flags & SORSVD_FLAG_NO_GRAPH);
+    // host-buffer call with A arriving in row chunks: the planes engine converts and sweeps chunk i
+    // (first pass T1 = A Omega, rows independent) while chunk i + 1 uploads
+    const bool pipe = up && up->chunked && P.ozaki && P.oz_planes && c->world == 1 && !baseline;
+    if (up && up->chunked && !pipe)  // not eligible after all: wait for the whole upload
+        CK(cudaStreamWaitEvent(c->stream, c->up_ev[(size_t)up->nchunks - 1], 0));
+    const bool use_graph = !timing && !c->emu && !(d->flags & SORSVD_FLAG_NO_GRAPH) && !pipe;
     CK(cudaEventRecord(c->ev_a, c->stream));
     const int launches0 = c->launches;
     int launches = 0;
-    auto enqueue_all = [&]() {
+    auto stage_omega = [&]() {
         // T2 <- Omega (padded; rounded to fp32 for the TF32 passes)
         if (P.tf32) {
             cast_to_f32(c, om, P.ell, b.T2f, P.Np32, P.n, P.ell, c->stream);
@@ -2667,6 +2774,23 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
             CK(cudaMemsetAsync(b.T2, 0, (size_t)P.n * P.Np * 8, c->stream));
             CK(cudaMemcpy2DAsync(b.T2, (size_t)P.Np * 8, om, (size_t)P.ell * 8, (size_t)P.ell * 8, (size_t)P.n,
                                  cudaMemcpyDeviceToDevice, c->stream));
+        }
+    };
+    auto enqueue_all = [&]() {
+        stage_omega();
+        if (pipe) {
+            const OzScales oz = oz_planes_of(c, P);
+            const OzX ox = oz_cut_x(c, P, false, oz, b.T2, c->stream);  // Omega's digit planes: once for all chunks
+            for (int i = 0; i < up->nchunks; ++i) {
+                const int64_t r0 = (int64_t)i * up->rows_per_chunk, rows = std::min(up->rows_per_chunk, P.m - r0);
+                CK(cudaStreamWaitEvent(c->stream, c->up_ev[(size_t)i], 0));
+                oz_convert_rows(c, P, oz, r0, rows, c->stream);
+                oz_launch_planes(c, P, false, oz, ox, b.T1 + r0 * P.Np, r0, rows, c->stream);
+            }
+            SorProblem Q = P;
+            Q.pre_first = true;
+            enqueue_sor(c, Q, b, p1, p2, pg, timing);
+            return;
         }
         if (method == SORSVD_TSR) {
             CK(cudaMemsetAsync(b.Psi2, 0, (size_t)P.m * P.Np * 8, c->stream));
@@ -3712,6 +3836,10 @@ int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
                 c->opt_jacobi = (int)value;
                 invalidate_graphs(c);  // captured calls baked the previous variant in
                 break;
+            case SORSVD_OPT_UPLOAD_CHUNK_MB:
+                if (value < 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: upload chunk must be >= 1 MiB"};
+                c->opt_upload_chunk_mb = value;
+                break;
             case SORSVD_OPT_FUSED_PAIR:
                 c->opt_fused_pair = value != 0;
                 invalidate_graphs(c);
@@ -3756,12 +3884,28 @@ static void host_call(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const 
     cudaEvent_t e0 = c->ev_h[0], e1 = c->ev_h[1], e2 = c->ev_h[2], e3 = c->ev_h[3];
     CK(cudaEventRecord(e0, c->stream));
     double* dA = dbuf(c, "hostA", (abytes + 7) / 8);
-    CK(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, c->stream));
+    HostUpload up;
+    {
+        // Ozaki planes engine on one rank: upload A in row chunks on the copy stream and let the
+        // device convert / sweep each chunk as it lands (sor_device); else one copy on the stream
+        SorProblem P{};
+        P.m = d->m;
+        P.n = d->n;
+        P.Np = npad(d->ell);
+        const bool planes = method == SORSVD_SOR_POWER && c->world == 1 &&
+                            !(d->dtype == SORSVD_F32 && (d->flags & SORSVD_FLAG_TF32)) &&
+                            ozaki_wanted(d->flags, d->m, d->n, d->ell) && oz_planes_fit(c, P);
+        if (planes) up = upload_chunked(c, A, dA, d->m, d->lda, esz, P.Np);
+        else CK(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, c->stream));
+    }
+    // A copy engine drains one stream's queued copies before it turns to another stream's, so with a
+    // chunked upload Omega's (small) copy rides the copy stream itself, between chunk 0 and the rest
+    cudaStream_t om_stream = up.chunked ? c->comm_stream : c->stream;
     const double* dOm = nullptr;
     sorsvd_desc dd = *d;
     if (omega && (d->flags & SORSVD_FLAG_OMEGA_GIVEN)) {
         double* p = dbuf(c, "hostOm", (size_t)d->n * d->ell);
-        CK(cudaMemcpyAsync(p, omega, (size_t)d->n * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(p, omega, (size_t)d->n * d->ell * 8, cudaMemcpyHostToDevice, om_stream));
         dOm = p;
     } else if (method != SORSVD_TSR) {
         // draw Omega = gaussian_matrix(n, ell, seed) (sketch.hpp:90) into a page-locked
@@ -3779,9 +3923,13 @@ static void host_call(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const 
         sorsvd_host::gaussian_fill(c->host_omega.data(), (uint64_t)cnt, d->seed, 0);
         memcpy(c->om_pin, c->host_omega.data(), cnt * sizeof(double));
         double* p = dbuf(c, "hostOm", cnt);
-        CK(cudaMemcpyAsync(p, c->om_pin, cnt * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(p, c->om_pin, cnt * 8, cudaMemcpyHostToDevice, om_stream));
         dOm = p;
         dd.flags |= SORSVD_FLAG_OMEGA_GIVEN;
+    }
+    if (up.chunked) {  // Omega rode the copy stream (behind chunk 0): the compute stream waits for it
+        CK(cudaEventRecord(c->ev_comm, c->comm_stream));
+        CK(cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
     }
     d = &dd;
     const double* dPsi2 = nullptr;
@@ -3790,12 +3938,13 @@ static void host_call(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const 
         CK(cudaMemcpyAsync(p, psi2, (size_t)d->m * d->ell * 8, cudaMemcpyHostToDevice, c->stream));
         dPsi2 = p;
     }
+    if (up.chunked) upload_issue(c, up, A, dA, d->m, d->lda, esz, up.nchunks);
     CK(cudaEventRecord(e1, c->stream));
     double* dU = dbuf(c, "hostU", (size_t)d->m * d->k);
     double* dS = dbuf(c, "hostS", (size_t)d->k);
     double* dV = dbuf(c, "hostV", (size_t)d->n * d->k);
     sorsvd_stats local{};
-    sor_device(c, d, dA, dOm, dU, dS, dV, &local, method, dPsi2);
+    sor_device(c, d, dA, dOm, dU, dS, dV, &local, method, dPsi2, up.chunked ? &up : nullptr);
     CK(cudaEventRecord(e2, c->stream));
     CK(cudaMemcpyAsync(U, dU, (size_t)d->m * d->k * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(V, dV, (size_t)d->n * d->k * 8, cudaMemcpyDeviceToHost, c->stream));

@@ -206,3 +206,27 @@ def test_auto_mode_selection(P):
     assert P.sor_svd_power(big, 200, P.SketchConfig(200, 0, 1), fp64_mode="dmma").stats["pass_kind"] == 0
     g = P.sor_svd_power(big, 200, P.SketchConfig(200, 0, 1), fp64_mode="dmma")
     np.testing.assert_allclose(f.sigma.cpu().numpy(), g.sigma.cpu().numpy(), rtol=1e-12)
+
+
+@pytest.mark.parametrize("f32", [False, True])
+def test_host_call_pipelined_upload_same_bits(P, f32):
+    """Host-buffer calls of the planes engine upload A in row chunks and convert / sweep each chunk as it lands
+    (first pass T1 = A Omega by row blocks): the result equals the device-resident call bit for bit, for several
+    chunk sizes (one chunk, ragged last chunk, many chunks)."""
+    import torch
+    A = O.gen_lowrank_decay(30000, 600, 40, lambda j: 2.0 ** (-j / 5), 1e-3, 17)
+    if f32:
+        A = A.astype(np.float32)
+    cfg = P.SketchConfig(40, 1, 5)
+    dev = P.sor_svd_power(torch.from_numpy(A).cuda(), 32, cfg, fp64_mode="ozaki")
+    assert dev.stats["oz_planes"] == 1
+    for mb in (1536, 24, 2):
+        ctx = P.Context(0)
+        ctx.set_option(P.Context.OPT_UPLOAD_CHUNK_MB, mb)
+        host = P.sor_svd_power(A, 32, cfg, fp64_mode="ozaki", ctx=ctx)
+        assert host.stats["oz_planes"] == 1
+        assert np.array_equal(np.asarray(host.sigma), dev.sigma.cpu().numpy())
+        assert np.array_equal(np.asarray(host.u), dev.u.cpu().numpy())
+        assert np.array_equal(np.asarray(host.v), dev.v.cpu().numpy())
+        host2 = P.sor_svd_power(A, 32, cfg, fp64_mode="ozaki", ctx=ctx)   # a second call on the same context
+        assert np.array_equal(np.asarray(host2.u), np.asarray(host.u))
