@@ -118,6 +118,10 @@ void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
  * these to cross-check kernel variants against each other). */
 #define SORSVD_OPT_JACOBI 1          /* value: sorsvd_jacobi_variant */
 #define SORSVD_OPT_SORD_CHUNK_MB 2   /* value: staging chunk of the SORD loader, MiB (default 64) */
+#define SORSVD_OPT_OZAKI_MULTICAST 6 /* value: 1 = the planes passes run the column-chunk CTAs of a row tile as one thread-block
+                                        cluster and load each A plane once per cluster (TMA multicast, multicast commits);
+                                        0 (default) = every CTA loads all 7 planes itself. Same results; measured no
+                                        faster on B200 (the pass is bound by shared-memory bandwidth, not by L2 -> SM) */
 #define SORSVD_OPT_UPLOAD_CHUNK_MB 5 /* value: MiB per row chunk of A in host-buffer calls of the Ozaki planes engine (default
                                         1536): A uploads in chunks on a copy stream and each chunk is converted and swept
                                         by the first pass T1 = A Omega while the next one crosses PCIe */

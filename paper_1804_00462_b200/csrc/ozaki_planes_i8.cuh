@@ -57,6 +57,25 @@ struct OzpArgs {
     int pred_skip;
 };
 
+// The same box delivered to the same shared-memory offset of every CTA in `mask` (cluster ranks),
+// each destination's mbarrier (same offset) credited with the bytes.
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z,
+                                               uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%4, "
+        "%5, %6}], [%2], %3;\n" ::"r"(dst),
+        "l"(map), "r"(bar), "h"(mask), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
@@ -212,7 +231,17 @@ __global__ void ozaki_xdigits_scaled_kernel(const double* __restrict__ X, int64_
     }
 }
 
-template <bool TA>
+// MC = true: the NC column-chunk CTAs of a row tile form a thread-block cluster (cluster = NC <= 8
+// CTAs along x). They need the SAME 7 A planes every K step, so cluster rank r loads planes r,
+// r + NC, ... once (one-plane boxes) and multicasts them into every CTA's ring: the L2 -> SM traffic
+// of A falls by NC. A stage is refilled when all NC CTAs' MMAs have retired it: each CTA's
+// tcgen05.commit arrives on the empty barrier of every CTA in the cluster (multicast commit, count
+// NC). Measured on B200 (m = 1e5 of C3): pass 11.67 -> 11.95 ms, the copy skeleton alone 7.84 ->
+// 8.92 ms: NOT faster, so it is off by default (SORSVD_OPT_OZAKI_MULTICAST). The pass is bound by
+// shared-memory bandwidth instead: per K step the MMAs read 44 KB of A planes and 68 KB of X planes
+// (each X plane is an operand of up to 7 MMAs) while TMA writes 42 KB -- 154 KB against
+// 128 B/clk x 1088 clk of MMA time.
+template <bool TA, bool MC>
 __global__ void __launch_bounds__(kOzpThreads, 1)
     ozaki_planes_gemm_kernel(const __grid_constant__ CUtensorMap tmA, OzpArgs p) {
     if (pred_off(p.pred, p.pred_skip)) return;
@@ -233,10 +262,13 @@ __global__ void __launch_bounds__(kOzpThreads, 1)
     const int kt_b = (int)blockIdx.y * p.kt_split;
     const int KT = (KT_all - kt_b < p.kt_split ? KT_all - kt_b : p.kt_split);  // >= 1 (host)
 
+    const uint32_t crank = MC ? cluster_ctarank() : 0u;
+    const uint32_t csize = MC ? (uint32_t)p.NC : 1u;
+    const uint16_t cmask = (uint16_t)((1u << csize) - 1u);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kOzpStages; ++s) {
             mbar_init(full(s), 1);
-            mbar_init(empty(s), 1);
+            mbar_init(empty(s), csize);  // one commit per CTA of the cluster
         }
         mbar_init(drain_full, 1);
         mbar_init(drain_empty, 8);  // one arrive per drain warp
@@ -249,6 +281,7 @@ __global__ void __launch_bounds__(kOzpThreads, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
+    if (MC) cluster_sync_all();  // every CTA's barriers are initialised before any multicast lands
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tmem = *tmem_slot;
 
@@ -259,10 +292,16 @@ __global__ void __launch_bounds__(kOzpThreads, 1)
                 const int s = i % kOzpStages;
                 const uint32_t ph = (uint32_t)(i / kOzpStages) & 1u;
                 mbar_wait(empty(s), ph ^ 1u);
-                mbar_expect_tx(full(s), (uint32_t)kOzStage);
+                mbar_expect_tx(full(s), (p.dbg & 2) ? (uint32_t)kOzXStep : (uint32_t)kOzStage);
                 const uint32_t dst = base + s * kOzStage;
                 const int kt = kt_b + i;
-                if (!TA) tma_load_3d(dst, &tmA, full(s), kt * kOzBK, p.mn0 + (int)m0, 0);
+                if (p.dbg & 2) {
+                } else if (MC) {  // this rank's planes, multicast to the whole cluster
+                    for (int t = (int)crank; t < kOzSlices; t += (int)csize) {
+                        if (!TA) tma_load_3d_mc(dst + t * kOzAPlane, &tmA, full(s), kt * kOzBK, p.mn0 + (int)m0, t, cmask);
+                        else tma_load_3d_mc(dst + t * kOzAPlane, &tmA, full(s), p.mn0 + (int)m0, kt * kOzBK, t, cmask);
+                    }
+                } else if (!TA) tma_load_3d(dst, &tmA, full(s), kt * kOzBK, p.mn0 + (int)m0, 0);
                 else tma_load_3d(dst, &tmA, full(s), p.mn0 + (int)m0, kt * kOzBK, 0);
                 oz_bulk_g2s(dst + kOzSlices * kOzAPlane, xsrc + (size_t)kt * p.NC * kOzXStep, (uint32_t)kOzXStep, full(s));
             }
@@ -291,7 +330,9 @@ __global__ void __launch_bounds__(kOzpThreads, 1)
                             tmem + (uint32_t)((t + u0 - kOzLevel0) * kOzBN)),
                         "l"(da), "l"(db), "r"(idesc));
                 };
-                if (!(p.dbg & 1)) {  // all digit pairs with t + u >= 5
+                if (p.dbg & 4) {  // experiment: only the five 4-plane MMAs (20 of the 34 products)
+                    mma(6, 0, 4); mma(5, 0, 4); mma(4, 1, 4); mma(3, 2, 4); mma(2, 3, 4);
+                } else if (!(p.dbg & 1)) {  // all digit pairs with t + u >= 5
                     mma(6, 0, 4); mma(6, 4, 3);
                     mma(5, 0, 4); mma(5, 4, 3);
                     mma(4, 1, 4); mma(4, 5, 2);
@@ -300,9 +341,16 @@ __global__ void __launch_bounds__(kOzpThreads, 1)
                     mma(1, 4, 3);
                     mma(0, 5, 2);
                 }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                                 empty(s))
-                             : "memory");
+                if (MC)
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                            empty(s)),
+                        "h"(cmask)
+                        : "memory");
+                else
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                     empty(s))
+                                 : "memory");
                 if (ck == kOzChunkSteps - 1 || i == KT - 1)
                     asm volatile(
                         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(drain_full)
@@ -385,6 +433,7 @@ __global__ void __launch_bounds__(kOzpThreads, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
+    if (MC) cluster_sync_all();  // no CTA leaves while a peer may still multicast into it / signal its barriers
     if (warp == 2) {
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));

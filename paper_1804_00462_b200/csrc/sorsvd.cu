@@ -201,6 +201,8 @@ struct sorsvd_emu_group {
 
 struct sorsvd_ctx {
     int opt_jacobi = SORSVD_JACOBI_AUTO;  // sorsvd_ctx_set_option(SORSVD_OPT_JACOBI)
+    int opt_oz_multicast = 0;             // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_MULTICAST): cluster + TMA multicast of the A planes
+                                          // (measured: no gain, the pass is shared-memory-bandwidth bound)
     int64_t opt_upload_chunk_mb = 1536;   // sorsvd_ctx_set_option(SORSVD_OPT_UPLOAD_CHUNK_MB): host-buffer calls of the planes engine
     int opt_fused_pair = 1;               // sorsvd_ctx_set_option(SORSVD_OPT_FUSED_PAIR): 0 = separate NN / TN GEMM passes
     int opt_oz_planes = 1;                // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_PLANES): 0 = convert inside every pass
@@ -2070,10 +2072,13 @@ void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScale
     a.c_split_stride = M * Np;
     double* ws = S > 1 ? dbuf(c, "oz_split", (size_t)S * M * Np) : nullptr;
     a.C = S > 1 ? ws : C;
+    // NC column-chunk CTAs of a row tile as one cluster sharing the A planes by TMA multicast
+    const bool mc = c->opt_oz_multicast && NC >= 2 && NC <= 8;
     CUtensorMap map{};
     cuuint64_t dims[3] = {(cuuint64_t)oz.pn, (cuuint64_t)oz.pm, (cuuint64_t)kOzSlices};
     cuuint64_t strides[2] = {(cuuint64_t)oz.pitch, (cuuint64_t)oz.plane_stride};
-    cuuint32_t box[3] = {(cuuint32_t)(ta ? kOzBM : kOzBK), (cuuint32_t)(ta ? kOzBK : kOzBM), (cuuint32_t)kOzSlices};
+    cuuint32_t box[3] = {(cuuint32_t)(ta ? kOzBM : kOzBK), (cuuint32_t)(ta ? kOzBK : kOzBM),
+                         (cuuint32_t)(mc ? 1 : kOzSlices)};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, oz.planes, dims, strides, box, es,
                                 CU_TENSOR_MAP_INTERLEAVE_NONE, ta ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
@@ -2081,12 +2086,28 @@ void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScale
     if (r != CUDA_SUCCESS)
         throw Error{SORSVD_ERR_CUDA, "cuda: cuTensorMapEncodeTiled (planes) failed " + std::to_string((int)r)};
     const dim3 grid((unsigned)tiles, (unsigned)S);
-    if (ta) {
-        allow_smem(ozaki_planes_gemm_kernel<true>);
-        ozaki_planes_gemm_kernel<true><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
+    if (mc) {
+        auto kern = ta ? ozaki_planes_gemm_kernel<true, true> : ozaki_planes_gemm_kernel<false, true>;
+        allow_smem(kern, true);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(kOzpThreads);
+        cfg.dynamicSmemBytes = kOzpSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)NC;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, kern, map, a));
+    } else if (ta) {
+        allow_smem(ozaki_planes_gemm_kernel<true, false>);
+        ozaki_planes_gemm_kernel<true, false><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
     } else {
-        allow_smem(ozaki_planes_gemm_kernel<false>);
-        ozaki_planes_gemm_kernel<false><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
+        allow_smem(ozaki_planes_gemm_kernel<false, false>);
+        ozaki_planes_gemm_kernel<false, false><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
     }
     check_launch(c);
     if (S > 1) {
@@ -3835,6 +3856,10 @@ int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
                     throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown Jacobi variant"};
                 c->opt_jacobi = (int)value;
                 invalidate_graphs(c);  // captured calls baked the previous variant in
+                break;
+            case SORSVD_OPT_OZAKI_MULTICAST:
+                c->opt_oz_multicast = value != 0;
+                invalidate_graphs(c);
                 break;
             case SORSVD_OPT_UPLOAD_CHUNK_MB:
                 if (value < 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: upload chunk must be >= 1 MiB"};

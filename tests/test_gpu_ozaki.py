@@ -230,3 +230,25 @@ def test_host_call_pipelined_upload_same_bits(P, f32):
         assert np.array_equal(np.asarray(host.v), dev.v.cpu().numpy())
         host2 = P.sor_svd_power(A, 32, cfg, fp64_mode="ozaki", ctx=ctx)   # a second call on the same context
         assert np.array_equal(np.asarray(host2.u), np.asarray(host.u))
+
+
+@pytest.mark.parametrize("m,n,ell,ta", [(3000, 2000, 256, 0), (2000, 3000, 256, 1), (1500, 900, 136, 0), (70000, 600, 128, 1),
+                                        (700, 500, 512, 0)])
+def test_ozaki_planes_multicast_same_bits(P, m, n, ell, ta):
+    """SORSVD_OPT_OZAKI_MULTICAST: the column-chunk CTAs of a row tile as one cluster sharing the A planes by TMA
+    multicast (clusters of 2, 3, 4 and 8 CTAs, split-K) give the bits of the one-CTA-per-tile pass."""
+    import torch
+    buf, A, X = _operands(m, n, ell, ta, m + n + ell)
+    outs = []
+    for mc in (0, 1):
+        ctx = P.Context(0)
+        ctx.set_option(P.Context.OPT_OZAKI_MULTICAST, mc)
+        ctx.set_stream(torch.cuda.current_stream(0).cuda_stream)
+        Np = _npad(ell)
+        T = torch.full(((n if ta else m), Np), float("nan"), device="cuda", dtype=torch.float64)
+        ms, msc = ctypes.c_double(), ctypes.c_double()
+        P._check(P._capi.lib().sorsvd_pass_ozaki_device(ctx.handle, ta, m, n, n, ell, 0, buf.data_ptr(), X.data_ptr(),
+                                                         T.data_ptr(), 1, ctypes.byref(ms), ctypes.byref(msc)), ctx.handle)
+        torch.cuda.synchronize()
+        outs.append(T)
+    assert torch.equal(outs[0], outs[1])
