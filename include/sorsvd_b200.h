@@ -65,8 +65,9 @@ typedef enum sorsvd_flop_variant {
                                          computed as exact int8 slice products on the tcgen05 tensor cores
                                          (Ozaki scheme: 7 signed byte digits of a 55-bit fixed point, the 34
                                          products with digit levels >= 5): error at or below the reference
-                                         dgemm's own sum rounding. Default for large passes (m n ell >= 2^36,
-                                         ell >= 32); this flag forces it */
+                                         dgemm's own sum rounding. Default for large passes: ell >= 32 and
+                                         m n ell >= 2^32 when the call's int8 digit planes of A fit in HBM
+                                         (SORSVD_OPT_OZAKI_PLANES), >= 2^36 otherwise; this flag forces it */
 #define SORSVD_FLAG_DMMA 0x40u        /* force the FP64 DMMA passes (the default below that size) */
 
 typedef struct sorsvd_ctx sorsvd_ctx;

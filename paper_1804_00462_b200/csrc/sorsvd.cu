@@ -2641,15 +2641,22 @@ void validate(const sorsvd_desc* d) {
     if (d->ell > 512) throw Error{SORSVD_ERR_UNSUPPORTED, "ell > 512 is not supported (core SVD / QR limit)"};
 }
 
-// FP64 passes on the int8 tensor cores (ozaki_i8.cuh) by default when a pass
-// is big enough to amortise the per-call scale read and the per-pass digit
-// cutting of the skinny operand (measured: C3 1.81x, C5 1.65x faster per call;
-// C1 / C2 / C4 shapes faster on the DMMA path); SORSVD_FLAG_OZAKI /
-// SORSVD_FLAG_DMMA force either.
+// FP64 passes on the int8 tensor cores by default when a pass is big enough to amortise the
+// per-call conversion of A and the per-pass digit cutting of the skinny operand. Measured call
+// times, Ozaki / DMMA (tools/oz_threshold.py, profiles/r02_oz_threshold.jsonl): with the per-call
+// digit planes 1.11 at m n ell = 2^30.6 (C2), 0.96 at 2^31.8, 0.76-0.82 from 2^32.9 up, 0.50 on C3;
+// converting inside every pass (planes do not fit) pays from ~2^36 (C5 1.65x faster). So: auto =
+// m n ell >= 2^32 when the planes fit, >= 2^36 otherwise, and ell >= 32 (oz_auto_keep below).
+// SORSVD_FLAG_OZAKI / SORSVD_FLAG_DMMA force either.
 bool ozaki_wanted(uint32_t flags, int64_t m, int64_t n, int ell) {
     if (flags & SORSVD_FLAG_DMMA) return false;
     if (flags & SORSVD_FLAG_OZAKI) return true;
-    return (double)m * (double)n * (double)ell >= 68719476736.0 /* 2^36 */ && ell >= 32;
+    return (double)m * (double)n * (double)ell >= 4294967296.0 /* 2^32 */ && ell >= 32;
+}
+// The automatic choice stands without the planes only from 2^36 up.
+bool oz_auto_keep(uint32_t flags, int64_t m, int64_t n, int ell, bool planes) {
+    if (flags & SORSVD_FLAG_OZAKI) return true;
+    return planes || (double)m * (double)n * (double)ell >= 68719476736.0 /* 2^36 */;
 }
 
 // Host-buffer calls: A's upload as row chunks on the copy stream (one event per chunk), so that the
@@ -2750,6 +2757,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     QrPlan *p1, *p2, *pg;
     SorBuffers b = prepare_sor(c, P, &p1, &p2, &pg);
     P.oz_planes = P.ozaki && oz_planes_fit(c, P);
+    if (P.ozaki && !oz_auto_keep(d->flags, P.m, P.n, P.ell, P.oz_planes)) P.ozaki = false;
     double* psi2_in = nullptr;
     if (method == SORSVD_TSR) {  // Psi2 = gaussian_matrix(m, ell, seed ^ 1)   (sketch.hpp:142)
         psi2_in = dbuf(c, "psi2_in", (size_t)P.m * P.ell);
