@@ -89,6 +89,7 @@ struct OzArgs {
     double* C;            // M x ldc output
     int64_t ldc;
     int vec;              // rows of A start 16-byte aligned (lda % (16 / sizeof(AT)) == 0): vector loads (NN)
+    int acc0;             // 1: add to C from the first chunk on (another launch wrote the rest of the K range)
     int dbg;              // timing experiments only: 1 = no MMAs, 2 = no A conversion, 4 = no digit stores
     const int* pred;
     int pred_skip;
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                             double out;
                             if (e_row == kOzNonFinite || f == kOzNonFinite) out = __longlong_as_double(0x7ff8000000000000ll);
                             else out = scalbn(part[c], e_row + f);
-                            crow[col] = chunk == 0 ? out : crow[col] + out;
+                            crow[col] = (chunk == 0 && !p.acc0) ? out : crow[col] + out;
                         }
                     }
                 }

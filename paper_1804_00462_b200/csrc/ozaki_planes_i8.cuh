@@ -7,8 +7,8 @@
 // CTAs of a row tile each repeat it again (16 converter warps per CTA; the
 // MMA pipe was ~46% active). Here the conversion is hoisted out of the passes:
 //
-//   * ozaki_planes_kernel: one read of A (FP64 or FP32 storage) per call ->
-//     7 int8 planes P_t (m x n bytes each, row pitch padded to 16): row i is
+//   * ozaki_rowplanes_kernel: one read of A (FP64 or FP32 storage) per call ->
+//     the row exponents and 7 int8 planes P_t (m x n bytes each, row pitch padded to 16): row i is
 //     scaled by 2^(54 - e_i) (e_i the exponent bound of its largest |entry|),
 //     rounded to a 55-bit integer and split into balanced base-256 digits
 //     exactly as ozaki_i8.cuh does. 7/8 of A's FP64 bytes, kept for the call.
@@ -52,7 +52,7 @@ struct OzpArgs {
     double* C;             // M x ldc (split s writes C + s * c_split_stride)
     int64_t ldc, c_split_stride;
     int kt_split;          // K steps per split (grid.y splits)
-    int dbg;               // timing / bring-up experiments: 1 = no MMAs
+    int dbg;               // timing experiments (tools/oz_pass.py): 1 = no MMAs, 2 = no A-plane TMA, 4 = only 20 of the 34 products
     const int* pred;
     int pred_skip;
 };

@@ -205,7 +205,7 @@ struct sorsvd_ctx {
                                           // (measured: no gain, the pass is shared-memory-bandwidth bound)
     int64_t opt_upload_chunk_mb = 1536;   // sorsvd_ctx_set_option(SORSVD_OPT_UPLOAD_CHUNK_MB): host-buffer calls of the planes engine
     int opt_fused_pair = 1;               // sorsvd_ctx_set_option(SORSVD_OPT_FUSED_PAIR): 0 = separate NN / TN GEMM passes
-    int opt_oz_planes = 1;                // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_PLANES): 0 = convert inside every pass
+    int64_t opt_oz_planes = 1;                // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_PLANES): 0 = convert inside every pass
     int64_t opt_sord_chunk_mb = 64;       // sorsvd_ctx_set_option(SORSVD_OPT_SORD_CHUNK_MB)
     int device = 0;
     int rank = 0, world = 1;
@@ -1707,6 +1707,7 @@ struct SorProblem {
     bool tf32;         // dtype F32 with SORSVD_FLAG_TF32: passes on the tcgen05 tensor cores
     bool ozaki;        // SORSVD_FLAG_OZAKI: FP64 passes as int8 slice products on the tcgen05 tensor cores
     bool oz_planes = false;  // ... from digit planes of A cut once per call (ozaki_planes_i8.cuh), memory permitting
+    int64_t oz_pm = 0;       // rows [0, oz_pm) of A have planes (== m: all; less: the rest is converted in the passes)
     bool pre_first = false;  // host-buffer call: planes and the first T1 = A Omega were produced chunk by chunk
                              // while A was uploading (sor_device's pipelined upload)
     int method = SORSVD_SOR_POWER;  // SORSVD_RSVD / SORSVD_TSR: the baselines of sketch.hpp:124-149
@@ -1873,21 +1874,34 @@ struct OzScales {
 
 int64_t oz_planes_pitch(int64_t n) { return (n + 15) / 16 * 16; }
 
-// Can this call keep 7 digit planes of A (7/8 of an FP64 A) beside A? Decided
-// before anything is enqueued (the answer is baked into the captured graph).
-bool oz_planes_fit(sorsvd_ctx* c, const SorProblem& P) {
-    if (c->opt_oz_planes == 0 || P.m >= INT_MAX || P.n >= INT_MAX) return false;
-    const size_t bytes = (size_t)kOzSlices * (size_t)P.m * (size_t)oz_planes_pitch(P.n);
+// How many leading rows of A can keep their 7 digit planes (7/8 of an FP64 A) beside A? All m when
+// they fit with room for the call's other workspaces; else as many whole 128-row tiles as fit, when
+// that is at least a quarter of A (config 5 on one GPU: 68.7 GB of FP32 A leaves room for the planes
+// of ~5/6 of its rows; the passes convert the remaining rows themselves); else 0. Decided before
+// anything is enqueued (the answer is baked into the captured graph).
+int64_t oz_planes_rows(sorsvd_ctx* c, const SorProblem& P) {
+    if (c->opt_oz_planes == 0 || P.m >= INT_MAX || P.n >= INT_MAX) return 0;
+    const size_t row_bytes = (size_t)kOzSlices * (size_t)oz_planes_pitch(P.n);
+    int64_t want = P.m;
+    if (c->opt_oz_planes > 1) want = std::min<int64_t>(want, c->opt_oz_planes / kOzBM * kOzBM);  // tests: cap the rows
     auto it = c->bufs.find("oz_planes");
     const size_t have = it == c->bufs.end() ? 0 : it->second.bytes;
-    if (have >= bytes) return true;
-    if (c->capturing) return false;
+    if (have >= row_bytes * (size_t)want) return want;
+    if (c->capturing) return 0;
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
     // growing frees the old buffer first; keep room for the call's other workspaces
-    const size_t reserve = (size_t)4 << 30;
-    return fr + have >= bytes + reserve + (size_t)(P.m + P.n) * P.Np * 8 * 4;
+    const size_t reserve = ((size_t)6 << 30) + (size_t)(P.m + P.n) * P.Np * 8 * 4;
+    const size_t avail = fr + have > reserve ? fr + have - reserve : 0;
+    if (avail >= row_bytes * (size_t)want) return want;
+    // partial cover: what fits now, but never fewer rows than the workspace this context already
+    // holds (a later call on the same A then splits its rows where the earlier one did: same bits)
+    int64_t rows = (int64_t)(avail / row_bytes) / kOzBM * kOzBM;
+    if (rows < std::max<int64_t>(P.m / 4, 1024)) rows = 0;
+    const int64_t rows_have = (int64_t)(have / row_bytes) / kOzBM * kOzBM;
+    return std::min(std::max(rows, rows_have), want);
 }
+bool oz_planes_fit(sorsvd_ctx* c, const SorProblem& P) { return oz_planes_rows(c, P) == P.m; }
 
 template <typename AT>
 void launch_rowplanes(sorsvd_ctx* c, const AT* A, const SorProblem& P, int* re, const OzScales& oz, cudaStream_t s) {
@@ -1906,9 +1920,10 @@ void launch_rowplanes(sorsvd_ctx* c, const AT* A, const SorProblem& P, int* re, 
 // The call's planes workspace (no kernels): exponents and the 7 digit planes of an m x n A.
 OzScales oz_planes_of(sorsvd_ctx* c, const SorProblem& P) {
     OzScales oz{reinterpret_cast<int*>(dbuf(c, "oz_rowe", (size_t)(P.m + 1) / 2)), nullptr};
+    const int64_t pm = P.oz_pm > 0 ? P.oz_pm : P.m;
     oz.pitch = oz_planes_pitch(P.n);
-    oz.plane_stride = oz.pitch * P.m;
-    oz.pm = P.m;
+    oz.plane_stride = oz.pitch * pm;
+    oz.pm = pm;
     oz.pn = P.n;
     oz.planes = reinterpret_cast<int8_t*>(dbuf(c, "oz_planes", (size_t)(kOzSlices * oz.plane_stride + 7) / 8));
     return oz;
@@ -1928,29 +1943,35 @@ void oz_convert_rows(sorsvd_ctx* c, const SorProblem& P, const OzScales& oz, int
 
 OzScales oz_prepare_a(sorsvd_ctx* c, const SorProblem& P, cudaStream_t s) {
     int* re = reinterpret_cast<int*>(dbuf(c, "oz_rowe", (size_t)(P.m + 1) / 2));
+    OzScales oz{re, nullptr};
+    int64_t r0 = 0;  // first row without planes
     if (P.oz_planes) {
         // cut A into its row-scaled digit planes once (row maxima and digits in one read of A);
         // every pass of the call streams the planes, TN passes fold the row scales into T1
-        OzScales oz = oz_planes_of(c, P);
-        oz_convert_rows(c, P, oz, 0, P.m, s);
-        return oz;
+        oz = oz_planes_of(c, P);
+        oz_convert_rows(c, P, oz, 0, oz.pm, s);
+        if (oz.pm >= P.m) return oz;
+        r0 = oz.pm;  // the planes cover rows [0, pm) only: the rest keeps the in-pass converter's scales
     }
-    auto* rmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_rowmax", (size_t)P.m));
+    // rows [r0, m): row exponents, and the column exponents over those rows (the TN left operand)
+    const int64_t mb = P.m - r0;
+    auto* rmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_rowmax", (size_t)mb));
     auto* cmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_colmax", (size_t)P.n));
     int* ce = reinterpret_cast<int*>(dbuf(c, "oz_cole", (size_t)(P.n + 1) / 2));
-    CK(cudaMemsetAsync(rmax, 0, (size_t)P.m * 8, s));
+    CK(cudaMemsetAsync(rmax, 0, (size_t)mb * 8, s));
     CK(cudaMemsetAsync(cmax, 0, (size_t)P.n * 8, s));
-    const dim3 grid((unsigned)cdiv(P.n, 512), (unsigned)cdiv(P.m, 64));
+    const dim3 grid((unsigned)cdiv(P.n, 512), (unsigned)cdiv(mb, 64));
     if (P.dtype == SORSVD_F32)
-        ozaki_absmax_kernel<float><<<grid, 256, 0, s>>>(P.Af, P.lda, P.m, P.n, rmax, cmax);
+        ozaki_absmax_kernel<float><<<grid, 256, 0, s>>>(P.Af + r0 * P.lda, P.lda, mb, P.n, rmax, cmax);
     else
-        ozaki_absmax_kernel<double><<<grid, 256, 0, s>>>(P.A, P.lda, P.m, P.n, rmax, cmax);
+        ozaki_absmax_kernel<double><<<grid, 256, 0, s>>>(P.A + r0 * P.lda, P.lda, mb, P.n, rmax, cmax);
     check_launch(c);
-    ozaki_exp_kernel<<<(unsigned)std::min<int64_t>(cdiv(P.m, 256), c->num_sms * 8), 256, 0, s>>>(rmax, P.m, re);
+    ozaki_exp_kernel<<<(unsigned)std::min<int64_t>(cdiv(mb, 256), c->num_sms * 8), 256, 0, s>>>(rmax, mb, re + r0);
     check_launch(c);
     ozaki_exp_kernel<<<(unsigned)std::min<int64_t>(cdiv(P.n, 256), c->num_sms * 8), 256, 0, s>>>(cmax, P.n, ce);
     check_launch(c);
-    return OzScales{re, ce};
+    oz.col_e = ce;
+    return oz;
 }
 
 template <bool TA, typename AT>
@@ -2118,31 +2139,29 @@ void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScale
     }
 }
 
-void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const double* X, double* C,
-               cudaStream_t s, int dbg = 0, int64_t n0 = 0) {
+// The in-pass converter engine (ozaki_i8.cuh) over rows [r0, m) of A (r0 = 0: all of A): NN writes
+// C's rows [r0, m); TN contracts over those rows only and, with acc, adds to C (the planes engine
+// wrote the contribution of rows [0, r0) first).
+void oz_launch_convert(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const OzX& x, double* C,
+                       int64_t r0, int64_t n0, bool acc, cudaStream_t s, int dbg) {
     const int Np = P.Np;
     const int NC = (int)cdiv(Np, kOzBN);
-    const int64_t M = ta ? P.n : P.m, K = ta ? P.m : P.n;
-    const OzX ox = oz_cut_x(c, P, ta, oz, X, s);
-    if (oz.planes) {
-        oz_launch_planes(c, P, ta, oz, ox, C, ta ? n0 : 0, M, s, dbg);
-        return;
-    }
-    int8_t* Xd = ox.Xd;
-    int* xexp = ox.xexp;
+    const int64_t mb = P.m - r0;
+    const int64_t M = ta ? P.n : mb, K = ta ? mb : P.n;
     OzArgs a{};
-    a.A = P.dtype == SORSVD_F32 ? static_cast<const void*>(P.Af) : static_cast<const void*>(P.A);
+    a.A = P.dtype == SORSVD_F32 ? static_cast<const void*>(P.Af + r0 * P.lda) : static_cast<const void*>(P.A + r0 * P.lda);
     a.lda = P.lda;
     a.M = M;
     a.K = K;
-    a.lexp = ta ? oz.col_e + n0 : oz.row_e;
-    a.Xd = Xd;
-    a.xexp = xexp;
+    a.lexp = ta ? oz.col_e + n0 : oz.row_e + r0;
+    a.Xd = x.Xd;
+    a.xexp = x.xexp;
     a.NC = NC;
     a.N = Np;
-    a.C = C;
+    a.C = ta ? C : C + r0 * Np;
     a.ldc = Np;
     a.dbg = dbg;
+    a.acc0 = acc ? 1 : 0;
     a.vec = ((uintptr_t)a.A % 16) == 0 && (P.dtype == SORSVD_F32 ? P.lda % 4 : P.lda % 2) == 0;
     a.pred = c->pred;
     a.pred_skip = c->pred_skip;
@@ -2155,6 +2174,42 @@ void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, 
         else launch_ozaki_t<false, double>(a, grid, s);
     }
     check_launch(c);
+}
+
+void run_ozaki(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const double* X, double* C,
+               cudaStream_t s, int dbg = 0, int64_t n0 = 0) {
+    const int64_t M = ta ? P.n : P.m;
+    const int64_t pm = oz.planes ? std::min(oz.pm, P.m) : 0;  // rows with planes
+    if (pm >= P.m) {  // all of A from its digit planes
+        const OzX ox = oz_cut_x(c, P, ta, oz, X, s);
+        oz_launch_planes(c, P, ta, oz, ox, C, ta ? n0 : 0, M, s, dbg);
+        return;
+    }
+    if (pm == 0) {  // A converted inside the pass
+        const OzX ox = oz_cut_x(c, P, ta, oz, X, s);
+        oz_launch_convert(c, P, ta, oz, ox, C, 0, n0, false, s, dbg);
+        return;
+    }
+    // planes for rows [0, pm), the in-pass converter for rows [pm, m)
+    if (!ta) {  // the two row ranges are independent outputs; X is cut once (plain per-column cut)
+        OzScales plain = oz;
+        plain.planes = nullptr;
+        const OzX ox = oz_cut_x(c, P, false, plain, X, s);
+        oz_launch_planes(c, P, false, oz, ox, C, 0, pm, s, dbg);
+        oz_launch_convert(c, P, false, oz, ox, C, pm, 0, false, s, dbg);
+        return;
+    }
+    // TN: T2 = A_top^T T1_top (planes; the top rows' scales ride on T1_top) + A_bot^T T1_bot
+    SorProblem Qt = P;
+    Qt.m = pm;
+    const OzX xt = oz_cut_x(c, Qt, true, oz, X, s);
+    oz_launch_planes(c, Qt, true, oz, xt, C, n0, M, s, dbg);
+    SorProblem Qb = P;
+    Qb.m = P.m - pm;
+    OzScales plain = oz;
+    plain.planes = nullptr;
+    const OzX xb = oz_cut_x(c, Qb, true, plain, X + pm * P.Np, s);  // stream order: after the top launch read xt
+    oz_launch_convert(c, P, true, oz, xb, C, pm, n0, true, s, dbg);
 }
 
 // Q = thin_qr(T).q of a row-sharded m x ell operand (the sketch T1 / Y; sketch.hpp:98, :129, :145):
@@ -2618,8 +2673,8 @@ void check_result_finite(sorsvd_ctx* c, const double* dS, int k, const void* A, 
 // on the same A must not replay it).
 std::string sor_key(const SorProblem& P, const int* pred, int pred_skip) {
     char buf[320];
-    snprintf(buf, sizeof buf, "sor%d:%d:%d:%d%d%d:%p:%lld:%lld:%lld:%d:%d:%d", P.method, P.dtype, (int)P.single_pass,
-             (int)P.tf32, (int)P.ozaki, (int)P.oz_planes,
+    snprintf(buf, sizeof buf, "sor%d:%d:%d:%d%d%lld:%p:%lld:%lld:%lld:%d:%d:%d", P.method, P.dtype, (int)P.single_pass,
+             (int)P.tf32, (int)P.ozaki, (long long)P.oz_pm,
              P.dtype == SORSVD_F32 ? (const void*)P.Af : (const void*)P.A, (long long)P.m, (long long)P.n,
              (long long)P.lda, P.k, P.ell, P.q);
     if (pred) snprintf(buf + strlen(buf), sizeof buf - strlen(buf), ":pred%p/%d", (const void*)pred, pred_skip);
@@ -2756,7 +2811,8 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     P.ozaki = !P.tf32 && !baseline && ozaki_wanted(d->flags, P.m, P.n, P.ell);
     QrPlan *p1, *p2, *pg;
     SorBuffers b = prepare_sor(c, P, &p1, &p2, &pg);
-    P.oz_planes = P.ozaki && oz_planes_fit(c, P);
+    P.oz_pm = P.ozaki ? oz_planes_rows(c, P) : 0;
+    P.oz_planes = P.oz_pm > 0;
     if (P.ozaki && !oz_auto_keep(d->flags, P.m, P.n, P.ell, P.oz_planes)) P.ozaki = false;
     double* psi2_in = nullptr;
     if (method == SORSVD_TSR) {  // Psi2 = gaussian_matrix(m, ell, seed ^ 1)   (sketch.hpp:142)
@@ -2788,7 +2844,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     const bool timing = (d->flags & SORSVD_FLAG_STAGE_TIMES) != 0;
     // host-buffer call with A arriving in row chunks: the planes engine converts and sweeps chunk i
     // (first pass T1 = A Omega, rows independent) while chunk i + 1 uploads
-    const bool pipe = up && up->chunked && P.ozaki && P.oz_planes && c->world == 1 && !baseline;
+    const bool pipe = up && up->chunked && P.ozaki && P.oz_pm == P.m && c->world == 1 && !baseline;
     if (up && up->chunked && !pipe)  // not eligible after all: wait for the whole upload
         CK(cudaStreamWaitEvent(c->stream, c->up_ev[(size_t)up->nchunks - 1], 0));
     const bool use_graph = !timing && !c->emu && !(d->flags & SORSVD_FLAG_NO_GRAPH) && !pipe;
@@ -2898,7 +2954,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         st->bytes_passes = (double)d->m * d->n * (d->dtype == SORSVD_F32 ? 4.0 : 8.0) * launched;
         st->launches = launches;
         st->pass_kind = P.tf32 ? 2 : P.ozaki ? 1 : 0;
-        st->oz_planes = P.oz_planes ? 1 : 0;
+        st->oz_planes = !P.ozaki ? 0 : P.oz_pm >= P.m ? 1 : P.oz_pm > 0 ? 2 : 0;
         int sw = 0;
         CK(cudaMemcpy(&sw, b.sweeps, sizeof(int), cudaMemcpyDeviceToHost));
         st->jacobi_sweeps = sw;
@@ -3878,7 +3934,8 @@ int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
                 invalidate_graphs(c);
                 break;
             case SORSVD_OPT_OZAKI_PLANES:
-                c->opt_oz_planes = value != 0;
+                if (value < 0) throw Error{SORSVD_ERR_PARAMETER, "parameter: OZAKI_PLANES must be >= 0"};
+                c->opt_oz_planes = (int64_t)value;
                 invalidate_graphs(c);
                 break;
             case SORSVD_OPT_SORD_CHUNK_MB:
@@ -3916,6 +3973,23 @@ static void host_call(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const 
     const size_t abytes = (size_t)d->m * d->lda * esz;
     cudaEvent_t e0 = c->ev_h[0], e1 = c->ev_h[1], e2 = c->ev_h[2], e3 = c->ev_h[3];
     CK(cudaEventRecord(e0, c->stream));
+    {
+        // the device copy of A comes first: a planes workspace left by an earlier (device-resident)
+        // call is given back when A would not fit beside it
+        auto ia = c->bufs.find("hostA");
+        const size_t have_a = ia == c->bufs.end() ? 0 : ia->second.bytes;
+        auto ip = c->bufs.find("oz_planes");
+        if (have_a < abytes && ip != c->bufs.end() && ip->second.p) {
+            size_t fr = 0, tot = 0;
+            CK(cudaMemGetInfo(&fr, &tot));
+            if (fr + have_a < abytes + ((size_t)8 << 30)) {
+                CK(cudaStreamSynchronize(c->stream));
+                invalidate_graphs(c);
+                CK(cudaFree(ip->second.p));
+                c->bufs.erase(ip);
+            }
+        }
+    }
     double* dA = dbuf(c, "hostA", (abytes + 7) / 8);
     HostUpload up;
     {
@@ -4645,7 +4719,8 @@ int sorsvd_pass_ozaki_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, in
         P.k = ell;
         P.Np = npad(ell);
         P.ozaki = true;
-        P.oz_planes = oz_planes_fit(c, P);
+        P.oz_pm = oz_planes_rows(c, P);
+        P.oz_planes = P.oz_pm > 0;
         CK(cudaEventRecord(c->ev_h[0], c->stream));
         OzScales oz = oz_prepare_a(c, P, c->stream);
         CK(cudaEventRecord(c->ev_h[1], c->stream));

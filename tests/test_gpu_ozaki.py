@@ -252,3 +252,37 @@ def test_ozaki_planes_multicast_same_bits(P, m, n, ell, ta):
         torch.cuda.synchronize()
         outs.append(T)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("m,n,ell,ta,f32", [(4000, 3000, 256, 0, False), (4000, 3000, 256, 1, False), (3001, 999, 64, 1, False),
+                                            (5000, 2000, 136, 0, True), (5000, 2000, 136, 1, True), (40000, 600, 512, 1, False)])
+def test_ozaki_partial_planes(P, m, n, ell, ta, f32):
+    """Planes for the leading rows only (what fits in HBM: config 5 on one GPU), the in-pass converter for
+    the rest: NN writes the two row ranges, TN sums the two K ranges. OPT_OZAKI_PLANES > 1 caps the rows."""
+    import torch
+    buf, A, X = _operands(m, n, ell, ta, m + 3 * n + ell, None, f32)
+    T = _pass(P, buf, X, ta, m, n, ell, dtype=1 if f32 else 0, planes=1280)
+    A64 = A.double()
+    ref = (A64.T if ta else A64) @ X
+    K = m if ta else n
+    amax = A64.abs().amax() if ta else A64.abs().amax(dim=1)[:, None]
+    xmax = X.abs().amax(dim=0).clamp_min(1e-300)
+    err = (T - ref).abs()[:, :ell] / (amax * xmax[None, :ell] * np.sqrt(K)).clamp_min(1e-300)
+    assert not torch.isnan(T[:, :ell]).any()
+    assert err.max().item() <= PASS_TOL, err.max().item()
+    again = _pass(P, buf, X, ta, m, n, ell, dtype=1 if f32 else 0, planes=1280)
+    assert torch.equal(T, again)
+
+
+def test_ozaki_partial_planes_whole_call(P):
+    import torch
+    A = O.gen_lowrank_decay(6000, 1500, 40, lambda j: 2.0 ** (-j / 4), 1e-3, 23)
+    cfg = O.SketchConfig(48, 2, 9)
+    base, ds, dl = O.perturbation_floor(A, 40, cfg)
+    ctx = P.Context(0)
+    ctx.set_option(P.Context.OPT_OZAKI_PLANES, 2560)
+    f = P.sor_svd_power(torch.from_numpy(A).cuda(), 40, P.SketchConfig(48, 2, 9), fp64_mode="ozaki", ctx=ctx)
+    assert f.stats["pass_kind"] == 1 and f.stats["oz_planes"] == 2
+    _check_parity(f, base, ds, dl)
+    h = P.sor_svd_power(A, 40, P.SketchConfig(48, 2, 9), fp64_mode="ozaki", ctx=ctx)   # host call: no pipelined upload
+    assert np.array_equal(np.asarray(h.sigma), f.sigma.cpu().numpy())
