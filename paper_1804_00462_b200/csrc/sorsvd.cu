@@ -148,6 +148,8 @@ struct QrPlan {
     double *G1 = nullptr, *G2 = nullptr, *Ri1 = nullptr, *Ri2 = nullptr, *R1 = nullptr, *Qtmp = nullptr,
            *cwork = nullptr;
     int* flag = nullptr;
+    bool hint_house = false;  // the CholeskyQR2 gate rejected this plan's last operands (RPCA reads the flag back
+                              // between batches): go straight to the Householder TSQR, skip the doomed attempt
     // k > 256: shifted CholeskyQR3 (cholc_f64.cuh); R lands in R[0] with row pitch ldR
     bool big = false;
     int ldR = 0;
@@ -1426,6 +1428,11 @@ void qr_run(sorsvd_ctx* c, QrPlan* p, double* T, int64_t ldt, double* Q, int64_t
         run_gemm(c, g, s);
     };
     if (ldt != Np) throw Error{SORSVD_ERR_INTERNAL, "qr_run: T must be padded to Np"};
+    if (p->hint_house) {  // Gram + Cholesky attempt skipped (it was rejected on the previous operands of this plan)
+        qr_factor(c, p, T, ldt, Q, ldq, true, s);
+        qr_formq(c, p, T, ldt, Q, ldq, nullptr, s);
+        return;
+    }
     // k > 160: the factor no longer fits one CTA's shared memory and chol_inv_kernel would run
     // its k sequential steps out of global memory (k = 256: 3.7 ms per factorisation); the
     // factor is then spread over a cluster (cholc_kernel in CholeskyQR2 mode, same gates) and
@@ -2896,7 +2903,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         CK(cudaMemcpyAsync(dS, b.Sk, (size_t)P.k * 8, cudaMemcpyDeviceToDevice, c->stream));
     };
     if (use_graph) {
-        const std::string key = sor_key(P, c->pred, c->pred_skip);
+        const std::string key = sor_key(P, c->pred, c->pred_skip) + (p1->hint_house ? ":h1" : "") + (p2->hint_house ? ":h2" : "");
         auto it = c->graphs.find(key);
         if (it == c->graphs.end()) {
             if (c->graphs.size() >= 32) invalidate_graphs(c);  // bound the cache (keys carry A's address)
@@ -3597,6 +3604,7 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
     int* stf = reinterpret_cast<int*>(dbuf(c, "rp_state", 2));  // [0] done, [1] iterations, [2] error
     double* rels = dbuf(c, "rp_rel", 1);
     CK(cudaMemsetAsync(stf, 0, 4 * sizeof(int), c->stream));
+    for (const char* tag : {"T1", "T2"}) get_qr_plan(c, tag[1] == '1' ? m : n, ell, 0, tag)->hint_house = false;
     std::vector<double> mus;
     mus.push_back(mu);
     int it = 0;
@@ -3663,6 +3671,18 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
         CK(cudaStreamSynchronize(c->stream));
         executed = hst[1];
         if (hst[2]) throw Error{SORSVD_ERR_NUMERICAL, "numerical: rpca produced a non-finite iterate"};
+        if (c->world == 1) {
+            // W's sketches are ill-conditioned from the first iterations on (a dominant low-rank part over the
+            // sparse residue): once the CholeskyQR2 gate has rejected them, later iterations of this solve go
+            // straight to the Householder TSQR (the attempt costs a Gram + a factorisation per QR)
+            for (const char* tag : {"T1", "T2"}) {
+                QrPlan* qp = get_qr_plan(c, tag[1] == '1' ? m : n, ell, 0, tag);
+                if (qp->big || qp->hint_house || !qp->flag) continue;
+                int fl = 0;
+                CK(cudaMemcpy(&fl, qp->flag, sizeof(int), cudaMemcpyDeviceToHost));
+                if (fl == 1) qp->hint_house = true;
+            }
+        }
         if (hst[0]) {
             conv = true;
             break;
@@ -3670,6 +3690,7 @@ void rpca_device(sorsvd_ctx* c, const sorsvd_rpca_desc* d, const double* dD, dou
         it += nb;
     }
     it = executed;
+    for (const char* tag : {"T1", "T2"}) get_qr_plan(c, tag[1] == '1' ? m : n, ell, 0, tag)->hint_house = false;
     // rank of the last executed iteration's shrunk spectrum
     const int fl = it - 1;
     U = Us + (size_t)(fl % kBatch) * m * ell;
