@@ -92,15 +92,17 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 // row -- still in L1 / L2: at most 2 blocks x 148 SMs x one 160 KB row are in
 // flight -- and cut it. A thread takes 4 consecutive values: 32 (16) bytes of
 // loads, one 4-byte store per plane, a warp 128 contiguous bytes per plane.
-template <typename AT>
+template <typename AT, bool LAST = false>
 __device__ __forceinline__ void oz_load4(const AT* __restrict__ src, int64_t col, int64_t n, int vec, double v[4]) {
     if (vec && col + 4 <= n) {
         if constexpr (sizeof(AT) == 8) {
-            const double2 x0 = __ldg(reinterpret_cast<const double2*>(src + col));
-            const double2 x1 = __ldg(reinterpret_cast<const double2*>(src + col) + 1);
+            const double2* q = reinterpret_cast<const double2*>(src + col);
+            const double2 x0 = LAST ? __ldcs(q) : __ldg(q);      // LAST: the row's second (final) read, evict first
+            const double2 x1 = LAST ? __ldcs(q + 1) : __ldg(q + 1);
             v[0] = x0.x, v[1] = x0.y, v[2] = x1.x, v[3] = x1.y;
         } else {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(src + col));
+            const float4* q = reinterpret_cast<const float4*>(src + col);
+            const float4 x = LAST ? __ldcs(q) : __ldg(q);
             v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
         }
     } else {
@@ -109,14 +111,14 @@ __device__ __forceinline__ void oz_load4(const AT* __restrict__ src, int64_t col
     }
 }
 
-template <typename AT, int G>
-__global__ void __launch_bounds__(512, 2) ozaki_rowplanes_kernel(const AT* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+template <typename AT, int G, int THREADS = 512>
+__global__ void __launch_bounds__(THREADS, 1024 / THREADS) ozaki_rowplanes_kernel(const AT* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                                                                  int* __restrict__ row_e, int8_t* __restrict__ planes,
                                                                  int64_t pitch, int64_t plane_stride, int vec,
                                                                  const int* pred, int pred_skip) {
     if (pred_off(pred, pred_skip)) return;
-    constexpr int RPB = 512 / G;  // rows per block
-    __shared__ unsigned long long sred[16];
+    constexpr int RPB = THREADS / G;  // rows per block
+    __shared__ unsigned long long sred[THREADS / 32];
     const int gi = threadIdx.x % G, gr = threadIdx.x / G;
     const int64_t ngroups = (n + 3) / 4;
     for (int64_t row0 = (int64_t)blockIdx.x * RPB; row0 < m; row0 += (int64_t)gridDim.x * RPB) {
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(512, 2) ozaki_rowplanes_kernel(const AT* __res
         const AT* src = A + (ok ? row : 0) * lda;
         unsigned long long mx = 0ull;
         if (ok) {
-#pragma unroll 4
+#pragma unroll 8
             for (int64_t g = gi; g < ngroups; g += G) {
                 double v[4];
                 oz_load4(src, 4 * g, n, vec, v);
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(512, 2) ozaki_rowplanes_kernel(const AT* __res
             if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = mx;
             __syncthreads();
 #pragma unroll
-            for (int w = 0; w < 16; ++w) mx = sred[w] > mx ? sred[w] : mx;
+            for (int w = 0; w < THREADS / 32; ++w) mx = sred[w] > mx ? sred[w] : mx;
         }
         // max < 2^e (frexp); the sentinel for NaN / Inf; 0 for an all-zero row (ozaki_exp_kernel)
         int e = 0;
@@ -158,10 +160,10 @@ __global__ void __launch_bounds__(512, 2) ozaki_rowplanes_kernel(const AT* __res
             if (gi == 0) row_e[row] = e;
             const double s = oz_scale(e);
             int8_t* drow = planes + row * pitch;
-#pragma unroll 2
+#pragma unroll 4
             for (int64_t g = gi; g < ngroups; g += G) {
                 double v[4];
-                oz_load4(src, 4 * g, n, vec, v);
+                oz_load4<AT, true>(src, 4 * g, n, vec, v);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) v[i] = e == kOzNonFinite ? 0.0 : v[i] * s;
                 uint32_t wd[kOzSlices];
