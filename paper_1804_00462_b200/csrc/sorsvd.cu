@@ -3910,6 +3910,8 @@ void sorsvd_ctx_destroy(sorsvd_ctx* c) {
     if (c->om_pin) cudaFreeHost(c->om_pin);
     for (cudaStream_t t : c->tstreams) cudaStreamDestroy(t);
     for (cudaEvent_t e : c->tevents) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->up_ev) cudaEventDestroy(e);
+    cudaStreamSynchronize(c->comm_stream);
     for (auto& e : c->ev_blk) cudaEventDestroy(e);
     cudaEventDestroy(c->ev_comm);
     cudaEventDestroy(c->ev_in);
@@ -4015,6 +4017,15 @@ static void host_call(sorsvd_ctx* c, const sorsvd_desc* d, const void* A, const 
     }
     double* dA = dbuf(c, "hostA", (abytes + 7) / 8);
     HostUpload up;
+    // whatever happens below (a validation error, a CUDA failure), the caller's A is not read after
+    // this function returns: the copy stream is drained on every exit path
+    struct DrainCopies {
+        sorsvd_ctx* c;
+        ~DrainCopies() {
+            cudaStreamSynchronize(c->comm_stream);
+            cudaStreamSynchronize(c->stream);
+        }
+    } drain{c};
     {
         // Ozaki planes engine on one rank: upload A in row chunks on the copy stream and let the
         // device convert / sweep each chunk as it lands (sor_device); else one copy on the stream
