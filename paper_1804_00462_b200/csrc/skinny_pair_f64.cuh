@@ -221,6 +221,218 @@ __global__ void __launch_bounds__(kPairThreads, 1) skinny_pair_kernel(PairArgs p
     }
 }
 
+// ---- two independent halves per CTA (n <= 320) ------------------------------------------------
+// The one-pipeline kernel above leaves the tensor pipe 43% active: stage, contract, sum the K
+// parts, contract again are a chain of short phases separated by block-wide barriers on a
+// 1-CTA-per-SM kernel (shared memory rules out a second CTA). Here the 16 warps run as two halves
+// of 8 warps that walk alternate 16-row blocks of the CTA's range, each with its own double-
+// buffered staging area, K-part buffer and named barrier (bar.sync 1 / 2 over 256 threads), and
+// share only X: while one half sits in a barrier or waits for cp.async, the other issues DMMAs.
+// The halves' accumulators are added through shared memory at the end (half 1 first into the
+// buffer, half 0 adds and writes the CTA's partial: fixed order).
+constexpr int kPair2MaxT2 = 5;   // output row tiles per warp: ceil(ceil(n / 8) / 8), n <= 320
+constexpr int kPair2Rb = 16;
+
+inline size_t pair2_smem_bytes(int n, bool proj) {
+    const int per_half = 2 * kPair2Rb * pair_nld(n) + 4 * kPair2Rb * kPairLd + (proj ? kPair2Rb * kPairLd : 0);
+    return (size_t)(n * kPairLd + 2 * per_half) * sizeof(double);
+}
+
+__device__ __forceinline__ void pair_half_sync(int half) {
+    asm volatile("bar.sync %0, 256;\n" ::"r"(1 + half) : "memory");
+}
+
+template <bool PROJ>
+__global__ void __launch_bounds__(kPairThreads, 1) skinny_pair2_kernel(PairArgs p) {
+    if (pred_off(p.pred, p.pred_skip)) return;
+    extern __shared__ __align__(16) double sm[];
+    constexpr int rb = kPair2Rb, mt1 = 2, ksplit = 4;
+    const int n = p.n, nld = pair_nld(n);
+    const int per_half = 2 * rb * nld + ksplit * rb * kPairLd + (PROJ ? rb * kPairLd : 0);
+    const int t = threadIdx.x, half = t >> 8, ht = t & 255, hw = ht >> 5, lane = t & 31, g = lane >> 2, t4 = lane & 3;
+    double* sX = sm;                                    // [n][kPairLd], shared by the halves
+    double* sW = sX + n * kPairLd + half * per_half;    // [2][rb][nld]
+    double* sT = sW + 2 * rb * nld;                     // [ksplit][rb][kPairLd]
+    double* sL = sT + ksplit * rb * kPairLd;            // [rb][kPairLd] (PROJ)
+
+    for (int e = t; e < n * kPairNP; e += kPairThreads) {
+        const int j = e >> 4, cc = e & 15;
+        sX[j * kPairLd + cc] = cc < p.np ? p.X[(int64_t)j * p.ldx + cc] : 0.0;
+    }
+    // the CTA's contiguous range of 16-row blocks; half h takes blocks b0 + h, b0 + h + 2, ...
+    const int64_t nblk = (p.m + rb - 1) / rb;
+    const int64_t per = (nblk + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = (int64_t)blockIdx.x * per + half;
+    const int64_t b1 = (int64_t)blockIdx.x * per + per < nblk ? (int64_t)blockIdx.x * per + per : nblk;
+
+    auto stage = [&](int64_t blk, int buf) {
+        double* dst = sW + (size_t)buf * rb * nld;
+        const int64_t row0 = blk * rb;
+        if (p.vec) {
+            const int cpr = (n + 1) >> 1;
+            const int dr = 256 / cpr, dc = 256 - dr * cpr;
+            int r = ht / cpr, ch = ht - r * cpr;
+            while (r < rb) {
+                const int64_t row = row0 + r;
+                const int rem = n - 2 * ch;
+                const int bytes = row < p.m ? (rem >= 2 ? 16 : 8) : 0;
+                cp_async16(dst + r * nld + 2 * ch, p.A + (row < p.m ? row : 0) * p.lda + 2 * ch, bytes);
+                r += dr;
+                ch += dc;
+                if (ch >= cpr) {
+                    ch -= cpr;
+                    ++r;
+                }
+            }
+        } else {
+            for (int e = ht; e < rb * n; e += 256) {
+                const int r = e / n, j = e - r * n;
+                const int64_t row = row0 + r;
+                cp_async8(dst + r * nld + j, p.A + (row < p.m ? row : 0) * p.lda + j, row < p.m ? 8 : 0);
+            }
+        }
+        cp_async_commit();
+    };
+
+    const int ks_all = (n + 3) >> 2;
+    const int ks_per = (ks_all + ksplit - 1) / ksplit;
+    const int mt2_all = PROJ ? 2 : (n + 7) >> 3;
+    double acc2[kPair2MaxT2][2][2];
+#pragma unroll
+    for (int i = 0; i < kPair2MaxT2; ++i) acc2[i][0][0] = acc2[i][0][1] = acc2[i][1][0] = acc2[i][1][1] = 0.0;
+
+    if (b0 < b1) stage(b0, 0);
+    __syncthreads();  // sX complete (the only block-wide barrier before the epilogue)
+    int trip = 0;
+    for (int64_t blk = b0; blk < b1; blk += 2, ++trip) {
+        const int buf = trip & 1;
+        if (blk + 2 < b1) {
+            stage(blk + 2, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        const int64_t row0 = blk * rb;
+        if (PROJ) {
+            const int r = ht >> 4, cc = ht & 15;  // rb * 16 = 256 elements: one per thread
+            const int64_t row = row0 + r;
+            sL[r * kPairLd + cc] = (row < p.m && cc < p.np) ? p.L[row * p.ldl + cc] : 0.0;
+        }
+        pair_half_sync(half);  // this half's block visible
+        const double* W = sW + (size_t)buf * rb * nld;
+        {   // stage 1: T1_b (16 x 16) = W_b X; warp = (row tile, K part), two interleaved DMMA chains
+            const int mt = hw % mt1, kp = hw / mt1;
+            double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0, d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+            const double* wrow = W + (8 * mt + g) * nld;
+            const int k_end = (kp + 1) * ks_per < ks_all ? (kp + 1) * ks_per : ks_all;
+            for (int ks = kp * ks_per; ks < k_end; ks += 2) {
+                const int j = 4 * ks + t4, j2 = j + 4;
+                const bool ok = j < n, ok2 = ks + 1 < k_end && j2 < n;
+                const double a = ok ? wrow[j] : 0.0;
+                const double x0 = ok ? sX[j * kPairLd + g] : 0.0;
+                const double x1 = ok ? sX[j * kPairLd + 8 + g] : 0.0;
+                const double a2 = ok2 ? wrow[j2] : 0.0;
+                const double y0 = ok2 ? sX[j2 * kPairLd + g] : 0.0;
+                const double y1 = ok2 ? sX[j2 * kPairLd + 8 + g] : 0.0;
+                dmma884(c00, c01, a, x0);
+                dmma884(c10, c11, a, x1);
+                dmma884(d00, d01, a2, y0);
+                dmma884(d10, d11, a2, y1);
+            }
+            double* tp = sT + (size_t)kp * rb * kPairLd + (8 * mt + g) * kPairLd + 2 * t4;
+            tp[0] = c00 + d00;
+            tp[1] = c01 + d01;
+            tp[8] = c10 + d10;
+            tp[9] = c11 + d11;
+        }
+        pair_half_sync(half);
+        {   // sum the K parts in order -> T1_b; 256 elements, one per thread
+            const int r = ht >> 4, cc = ht & 15;
+            double v = sT[r * kPairLd + cc];
+#pragma unroll
+            for (int q = 1; q < ksplit; ++q) v += sT[(size_t)q * rb * kPairLd + r * kPairLd + cc];
+            sT[r * kPairLd + cc] = v;
+            if (cc < p.np && row0 + r < p.m) p.T1[(row0 + r) * p.ldt + cc] = v;
+        }
+        pair_half_sync(half);
+        if (!PROJ) {  // stage 2: T2 (n x 16) += W_b^T T1_b
+#pragma unroll
+            for (int ks = 0; ks < (rb >> 2); ++ks) {
+                const int r = 4 * ks + t4;
+                const double y0 = sT[r * kPairLd + g], y1 = sT[r * kPairLd + 8 + g];
+#pragma unroll
+                for (int i = 0; i < kPair2MaxT2; ++i) {
+                    const int mt2 = hw + 8 * i;
+                    if (mt2 < mt2_all) {
+                        const int j = 8 * mt2 + g;
+                        const double a = j < n ? W[r * nld + j] : 0.0;
+                        dmma884(acc2[i][0][0], acc2[i][0][1], a, y0);
+                        dmma884(acc2[i][1][0], acc2[i][1][1], a, y1);
+                    }
+                }
+            }
+        } else if (hw < 2) {
+#pragma unroll
+            for (int ks = 0; ks < (rb >> 2); ++ks) {
+                const int r = 4 * ks + t4;
+                const double a = sL[r * kPairLd + 8 * hw + g];
+                const double y0 = sT[r * kPairLd + g], y1 = sT[r * kPairLd + 8 + g];
+                dmma884(acc2[0][0][0], acc2[0][0][1], a, y0);
+                dmma884(acc2[0][1][0], acc2[0][1][1], a, y1);
+            }
+        }
+        pair_half_sync(half);  // this half's buffers are rewritten by its next trips
+    }
+    // epilogue: half 1's accumulators through shared memory (its own staging area), half 0 adds
+    const int rows2 = PROJ ? kPairNP : n;
+    double* xch = sm + n * kPairLd + per_half;  // half 1's area: rows2 x 16 doubles fit in its staging buffers
+    __syncthreads();
+    if (half == 1) {
+        if (!PROJ) {
+#pragma unroll
+            for (int i = 0; i < kPair2MaxT2; ++i) {
+                const int mt2 = hw + 8 * i;
+                if (mt2 >= mt2_all) break;
+                const int j = 8 * mt2 + g;
+                if (j < n) {
+                    double* o = xch + j * kPairNP + 2 * t4;
+                    o[0] = acc2[i][0][0], o[1] = acc2[i][0][1], o[8] = acc2[i][1][0], o[9] = acc2[i][1][1];
+                }
+            }
+        } else if (hw < 2) {
+            double* o = xch + (8 * hw + g) * kPairNP + 2 * t4;
+            o[0] = acc2[0][0][0], o[1] = acc2[0][0][1], o[8] = acc2[0][1][0], o[9] = acc2[0][1][1];
+        }
+    }
+    __syncthreads();
+    if (half == 0) {
+        double* out = p.part + (size_t)blockIdx.x * rows2 * kPairNP;
+        if (!PROJ) {
+#pragma unroll
+            for (int i = 0; i < kPair2MaxT2; ++i) {
+                const int mt2 = hw + 8 * i;
+                if (mt2 >= mt2_all) break;
+                const int j = 8 * mt2 + g;
+                if (j < n) {
+                    const double* x = xch + j * kPairNP + 2 * t4;
+                    double* o = out + j * kPairNP + 2 * t4;
+                    o[0] = acc2[i][0][0] + x[0];
+                    o[1] = acc2[i][0][1] + x[1];
+                    o[8] = acc2[i][1][0] + x[8];
+                    o[9] = acc2[i][1][1] + x[9];
+                }
+            }
+        } else if (hw < 2) {
+            const double* x = xch + (8 * hw + g) * kPairNP + 2 * t4;
+            double* o = out + (8 * hw + g) * kPairNP + 2 * t4;
+            o[0] = acc2[0][0][0] + x[0];
+            o[1] = acc2[0][0][1] + x[1];
+            o[8] = acc2[0][1][0] + x[8];
+            o[9] = acc2[0][1][1] + x[9];
+        }
+    }
+}
+
 // out[j][c] = sum over CTAs of part[cta][j][c] (c < np, j < rows_out: the projection's partials carry
 // 16 rows, M has np). A block owns 32 consecutive outputs; its 8 warps each sum a contiguous slice of
 // the CTAs (independent, coalesced loads), and warp 0 adds the 8 slice sums in slice order:

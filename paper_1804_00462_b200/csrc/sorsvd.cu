@@ -2322,12 +2322,20 @@ void run_pair(sorsvd_ctx* c, const SorProblem& P, const double* X, double* T1, d
     a.vec = ((uintptr_t)P.A % 16) == 0 && P.lda % 2 == 0;
     a.pred = c->pred;
     a.pred_skip = c->pred_skip;
-    a.rb = pair_smem_bytes(a.n, 32, proj) <= (size_t)227 * 1024 ? 32 : 16;
-    const size_t smem = pair_smem_bytes(a.n, a.rb, proj);
+    // n <= 320: two independent 8-warp halves per CTA on alternate 16-row blocks (skinny_pair2_kernel)
+    const bool two = c->opt_fused_pair == 1 && a.n <= 320 && pair2_smem_bytes(a.n, proj) <= (size_t)227 * 1024;
+    a.rb = two ? kPair2Rb : pair_smem_bytes(a.n, 32, proj) <= (size_t)227 * 1024 ? 32 : 16;
+    const size_t smem = two ? pair2_smem_bytes(a.n, proj) : pair_smem_bytes(a.n, a.rb, proj);
     const int rows2 = proj ? kPairNP : a.n;
-    const int grid = (int)std::min<int64_t>(c->num_sms, cdiv(P.m, a.rb));
+    const int grid = (int)std::min<int64_t>(c->num_sms, cdiv(P.m, two ? 2 * a.rb : a.rb));
     a.part = dbuf(c, proj ? "pair_part_p" : "pair_part", (size_t)grid * rows2 * kPairNP);
-    if (proj) {
+    if (two && proj) {
+        allow_smem(skinny_pair2_kernel<true>);
+        skinny_pair2_kernel<true><<<grid, kPairThreads, smem, s>>>(a);
+    } else if (two) {
+        allow_smem(skinny_pair2_kernel<false>);
+        skinny_pair2_kernel<false><<<grid, kPairThreads, smem, s>>>(a);
+    } else if (proj) {
         allow_smem(skinny_pair_kernel<true>);
         skinny_pair_kernel<true><<<grid, kPairThreads, smem, s>>>(a);
     } else {
@@ -3955,7 +3963,8 @@ int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
                 c->opt_upload_chunk_mb = value;
                 break;
             case SORSVD_OPT_FUSED_PAIR:
-                c->opt_fused_pair = value != 0;
+                if (value < 0 || value > 2) throw Error{SORSVD_ERR_PARAMETER, "parameter: FUSED_PAIR is 0, 1 or 2"};
+                c->opt_fused_pair = (int)value;  // 2: the one-pipeline kernel also for n <= 320 (A/B timing)
                 invalidate_graphs(c);
                 break;
             case SORSVD_OPT_OZAKI_PLANES:
