@@ -664,6 +664,11 @@ def main():
         roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TFLOP/s",
                 "frac": achieved / tensor_peak, "traffic": traffic, "kernel": kname + ", NN pass T1 = A*X",
                 "peak_source": peak_src, "ms_per_launch": ms_pass.value, "flops_per_launch": pass_flops,
+                **({"frac_of_half_measured_bf16": achieved / (0.5 * mp.get("bf16_tflops", 1590.0)),
+                    "frac_of_nominal_tf32_1125": achieved / 1125.0,
+                    "note_peaks": "TF32 dense is half the BF16 rate: also shown against 0.5 x MEASURED_PEAKS bf16_tflops "
+                                  "and against the nominal 1125 TFLOP/s (the live cuBLAS TF32 GEMM reaches ~2/3 of nominal)"}
+                   if tf32 else {}),
                 "tn_pass": {"ms": ms_pass_t.value, "achieved": pass_flops / (ms_pass_t.value * 1e-3) / 1e12},
                 "hbm_gbs_measured": hbm_peak, "hbm_frac": pass_bytes / (ms_pass.value * 1e-3) / 1e9 / hbm_peak}
     else:
