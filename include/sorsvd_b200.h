@@ -123,6 +123,9 @@ void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
                                         cluster and load each A plane once per cluster (TMA multicast, multicast commits);
                                         0 (default) = every CTA loads all 7 planes itself. Same results; measured no
                                         faster on B200 (the pass is bound by shared-memory bandwidth, not by L2 -> SM) */
+#define SORSVD_OPT_OZAKI_OVERLAP 7   /* value: 1 (default) = device-resident calls of the planes engine cut row chunk i + 1 into
+                                        planes on a second stream while the first pass sweeps chunk i; 0 = convert all of A,
+                                        then pass (same bits) */
 #define SORSVD_OPT_UPLOAD_CHUNK_MB 5 /* value: MiB per row chunk of A in host-buffer calls of the Ozaki planes engine (default
                                         1536): A uploads in chunks on a copy stream and each chunk is converted and swept
                                         by the first pass T1 = A Omega while the next one crosses PCIe */

@@ -38,6 +38,8 @@ namespace sorsvd_dev {
 
 constexpr int kOzpStages = 5;     // (A planes + X planes) ring: 5 x 43008 B
 constexpr int kOzpThreads = 384;  // 4 control warps + 8 drain warps
+constexpr int kOzpMaxRegs = 96;   // 384 x 96 registers leave room for one 512-thread block of the conversion kernel
+                                  // on the same SM (the first pass runs while the next row chunk is being cut)
 constexpr size_t kOzpSmem = 1024 + (size_t)kOzpStages * kOzStage + 256;
 
 struct OzpArgs {
@@ -244,7 +246,7 @@ __global__ void ozaki_xdigits_scaled_kernel(const double* __restrict__ X, int64_
 // (each X plane is an operand of up to 7 MMAs) while TMA writes 42 KB -- 154 KB against
 // 128 B/clk x 1088 clk of MMA time.
 template <bool TA, bool MC>
-__global__ void __launch_bounds__(kOzpThreads, 1)
+__global__ void __maxnreg__(kOzpMaxRegs)
     ozaki_planes_gemm_kernel(const __grid_constant__ CUtensorMap tmA, OzpArgs p) {
     if (pred_off(p.pred, p.pred_skip)) return;
     extern __shared__ __align__(1024) uint8_t smraw[];

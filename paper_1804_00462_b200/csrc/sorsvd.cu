@@ -203,6 +203,8 @@ struct sorsvd_emu_group {
 
 struct sorsvd_ctx {
     int opt_jacobi = SORSVD_JACOBI_AUTO;  // sorsvd_ctx_set_option(SORSVD_OPT_JACOBI)
+    int opt_oz_overlap = 1;               // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_OVERLAP): conversion of row chunk i + 1
+                                          // under the first pass over chunk i (device-resident calls)
     int opt_oz_multicast = 0;             // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_MULTICAST): cluster + TMA multicast of the A planes
                                           // (measured: no gain, the pass is shared-memory-bandwidth bound)
     int64_t opt_upload_chunk_mb = 1536;   // sorsvd_ctx_set_option(SORSVD_OPT_UPLOAD_CHUNK_MB): host-buffer calls of the planes engine
@@ -2355,7 +2357,51 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
     const int Np = P.Np, ell = P.ell;
     record_stage(c, timing, 0);
     OzScales oz;
-    if (P.ozaki) oz = P.pre_first ? oz_planes_of(c, P) : oz_prepare_a(c, P, s);
+    bool first_done = P.pre_first;  // T1 = A Omega of pass 0 already produced (with the planes)
+    if (P.ozaki && P.pre_first) {
+        oz = oz_planes_of(c, P);
+    } else if (P.ozaki && P.oz_pm == P.m && c->opt_oz_overlap && !P.single_pass) {
+        // Conversion and first pass interleaved by row chunks: chunk i + 1 is cut into planes on the side
+        // stream (HBM-bound, one 512-thread block fits beside a pass CTA: the pass kernel is capped at 96
+        // registers for this) while the first pass T1 = A Omega sweeps chunk i (tensor-bound). Rows are
+        // independent, so the bits are those of convert-all-then-pass.
+        oz = oz_planes_of(c, P);
+        const OzX ox = oz_cut_x(c, P, false, oz, b.T2, s);
+        const int NC = (int)cdiv(Np, kOzBN);
+        int g = c->num_sms, h = NC;
+        while (h) {
+            const int t = g % h;
+            g = h;
+            h = t;
+        }
+        const int64_t unit_rows = (int64_t)(c->num_sms / g) * kOzBM;  // whole waves of 128-row tiles
+        const int64_t units = cdiv(P.m, unit_rows);
+        const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(10, units));
+        const int64_t rows_per = cdiv(units, nch) * unit_rows;
+        const int nchunks = (int)cdiv(P.m, rows_per);
+        while ((int)c->up_ev.size() < nchunks) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->up_ev.push_back(e);
+        }
+        CK(cudaEventRecord(c->ev_fork, s));
+        CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        oz_convert_rows(c, P, oz, 0, std::min(rows_per, P.m), c->side);
+        CK(cudaEventRecord(c->up_ev[0], c->side));
+        for (int i = 0; i < nchunks; ++i) {
+            const int64_t r0 = (int64_t)i * rows_per, rows = std::min(rows_per, P.m - r0);
+            if (i + 1 < nchunks) {
+                const int64_t r1 = r0 + rows_per;
+                oz_convert_rows(c, P, oz, r1, std::min(rows_per, P.m - r1), c->side);
+                CK(cudaEventRecord(c->up_ev[(size_t)i + 1], c->side));
+            }
+            CK(cudaStreamWaitEvent(s, c->up_ev[(size_t)i], 0));
+            oz_launch_planes(c, P, false, oz, ox, b.T1 + r0 * Np, r0, rows, s);
+        }
+        first_done = true;
+    } else if (P.ozaki) {
+        oz = oz_prepare_a(c, P, s);
+    }
     for (int i = 0; i <= P.q; ++i) {
         if (P.single_pass && i == P.q) {  // t2_pre: the row sketch entering the last iteration (sketch.hpp:94)
             if (P.tf32)
@@ -2370,7 +2416,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
             continue;
         }
         if (P.ozaki) {  // FP64 passes as int8 slice products (ozaki_i8.cuh)
-            if (!(P.pre_first && i == 0)) run_ozaki(c, P, false, oz, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
+            if (!(first_done && i == 0)) run_ozaki(c, P, false, oz, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
             tn_pass_reduced(c, P, b.T1, b.T2, s, &oz);  // T2 = A^T T1 (sketch.hpp:96), summed over ranks
             continue;
         }
@@ -3953,6 +3999,10 @@ int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
                     throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown Jacobi variant"};
                 c->opt_jacobi = (int)value;
                 invalidate_graphs(c);  // captured calls baked the previous variant in
+                break;
+            case SORSVD_OPT_OZAKI_OVERLAP:
+                c->opt_oz_overlap = value != 0;
+                invalidate_graphs(c);
                 break;
             case SORSVD_OPT_OZAKI_MULTICAST:
                 c->opt_oz_multicast = value != 0;
