@@ -179,19 +179,36 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) ozaki_rowplanes_kerne
     }
 }
 
-// max_k |X_kn 2^(kexp_k)| per column (the TN right operand with A's row scales folded in).
-__global__ void ozaki_colmax_scaled_kernel(const double* __restrict__ X, int64_t ldx, int64_t K, int N,
-                                           const int* __restrict__ kexp, unsigned long long* __restrict__ xmax) {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= N) return;
-    const int64_t k0 = (int64_t)blockIdx.y * 256, k1 = K < k0 + 256 ? K : k0 + 256;
+// max_k |X_kn 2^(kexp_k)| per column (the TN right operand with A's row scales folded in); the
+// block shape of ozaki_colmax_kernel.
+__global__ void __launch_bounds__(256) ozaki_colmax_scaled_kernel(const double* __restrict__ X, int64_t ldx, int64_t K,
+                                                                  int N, const int* __restrict__ kexp,
+                                                                  unsigned long long* __restrict__ xmax) {
+    __shared__ double red[8][33];
+    const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+    const int n = blockIdx.x * 32 + cx;
     double mv = 0.0;
-    for (int64_t k = k0; k < k1; ++k) {
-        const int e = kexp[k];
-        const double v = e == kOzNonFinite ? __longlong_as_double(0x7ff8000000000000ll) : fabs(scalbn(X[k * ldx + n], e));
-        mv = (v > mv || v != v) ? v : mv;
+    if (n < N) {
+        for (int64_t k0 = (int64_t)blockIdx.y * kOzCmRows; k0 < K; k0 += (int64_t)gridDim.y * kOzCmRows) {
+#pragma unroll
+            for (int i = 0; i < kOzCmRows / 8; ++i) {
+                const int64_t k = k0 + ry + 8 * i;
+                if (k < K) {
+                    const int e = kexp[k];
+                    const double v =
+                        e == kOzNonFinite ? __longlong_as_double(0x7ff8000000000000ll) : fabs(scalbn(X[k * ldx + n], e));
+                    mv = oz_nanmax(mv, v);
+                }
+            }
+        }
     }
-    oz_atomic_max(xmax + n, mv);
+    red[ry][cx] = mv;
+    __syncthreads();
+    if (ry == 0 && n < N) {
+#pragma unroll
+        for (int q = 1; q < 8; ++q) mv = oz_nanmax(mv, red[q][cx]);
+        oz_atomic_max(xmax + n, mv);
+    }
 }
 
 // ozaki_xdigits_kernel with the per-K-row factor 2^(kexp_k) applied first.

@@ -2056,7 +2056,7 @@ OzX oz_cut_x(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, co
     x.xexp = reinterpret_cast<int*>(dbuf(c, "oz_xexp", (size_t)(Np + 1) / 2));
     x.Xd = reinterpret_cast<int8_t*>(dbuf(c, ta ? "oz_xd_tn" : "oz_xd_nn", (size_t)(KT * NC * kOzXStep + 7) / 8));
     CK(cudaMemsetAsync(xmax, 0, (size_t)Np * 8, s));
-    const dim3 cgrid((unsigned)cdiv(Np, 256), (unsigned)cdiv(K, 256));
+    const dim3 cgrid((unsigned)cdiv(Np, 32), (unsigned)std::min<int64_t>(cdiv(K, kOzCmRows), 32768));
     const int64_t items = KT * 2 * (int64_t)NC * kOzBN;
     const unsigned xblocks = (unsigned)std::min<int64_t>(cdiv(items, 256), (int64_t)c->num_sms * 16);
     if (planes && ta) {  // the planes are row-scaled: A's row scales ride on the right operand
@@ -2762,14 +2762,14 @@ void validate(const sorsvd_desc* d) {
 // FP64 passes on the int8 tensor cores by default when a pass is big enough to amortise the
 // per-call conversion of A and the per-pass digit cutting of the skinny operand. Measured call
 // times, Ozaki / DMMA (tools/oz_threshold.py, profiles/r02_oz_threshold.jsonl): with the per-call
-// digit planes 1.11 at m n ell = 2^30.6 (C2), 0.96 at 2^31.8, 0.76-0.82 from 2^32.9 up, 0.50 on C3;
-// converting inside every pass (planes do not fit) pays from ~2^36 (C5 1.65x faster). So: auto =
-// m n ell >= 2^32 when the planes fit, >= 2^36 otherwise, and ell >= 32 (oz_auto_keep below).
+// digit planes 1.01 at m n ell = 2^30.6 (C2's shape), 0.89 at 2^31.8, 0.70-0.81 from 2^32.9 up, 0.49 on
+// C3; converting inside every pass (planes do not fit) pays from ~2^36 (C5 1.65x faster). So: auto =
+// m n ell >= 2^31.5 when the planes fit, >= 2^36 otherwise, and ell >= 32 (oz_auto_keep below).
 // SORSVD_FLAG_OZAKI / SORSVD_FLAG_DMMA force either.
 bool ozaki_wanted(uint32_t flags, int64_t m, int64_t n, int ell) {
     if (flags & SORSVD_FLAG_DMMA) return false;
     if (flags & SORSVD_FLAG_OZAKI) return true;
-    return (double)m * (double)n * (double)ell >= 4294967296.0 /* 2^32 */ && ell >= 32;
+    return (double)m * (double)n * (double)ell >= 3037000500.0 /* 2^31.5 */ && ell >= 32;
 }
 // The automatic choice stands without the planes only from 2^36 up.
 bool oz_auto_keep(uint32_t flags, int64_t m, int64_t n, int ell, bool planes) {
