@@ -66,7 +66,7 @@ typedef enum sorsvd_flop_variant {
                                          (Ozaki scheme: 7 signed byte digits of a 55-bit fixed point, the 34
                                          products with digit levels >= 5): error at or below the reference
                                          dgemm's own sum rounding. Default for large passes: ell >= 32 and
-                                         m n ell >= 2^31.5 when the call's int8 digit planes of A fit in HBM
+                                         m n ell >= 2^30.5 when the call's int8 digit planes of A fit in HBM
                                          (SORSVD_OPT_OZAKI_PLANES), >= 2^36 otherwise; this flag forces it */
 #define SORSVD_FLAG_DMMA 0x40u        /* force the FP64 DMMA passes (the default below that size) */
 

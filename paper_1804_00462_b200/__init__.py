@@ -377,7 +377,7 @@ def sor_svd_power(a, k: int, cfg: SketchConfig, omega=None, ctx: Optional[Contex
     the core SVD are FP64 and results are FP64 either way.
     fp64_mode: how the FP64 passes are computed: "dmma" (the FP64 tensor pipe),
     "ozaki" (exact int8 slice products on the tcgen05 tensor cores, ozaki_i8.cuh),
-    or "auto" (default: ozaki for large passes, ell >= 32 and m*n*ell >= 2^31.5 with the
+    or "auto" (default: ozaki for large passes, ell >= 32 and m*n*ell >= 2^30.5 with the
     per-call digit planes of A, >= 2^36 without).
     omega: optional (n, ell) test matrix; default gaussian_matrix(n, ell, seed)
     exactly as the reference draws it (sketch.hpp:90)."""

@@ -2015,12 +2015,12 @@ void launch_ozaki_t(const OzArgs& a0, unsigned grid, cudaStream_t s) {
 // Split-K for the planes engine: the number of K splits that minimises the modelled pass
 // time on `sms` SMs (waves x (steps per split + fixed cost per CTA) + the partial sum).
 int oz_pick_splits(int64_t tiles, int KT, int64_t out_bytes, int sms) {
-    const double t_step = 0.62, t_fixed = 8.0;  // us: one 32-deep K step (34 digit MMAs); CTA prologue + drain
+    const double t_step = 0.62, t_fixed = 12.0;  // us: one 32-deep K step (34 digit MMAs); CTA prologue + drain
     int best = 1;
     double best_cost = 1e300;
     for (int S = 1; S <= 16; ++S) {
         const int per = (int)cdiv(KT, S);
-        if (S > 1 && per < 96) break;
+        if (S > 1 && per < 24) break;
         const int Se = (int)cdiv(KT, per);
         const double waves = (double)cdiv(tiles * Se, sms);
         double cost = waves * (per * t_step + t_fixed);
@@ -2762,14 +2762,14 @@ void validate(const sorsvd_desc* d) {
 // FP64 passes on the int8 tensor cores by default when a pass is big enough to amortise the
 // per-call conversion of A and the per-pass digit cutting of the skinny operand. Measured call
 // times, Ozaki / DMMA (tools/oz_threshold.py, profiles/r02_oz_threshold.jsonl): with the per-call
-// digit planes 1.01 at m n ell = 2^30.6 (C2's shape), 0.89 at 2^31.8, 0.70-0.81 from 2^32.9 up, 0.49 on
+// digit planes 0.93 at m n ell = 2^30.6 (C2's shape), 0.86 at 2^31.8, 0.70-0.81 from 2^32.9 up, 0.49 on
 // C3; converting inside every pass (planes do not fit) pays from ~2^36 (C5 1.65x faster). So: auto =
-// m n ell >= 2^31.5 when the planes fit, >= 2^36 otherwise, and ell >= 32 (oz_auto_keep below).
+// m n ell >= 2^30.5 when the planes fit, >= 2^36 otherwise, and ell >= 32 (oz_auto_keep below).
 // SORSVD_FLAG_OZAKI / SORSVD_FLAG_DMMA force either.
 bool ozaki_wanted(uint32_t flags, int64_t m, int64_t n, int ell) {
     if (flags & SORSVD_FLAG_DMMA) return false;
     if (flags & SORSVD_FLAG_OZAKI) return true;
-    return (double)m * (double)n * (double)ell >= 3037000500.0 /* 2^31.5 */ && ell >= 32;
+    return (double)m * (double)n * (double)ell >= 1518500250.0 /* 2^30.5 */ && ell >= 32;
 }
 // The automatic choice stands without the planes only from 2^36 up.
 bool oz_auto_keep(uint32_t flags, int64_t m, int64_t n, int ell, bool planes) {
