@@ -126,6 +126,10 @@ void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
 #define SORSVD_OPT_OZAKI_OVERLAP 7   /* value: 1 (default) = device-resident calls of the planes engine cut row chunk i + 1 into
                                         planes on a second stream while the first pass sweeps chunk i; 0 = convert all of A,
                                         then pass (same bits) */
+#define SORSVD_OPT_UPLOAD_TN 8       /* value: 1 (default) = the pipelined host upload also runs the first A^T T1 pass chunk by chunk
+                                        (one K range per row chunk, added in chunk order): same accuracy, last bits differ
+                                        from the device-resident call; 0 = only the first pass rides under the upload and
+                                        the host call returns the device call's bits */
 #define SORSVD_OPT_UPLOAD_CHUNK_MB 5 /* value: MiB per row chunk of A in host-buffer calls of the Ozaki planes engine (default
                                         1536): A uploads in chunks on a copy stream and each chunk is converted and swept
                                         by the first pass T1 = A Omega while the next one crosses PCIe */

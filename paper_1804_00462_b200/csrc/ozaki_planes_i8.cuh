@@ -54,6 +54,8 @@ struct OzpArgs {
     double* C;             // M x ldc (split s writes C + s * c_split_stride)
     int64_t ldc, c_split_stride;
     int kt_split;          // K steps per split (grid.y splits)
+    int kt0;               // first K step of this launch inside the planes (a K range of the TN pass: rows [32 kt0, ..))
+    int acc0;              // 1: add to C from the first drain on (an earlier launch wrote the preceding K range)
     int dbg;               // timing experiments (tools/oz_pass.py): 1 = no MMAs, 2 = no A-plane TMA, 4 = only 20 of the 34 products
     const int* pred;
     int pred_skip;
@@ -320,10 +322,10 @@ __global__ void __maxnreg__(kOzpMaxRegs)
                 } else if (MC) {  // this rank's planes, multicast to the whole cluster
                     for (int t = (int)crank; t < kOzSlices; t += (int)csize) {
                         if (!TA) tma_load_3d_mc(dst + t * kOzAPlane, &tmA, full(s), kt * kOzBK, p.mn0 + (int)m0, t, cmask);
-                        else tma_load_3d_mc(dst + t * kOzAPlane, &tmA, full(s), p.mn0 + (int)m0, kt * kOzBK, t, cmask);
+                        else tma_load_3d_mc(dst + t * kOzAPlane, &tmA, full(s), p.mn0 + (int)m0, (p.kt0 + kt) * kOzBK, t, cmask);
                     }
                 } else if (!TA) tma_load_3d(dst, &tmA, full(s), kt * kOzBK, p.mn0 + (int)m0, 0);
-                else tma_load_3d(dst, &tmA, full(s), p.mn0 + (int)m0, kt * kOzBK, 0);
+                else tma_load_3d(dst, &tmA, full(s), p.mn0 + (int)m0, (p.kt0 + kt) * kOzBK, 0);
                 oz_bulk_g2s(dst + kOzSlices * kOzAPlane, xsrc + (size_t)kt * p.NC * kOzXStep, (uint32_t)kOzXStep, full(s));
             }
         }
@@ -446,7 +448,7 @@ __global__ void __maxnreg__(kOzpMaxRegs)
                             double out;
                             if (e_row == kOzNonFinite || f == kOzNonFinite) out = __longlong_as_double(0x7ff8000000000000ll);
                             else out = scalbn(part[h][c], e_row + f);
-                            crow[col] = chunk == 0 ? out : crow[col] + out;
+                            crow[col] = (chunk == 0 && !p.acc0) ? out : crow[col] + out;
                         }
                     }
             }
@@ -458,6 +460,18 @@ __global__ void __maxnreg__(kOzpMaxRegs)
     if (warp == 2) {
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    }
+}
+
+// out = (acc ? out : 0) + sum of the S split partials, in split order (a K range of the TN pass added
+// to the ranges before it).
+__global__ void oz_reduce_acc_kernel(const double* __restrict__ ws, int64_t count, int S, int64_t stride,
+                                     double* __restrict__ out, int acc, const int* pred, int pred_skip) {
+    if (pred_off(pred, pred_skip)) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = acc ? out[i] : 0.0;
+        for (int sidx = 0; sidx < S; ++sidx) v += ws[(int64_t)sidx * stride + i];
+        out[i] = v;
     }
 }
 

@@ -207,6 +207,9 @@ struct sorsvd_ctx {
                                           // under the first pass over chunk i (device-resident calls)
     int opt_oz_multicast = 0;             // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_MULTICAST): cluster + TMA multicast of the A planes
                                           // (measured: no gain, the pass is shared-memory-bandwidth bound)
+    int opt_upload_tn = 1;                // sorsvd_ctx_set_option(SORSVD_OPT_UPLOAD_TN): host-buffer planes calls also run the
+                                          // first A^T pass chunk by chunk under the upload (results differ from the
+                                          // device-resident call in the last bits: K ranges summed in chunk order)
     int64_t opt_upload_chunk_mb = 1536;   // sorsvd_ctx_set_option(SORSVD_OPT_UPLOAD_CHUNK_MB): host-buffer calls of the planes engine
     int opt_fused_pair = 1;               // sorsvd_ctx_set_option(SORSVD_OPT_FUSED_PAIR): 0 = separate NN / TN GEMM passes
     int64_t opt_oz_planes = 1;                // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_PLANES): 0 = convert inside every pass
@@ -1717,6 +1720,7 @@ struct SorProblem {
     bool ozaki;        // SORSVD_FLAG_OZAKI: FP64 passes as int8 slice products on the tcgen05 tensor cores
     bool oz_planes = false;  // ... from digit planes of A cut once per call (ozaki_planes_i8.cuh), memory permitting
     int64_t oz_pm = 0;       // rows [0, oz_pm) of A have planes (== m: all; less: the rest is converted in the passes)
+    bool pre_tn = false;     // ... and the first T2 = A^T T1 too (chunk by chunk, K ranges added in order)
     bool pre_first = false;  // host-buffer call: planes and the first T1 = A Omega were produced chunk by chunk
                              // while A was uploading (sor_device's pipelined upload)
     int method = SORSVD_SOR_POWER;  // SORSVD_RSVD / SORSVD_TSR: the baselines of sketch.hpp:124-149
@@ -2051,9 +2055,9 @@ OzX oz_cut_x(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, co
     const int64_t K = ta ? P.m : P.n;
     const int64_t KT = cdiv(K, kOzBK);
     const bool planes = oz.planes != nullptr;
-    auto* xmax = reinterpret_cast<unsigned long long*>(dbuf(c, "oz_xmax", (size_t)Np));
+    auto* xmax = reinterpret_cast<unsigned long long*>(dbuf(c, ta ? "oz_xmax_tn" : "oz_xmax_nn", (size_t)Np));
     OzX x;
-    x.xexp = reinterpret_cast<int*>(dbuf(c, "oz_xexp", (size_t)(Np + 1) / 2));
+    x.xexp = reinterpret_cast<int*>(dbuf(c, ta ? "oz_xexp_tn" : "oz_xexp_nn", (size_t)(Np + 1) / 2));
     x.Xd = reinterpret_cast<int8_t*>(dbuf(c, ta ? "oz_xd_tn" : "oz_xd_nn", (size_t)(KT * NC * kOzXStep + 7) / 8));
     CK(cudaMemsetAsync(xmax, 0, (size_t)Np * 8, s));
     const dim3 cgrid((unsigned)cdiv(Np, 32), (unsigned)std::min<int64_t>(cdiv(K, kOzCmRows), 32768));
@@ -2079,8 +2083,9 @@ OzX oz_cut_x(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, co
 
 // One launch of the planes engine over left rows [l0, l0 + M) of the planes (NN: rows of A; TN:
 // columns of A): C (M x Np, the caller's pointer to the block's first row) = op(A)[l0 ..] X.
+// TN only: k0 = first row of the K range this launch contracts over (P.m = its length), acc = add to C.
 void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const OzX& x, double* C,
-                      int64_t l0, int64_t M, cudaStream_t s, int dbg = 0) {
+                      int64_t l0, int64_t M, cudaStream_t s, int dbg = 0, int64_t k0 = 0, bool acc = false) {
     const int Np = P.Np;
     const int NC = (int)cdiv(Np, kOzBN);
     const int64_t K = ta ? P.m : P.n;
@@ -2089,6 +2094,8 @@ void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScale
     a.M = M;
     a.K = K;
     a.mn0 = (int)l0;
+    a.kt0 = (int)(k0 / kOzBK);
+    a.acc0 = (acc && true) ? 1 : 0;
     a.lexp = ta ? nullptr : oz.row_e + l0;
     a.Xd = x.Xd;
     a.xexp = x.xexp;
@@ -2104,6 +2111,7 @@ void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScale
     a.c_split_stride = M * Np;
     double* ws = S > 1 ? dbuf(c, "oz_split", (size_t)S * M * Np) : nullptr;
     a.C = S > 1 ? ws : C;
+    if (S > 1) a.acc0 = 0;  // the partials start from zero; the reduction adds them to C
     // NC column-chunk CTAs of a row tile as one cluster sharing the A planes by TMA multicast
     const bool mc = c->opt_oz_multicast && NC >= 2 && NC <= 8;
     CUtensorMap map{};
@@ -2142,7 +2150,11 @@ void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScale
         ozaki_planes_gemm_kernel<false, false><<<grid, kOzpThreads, kOzpSmem, s>>>(map, a);
     }
     check_launch(c);
-    if (S > 1) {
+    if (S > 1 && acc) {
+        const int blocks = (int)std::min<int64_t>(cdiv(M * Np, 256), (int64_t)c->num_sms * 8);
+        oz_reduce_acc_kernel<<<blocks, 256, 0, s>>>(ws, M * Np, S, M * Np, C, 1, c->pred, c->pred_skip);
+        check_launch(c);
+    } else if (S > 1) {
         const int64_t count2 = M * Np / 2;
         const int blocks = (int)std::min<int64_t>(cdiv(count2, 256), (int64_t)c->num_sms * 8);
         reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, count2, S, M * Np, C, c->pred, c->pred_skip);
@@ -2417,7 +2429,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
         }
         if (P.ozaki) {  // FP64 passes as int8 slice products (ozaki_i8.cuh)
             if (!(first_done && i == 0)) run_ozaki(c, P, false, oz, b.T2, b.T1, s);  // T1 = A T2   (sketch.hpp:95)
-            tn_pass_reduced(c, P, b.T1, b.T2, s, &oz);  // T2 = A^T T1 (sketch.hpp:96), summed over ranks
+            if (!(P.pre_tn && i == 0)) tn_pass_reduced(c, P, b.T1, b.T2, s, &oz);  // T2 = A^T T1 (sketch.hpp:96), summed over ranks
             continue;
         }
         if (pair_ok(c, P)) {  // T1 = A T2 and T2 = A^T T1 in one sweep over A (skinny_pair_f64.cuh)
@@ -2929,14 +2941,30 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         if (pipe) {
             const OzScales oz = oz_planes_of(c, P);
             const OzX ox = oz_cut_x(c, P, false, oz, b.T2, c->stream);  // Omega's digit planes: once for all chunks
+            // the first T2 = A^T T1 as well, one K range per chunk (its rows of T1 exist as soon as the chunk's
+            // first pass is done), into a second buffer (T2 still holds Omega for the later chunks' first pass)
+            const bool tn_too = c->opt_upload_tn && P.q >= 1 && !P.single_pass;
+            double* T2n = tn_too ? dbuf(c, "T2_next", (size_t)P.n * P.Np) : nullptr;
             for (int i = 0; i < up->nchunks; ++i) {
                 const int64_t r0 = (int64_t)i * up->rows_per_chunk, rows = std::min(up->rows_per_chunk, P.m - r0);
                 CK(cudaStreamWaitEvent(c->stream, c->up_ev[(size_t)i], 0));
                 oz_convert_rows(c, P, oz, r0, rows, c->stream);
                 oz_launch_planes(c, P, false, oz, ox, b.T1 + r0 * P.Np, r0, rows, c->stream);
+                if (tn_too) {
+                    SorProblem Qc = P;
+                    Qc.m = rows;
+                    OzScales ozc = oz;
+                    ozc.row_e = oz.row_e + r0;  // the chunk's rows' scales ride on its rows of T1
+                    const OzX xt = oz_cut_x(c, Qc, true, ozc, b.T1 + r0 * P.Np, c->stream);
+                    oz_launch_planes(c, Qc, true, oz, xt, T2n, 0, P.n, c->stream, 0, r0, i > 0);
+                }
             }
             SorProblem Q = P;
             Q.pre_first = true;
+            if (tn_too) {
+                CK(cudaMemcpyAsync(b.T2, T2n, (size_t)P.n * P.Np * 8, cudaMemcpyDeviceToDevice, c->stream));
+                Q.pre_tn = true;
+            }
             enqueue_sor(c, Q, b, p1, p2, pg, timing);
             return;
         }
@@ -4007,6 +4035,9 @@ int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
             case SORSVD_OPT_OZAKI_MULTICAST:
                 c->opt_oz_multicast = value != 0;
                 invalidate_graphs(c);
+                break;
+            case SORSVD_OPT_UPLOAD_TN:
+                c->opt_upload_tn = value != 0;
                 break;
             case SORSVD_OPT_UPLOAD_CHUNK_MB:
                 if (value < 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: upload chunk must be >= 1 MiB"};

@@ -209,10 +209,12 @@ def test_auto_mode_selection(P):
 
 
 @pytest.mark.parametrize("f32", [False, True])
-def test_host_call_pipelined_upload_same_bits(P, f32):
-    """Host-buffer calls of the planes engine upload A in row chunks and convert / sweep each chunk as it lands
-    (first pass T1 = A Omega by row blocks): the result equals the device-resident call bit for bit, for several
-    chunk sizes (one chunk, ragged last chunk, many chunks)."""
+def test_host_call_pipelined_upload(P, f32):
+    """Host-buffer calls of the planes engine upload A in row chunks and convert / sweep each chunk as it lands.
+    With only the first pass T1 = A Omega under the upload (OPT_UPLOAD_TN = 0; rows are independent) the result
+    equals the device-resident call bit for bit, for several chunk sizes (one chunk, ragged last chunk, many
+    chunks). With the first A^T T1 pass chunked too (default; its K ranges are added in chunk order) the call is
+    repeatable bit for bit and agrees with the device call to rounding."""
     import torch
     A = O.gen_lowrank_decay(30000, 600, 40, lambda j: 2.0 ** (-j / 5), 1e-3, 17)
     if f32:
@@ -220,16 +222,31 @@ def test_host_call_pipelined_upload_same_bits(P, f32):
     cfg = P.SketchConfig(40, 1, 5)
     dev = P.sor_svd_power(torch.from_numpy(A).cuda(), 32, cfg, fp64_mode="ozaki")
     assert dev.stats["oz_planes"] == 1
+    ds, du, dv = dev.sigma.cpu().numpy(), dev.u.cpu().numpy(), dev.v.cpu().numpy()
     for mb in (1536, 24, 2):
         ctx = P.Context(0)
         ctx.set_option(P.Context.OPT_UPLOAD_CHUNK_MB, mb)
+        ctx.set_option(P.Context.OPT_UPLOAD_TN, 0)
         host = P.sor_svd_power(A, 32, cfg, fp64_mode="ozaki", ctx=ctx)
         assert host.stats["oz_planes"] == 1
-        assert np.array_equal(np.asarray(host.sigma), dev.sigma.cpu().numpy())
-        assert np.array_equal(np.asarray(host.u), dev.u.cpu().numpy())
-        assert np.array_equal(np.asarray(host.v), dev.v.cpu().numpy())
+        assert np.array_equal(np.asarray(host.sigma), ds)
+        assert np.array_equal(np.asarray(host.u), du)
+        assert np.array_equal(np.asarray(host.v), dv)
         host2 = P.sor_svd_power(A, 32, cfg, fp64_mode="ozaki", ctx=ctx)   # a second call on the same context
         assert np.array_equal(np.asarray(host2.u), np.asarray(host.u))
+        ctx.set_option(P.Context.OPT_UPLOAD_TN, 1)
+        h1 = P.sor_svd_power(A, 32, cfg, fp64_mode="ozaki", ctx=ctx)
+        h2 = P.sor_svd_power(A, 32, cfg, fp64_mode="ozaki", ctx=ctx)
+        assert np.array_equal(np.asarray(h1.u), np.asarray(h2.u)) and np.array_equal(np.asarray(h1.sigma), np.asarray(h2.sigma))
+        assert O.sigma_rel_err(np.asarray(h1.sigma), ds).max() <= 1e-12
+        assert O.lowrank_rel_diff(np.asarray(h1.u), np.asarray(h1.sigma), np.asarray(h1.v), du, ds, dv) <= 1e-11
+    # q = 0 (no A^T pass before the QR) and single_pass keep the first-pass-only pipeline
+    ctx = P.Context(0)
+    ctx.set_option(P.Context.OPT_UPLOAD_CHUNK_MB, 8)
+    for c0 in (P.SketchConfig(40, 0, 5), P.SketchConfig(40, 1, 5, single_pass=True)):
+        d0 = P.sor_svd_power(torch.from_numpy(A).cuda(), 32, c0, fp64_mode="ozaki")
+        h0 = P.sor_svd_power(A, 32, c0, fp64_mode="ozaki", ctx=ctx)
+        assert np.array_equal(np.asarray(h0.sigma), d0.sigma.cpu().numpy())
 
 
 @pytest.mark.parametrize("m,n,ell,ta", [(3000, 2000, 256, 0), (2000, 3000, 256, 1), (1500, 900, 136, 0), (70000, 600, 128, 1),
