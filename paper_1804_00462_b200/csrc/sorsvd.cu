@@ -3896,7 +3896,7 @@ void ctx_init(sorsvd_ctx* c, int device) {
 // ================================================================ C ABI ====
 extern "C" {
 
-const char* sorsvd_version(void) { return "sorsvd-b200 0.1 (sm_100a, fp64 DMMA)"; }
+const char* sorsvd_version(void) { return "sorsvd-b200 0.2 (sm_100a: tcgen05 int8 digit-plane passes, FP64 DMMA, TF32)"; }
 
 int sorsvd_ctx_create(int device, sorsvd_ctx** out) {
     if (!out) return SORSVD_ERR_PARAMETER;
