@@ -32,12 +32,22 @@
 //   * split-K over grid.y for short grids (TN: n/128 x 4 tiles is 4.2 waves on
 //     148 SMs): partial tiles summed in split order by reduce_splits_kernel.
 #pragma once
+#include <type_traits>
+
 #include "ozaki_i8.cuh"
 
 namespace sorsvd_dev {
 
 constexpr int kOzpStages = 5;     // (A planes + X planes) ring: 5 x 43008 B
 constexpr int kOzpThreads = 384;  // 4 control warps + 8 drain warps
+#ifndef OZP_COLLECTOR
+#define OZP_COLLECTOR 1
+#endif
+constexpr bool kOzpCollector = OZP_COLLECTOR != 0;  // A-collector reuse between the two MMAs of planes 3-6
+#ifndef OZP_ISSUERS
+#define OZP_ISSUERS 2
+#endif
+constexpr int kOzpIssuers = OZP_ISSUERS;  // MMA-issuing threads per CTA (1, 2 or 3; measured best: 2)
 constexpr int kOzpMaxRegs = 96;   // 384 x 96 registers leave room for one 512-thread block of the conversion kernel
                                   // on the same SM (the first pass runs while the next row chunk is being cut)
 constexpr size_t kOzpSmem = 1024 + (size_t)kOzpStages * kOzStage + 256;
@@ -56,7 +66,7 @@ struct OzpArgs {
     int kt_split;          // K steps per split (grid.y splits)
     int kt0;               // first K step of this launch inside the planes (a K range of the TN pass: rows [32 kt0, ..))
     int acc0;              // 1: add to C from the first drain on (an earlier launch wrote the preceding K range)
-    int dbg;               // timing experiments (tools/oz_pass.py): 1 = no MMAs, 2 = no A-plane TMA, 4 = only 20 of the 34 products
+    int dbg;               // timing experiments (tools/oz_pass.py): 1 = no MMAs, 2 = no A-plane TMA
     const int* pred;
     int pred_skip;
 };
@@ -291,9 +301,9 @@ __global__ void __maxnreg__(kOzpMaxRegs)
     if (threadIdx.x == 0) {
         for (int s = 0; s < kOzpStages; ++s) {
             mbar_init(full(s), 1);
-            mbar_init(empty(s), csize);  // one commit per CTA of the cluster
+            mbar_init(empty(s), kOzpIssuers * csize);  // one commit per issuing thread per CTA of the cluster
         }
-        mbar_init(drain_full, 1);
+        mbar_init(drain_full, kOzpIssuers);
         mbar_init(drain_empty, 8);  // one arrive per drain warp
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
@@ -329,8 +339,13 @@ __global__ void __maxnreg__(kOzpMaxRegs)
                 oz_bulk_g2s(dst + kOzSlices * kOzAPlane, xsrc + (size_t)kt * p.NC * kOzXStep, (uint32_t)kOzXStep, full(s));
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer ----
+    } else if (warp >= 1 && warp <= kOzpIssuers) {
+        // ---- MMA issuers: kOzpIssuers threads (warps 1.., one lane each) share the 11 MMAs of a K step by A
+        // plane (two: planes 6-4 / 3-0). The int32 levels are exact, so the order in which the streams of
+        // MMAs land does not matter; one thread alone was close to issue-bound (a run-time branch in its
+        // loop cost 16% of the pass; two threads: 24.8 -> 23.3 ms on C3; three: no better).
+        const int who = warp - 1;
+        if (lane == 0) {
             for (int i = 0; i < KT; ++i) {
                 const int s = i % kOzpStages;
                 const uint32_t ph = (uint32_t)(i / kOzpStages) & 1u;
@@ -340,29 +355,72 @@ __global__ void __maxnreg__(kOzpMaxRegs)
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 const uint32_t a_s = base + s * kOzStage;
                 const uint32_t x_s = a_s + kOzSlices * kOzAPlane;
-                auto mma = [&](int t, int u0, int cnt) {
+                // COLL: 0 = plain; 1 = keep this A plane in the MMA's A collector (collector::a::fill); 2 = the
+                // next MMA on the same plane takes it from there (collector::a::lastuse) instead of reading
+                // its 4 KB from shared memory again (planes 3-6 are operands of two MMAs: N <= 256 each).
+                // Compile-time: a run-time selector in this one-thread issue loop cost 16% of the pass.
+                auto mma = [&](int t, int u0, int cnt, auto coll_tag) {
+                    constexpr int COLL = decltype(coll_tag)::value;
                     // NN: K-major, 32-byte swizzle atoms (8 rows x 32 B), 8-row groups 256 B apart.
                     // TN: MN-major, 128-byte swizzle atoms (8 K rows x 128 columns), K groups 1024 B apart.
                     const uint64_t da = TA ? umma_desc(a_s + t * kOzAPlane, 4096, 1024, 2)
                                            : umma_desc(a_s + t * kOzAPlane, 0, 256, 6);
                     const uint64_t db = umma_desc(x_s + u0 * 1024, kOzXStep / 2, 128, 0);
                     const uint32_t idesc = i8_idesc(kOzBM, kOzBN * cnt) | (TA ? (1u << 15) : 0u);
-                    asm volatile(
-                        "{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\n"
-                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
-                            tmem + (uint32_t)((t + u0 - kOzLevel0) * kOzBN)),
-                        "l"(da), "l"(db), "r"(idesc));
+                    const uint32_t d = tmem + (uint32_t)((t + u0 - kOzLevel0) * kOzBN);
+                    if constexpr (COLL == 1)
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                            "l"(da), "l"(db), "r"(idesc));
+                    else if constexpr (COLL == 2)
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                            "l"(da), "l"(db), "r"(idesc));
+                    else
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                            "l"(da), "l"(db), "r"(idesc));
                 };
-                if (p.dbg & 4) {  // experiment: only the five 4-plane MMAs (20 of the 34 products)
-                    mma(6, 0, 4); mma(5, 0, 4); mma(4, 1, 4); mma(3, 2, 4); mma(2, 3, 4);
-                } else if (!(p.dbg & 1)) {  // all digit pairs with t + u >= 5
-                    mma(6, 0, 4); mma(6, 4, 3);
-                    mma(5, 0, 4); mma(5, 4, 3);
-                    mma(4, 1, 4); mma(4, 5, 2);
-                    mma(3, 2, 4); mma(3, 6, 1);
-                    mma(2, 3, 4);
-                    mma(1, 4, 3);
-                    mma(0, 5, 2);
+                using C0 = std::integral_constant<int, 0>;
+                using C1 = std::integral_constant<int, kOzpCollector ? 1 : 0>;
+                using C2 = std::integral_constant<int, kOzpCollector ? 2 : 0>;
+                // all digit pairs with t + u >= 5, split over the issuing threads by A plane (straight-line
+                // blocks: the loop-invariant choice is one branch per step)
+                if (p.dbg & 1) {
+                } else if constexpr (kOzpIssuers == 1) {
+                    mma(6, 0, 4, C1{}); mma(6, 4, 3, C2{});
+                    mma(5, 0, 4, C1{}); mma(5, 4, 3, C2{});
+                    mma(4, 1, 4, C1{}); mma(4, 5, 2, C2{});
+                    mma(3, 2, 4, C1{}); mma(3, 6, 1, C2{});
+                    mma(2, 3, 4, C0{});
+                    mma(1, 4, 3, C0{});
+                    mma(0, 5, 2, C0{});
+                } else if constexpr (kOzpIssuers == 2) {
+                    if (who == 0) {  // 20 products
+                        mma(6, 0, 4, C1{}); mma(6, 4, 3, C2{});
+                        mma(5, 0, 4, C1{}); mma(5, 4, 3, C2{});
+                        mma(4, 1, 4, C1{}); mma(4, 5, 2, C2{});
+                    } else {         // 14 products
+                        mma(3, 2, 4, C1{}); mma(3, 6, 1, C2{});
+                        mma(2, 3, 4, C0{});
+                        mma(1, 4, 3, C0{});
+                        mma(0, 5, 2, C0{});
+                    }
+                } else {
+                    if (who == 0) {
+                        mma(6, 0, 4, C1{}); mma(6, 4, 3, C2{});
+                        mma(5, 0, 4, C1{}); mma(5, 4, 3, C2{});
+                    } else if (who == 1) {
+                        mma(4, 1, 4, C1{}); mma(4, 5, 2, C2{});
+                        mma(3, 2, 4, C1{}); mma(3, 6, 1, C2{});
+                    } else {
+                        mma(2, 3, 4, C0{});
+                        mma(1, 4, 3, C0{});
+                        mma(0, 5, 2, C0{});
+                    }
                 }
                 if (MC)
                     asm volatile(

@@ -4828,7 +4828,7 @@ int sorsvd_pass_ozaki_device(sorsvd_ctx* c, int32_t ta, int64_t m, int64_t n, in
                              double* ms_scales) {
     if (!c) return SORSVD_ERR_PARAMETER;
     return guarded(c, [&] {
-        const int dbg = (dtype >> 8) & 7;  // kernel timing experiments (tools/oz_pass.py): bits 8-10 of dtype
+        const int dbg = (dtype >> 8) & 15;  // kernel timing experiments (tools/oz_pass.py): bits 8-11 of dtype
         dtype &= 0xff;
         (void)dbg;
         if (dtype != SORSVD_F64 && dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
