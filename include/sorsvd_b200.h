@@ -176,8 +176,9 @@ int sorsvd_sor_svd_power_device(sorsvd_ctx* ctx, const sorsvd_desc* desc, const 
  * pass over A serves all trials in one launch. Outputs are stacked per trial:
  * U trials x m x k, sigma trials x k, V trials x n x k. Each trial matches the
  * single call with its seed to the parity tolerances (not bitwise: the wider
- * passes sum in a different order). Single rank; ell <= 256; no TF32, no
- * single_pass. */
+ * passes sum in a different order). Row-sharded contexts: every rank passes its
+ * row block (desc.m local, desc.m_global total) and the same seeds; U comes back
+ * row-sharded per trial. ell <= 256; no TF32, no single_pass. */
 int sorsvd_sor_svd_power_batch(sorsvd_ctx* ctx, const sorsvd_desc* desc, int32_t trials, const uint64_t* seeds,
                                const void* A, const double* omegas, double* U, double* sigma, double* V,
                                sorsvd_stats* stats);
@@ -191,7 +192,10 @@ int sorsvd_sor_svd_power_batch_device(sorsvd_ctx* ctx, const sorsvd_desc* desc, 
  * r_svd: Omega = gaussian_matrix(n, ell, seed) unless OMEGA_GIVEN; passes 2q+2.
  * tsr_svd: Psi1 = gaussian_matrix(n, ell, seed), Psi2 = gaussian_matrix(m, ell,
  * seed ^ 1) unless OMEGA_GIVEN (then both must be given); passes 1 (the two
- * sketches are two launches over A in this build). Single rank; no TF32. */
+ * sketches are two launches over A in this build). Row-sharded contexts
+ * (desc.m_global): the rank's rows of A, and for tsr_svd the rank's rows of Psi2
+ * (drawn as rows [row0, row0 + m) of the m_global x ell matrix, sorsvd_gaussian_rows);
+ * U row-sharded, sigma and V replicated. No TF32. */
 int sorsvd_r_svd(sorsvd_ctx* ctx, const sorsvd_desc* desc, const void* A, const double* omega, double* U,
                  double* sigma, double* V, sorsvd_stats* stats);
 int sorsvd_r_svd_device(sorsvd_ctx* ctx, const sorsvd_desc* desc, const void* dA, const double* dOmega,
