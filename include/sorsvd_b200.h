@@ -252,7 +252,8 @@ int sorsvd_rpca_telemetry(sorsvd_ctx* ctx, int32_t cap_rows, double* out, int32_
 /* estimate_rank_bound(x) = ceil((||X||_* / ||X||_F)^2) (PAPER Eq. 66), the input of
  * rpca_default_config's ell = min(2 * bound, min(m,n) - 1). Device FP64 X, min(m,n) <=
  * 512 (thin QR + Jacobi SVD of R). Zero matrix -> SORSVD_ERR_PARAMETER. nuclear / frobenius (may be
- * NULL) receive the two norms. */
+ * NULL) receive the two norms. Row-sharded contexts (dX = this rank's rows, m >= n on every rank,
+ * n <= 256): the ranks' R factors are gathered and factored again; every rank gets the same bound. */
 int sorsvd_estimate_rank_bound_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const double* dX, int64_t ldx,
                                       int64_t* bound, double* nuclear, double* frobenius);
 /* The same on a host matrix (uploaded inside). */
@@ -270,8 +271,9 @@ int sorsvd_approx_error_fro_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const 
 
 /* approx_error(a, x, NormKind::spectral) (sketch.hpp:168-172; the reference: dgesdd 'N' of the
  * dense difference, dense.hpp:173-176): E = A - U diag(sigma) V^T is formed on the device and
- * sigma_1(E) comes from norm(spectral) below. Single rank. The bound harness (bounds.hpp:289-290)
- * asks for both norms per trial. */
+ * sigma_1(E) comes from norm(spectral) below. Row-sharded contexts (A, U = this rank's rows;
+ * n <= 1024): the Gram matrix of E is summed over the ranks. The bound harness
+ * (bounds.hpp:289-290) asks for both norms per trial. */
 int sorsvd_approx_error_spectral_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const void* dA, int64_t lda,
                                         int32_t dtype, int32_t k, const double* dU, int64_t ldu,
                                         const double* dSigma, const double* dV, int64_t ldv, double* err);
@@ -279,7 +281,8 @@ int sorsvd_approx_error_spectral_device(sorsvd_ctx* ctx, int64_t m, int64_t n, c
 /* norm(a, NormKind::spectral) (dense.hpp:173-176) of a device FP64 matrix: min(m, n) <= 1024 ->
  * Gram matrix, 12 rescaled squarings and a 16-column Rayleigh-Ritz step (<= 1e-12 relative
  * against dgesdd, clustered leading values included); larger -> block subspace iteration with
- * Rayleigh-Ritz to a stationary value (seed draws its start block). Also RPCA's mu0. */
+ * Rayleigh-Ritz to a stationary value (seed draws its start block). Also RPCA's mu0.
+ * Row-sharded contexts (dA = this rank's rows): n <= 1024, G = sum over ranks of A_r^T A_r. */
 int sorsvd_norm_spectral_device(sorsvd_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, uint64_t seed,
                                 double* out);
 

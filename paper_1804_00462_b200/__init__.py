@@ -491,7 +491,8 @@ def approx_error(a, x: LowRankApprox, kind: str = "frobenius", ctx: Optional[Con
     """sketch.hpp:168-172: ||a - reconstruct(x)||. kind "frobenius": one fused pass
     over a on the device (the m x n reconstruction is never formed). kind
     "spectral": the difference is formed on the device and its sigma_1 comes from
-    `norm(., "spectral")` (the reference: dgesdd of the dense difference)."""
+    `norm(., "spectral")` (the reference: dgesdd of the dense difference). On a row-sharded
+    context a and x.u are the rank's rows (spectral: n <= 1024)."""
     import torch
     if kind not in ("frobenius", "spectral"):
         raise ParameterError("parameter: approx_error supports frobenius and spectral norms")
@@ -517,7 +518,8 @@ def approx_error(a, x: LowRankApprox, kind: str = "frobenius", ctx: Optional[Con
 def norm(a, kind: str = "frobenius", ctx: Optional[Context] = None, seed: int = 0) -> float:
     """dense.hpp:163-176 on a CUDA (or host) float64 matrix: "frobenius" or "spectral"
     (sigma_1 by Gram squaring + Rayleigh-Ritz for min(m, n) <= 1024, else block
-    subspace iteration; the reference runs dgesdd on the whole matrix)."""
+    subspace iteration; the reference runs dgesdd on the whole matrix). On a row-sharded
+    context a is the rank's row block (spectral: n <= 1024, the Gram matrix is summed over ranks)."""
     import torch
     if kind not in ("frobenius", "spectral"):
         raise ParameterError("parameter: norm supports frobenius and spectral")
@@ -693,7 +695,8 @@ def matmul(a, b, transpose_a: bool = False, ctx: Optional[Context] = None):
 # ------------------------------------------------------------------- RPCA --
 def estimate_rank_bound(x, ctx: Optional[Context] = None) -> int:
     """SPEC.md:377-385 (PAPER Eq. 66): ceil((||X||_* / ||X||_F)^2); the spectrum comes from
-    thin QR + Jacobi SVD on the device (min(m, n) <= 512). Zero matrix -> ParameterError."""
+    thin QR + Jacobi SVD on the device (min(m, n) <= 512). Zero matrix -> ParameterError.
+    Row-sharded context: x is the rank's rows (n <= 256, at least n rows per rank)."""
     import torch
     dev = x.device if _is_torch_cuda(x) else torch.device("cuda", 0)
     X = x if _is_torch_cuda(x) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)

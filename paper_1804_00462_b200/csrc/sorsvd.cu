@@ -4344,14 +4344,16 @@ int sorsvd_norm_spectral_device(sorsvd_ctx* c, int64_t m, int64_t n, const doubl
     return guarded(c, [&] {
         if (m < 1 || n < 1 || lda < n) throw Error{SORSVD_ERR_SHAPE, "shape: matrix dimensions must be positive"};
         if (!dA || !out) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
-        if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "norm(spectral): single-rank only"};
+        // row-sharded A (dA = this rank's rows): the Gram path sums G = A_r^T A_r over the ranks
+        if (c->world > 1 && n > 1024)
+            throw Error{SORSVD_ERR_UNSUPPORTED, "norm(spectral): row-sharded contexts need n <= 1024"};
         const double ss = device_sumsq(c, dA, m, n, lda);
         if (!std::isfinite(ss)) throw Error{SORSVD_ERR_PARAMETER, "parameter: matrix entries must be finite"};
         if (ss == 0.0) {
             *out = 0.0;
             return;
         }
-        *out = std::min(m, n) <= 1024 ? estimate_sigma1_gram(c, dA, m, n, lda)
+        *out = (std::min(m, n) <= 1024 || c->world > 1) ? estimate_sigma1_gram(c, dA, m, n, lda)
                : std::min(m, n) < 3  ? std::sqrt(ss)  // unreachable for the harness; rank-1-ish edge
                                       : estimate_sigma1(c, dA, m, n, lda, seed);
     });
@@ -4368,7 +4370,8 @@ int sorsvd_approx_error_spectral_device(sorsvd_ctx* c, int64_t m, int64_t n, con
             throw Error{SORSVD_ERR_SHAPE, "shape: approx_error: approximation does not match matrix dims"};
         if (!dA || !dU || !dSigma || !dV || !err) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
         if (dtype != SORSVD_F64 && dtype != SORSVD_F32) throw Error{SORSVD_ERR_PARAMETER, "parameter: unknown dtype"};
-        if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "approx_error(spectral): single-rank only"};
+        if (c->world > 1 && n > 1024)  // dA, dU: this rank's rows; sigma, V replicated
+            throw Error{SORSVD_ERR_UNSUPPORTED, "approx_error(spectral): row-sharded contexts need n <= 1024"};
         const int64_t lde = (n + 7) / 8 * 8;
         double* E = dbuf(c, "ae_E", (size_t)m * lde, true);
         const dim3 grid((unsigned)cdiv(n, 16), (unsigned)cdiv(m, 16));
@@ -4385,8 +4388,8 @@ int sorsvd_approx_error_spectral_device(sorsvd_ctx* c, int64_t m, int64_t n, con
             *err = 0.0;
             return;
         }
-        *err = std::min(m, n) <= 1024 ? estimate_sigma1_gram(c, E, m, n, lde)
-                                      : estimate_sigma1(c, E, m, n, lde, 0x5eedULL);
+        *err = (std::min(m, n) <= 1024 || c->world > 1) ? estimate_sigma1_gram(c, E, m, n, lde)
+                                                        : estimate_sigma1(c, E, m, n, lde, 0x5eedULL);
     });
 }
 
@@ -4457,7 +4460,11 @@ int sorsvd_estimate_rank_bound_device(sorsvd_ctx* c, int64_t m, int64_t n, const
     return guarded(c, [&] {
         if (m < 1 || n < 1 || ldx < n) throw Error{SORSVD_ERR_SHAPE, "shape: matrix dimensions must be positive"};
         if (!dX || !bound) throw Error{SORSVD_ERR_PARAMETER, "parameter: null buffer"};
-        if (c->world > 1) throw Error{SORSVD_ERR_UNSUPPORTED, "estimate_rank_bound: single-rank only"};
+        // row-sharded X (dX = this rank's rows): local thin QR, the ranks' R factors gathered and
+        // factored again (the TSQR of qr_rows without forming Q), so every rank gets the same spectrum
+        const bool sharded = c->world > 1;
+        if (sharded && (m < n || n > kHouseMaxK))
+            throw Error{SORSVD_ERR_UNSUPPORTED, "estimate_rank_bound: row-sharded contexts need n <= 256 and >= n rows per rank"};
         const double ss = device_sumsq(c, dX, m, n, ldx);
         if (!std::isfinite(ss)) throw Error{SORSVD_ERR_PARAMETER, "parameter: matrix entries must be finite"};
         if (ss == 0.0) throw Error{SORSVD_ERR_PARAMETER, "parameter: estimate_rank_bound of the zero matrix"};
@@ -4481,7 +4488,16 @@ int sorsvd_estimate_rank_bound_device(sorsvd_ctx* c, int64_t m, int64_t n, const
             nuc = fro;
         } else {
             QrPlan* p = get_qr_plan(c, rows, k, 0, "er");
-            qr_run(c, p, T, Np, Q, Np, c->stream);
+            if (sharded) {
+                qr_factor(c, p, T, Np, Q, Np, false, c->stream);
+                const int L1 = (int)p->nodes.size() - 1;
+                double* Rg = dbuf(c, "erRg", (size_t)c->world * k * k);
+                comm_allgather(c, p->R[L1], Rg, (size_t)k * k, c->stream);
+                p = get_qr_plan(c, (int64_t)c->world * k, k, c->world, "erG");
+                qr_factor(c, p, nullptr, 0, nullptr, 0, true, c->stream, Rg);
+            } else {
+                qr_run(c, p, T, Np, Q, Np, c->stream);
+            }
             const int L = (int)p->nodes.size() - 1;
             double* U = dbuf(c, "erU", (size_t)k * k);
             double* V = dbuf(c, "erV", (size_t)k * k);

@@ -358,3 +358,48 @@ def test_sharded_single_pass_matches_oracle(env, world, m, n, k, ell, q):
     s0 = out[0].sigma.cpu().numpy()
     assert O.sigma_rel_err(s0, ref.sigma).max() <= 1e-9
     assert out[0].passes == 2 * q + 2
+
+
+@pytest.mark.parametrize("world,m,n", [(2, 2000, 300), (3, 1501, 640)])
+def test_sharded_spectral_norm_and_error_match_lapack(env, world, m, n):
+    """norm(a, spectral) and approx_error(a, x, spectral) (dense.hpp:173-176, sketch.hpp:168-172) over
+    row blocks: the Gram matrix is summed over the ranks; every rank returns the same value, equal to
+    LAPACK's sigma_1 of the full matrix / of the full difference."""
+    P, torch = env
+    A = O.gen_lowrank_decay(m, n, 25, lambda j: 2.0 ** (-j / 3), 1e-3, 1000 + m)
+    k = 12
+    x = O.sor_svd_power(A, k, O.SketchConfig(16, 1, 9))
+    ref_n = np.linalg.norm(A, 2)
+    ref_e = np.linalg.norm(A - (x.u * x.sigma) @ x.v.T, 2)
+    base, extra = divmod(m, world)
+    starts = np.cumsum([0] + [base + (1 if r < extra else 0) for r in range(world)])
+
+    def fn(blk, ctx, mg):
+        r = ctx.rank
+        xr = O.LowRankApprox(x.u[starts[r]:starts[r + 1]], x.sigma, x.v, 0, 0, k, 1, 9)
+        return P.norm(blk, "spectral", ctx=ctx), P.approx_error(blk, xr, "spectral", ctx=ctx)
+
+    out = _sharded_call(P, torch, A, world, fn)
+    assert all(o == out[0] for o in out)
+    assert abs(out[0][0] - ref_n) <= 1e-11 * ref_n
+    assert abs(out[0][1] - ref_e) <= 1e-9 * ref_e
+
+
+@pytest.mark.parametrize("world,m,n,r", [(2, 1200, 96, 7), (4, 4000, 200, 30)])
+def test_sharded_estimate_rank_bound_matches_oracle(env, world, m, n, r):
+    """estimate_rank_bound of a row-sharded matrix: local thin QR, the ranks' R
+    factors gathered and factored again; the bound equals the single-matrix value on every rank."""
+    P, torch = env
+    A = O.gen_lowrank_decay(m, n, r, lambda j: 1.0 / j, 1e-6, 31 + m)
+    ref = O.estimate_rank_bound(A)
+    out = _sharded_call(P, torch, A, world, lambda blk, ctx, mg: P.estimate_rank_bound(blk, ctx=ctx))
+    assert out == [ref] * world
+    single = P.estimate_rank_bound(torch.from_numpy(A).cuda())
+    assert single == ref
+
+
+def test_sharded_spectral_norm_wide_n_unsupported(env):
+    P, torch = env
+    A = np.ones((64, 1100))
+    with pytest.raises(P.UnsupportedError):
+        _sharded_call(P, torch, A, 2, lambda blk, ctx, mg: P.norm(blk, "spectral", ctx=ctx))
