@@ -2037,6 +2037,11 @@ int oz_pick_splits(int64_t tiles, int KT, int64_t out_bytes, int sms) {
     return best;
 }
 
+// The K partition of the one-launch NN pass T1 = A X of problem P (its row chunks reuse it).
+int oz_nn_splits(sorsvd_ctx* c, const SorProblem& P) {
+    return oz_pick_splits(cdiv(P.m, kOzBM) * cdiv(P.Np, kOzBN), (int)cdiv(P.n, kOzBK), P.m * P.Np * 8, c->num_sms);
+}
+
 // C (M x Np) = op(A) X with X (K x Np row-major): NN (M = m, K = n, left rows = rows
 // of A) or TN (M = n, K = m, left rows = columns [n0, n0 + P.n) of the call's A; P
 // describes that column block). X is cut into digit planes first. With the call's
@@ -2085,7 +2090,8 @@ OzX oz_cut_x(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, co
 // columns of A): C (M x Np, the caller's pointer to the block's first row) = op(A)[l0 ..] X.
 // TN only: k0 = first row of the K range this launch contracts over (P.m = its length), acc = add to C.
 void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScales& oz, const OzX& x, double* C,
-                      int64_t l0, int64_t M, cudaStream_t s, int dbg = 0, int64_t k0 = 0, bool acc = false) {
+                      int64_t l0, int64_t M, cudaStream_t s, int dbg = 0, int64_t k0 = 0, bool acc = false,
+                      int splits = 0) {
     const int Np = P.Np;
     const int NC = (int)cdiv(Np, kOzBN);
     const int64_t K = ta ? P.m : P.n;
@@ -2106,7 +2112,9 @@ void oz_launch_planes(sorsvd_ctx* c, const SorProblem& P, bool ta, const OzScale
     a.pred = c->pred;
     a.pred_skip = c->pred_skip;
     const int64_t tiles = cdiv(M, kOzBM) * NC;
-    const int S = oz_pick_splits(tiles, (int)KT, M * Np * 8, c->num_sms);
+    // splits > 0: the caller's K partition (a row chunk of a pass keeps the whole pass's, so that
+    // its rows come out with the same bits as from the one-launch pass)
+    const int S = splits > 0 ? splits : oz_pick_splits(tiles, (int)KT, M * Np * 8, c->num_sms);
     a.kt_split = (int)cdiv(KT, S);
     a.c_split_stride = M * Np;
     double* ws = S > 1 ? dbuf(c, "oz_split", (size_t)S * M * Np) : nullptr;
@@ -2386,6 +2394,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
             g = h;
             h = t;
         }
+        const int s_full = oz_nn_splits(c, P);
         const int64_t unit_rows = (int64_t)(c->num_sms / g) * kOzBM;  // whole waves of 128-row tiles
         const int64_t units = cdiv(P.m, unit_rows);
         const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(10, units));
@@ -2408,7 +2417,7 @@ void enqueue_sor(sorsvd_ctx* c, const SorProblem& P, const SorBuffers& b, QrPlan
                 CK(cudaEventRecord(c->up_ev[(size_t)i + 1], c->side));
             }
             CK(cudaStreamWaitEvent(s, c->up_ev[(size_t)i], 0));
-            oz_launch_planes(c, P, false, oz, ox, b.T1 + r0 * Np, r0, rows, s);
+            oz_launch_planes(c, P, false, oz, ox, b.T1 + r0 * Np, r0, rows, s, 0, 0, false, s_full);
         }
         first_done = true;
     } else if (P.ozaki) {
@@ -2941,6 +2950,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
         if (pipe) {
             const OzScales oz = oz_planes_of(c, P);
             const OzX ox = oz_cut_x(c, P, false, oz, b.T2, c->stream);  // Omega's digit planes: once for all chunks
+            const int s_full = oz_nn_splits(c, P);
             // the first T2 = A^T T1 as well, one K range per chunk (its rows of T1 exist as soon as the chunk's
             // first pass is done), into a second buffer (T2 still holds Omega for the later chunks' first pass)
             const bool tn_too = c->opt_upload_tn && P.q >= 1 && !P.single_pass;
@@ -2949,7 +2959,7 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
                 const int64_t r0 = (int64_t)i * up->rows_per_chunk, rows = std::min(up->rows_per_chunk, P.m - r0);
                 CK(cudaStreamWaitEvent(c->stream, c->up_ev[(size_t)i], 0));
                 oz_convert_rows(c, P, oz, r0, rows, c->stream);
-                oz_launch_planes(c, P, false, oz, ox, b.T1 + r0 * P.Np, r0, rows, c->stream);
+                oz_launch_planes(c, P, false, oz, ox, b.T1 + r0 * P.Np, r0, rows, c->stream, 0, 0, false, s_full);
                 if (tn_too) {
                     SorProblem Qc = P;
                     Qc.m = rows;

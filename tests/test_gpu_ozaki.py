@@ -303,3 +303,30 @@ def test_ozaki_partial_planes_whole_call(P):
     _check_parity(f, base, ds, dl)
     h = P.sor_svd_power(A, 40, P.SketchConfig(48, 2, 9), fp64_mode="ozaki", ctx=ctx)   # host call: no pipelined upload
     assert np.array_equal(np.asarray(h.sigma), f.sigma.cpu().numpy())
+
+
+def test_chunked_first_pass_keeps_split_k_bits(P):
+    """The first pass T1 = A Omega run by row chunks (conversion under the pass, SORSVD_OPT_OZAKI_OVERLAP; host
+    calls: under the upload) keeps the K partition of the one-launch pass: a long K (n = 4096) and a short last
+    chunk, for which the split-K heuristic alone would pick another partition, give the same bits with the
+    overlap on and off and through the host-buffer call."""
+    import torch
+    m, n, ell = 40000, 4096, 64
+    A = P.gen_lowrank_device(m, n, 2.0 ** (-np.arange(1, 31) / 4.0), 1e-3, 91, x_scale=m ** -0.5, y_scale=n ** -0.5)
+    cfg = P.SketchConfig(ell, 1, 3)
+    outs = []
+    for ov in (1, 0):
+        ctx = P.Context(0)
+        ctx.set_option(P.Context.OPT_OZAKI_OVERLAP, ov)
+        f = P.sor_svd_power(A, 48, cfg, fp64_mode="ozaki", ctx=ctx)
+        assert f.stats["oz_planes"] == 1
+        outs.append((f.sigma.cpu().numpy(), f.u.cpu().numpy(), f.v.cpu().numpy()))
+        ctx.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    ctx = P.Context(0)
+    ctx.set_option(P.Context.OPT_UPLOAD_CHUNK_MB, 300)   # 9156-row chunks: 4 full + one ragged
+    ctx.set_option(P.Context.OPT_UPLOAD_TN, 0)
+    h = P.sor_svd_power(A.cpu().numpy(), 48, cfg, fp64_mode="ozaki", ctx=ctx)
+    assert np.array_equal(np.asarray(h.sigma), outs[0][0]) and np.array_equal(np.asarray(h.u), outs[0][1])
+    ctx.close()
