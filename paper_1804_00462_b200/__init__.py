@@ -711,13 +711,15 @@ def estimate_rank_bound(x, ctx: Optional[Context] = None) -> int:
 
 
 def rpca_default_config(x_or_m, n: Optional[int] = None, ell: Optional[int] = None, q: int = 1, seed: int = 0,
-                        ctx: Optional[Context] = None) -> RpcaConfig:
+                        ctx: Optional[Context] = None, m_global: int = 0) -> RpcaConfig:
     """lambda = 1/sqrt(max(m,n)), mu0 = 1.25/sigma_1(X) (estimated on the device by
     rpca_alm: mu0 = 0 here), mu_bar = 1e7 mu0, rho = 1.6, tol = 1e-7, max_iter = 500, q = 1 and
     ell = min(2 * estimate_rank_bound(x), min(m,n) - 1). Call with the matrix (the spec's form),
-    or with (m, n, ell) when the sketch size is chosen by the caller."""
+    or with (m, n, ell) when the sketch size is chosen by the caller. Row-sharded: the rank's
+    row block with ctx and m_global (lambda and the ell cap use the global row count)."""
     if hasattr(x_or_m, "shape"):
         m, nn = x_or_m.shape
+        m = m_global or m
         if ell is None:
             ell = max(1, min(2 * estimate_rank_bound(x_or_m, ctx=ctx), min(m, nn) - 1))
     else:

@@ -394,6 +394,10 @@ def test_sharded_estimate_rank_bound_matches_oracle(env, world, m, n, r):
     ref = O.estimate_rank_bound(A)
     out = _sharded_call(P, torch, A, world, lambda blk, ctx, mg: P.estimate_rank_bound(blk, ctx=ctx))
     assert out == [ref] * world
+    # rpca_default_config from a row block: lambda and the ell cap use the global row count
+    cfgs = _sharded_call(P, torch, A, world, lambda blk, ctx, mg: P.rpca_default_config(blk, ctx=ctx, m_global=mg))
+    one = P.rpca_default_config(torch.from_numpy(A).cuda())
+    assert all(c.ell == one.ell and c.lam == one.lam for c in cfgs)
     single = P.estimate_rank_bound(torch.from_numpy(A).cuda())
     assert single == ref
 
