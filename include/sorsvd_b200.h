@@ -113,6 +113,11 @@ int sorsvd_ctx_create(int device, sorsvd_ctx** out);
  * 128-byte NCCL id produced by sorsvd_nccl_unique_id on rank 0 and broadcast
  * by the caller (e.g. torch.distributed). */
 int sorsvd_nccl_unique_id(void* out128);
+/* One-GPU check of the NCCL binding (dlopen of libnccl.so.2, call signatures, stream order): a
+ * one-rank communicator on `device`, in-place all-reduce + all-gather of `count` doubles; both must
+ * return the input (max_abs_err = 0). Only one GPU is reachable in the build environment, so this
+ * is the hardware test of the calls the row-sharded contexts issue. */
+int sorsvd_nccl_selftest(int device, int64_t count, double* max_abs_err);
 int sorsvd_ctx_create_dist(int device, int rank, int world, const void* unique_id128, sorsvd_ctx** out);
 void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
 /* Per-context algorithm options (defaults are the tuned choices; tests use

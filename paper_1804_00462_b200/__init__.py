@@ -185,6 +185,14 @@ class Context:
         _check(C.lib().sorsvd_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
         return buf.raw
 
+    @staticmethod
+    def nccl_selftest(device: int = 0, count: int = 1 << 16) -> float:
+        """One-rank NCCL communicator on `device`: all-reduce + all-gather of `count` doubles through the
+        library's dlopen binding; returns the largest deviation from the input (0.0 expected)."""
+        err = ctypes.c_double(-1.0)
+        _check(C.lib().sorsvd_nccl_selftest(device, count, ctypes.byref(err)))
+        return err.value
+
     @property
     def handle(self):
         return self._h

@@ -3930,6 +3930,50 @@ int sorsvd_nccl_unique_id(void* out128) {
     });
 }
 
+// One-GPU check of the NCCL binding the multi-rank contexts use (libnccl resolved by dlopen, the
+// entry points' signatures, ncclDouble / ncclSum, stream-ordered calls): a communicator of ONE rank on
+// `device`, an in-place all-reduce and an all-gather of `count` doubles on a fresh stream; both must
+// return the input. max_abs_err receives the largest deviation (0 expected).
+int sorsvd_nccl_selftest(int device, int64_t count, double* max_abs_err) {
+    if (count < 1 || !max_abs_err) return SORSVD_ERR_PARAMETER;
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        ncclUniqueId id;
+        NCK(nccl().GetUniqueId(&id));
+        ncclComm_t comm = nullptr;
+        NCK(nccl().CommInitRank(&comm, 1, id, 0));
+        cudaStream_t st = nullptr;
+        double *a = nullptr, *b = nullptr;
+        std::vector<double> h((size_t)count), r((size_t)count), g((size_t)count);
+        for (int64_t i = 0; i < count; ++i) h[(size_t)i] = 1.0 / (double)(i + 1) - 0.25 * (double)(i % 7);
+        try {
+            CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            CK(cudaMalloc(&a, (size_t)count * 8));
+            CK(cudaMalloc(&b, (size_t)count * 8));
+            CK(cudaMemcpyAsync(a, h.data(), (size_t)count * 8, cudaMemcpyHostToDevice, st));
+            NCK(nccl().AllReduce(a, a, (size_t)count, ncclDouble, ncclSum, comm, st));
+            NCK(nccl().AllGather(a, b, (size_t)count, ncclDouble, comm, st));
+            CK(cudaMemcpyAsync(r.data(), a, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(g.data(), b, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } catch (...) {
+            cudaFree(a);
+            cudaFree(b);
+            if (st) cudaStreamDestroy(st);
+            nccl().CommDestroy(comm);
+            throw;
+        }
+        cudaFree(a);
+        cudaFree(b);
+        cudaStreamDestroy(st);
+        NCK(nccl().CommDestroy(comm));
+        double e = 0.0;
+        for (int64_t i = 0; i < count; ++i)
+            e = std::max(e, std::max(std::fabs(r[(size_t)i] - h[(size_t)i]), std::fabs(g[(size_t)i] - h[(size_t)i])));
+        *max_abs_err = e;
+    });
+}
+
 int sorsvd_ctx_create_dist(int device, int rank, int world, const void* unique_id128, sorsvd_ctx** out) {
     if (!out || world < 1 || rank < 0 || rank >= world) return SORSVD_ERR_PARAMETER;
     auto* c = new sorsvd_ctx();

@@ -407,3 +407,14 @@ def test_sharded_spectral_norm_wide_n_unsupported(env):
     A = np.ones((64, 1100))
     with pytest.raises(P.UnsupportedError):
         _sharded_call(P, torch, A, 2, lambda blk, ctx, mg: P.norm(blk, "spectral", ctx=ctx))
+
+
+def test_nccl_binding_selftest_one_rank(env):
+    """The NCCL calls of the row-sharded contexts (libnccl resolved by dlopen inside the library: unique id,
+    ncclCommInitRank, in-place ncclAllReduce(ncclDouble, ncclSum), ncclAllGather, ncclCommDestroy) run on the
+    one GPU that is reachable here as a one-rank communicator and return their input unchanged; a 128-byte id
+    comes back from nccl_unique_id."""
+    P, torch = env
+    assert P.Context.nccl_selftest(0, 1 << 16) == 0.0
+    assert P.Context.nccl_selftest(0, 3) == 0.0
+    assert len(P.Context.nccl_unique_id()) == 128
