@@ -135,6 +135,9 @@ void sorsvd_ctx_destroy(sorsvd_ctx* ctx);
                                         (one K range per row chunk, added in chunk order): same accuracy, last bits differ
                                         from the device-resident call; 0 = only the first pass rides under the upload and
                                         the host call returns the device call's bits */
+#define SORSVD_OPT_NCCL_GRAPH 9      /* value: 0 (default) = contexts with an NCCL communicator enqueue every call stream-ordered
+                                        (the schedule the emulated-group tests cover); 1 = capture the call, collectives
+                                        included, in a CUDA graph like single-GPU contexts do */
 #define SORSVD_OPT_UPLOAD_CHUNK_MB 5 /* value: MiB per row chunk of A in host-buffer calls of the Ozaki planes engine (default
                                         1536): A uploads in chunks on a copy stream and each chunk is converted and swept
                                         by the first pass T1 = A Omega while the next one crosses PCIe */

@@ -201,7 +201,7 @@ class Context:
         _check(C.lib().sorsvd_set_stream(self._h, ctypes.c_void_p(stream_ptr)), self._h)
 
     # sorsvd_ctx_set_option keys / Jacobi variants (include/sorsvd_b200.h)
-    OPT_JACOBI, OPT_SORD_CHUNK_MB, OPT_OZAKI_PLANES, OPT_FUSED_PAIR, OPT_UPLOAD_CHUNK_MB, OPT_OZAKI_MULTICAST, OPT_OZAKI_OVERLAP, OPT_UPLOAD_TN = 1, 2, 3, 4, 5, 6, 7, 8
+    OPT_JACOBI, OPT_SORD_CHUNK_MB, OPT_OZAKI_PLANES, OPT_FUSED_PAIR, OPT_UPLOAD_CHUNK_MB, OPT_OZAKI_MULTICAST, OPT_OZAKI_OVERLAP, OPT_UPLOAD_TN, OPT_NCCL_GRAPH = 1, 2, 3, 4, 5, 6, 7, 8, 9
     JACOBI_AUTO, JACOBI_BARRIER, JACOBI_ROTLOG = 0, 1, 2
 
     def set_option(self, key: int, value: int):

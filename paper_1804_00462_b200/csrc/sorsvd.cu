@@ -207,6 +207,7 @@ struct sorsvd_ctx {
                                           // under the first pass over chunk i (device-resident calls)
     int opt_oz_multicast = 0;             // sorsvd_ctx_set_option(SORSVD_OPT_OZAKI_MULTICAST): cluster + TMA multicast of the A planes
                                           // (measured: no gain, the pass is shared-memory-bandwidth bound)
+    int opt_nccl_graph = 0;               // sorsvd_ctx_set_option(SORSVD_OPT_NCCL_GRAPH): capture NCCL collectives in the call's CUDA graph
     int opt_upload_tn = 1;                // sorsvd_ctx_set_option(SORSVD_OPT_UPLOAD_TN): host-buffer planes calls also run the
                                           // first A^T pass chunk by chunk under the upload (results differ from the
                                           // device-resident call in the last bits: K ranges summed in chunk order)
@@ -2931,7 +2932,11 @@ void sor_device(sorsvd_ctx* c, const sorsvd_desc* d, const void* dA, const doubl
     const bool pipe = up && up->chunked && P.ozaki && P.oz_pm == P.m && c->world == 1 && !baseline;
     if (up && up->chunked && !pipe)  // not eligible after all: wait for the whole upload
         CK(cudaStreamWaitEvent(c->stream, c->up_ev[(size_t)up->nchunks - 1], 0));
-    const bool use_graph = !timing && !c->emu && !(d->flags & SORSVD_FLAG_NO_GRAPH) && !pipe;
+    // NCCL contexts enqueue stream-ordered calls by default: collectives captured into a graph (two
+    // streams, fork/join) could not be run in the one-GPU build environment, the plain form is the
+    // schedule the emulated-group tests run; SORSVD_OPT_NCCL_GRAPH opts in.
+    const bool use_graph = !timing && !c->emu && !(c->comm && !c->opt_nccl_graph) &&
+                           !(d->flags & SORSVD_FLAG_NO_GRAPH) && !pipe;
     CK(cudaEventRecord(c->ev_a, c->stream));
     const int launches0 = c->launches;
     int launches = 0;
@@ -4092,6 +4097,10 @@ int sorsvd_ctx_set_option(sorsvd_ctx* c, int32_t key, int64_t value) {
                 break;
             case SORSVD_OPT_UPLOAD_TN:
                 c->opt_upload_tn = value != 0;
+                break;
+            case SORSVD_OPT_NCCL_GRAPH:
+                c->opt_nccl_graph = value != 0;
+                invalidate_graphs(c);
                 break;
             case SORSVD_OPT_UPLOAD_CHUNK_MB:
                 if (value < 1) throw Error{SORSVD_ERR_PARAMETER, "parameter: upload chunk must be >= 1 MiB"};
