@@ -634,7 +634,7 @@ def main():
         # the library's pass engine here: ozaki_planes_gemm_kernel (A's digit planes cut once per
         # call, ozaki_planes_i8.cuh) or ozaki_gemm_kernel (A converted inside the pass), both
         # tcgen05 kind::i8. Its roofline is the
-        # INT8 tensor rate: 34 int8 digit products per FP64 multiply-add (ozaki_i8.cuh), against
+        # INT8 tensor rate: sorsvd_ozaki_products() int8 digit products per FP64 multiply-add (ozaki_i8.cuh), against
         # 2 x the measured BF16 burst (the INT8 dense rate is twice BF16 on B200; MEASURED_PEAKS.json
         # has no INT8 entry). The FP64-equivalent rate is reported beside it.
         oz = P._capi.lib().sorsvd_pass_ozaki_device
@@ -645,14 +645,15 @@ def main():
         ms_ot = ctypes.c_double()
         P._check(oz(ctx.handle, 1, m_local, n, n, ell, dt_code, A.data_ptr(), T.data_ptr(), T2.data_ptr(),
                     max(args.steps, 5), ctypes.byref(ms_ot), ctypes.byref(ms_sc)), ctx.handle)
-        int8_ops = 34.0 * pass_flops
+        n_prod = int(P._capi.lib().sorsvd_ozaki_products())
+        int8_ops = float(n_prod) * pass_flops
         i8_peak = 2.0 * mp.get("bf16_tflops", 1590.0)
         achieved = int8_ops / (ms_o.value * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOPS (int8)",
                 "frac": achieved / i8_peak, "traffic": traffic,
                 "kernel": ("ozaki_planes_gemm_kernel (tcgen05.mma kind::i8 on A's int8 digit planes, cut once per call "
-                           "and streamed by 3-D TMA; 34 digit products / FP64 FMA), NN pass T1 = A*X" if oz_planes else
-                           "ozaki_gemm_kernel (tcgen05.mma kind::i8, TMA-staged A converted in the pass, 34 digit "
+                           f"and streamed by 3-D TMA; {n_prod} digit products / FP64 FMA), NN pass T1 = A*X" if oz_planes else
+                           f"ozaki_gemm_kernel (tcgen05.mma kind::i8, TMA-staged A converted in the pass, {n_prod} digit "
                            "products / FP64 FMA), NN pass T1 = A*X"),
                 "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (burst): INT8 dense = 2x BF16 on B200",
                 "ms_per_launch": ms_o.value, "int8_ops_per_launch": int8_ops, "flops_per_launch": pass_flops,

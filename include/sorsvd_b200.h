@@ -113,6 +113,8 @@ int sorsvd_ctx_create(int device, sorsvd_ctx** out);
  * 128-byte NCCL id produced by sorsvd_nccl_unique_id on rank 0 and broadcast
  * by the caller (e.g. torch.distributed). */
 int sorsvd_nccl_unique_id(void* out128);
+/* int8 digit products per FP64 multiply-add in this build's Ozaki passes (bench.py's int8 op count). */
+int sorsvd_ozaki_products(void);
 /* One-GPU check of the NCCL binding (dlopen of libnccl.so.2, call signatures, stream order): a
  * one-rank communicator on `device`, in-place all-reduce + all-gather of `count` doubles; both must
  * return the input (max_abs_err = 0). Only one GPU is reachable in the build environment, so this

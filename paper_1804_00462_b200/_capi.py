@@ -64,6 +64,7 @@ class RpcaRes(ctypes.Structure):
 SIGNATURES = [
     ("sorsvd_ctx_create", c_i32, [ctypes.c_int, ctypes.POINTER(c_vp)]),
     ("sorsvd_nccl_unique_id", c_i32, [c_vp]),
+    ("sorsvd_ozaki_products", c_i32, []),
     ("sorsvd_nccl_selftest", c_i32, [c_i32, c_i64, c_dp]),
     ("sorsvd_ctx_create_dist", c_i32, [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, ctypes.POINTER(c_vp)]),
     ("sorsvd_ctx_destroy", None, [c_vp]),

@@ -45,6 +45,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(OUT_DIR, src + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
                "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
+        # SORSVD_OZ_LEVEL0=6: the 28-product cut of the Ozaki passes (default 5 = 34 products)
+        if os.environ.get("SORSVD_OZ_LEVEL0"):
+            cmd.insert(1, "-DOZ_LEVEL0=" + str(int(os.environ["SORSVD_OZ_LEVEL0"])))
         if src.endswith(".cpp"):
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-I", os.path.join(ROOT, "include"), "-c",
                    os.path.join(CSRC, src), "-o", obj]

@@ -58,8 +58,16 @@
 namespace sorsvd_dev {
 
 constexpr int kOzSlices = 7;            // 7 signed base-256 digits of a 55-bit integer
-constexpr int kOzLevels = 8;            // t + u in [5, 12]
-constexpr int kOzLevel0 = 5;            // lowest level kept
+// Lowest digit-pair level t + u kept. 5: 34 of the 49 products, dropped terms <= 5 * 2^-62 of
+// max|a| max|x| (below the 2^-55 grid of the operands themselves). 6: 28 products, dropped terms
+// <= 6 * 2^-56 (the size of FP64's own product rounding).
+#ifndef OZ_LEVEL0
+#define OZ_LEVEL0 5
+#endif
+constexpr int kOzLevel0 = OZ_LEVEL0;    // lowest level kept
+constexpr int kOzLevels = 13 - kOzLevel0;  // t + u in [kOzLevel0, 12]
+constexpr int kOzProducts = kOzLevel0 == 5 ? 34 : 28;
+static_assert(kOzLevel0 == 5 || kOzLevel0 == 6, "digit-pair lists exist for level 5 and 6 cuts");
 constexpr int kOzBM = 128;              // left rows per tile (TMEM lanes)
 constexpr int kOzBN = 64;               // right columns per tile (8 levels x 64 = 512 TMEM columns)
 constexpr int kOzBK = 32;               // K per step (one i8 MMA)
@@ -375,14 +383,23 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                         "l"(da), "l"(db), "r"(idesc));
                 };
                 // all pairs with t + u >= 5 (digits 0..6, 6 = top)
-                if (!(p.dbg & 1)) {
-                mma(6, 0, 4); mma(6, 4, 3);
-                mma(5, 0, 4); mma(5, 4, 3);
-                mma(4, 1, 4); mma(4, 5, 2);
-                mma(3, 2, 4); mma(3, 6, 1);
-                mma(2, 3, 4);
-                mma(1, 4, 3);
-                mma(0, 5, 2);
+                if (p.dbg & 1) {
+                } else if constexpr (kOzLevel0 == 5) {
+                    mma(6, 0, 4); mma(6, 4, 3);
+                    mma(5, 0, 4); mma(5, 4, 3);
+                    mma(4, 1, 4); mma(4, 5, 2);
+                    mma(3, 2, 4); mma(3, 6, 1);
+                    mma(2, 3, 4);
+                    mma(1, 4, 3);
+                    mma(0, 5, 2);
+                } else {  // t + u >= 6
+                    mma(6, 0, 4); mma(6, 4, 3);
+                    mma(5, 1, 4); mma(5, 5, 2);
+                    mma(4, 2, 4); mma(4, 6, 1);
+                    mma(3, 3, 4);
+                    mma(2, 4, 3);
+                    mma(1, 5, 2);
+                    mma(0, 6, 1);
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                                  empty(s))

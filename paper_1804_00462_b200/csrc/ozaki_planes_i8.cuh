@@ -390,6 +390,18 @@ __global__ void __maxnreg__(kOzpMaxRegs)
                 // all digit pairs with t + u >= 5, split over the issuing threads by A plane (straight-line
                 // blocks: the loop-invariant choice is one branch per step)
                 if (p.dbg & 1) {
+                } else if constexpr (kOzLevel0 == 6) {  // the 28 pairs with t + u >= 6
+                    if (kOzpIssuers == 1 || who == 0) {  // 13 products
+                        mma(6, 0, 4, C1{}); mma(6, 4, 3, C2{});
+                        mma(5, 1, 4, C1{}); mma(5, 5, 2, C2{});
+                    }
+                    if (kOzpIssuers == 1 || who == 1) {  // 15 products
+                        mma(4, 2, 4, C1{}); mma(4, 6, 1, C2{});
+                        mma(3, 3, 4, C0{});
+                        mma(2, 4, 3, C0{});
+                        mma(1, 5, 2, C0{});
+                        mma(0, 6, 1, C0{});
+                    }
                 } else if constexpr (kOzpIssuers == 1) {
                     mma(6, 0, 4, C1{}); mma(6, 4, 3, C2{});
                     mma(5, 0, 4, C1{}); mma(5, 4, 3, C2{});

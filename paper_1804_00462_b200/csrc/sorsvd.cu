@@ -3926,6 +3926,9 @@ int sorsvd_ctx_create(int device, sorsvd_ctx** out) {
     return SORSVD_OK;
 }
 
+// Digit products per FP64 multiply-add of this build's Ozaki engines (34: pairs t + u >= 5; 28: >= 6).
+int sorsvd_ozaki_products(void) { return kOzProducts; }
+
 int sorsvd_nccl_unique_id(void* out128) {
     return guarded(nullptr, [&] {
         ncclUniqueId id;
