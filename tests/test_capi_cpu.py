@@ -139,3 +139,10 @@ def test_gaussian_rows_is_a_slice_of_the_full_draw():
                 out = np.full((rows, cols), np.nan)
                 assert lib.sorsvd_gaussian_rows(cols, row0, rows, seed, out.ctypes.data_as(P._capi.c_dp), nt) == 0
                 assert np.array_equal(out, full[row0:row0 + rows]), (cols, total, row0, rows, nt)
+
+
+def test_default_build_keeps_34_digit_products():
+    """The shipped library is the 34-product cut of the Ozaki passes (pairs t + u >= 5, error below FP64's own
+    rounding); the 28-product cut is a build option (SORSVD_OZ_LEVEL0=6) and must not ship by accident."""
+    from paper_1804_00462_b200 import _capi
+    assert _capi.lib().sorsvd_ozaki_products() == 34
